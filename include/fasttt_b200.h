@@ -1,0 +1,199 @@
+/*
+ * fasttt_b200.h -- C ABI of the B200-native FastTT decomposition path.
+ *
+ * The reference (`sparsett`, pure Python, /root/reference/pkg/src/sparsett)
+ * has no FFI; its boundary is the Python namespace.  Each entry point below
+ * replaces the numpy/LAPACK body of one reference function on the hot path
+ * (file:line cited per function).  The Python mirror of the reference API
+ * (paper_1908_02721_b200/) binds these through ctypes.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless the name ends in `_host`.
+ *  - Dense matrices are column-major with an explicit leading dimension
+ *    (LAPACK convention); a row-major (numpy C-order) r x c array is the
+ *    column-major c x r array of its transpose.
+ *  - Sizes are int64_t; every call is enqueued on the context's stream.
+ *    Calls that return a size to the host (`*_out` host pointers)
+ *    synchronise that stream.
+ *  - Return value: FTT_OK or an ftt_status error; ftt_last_error() gives a
+ *    message.  No exception crosses the ABI.
+ *  - Workspaces are owned by the context (grow-only, stream-ordered).
+ */
+#ifndef FASTTT_B200_H
+#define FASTTT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FTT_OK = 0,
+  FTT_ERR_INVALID = 1,   /* -> ValueError / TypeError in the Python mirror */
+  FTT_ERR_OOM = 2,       /* -> MemoryError */
+  FTT_ERR_NONFINITE = 3, /* -> ValueError("matrix entries must be finite") */
+  FTT_ERR_CUDA = 4,      /* -> RuntimeError */
+  FTT_ERR_NOCONV = 5     /* -> numpy.linalg.LinAlgError (SVD did not converge) */
+} ftt_status;
+
+typedef struct ftt_ctx ftt_ctx;
+
+/* ------------------------------------------------------------ context */
+const char *ftt_version(void);
+const char *ftt_last_error(void);
+/* stream: a cudaStream_t passed as an opaque pointer (0 = legacy default). */
+int ftt_create(int device, void *stream, ftt_ctx **ctx_out);
+int ftt_destroy(ftt_ctx *ctx);
+int ftt_set_stream(ftt_ctx *ctx, void *stream);
+/* Number of kernels this context launched since creation (instrumentation). */
+int64_t ftt_kernel_launches(const ftt_ctx *ctx);
+
+/* ---------------------------------------------------- index path (int) */
+
+/* Distinct fixed tuples for one pivot mode: the fiber count R_p computed
+ * by select_p, `np.unique(linearize(rest_dims, coords[:, rest])).size`
+ * (fasttt.py:537-541).  coords: nnz x d int64 row-major. */
+int ftt_fiber_count(ftt_ctx *ctx, const int64_t *coords, int64_t nnz,
+                    int32_t d, const int64_t *dims_host, int32_t pivot,
+                    int64_t *count_out);
+
+/* Fiber counts for every pivot 0..d-1 (select_p's loop, fasttt.py:536-541),
+ * written to counts_host[d]. */
+int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz,
+                         int32_t d, const int64_t *dims_host,
+                         int64_t *counts_host);
+
+/* extract_nonzero_fibers (tensor.py:374-403) / build_structured_tt
+ * (fasttt.py:170-178).  Sorts by key lin(fixed)*n_p + i_p (the lexsort of
+ * tensor.py:387-389 as one integer key) and segments where the fixed tuple
+ * changes.  Outputs (capacity nnz, resp. nnz+1):
+ *   fixed_lin[R]   C-order linear index of the fixed tuple over rest dims
+ *   indptr[R+1]    fiber f owns entries indptr[f]..indptr[f+1]
+ *   fiber_of[nnz]  fiber id of every sorted entry (may be NULL)
+ *   pivot_index[nnz], values_out[nnz]  entries in fiber order
+ * num_fibers_out (host) receives R. */
+int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords,
+                       const double *values, int64_t nnz, int32_t d,
+                       const int64_t *dims_host, int32_t pivot,
+                       int64_t *fixed_lin, int64_t *indptr, int64_t *fiber_of,
+                       int64_t *pivot_index, double *values_out,
+                       int64_t *num_fibers_out);
+
+/* depar_quasi_perm (fasttt.py:148-167): kept = ascending distinct rows of
+ * col_to_row, t_map[j] = rank of col_to_row[j] among kept.  kept capacity
+ * min(n_rows, n_cols). n_kept_out (host). */
+int ftt_depar_quasi_perm(ftt_ctx *ctx, int64_t n_rows, int64_t n_cols,
+                         const int64_t *col_to_row, int64_t *kept,
+                         int64_t *t_map, int64_t *n_kept_out);
+
+/* One step of _index_sweeps (fasttt.py:192-210) fused with its key build:
+ *   side 0 (left of pivot):  key[f] = map_in[f] * n_k + i_k(f)
+ *   side 1 (right of pivot): key[f] = i_k(f) * r_other + map_in[f]
+ * with i_k(f) = (fixed_lin[f] / stride_k) % n_k, and n_rows = r_other*n_k.
+ * map_in may be NULL (all zeros, first step of a side).  Then
+ * depar_quasi_perm on (n_rows, R, key): kept (capacity min(R, n_rows)),
+ * map_out[R], n_kept_out (host). */
+int ftt_index_sweep_step(ftt_ctx *ctx, int32_t side, const int64_t *fixed_lin,
+                         int64_t R, int64_t stride_k, int64_t n_k,
+                         const int64_t *map_in, int64_t r_other,
+                         int64_t *kept, int64_t *map_out,
+                         int64_t *n_kept_out);
+
+/* Per-fiber coordinate of one rest mode: (fixed_lin / stride) % n
+ * (StructuredTT.mode_index, ttformat.py:322-327). */
+int ftt_mode_index(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R,
+                   int64_t stride, int64_t n, int64_t *out);
+
+/* Pivot core of parallel_vector_round (fasttt.py:256-259): zero-fills the
+ * dense r_prev x n_p x r_next C-order core and scatters
+ * core[t_map[f], pivot_index[e], s_map[f]] = values[e] for every entry e of
+ * fiber f = fiber_of[e].  t_map / s_map may be NULL (all zeros).  Also
+ * returns the 2-norm of the values (the _budget_norm of fasttt.py:359-361)
+ * in norm_out (host) when norm_out != NULL. */
+int ftt_pivot_core_scatter(ftt_ctx *ctx, int64_t nnz, const int64_t *fiber_of,
+                           const int64_t *pivot_index, const double *values,
+                           const int64_t *t_map, const int64_t *s_map,
+                           int64_t r_prev, int64_t n_p, int64_t r_next,
+                           double *core, double *norm_out);
+
+/* Dense 0/1 side cores (fasttt.py:246-255), materialised only for the
+ * standalone parallel_vector_round API and the capped error measure.
+ * side 0: core (r_other, n, K) with core[kept[j]//n, kept[j]%n, j] = 1
+ * side 1: core (K, n, r_other) with core[j, kept[j]//r_other, kept[j]%r_other] = 1 */
+int ftt_side_core_dense(ftt_ctx *ctx, int32_t side, const int64_t *kept,
+                        int64_t K, int64_t n, int64_t r_other, double *core);
+
+/* --------------------------------------------- carries into 0/1 cores */
+/* First-sweep carry into a right 0/1 core (fasttt.py:340-341 with the core
+ * of :251-255): dst (rank x ncols_new, row-major) = 0, then
+ * dst[a, kept[j]] = src[a*lds + j] for j < K. */
+int ftt_scatter_cols(ftt_ctx *ctx, int64_t rank, int64_t K, const int64_t *kept,
+                     const double *src, int64_t lds, int64_t ncols_new,
+                     double *dst);
+/* Second-sweep carry into a left 0/1 core (fasttt.py:354-355 with the core
+ * of :246-250): dst (nrows_new x rank, row-major) = 0, then
+ * dst[kept[j], :] = src[j*lds + 0..rank). */
+int ftt_scatter_rows(ftt_ctx *ctx, int64_t K, int64_t rank, const int64_t *kept,
+                     const double *src, int64_t lds, int64_t nrows_new,
+                     double *dst);
+
+/* ------------------------------------------------------ dense fp64 */
+/* C = alpha*op(A)*op(B) + beta*C, column-major, BLAS dgemm semantics
+ * (trans = 0 'N', 1 'T').  Replaces np.tensordot / np.einsum / @ on the
+ * dense carries (fasttt.py:341, 347, 355). DMMA (mma.sync m8n8k4 f64). */
+int ftt_dgemm(ftt_ctx *ctx, int32_t transa, int32_t transb, int64_t m,
+              int64_t n, int64_t k, double alpha, const double *A, int64_t lda,
+              const double *B, int64_t ldb, double beta, double *C,
+              int64_t ldc);
+
+/* max |G - I| over an n x n column-major Gram (the orthonormality test of
+ * _check_pivot_orthogonal, fasttt.py:303-321), to out_host. */
+int ftt_orth_defect(ftt_ctx *ctx, int64_t n, const double *G, int64_t ldg,
+                    double *out_host);
+
+/* dst (cols x rows, ldd) = src^T (src rows x cols, lds), column-major. */
+int ftt_transpose(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *src,
+                  int64_t lds, double *dst, int64_t ldd);
+
+/* qr_economic (linalg.py:128-140): reduced Householder QR of the m x n
+ * column-major A; Q (m x k) and R (k x n), k = min(m, n), diag(R) >= 0.
+ * A is not modified. Non-finite input -> FTT_ERR_NONFINITE. */
+int ftt_qr_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
+               int64_t lda, double *Q, int64_t ldq, double *R, int64_t ldr);
+
+/* _full_svd (linalg.py:48-53), phase 1: thin SVD of the m x n matrix A,
+ * column-major (a_row_major = 0) or row-major / numpy C-order
+ * (a_row_major = 1), leading dimension lda (Householder QR + one-sided block
+ * Jacobi).  Writes the k = min(m,n) singular values, descending, to s_host.
+ * Factors stay in the context for phase 2.  A is not modified. */
+int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
+                int64_t lda, int32_t a_row_major, double *s_host);
+/* Phase 2: the leading `rank` singular triplets of the last ftt_svd_f64, with
+ * the sign convention of _fix_signs (linalg.py:56-63) applied to U: U (m x
+ * rank) and V (n x rank, i.e. vt.T), each column- or row-major per its flag;
+ * scale_v != 0 multiplies column j of V by s[j] (the carry vt.T * s of
+ * fasttt.py:340/354).  U or V may be NULL. */
+int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ldu,
+                    int32_t u_row_major, double *V, int64_t ldv,
+                    int32_t v_row_major, int32_t scale_v);
+
+/* sum of squares of x (n values), written to out_host (frobenius_norm,
+ * tensor.py:298-302, and the sparse_inner_error dot, fasttt.py:596-599 when
+ * y != NULL: sum x*y). */
+int ftt_dot(ftt_ctx *ctx, int64_t n, const double *x, const double *y,
+            double *out_host);
+
+/* tt_entries (ttformat.py:124-136): out[i] = G0[:, c[i,0], :] @ ... @
+ * G_{d-1}[:, c[i,d-1], :] for n coordinates (n x d int64 row-major).
+ * cores_host[k] is a device pointer to the C-order (r_k, n_k, r_{k+1}) core;
+ * ranks_host has d+1 entries, dims_host d. */
+int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
+                   const int64_t *ranks_host, const double *const *cores_host,
+                   const int64_t *coords, int64_t n, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTTT_B200_H */

@@ -1,0 +1,120 @@
+// Shared internals of libfasttt_b200: context, workspace arena, errors.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fasttt_b200.h"
+
+namespace ftt {
+
+constexpr int kNumSMs = 148;  // B200
+
+void set_error(const char *fmt, ...);
+
+struct SvdState;  // ftt_svd.cu
+
+// Grow-only device arena.  Every API call resets it; allocations are
+// 256-byte aligned bumps.  Growth frees the old block stream-ordered and
+// allocates a larger one (so pointers from before a growth in the same call
+// are invalid -- callers reserve the total up front with `reserve`).
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+};
+
+}  // namespace ftt
+
+struct ftt_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ftt::Arena arena;
+  // persistent, independently sized buffers (SVD factors etc.)
+  std::vector<std::pair<void *, size_t>> owned;
+  ftt::SvdState *svd = nullptr;
+  int64_t launches = 0;
+  int num_sms = ftt::kNumSMs;
+  void *pinned = nullptr;  // small pinned host scratch (64 KiB)
+};
+
+namespace ftt {
+
+#define FTT_CUDA(expr)                                                      \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) {                                                \
+      ::ftt::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,          \
+                       cudaGetErrorString(_e));                             \
+      return _e == cudaErrorMemoryAllocation ? FTT_ERR_OOM : FTT_ERR_CUDA;  \
+    }                                                                       \
+  } while (0)
+
+#define FTT_CHECK(expr)            \
+  do {                             \
+    int _s = (expr);               \
+    if (_s != FTT_OK) return _s;   \
+  } while (0)
+
+#define FTT_LAUNCHED(ctx)                                                  \
+  do {                                                                     \
+    (ctx)->launches++;                                                     \
+    cudaError_t _e = cudaGetLastError();                                   \
+    if (_e != cudaSuccess) {                                               \
+      ::ftt::set_error("%s:%d launch: %s", __FILE__, __LINE__,             \
+                       cudaGetErrorString(_e));                            \
+      return FTT_ERR_CUDA;                                                 \
+    }                                                                      \
+  } while (0)
+
+// Reserve at least `bytes` of arena for this call (must be called before
+// taking pointers).  Resets `used`.
+int arena_reserve(ftt_ctx *ctx, size_t bytes);
+// Bump-allocate from the reserved arena (fails if the reservation is short).
+void *arena_take(ftt_ctx *ctx, size_t bytes);
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+template <class T>
+inline T *take(ftt_ctx *ctx, size_t count) {
+  return static_cast<T *>(arena_take(ctx, align_up(count * sizeof(T))));
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int grid_for(int64_t n, int threads, int per_thread = 1, int max_blocks = 148 * 16) {
+  int64_t b = ceil_div(n, (int64_t)threads * per_thread);
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+// Synchronous device->host copy of a few scalars through pinned scratch.
+int copy_to_host(ftt_ctx *ctx, void *host, const void *dev, size_t bytes);
+int copy_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes);
+
+// Persistent device buffer owned by the context (freed on destroy).
+int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes);
+void owned_free(ftt_ctx *ctx, void *p);
+
+// ----- primitives shared across translation units (ftt_index.cu)
+// LSD radix sort of 64-bit keys with optional 32-bit payload over bits
+// [0, end_bit).  Result lands in keys_out/vals_out.  Scratch from the arena
+// (reserved by the caller with radix_sort_scratch_bytes).
+size_t radix_sort_scratch_bytes(int64_t n, bool with_vals);
+int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in,
+               uint64_t *keys_out, uint32_t *vals_out, int64_t n, int end_bit);
+
+// Deterministic sum of squares (partial must hold kSumSqBlocks + 1 doubles).
+constexpr int kSumSqBlocks = 148 * 8;
+int sum_squares(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_host);
+
+// Exclusive scan of int64 block counts (small arrays, single block).
+int scan_block_counts(ftt_ctx *ctx, int64_t *counts, int64_t nblocks, int64_t *total_dev);
+
+}  // namespace ftt

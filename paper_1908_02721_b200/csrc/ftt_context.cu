@@ -1,0 +1,160 @@
+// Context, arena and error plumbing of the C ABI.
+#include <stdarg.h>
+
+#include "ftt_common.cuh"
+
+namespace ftt {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int arena_reserve(ftt_ctx *ctx, size_t bytes) {
+  ctx->arena.used = 0;
+  if (bytes <= ctx->arena.cap) return FTT_OK;
+  size_t want = align_up(bytes + bytes / 4, 1 << 20);
+  if (ctx->arena.base) {
+    FTT_CUDA(cudaFreeAsync(ctx->arena.base, ctx->stream));
+    ctx->arena.base = nullptr;
+    ctx->arena.cap = 0;
+  }
+  void *p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, want, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    // retry with the exact size
+    e = cudaMallocAsync(&p, align_up(bytes, 1 << 20), ctx->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_error("workspace allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+      return FTT_ERR_OOM;
+    }
+    want = align_up(bytes, 1 << 20);
+  }
+  ctx->arena.base = static_cast<char *>(p);
+  ctx->arena.cap = want;
+  return FTT_OK;
+}
+
+void *arena_take(ftt_ctx *ctx, size_t bytes) {
+  bytes = align_up(bytes);
+  if (ctx->arena.used + bytes > ctx->arena.cap) return nullptr;
+  void *p = ctx->arena.base + ctx->arena.used;
+  ctx->arena.used += bytes;
+  return p;
+}
+
+int copy_to_host(ftt_ctx *ctx, void *host, const void *dev, size_t bytes) {
+  if (bytes == 0) return FTT_OK;
+  if (bytes <= 65536) {
+    FTT_CUDA(cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+    memcpy(host, ctx->pinned, bytes);
+  } else {
+    FTT_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FTT_OK;
+}
+
+int copy_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes) {
+  if (bytes == 0) return FTT_OK;
+  if (bytes <= 65536) {
+    // the pinned scratch may still be read by an earlier async copy
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+    memcpy(ctx->pinned, host, bytes);
+    FTT_CUDA(cudaMemcpyAsync(dev, ctx->pinned, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    FTT_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FTT_OK;
+}
+
+int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 256;
+  cudaError_t e = cudaMallocAsync(p, bytes, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    return FTT_ERR_OOM;
+  }
+  ctx->owned.push_back({*p, bytes});
+  return FTT_OK;
+}
+
+void owned_free(ftt_ctx *ctx, void *p) {
+  if (!p) return;
+  for (size_t i = 0; i < ctx->owned.size(); ++i) {
+    if (ctx->owned[i].first == p) {
+      cudaFreeAsync(p, ctx->stream);
+      ctx->owned.erase(ctx->owned.begin() + i);
+      return;
+    }
+  }
+}
+
+void svd_state_free(ftt_ctx *ctx);  // ftt_svd.cu
+
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" {
+
+const char *ftt_version(void) { return "fasttt_b200 0.1.0 (sm_100a)"; }
+
+const char *ftt_last_error(void) { return g_err; }
+
+int ftt_create(int device, void *stream, ftt_ctx **ctx_out) {
+  if (!ctx_out) {
+    set_error("ctx_out is NULL");
+    return FTT_ERR_INVALID;
+  }
+  *ctx_out = nullptr;
+  FTT_CUDA(cudaSetDevice(device));
+  ftt_ctx *ctx = new ftt_ctx();
+  ctx->device = device;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+    ctx->num_sms = sms;
+  cudaError_t e = cudaMallocHost(&ctx->pinned, 65536);
+  if (e != cudaSuccess) {
+    delete ctx;
+    set_error("pinned scratch: %s", cudaGetErrorString(e));
+    return FTT_ERR_CUDA;
+  }
+  *ctx_out = ctx;
+  return FTT_OK;
+}
+
+int ftt_destroy(ftt_ctx *ctx) {
+  if (!ctx) return FTT_OK;
+  cudaSetDevice(ctx->device);
+  svd_state_free(ctx);
+  for (auto &p : ctx->owned) cudaFreeAsync(p.first, ctx->stream);
+  ctx->owned.clear();
+  if (ctx->arena.base) cudaFreeAsync(ctx->arena.base, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+  return FTT_OK;
+}
+
+int ftt_set_stream(ftt_ctx *ctx, void *stream) {
+  if (!ctx) return FTT_ERR_INVALID;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return FTT_OK;
+}
+
+int64_t ftt_kernel_launches(const ftt_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

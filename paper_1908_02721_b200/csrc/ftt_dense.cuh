@@ -1,0 +1,35 @@
+// Internal dense fp64 building blocks shared by the QR / SVD / TT files.
+#pragma once
+#include "ftt_common.cuh"
+
+namespace ftt {
+
+// Column-major DMMA GEMM (see ftt_gemm.cu).  splitk_ws may be NULL (no
+// split-K); otherwise it must hold gemm_splitk_elems(m, n, k) doubles.
+int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+         const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+         int64_t ldc, double *splitk_ws, size_t splitk_ws_elems);
+size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k);
+int transpose(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *src, int64_t lds,
+              double *dst, int64_t ldd);
+
+// Blocked Householder QR (ftt_qr.cu).  Factors the m x n column-major A in
+// place (LAPACK dgeqrf layout: R on and above the diagonal, reflectors
+// below, tau[min(m,n)]) and stores the block T factors (NBO x NBO each) in
+// Tblk.  Workspace sizes from qr_workspace_elems.
+constexpr int QR_NBO = 128;  // outer block (trailing update)
+constexpr int QR_NBI = 32;   // inner panel (cooperative column-by-column)
+size_t qr_workspace_elems(int64_t m, int64_t n);
+size_t qr_tblk_elems(int64_t m, int64_t n);
+int qr_factor(ftt_ctx *ctx, int64_t m, int64_t n, double *A, int64_t lda, double *tau,
+              double *Tblk, double *ws, size_t ws_elems);
+// Z (m x r, ldz) <- Q * Z using the factorization above (Q = H_1 ... H_k).
+int qr_apply_q(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, const double *Tblk,
+               int64_t r, double *Z, int64_t ldz, double *ws, size_t ws_elems);
+size_t qr_apply_workspace_elems(int64_t m, int64_t n, int64_t r);
+
+int check_finite(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, bool *ok);
+int copy_matrix(ftt_ctx *ctx, int64_t m, int64_t n, const double *src, int64_t lds, double *dst,
+                int64_t ldd);
+
+}  // namespace ftt

@@ -1,0 +1,203 @@
+// tt_entries (ttformat.py:124-136): entries of a train at many coordinates.
+// Used by the error report of fasttt (sparse_inner_error, fasttt.py:587-602)
+// and by the parity checks.
+//  * max rank <= 64: one warp per coordinate, the running row vector lives
+//    in two registers per lane, slices are read coalesced along r_{k+1}.
+//  * larger ranks: level-by-level grouped GEMMs -- rows are stably sorted by
+//    the mode-k index so that every group shares one (r_k x r_{k+1}) slice,
+//    which turns the per-coordinate GEMVs into DMMA GEMMs.
+#include <algorithm>
+#include <vector>
+
+#include "ftt_dense.cuh"
+
+namespace ftt {
+namespace {
+
+struct TrainDesc {
+  int d;
+  int64_t dims[32];
+  int64_t ranks[33];
+  const double *cores[32];
+};
+
+__global__ void k_entries_small(TrainDesc t, const int64_t *__restrict__ coords, int64_t n,
+                                double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    double v0 = lane == 0 ? 1.0 : 0.0, v1 = 0.0;
+    for (int k = 0; k < t.d; ++k) {
+      const int64_t r0 = t.ranks[k], r1 = t.ranks[k + 1], nk = t.dims[k];
+      const int64_t idx = coords[i * t.d + k];
+      const double *G = t.cores[k] + idx * r1;
+      const int64_t rowst = nk * r1;
+      double a0 = 0.0, a1 = 0.0;
+      for (int64_t a = 0; a < r0; ++a) {
+        double va = __shfl_sync(0xffffffffu, a < 32 ? v0 : v1, (int)(a & 31));
+        if (lane < r1) a0 += va * G[a * rowst + lane];
+        if (lane + 32 < r1) a1 += va * G[a * rowst + lane + 32];
+      }
+      v0 = a0;
+      v1 = a1;
+    }
+    if (lane == 0) out[i] = v0;
+  }
+}
+
+__global__ void k_first_rows(int64_t n, const int64_t *__restrict__ coords, int d, const double *core0,
+                             int64_t r1, const int64_t *__restrict__ idx, double *__restrict__ V) {
+  int64_t total = n * r1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / r1, j = t - i * r1;
+    V[t] = core0[coords[idx[i] * d] * r1 + j];
+  }
+}
+
+__global__ void k_level_keys(int64_t n, const int64_t *__restrict__ coords, int d, int k,
+                             const int64_t *__restrict__ idx, uint64_t *__restrict__ keys,
+                             uint32_t *__restrict__ pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint64_t)coords[idx[i] * d + k];
+    pos[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_permute_rows(int64_t n, int64_t r, const uint32_t *__restrict__ perm,
+                               const double *__restrict__ V, double *__restrict__ Vs,
+                               const int64_t *__restrict__ idx, int64_t *__restrict__ idx_new) {
+  int64_t total = n * r;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / r, j = t - i * r;
+    int64_t src = perm[i];
+    Vs[t] = V[src * r + j];
+    if (j == 0) idx_new[i] = idx[src];
+  }
+}
+
+__global__ void k_bounds(int64_t n, const uint64_t *__restrict__ skeys, int64_t nk, int64_t *__restrict__ off) {
+  // off[v] = first position with key >= v (sorted keys), off[nk] = n
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = i == 0 ? 0 : (int64_t)skeys[i - 1] + 1;
+    int64_t hi = i == n ? nk : (int64_t)skeys[i];
+    for (int64_t v = lo; v <= hi && v <= nk; ++v) off[v] = i;
+  }
+}
+
+__global__ void k_scatter_out(int64_t n, int64_t r, const double *__restrict__ V,
+                              const int64_t *__restrict__ idx, double *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[idx[i]] = V[i * r];
+}
+
+__global__ void k_iota64(int64_t n, int64_t base, int64_t *p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = base + i;
+}
+
+int bitlen(uint64_t x) {
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+}  // namespace
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
+                              const int64_t *ranks_host, const double *const *cores_host,
+                              const int64_t *coords, int64_t n, double *out) {
+  if (!ctx || d < 1 || d > 32) {
+    set_error("ftt_tt_entries: invalid train");
+    return FTT_ERR_INVALID;
+  }
+  if (n == 0) return FTT_OK;
+  TrainDesc t;
+  t.d = d;
+  int64_t rmax = 1;
+  for (int k = 0; k < d; ++k) {
+    t.dims[k] = dims_host[k];
+    t.cores[k] = cores_host[k];
+  }
+  for (int k = 0; k <= d; ++k) {
+    t.ranks[k] = ranks_host[k];
+    rmax = std::max(rmax, ranks_host[k]);
+  }
+  if (ranks_host[0] != 1 || ranks_host[d] != 1) {
+    set_error("edge ranks must be 1");
+    return FTT_ERR_INVALID;
+  }
+  if (rmax <= 64) {
+    k_entries_small<<<grid_for(n, 8, 1, 148 * 64), 256, 0, ctx->stream>>>(t, coords, n, out);
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
+  // grouped GEMM path, in chunks to bound memory
+  const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(4096, (int64_t)(1ll << 31) / (8 * rmax)));
+  int64_t nkmax = 1;
+  for (int k = 0; k < d; ++k) nkmax = std::max(nkmax, dims_host[k]);
+  size_t need = 2 * align_up(8 * (size_t)chunk * rmax) + 2 * align_up(8 * chunk) +
+                align_up(8 * chunk) + align_up(4 * chunk) + align_up(8 * (nkmax + 1)) +
+                radix_sort_scratch_bytes(chunk, true) + align_up(8 * chunk) + align_up(4 * chunk) +
+                4096;
+  FTT_CHECK(arena_reserve(ctx, need));
+  double *V = take<double>(ctx, (size_t)chunk * rmax);
+  double *Vs = take<double>(ctx, (size_t)chunk * rmax);
+  int64_t *idx = take<int64_t>(ctx, chunk);
+  int64_t *idx2 = take<int64_t>(ctx, chunk);
+  uint64_t *keys = take<uint64_t>(ctx, chunk);
+  uint32_t *pos = take<uint32_t>(ctx, chunk);
+  int64_t *off = take<int64_t>(ctx, nkmax + 1);
+  uint64_t *skeys = take<uint64_t>(ctx, chunk);
+  uint32_t *perm = take<uint32_t>(ctx, chunk);
+  if (!perm) {
+    set_error("ftt_tt_entries: arena too small");
+    return FTT_ERR_INVALID;
+  }
+  std::vector<int64_t> hoff(nkmax + 1);
+  for (int64_t c0 = 0; c0 < n; c0 += chunk) {
+    const int64_t cn = std::min(chunk, n - c0);
+    k_iota64<<<grid_for(cn, 256, 4), 256, 0, ctx->stream>>>(cn, c0, idx);
+    FTT_LAUNCHED(ctx);
+    int64_t r = ranks_host[1];
+    k_first_rows<<<grid_for(cn * r, 256, 4), 256, 0, ctx->stream>>>(cn, coords, d, cores_host[0], r,
+                                                                     idx, V);
+    FTT_LAUNCHED(ctx);
+    for (int k = 1; k < d; ++k) {
+      const int64_t nk = dims_host[k], r0 = ranks_host[k], r1 = ranks_host[k + 1];
+      k_level_keys<<<grid_for(cn, 256, 4), 256, 0, ctx->stream>>>(cn, coords, d, k, idx, keys, pos);
+      FTT_LAUNCHED(ctx);
+      size_t mark = ctx->arena.used;
+      FTT_CHECK(radix_sort(ctx, keys, pos, skeys, perm, cn, std::max(1, bitlen((uint64_t)(nk - 1)))));
+      ctx->arena.used = mark;
+      k_permute_rows<<<grid_for(cn * r0, 256, 4), 256, 0, ctx->stream>>>(cn, r0, perm, V, Vs, idx, idx2);
+      FTT_LAUNCHED(ctx);
+      std::swap(idx, idx2);
+      k_bounds<<<grid_for(cn + 1, 256, 4), 256, 0, ctx->stream>>>(cn, skeys, nk, off);
+      FTT_LAUNCHED(ctx);
+      FTT_CHECK(copy_to_host(ctx, hoff.data(), off, 8 * (nk + 1)));
+      for (int64_t v = 0; v < nk; ++v) {
+        int64_t cnt = hoff[v + 1] - hoff[v];
+        if (cnt <= 0) continue;
+        // (cnt x r0) @ (r0 x r1) row-major == col-major (r1 x cnt) = G^T (r1 x r0) * Vs^T (r0 x cnt)
+        FTT_CHECK(gemm(ctx, 0, 0, r1, cnt, r0, 1.0, cores_host[k] + v * r1, nk * r1,
+                       Vs + hoff[v] * r0, r0, 0.0, V + hoff[v] * r1, r1, nullptr, 0));
+      }
+      r = r1;
+    }
+    k_scatter_out<<<grid_for(cn, 256, 4), 256, 0, ctx->stream>>>(cn, 1, V, idx, out);
+    FTT_LAUNCHED(ctx);
+  }
+  return FTT_OK;
+}

@@ -1,0 +1,319 @@
+// fp64 GEMM on the B200 DMMA pipe (mma.sync.aligned.m8n8k4 .f64) with
+// BLAS dgemm semantics (column-major, op = N/T).  Used for every dense core
+// contraction of the rounding sweeps (fasttt.py:341, 347, 355) and inside
+// the blocked Householder QR / Jacobi SVD.  tcgen05 has no f64 kind on
+// sm_100a (ptxas rejects .kind::f64), so DMMA is the fp64 tensor path.
+//
+// CTA tile 64x64x16, 4 warps (2x2, 32x32 each = 4x4 DMMA tiles), register
+// prefetch of the next k-tile into a second shared buffer.  Split-K with a
+// deterministic reduction when the output has too few tiles for 148 SMs.
+#include "ftt_common.cuh"
+#include "ftt_dense.cuh"
+
+#include <vector>
+
+namespace ftt {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, GT = 128;
+constexpr int PAD = 4;  // (64+4) doubles = 136 words == 8 banks: conflict-free fragment loads
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, double alpha,
+                                              const double *__restrict__ A, int64_t lda,
+                                              const double *__restrict__ B, int64_t ldb, double beta,
+                                              double *__restrict__ C, int64_t ldc, int64_t kps,
+                                              double *__restrict__ partial) {
+  __shared__ double As[2][BK][BM + PAD];
+  __shared__ double Bs[2][BK][BN + PAD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int64_t tm = (int64_t)blockIdx.x * BM, tn = (int64_t)blockIdx.y * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kps;
+  const int64_t ke = min(k, kb + kps);
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double ra[8], rb[8];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int e = r * GT + tid;
+      int i, kk;
+      if (!TA) {
+        i = e % BM;
+        kk = e / BM;
+      } else {
+        kk = e % BK;
+        i = e / BK;
+      }
+      int64_t gi = tm + i, gk = k0 + kk;
+      double v = 0.0;
+      if (gi < m && gk < ke) v = TA ? A[gk + gi * lda] : A[gi + gk * lda];
+      ra[r] = v;
+      int j;
+      if (!TB) {
+        kk = e % BK;
+        j = e / BK;
+      } else {
+        j = e % BN;
+        kk = e / BN;
+      }
+      int64_t gj = tn + j;
+      gk = k0 + kk;
+      double w = 0.0;
+      if (gj < n && gk < ke) w = TB ? B[gj + gk * ldb] : B[gk + gj * ldb];
+      rb[r] = w;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int e = r * GT + tid;
+      int i, kk, j;
+      if (!TA) {
+        i = e % BM;
+        kk = e / BM;
+      } else {
+        kk = e % BK;
+        i = e / BK;
+      }
+      As[buf][kk][i] = ra[r];
+      if (!TB) {
+        kk = e % BK;
+        j = e / BK;
+      } else {
+        j = e % BN;
+        kk = e / BN;
+      }
+      Bs[buf][kk][j] = rb[r];
+    }
+  };
+
+  int buf = 0;
+  if (kb < ke) {
+    load(kb);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) load(k0 + BK);
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t row = tm + wm + i * 8 + (lane >> 2);
+    if (row >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int64_t col = tn + wn + j * 8 + 2 * (lane & 3) + h;
+        if (col >= n) continue;
+        if (partial) {
+          partial[((int64_t)blockIdx.z * n + col) * m + row] = acc[i][j][h];
+        } else {
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * C[row + col * ldc];
+          C[row + col * ldc] = v;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *__restrict__ partial,
+                                double alpha, double beta, double *__restrict__ C, int64_t ldc) {
+  int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t col = t / m, row = t - col * m;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + t];
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * C[row + col * ldc];
+    C[row + col * ldc] = v;
+  }
+}
+
+__global__ void k_scale_c(int64_t m, int64_t n, double beta, double *C, int64_t ldc) {
+  int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t col = t / m, row = t - col * m;
+    C[row + col * ldc] = beta == 0.0 ? 0.0 : beta * C[row + col * ldc];
+  }
+}
+
+__global__ void k_transpose(int64_t rows, int64_t cols, const double *__restrict__ src, int64_t lds,
+                            double *__restrict__ dst, int64_t ldd) {
+  __shared__ double t[32][33];
+  int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int64_t r = r0 + threadIdx.x, c = c0 + j;
+    if (r < rows && c < cols) t[j][threadIdx.x] = src[r + c * lds];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int64_t c = c0 + threadIdx.x, r = r0 + j;  // dst(c, r) = src(r, c)
+    if (r < rows && c < cols) dst[c + r * ldd] = t[threadIdx.x][j];
+  }
+}
+
+__global__ void k_orth_defect(int64_t n, const double *__restrict__ G, int64_t ldg,
+                              double *__restrict__ partial) {
+  double mx = 0.0;
+  int64_t total = n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / n, i = t - j * n;
+    double v = fabs(G[i + j * ldg] - (i == j ? 1.0 : 0.0));
+    mx = fmax(mx, v);
+  }
+  for (int off = 16; off; off >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, off));
+  __shared__ double s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, s[w]);
+    partial[blockIdx.x] = t;
+  }
+}
+
+}  // namespace
+
+int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+         const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
+         int64_t ldc, double *splitk_ws, size_t splitk_ws_elems) {
+  if (m <= 0 || n <= 0) return FTT_OK;
+  if (k <= 0 || alpha == 0.0) {
+    if (beta == 1.0) return FTT_OK;
+    k_scale_c<<<grid_for(m * n, 256, 4), 256, 0, ctx->stream>>>(m, n, beta, C, ldc);
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
+  int64_t tiles_m = ceil_div(m, BM), tiles_n = ceil_div(n, BN);
+  int64_t tiles = tiles_m * tiles_n;
+  int splits = 1;
+  if (tiles < 2 * ctx->num_sms && k >= 4 * 256) {
+    int64_t s = ceil_div(2 * ctx->num_sms, tiles);
+    s = std::min<int64_t>(s, k / 256);
+    s = std::min<int64_t>(s, 64);
+    if (splitk_ws) s = std::min<int64_t>(s, (int64_t)(splitk_ws_elems / (size_t)(m * n)));
+    else s = 1;
+    if (s > 1) splits = (int)s;
+  }
+  int64_t kps = ceil_div(ceil_div(k, splits), BK) * BK;
+  splits = (int)ceil_div(k, kps);
+  if (tiles_m > 65535 * 1024LL || tiles_n > 65535) {
+    set_error("gemm: grid too large (%lld x %lld tiles)", (long long)tiles_m, (long long)tiles_n);
+    return FTT_ERR_INVALID;
+  }
+  dim3 grid((unsigned)tiles_m, (unsigned)tiles_n, (unsigned)splits);
+  double *part = splits > 1 ? splitk_ws : nullptr;
+#define FTT_GEMM_LAUNCH(TA_, TB_)                                                          \
+  k_dgemm<TA_, TB_><<<grid, GT, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, \
+                                                  ldc, kps, part)
+  if (!ta && !tb) FTT_GEMM_LAUNCH(false, false);
+  else if (!ta && tb) FTT_GEMM_LAUNCH(false, true);
+  else if (ta && !tb) FTT_GEMM_LAUNCH(true, false);
+  else FTT_GEMM_LAUNCH(true, true);
+#undef FTT_GEMM_LAUNCH
+  FTT_LAUNCHED(ctx);
+  if (splits > 1) {
+    k_splitk_reduce<<<grid_for(m * n, 256, 2), 256, 0, ctx->stream>>>(m, n, splits, part, alpha,
+                                                                     beta, C, ldc);
+    FTT_LAUNCHED(ctx);
+  }
+  return FTT_OK;
+}
+
+size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k) {
+  int64_t tiles = ceil_div(m, BM) * ceil_div(n, BN);
+  if (tiles >= 2 * kNumSMs || k < 4 * 256) return 0;
+  int64_t s = std::min<int64_t>(std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), k / 256), 64);
+  return s > 1 ? (size_t)(s * m * n) : 0;
+}
+
+int transpose(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst,
+              int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return FTT_OK;
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(cols, 32));
+  k_transpose<<<grid, dim3(32, 8), 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd);
+  FTT_LAUNCHED(ctx);
+  return FTT_OK;
+}
+
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" {
+
+int ftt_dgemm(ftt_ctx *ctx, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
+              double alpha, const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+              double *C, int64_t ldc) {
+  if (!ctx || m < 0 || n < 0 || k < 0) {
+    set_error("ftt_dgemm: invalid sizes");
+    return FTT_ERR_INVALID;
+  }
+  size_t ws = gemm_splitk_elems(m, n, k);
+  double *part = nullptr;
+  if (ws) {
+    FTT_CHECK(arena_reserve(ctx, align_up(ws * sizeof(double))));
+    part = take<double>(ctx, ws);
+  }
+  return gemm(ctx, transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, part, ws);
+}
+
+int ftt_orth_defect(ftt_ctx *ctx, int64_t n, const double *G, int64_t ldg, double *out_host) {
+  if (!ctx || !out_host || n < 0) return FTT_ERR_INVALID;
+  *out_host = 0.0;
+  if (n == 0) return FTT_OK;
+  int nb = grid_for(n * n, 256, 4, 1024);
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * nb) + 256));
+  double *part = take<double>(ctx, nb);
+  k_orth_defect<<<nb, 256, 0, ctx->stream>>>(n, G, ldg, part);
+  FTT_LAUNCHED(ctx);
+  std::vector<double> h(nb);
+  FTT_CHECK(copy_to_host(ctx, h.data(), part, 8 * nb));
+  double mx = 0.0;
+  for (double v : h) mx = v > mx ? v : mx;
+  *out_host = mx;
+  return FTT_OK;
+}
+
+int ftt_transpose(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *src, int64_t lds,
+                  double *dst, int64_t ldd) {
+  if (!ctx) return FTT_ERR_INVALID;
+  return transpose(ctx, rows, cols, src, lds, dst, ldd);
+}
+
+}  // extern "C"

@@ -1,0 +1,1039 @@
+// Index path of FastTT on B200: radix sort of linearised COO keys, fiber
+// segmentation, per-pivot fiber counts, deparallelisation sweeps and the
+// pivot-core scatter.  All integer work is bit-exact with the reference
+// (tensor.py:374-403, fasttt.py:148-211, 256-259, 537-541).
+//
+// Design:
+//  * keys: one 64-bit mixed-radix key per nonzero, lin(fixed)*n_p + i_p
+//    (< prod(dims) < 2^63, check_shape tensor.py:62-66).  Sorting it is the
+//    reference's lexsort (pivot coordinate fastest, tensor.py:387-389).
+//  * sort: LSD "onesweep" radix sort -- one fused key-build + all-pass
+//    histogram kernel, then one kernel per 8-bit digit that ranks a 4096-key
+//    tile with warp match.any, finds its global offset by decoupled
+//    look-back over per-tile digit counts, stages the tile in shared memory
+//    in digit order and writes runs coalesced.  Passes whose digit is
+//    constant over all keys are skipped (decided from the histogram).
+//  * segment / compaction: warp-striped ballot scans, 4096 items per block,
+//    3 phases (count, scan block counts, emit) -- ascending order preserved.
+#include <cooperative_groups.h>
+
+#include "ftt_common.cuh"
+
+namespace ftt {
+namespace {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys
+constexpr int RADIX = 256;
+constexpr uint32_t FLAG_AGG = 1u << 30;
+constexpr uint32_t FLAG_INC = 2u << 30;
+constexpr uint32_t VAL_MASK = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+struct KeySpec {
+  // key = sum_k coord[k] * mult[k]  (mixed radix, C order over the modes
+  // in key order).  mult[pivot] = 1 for fiber keys, 0 for count keys where
+  // the pivot is dropped.
+  int32_t d;
+  int64_t mult[32];
+};
+
+// Fused: build one key per nonzero from coords + per-block digit
+// histograms of every pass.  Writes keys and the identity payload.
+__global__ void __launch_bounds__(256) k_keys_hist(const int64_t *__restrict__ coords, int64_t n,
+                                                   KeySpec spec, int num_passes,
+                                                   uint64_t *__restrict__ keys,
+                                                   uint32_t *__restrict__ idx,
+                                                   uint32_t *__restrict__ ghist) {
+  __shared__ uint32_t sh[8][RADIX];
+  for (int i = threadIdx.x; i < 8 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const int d = spec.d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t *c = coords + i * d;
+    uint64_t key = 0;
+    for (int k = 0; k < d; ++k) key += (uint64_t)c[k] * (uint64_t)spec.mult[k];
+    keys[i] = key;
+    if (idx) idx[i] = (uint32_t)i;
+    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < num_passes * RADIX; i += blockDim.x) {
+    uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(&ghist[i], v);
+  }
+}
+
+// Histogram of already-built keys (for sorts whose keys come from elsewhere).
+__global__ void __launch_bounds__(256) k_hist(const uint64_t *__restrict__ keys, int64_t n,
+                                              int num_passes, uint32_t *__restrict__ ghist,
+                                              uint32_t *__restrict__ idx) {
+  __shared__ uint32_t sh[8][RADIX];
+  for (int i = threadIdx.x; i < 8 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = keys[i];
+    if (idx) idx[i] = (uint32_t)i;
+    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < num_passes * RADIX; i += blockDim.x) {
+    uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(&ghist[i], v);
+  }
+}
+
+// Exclusive scan of each pass histogram (one block of 256 threads per pass).
+__global__ void k_hist_scan(uint32_t *ghist) {
+  __shared__ uint32_t s[RADIX];
+  uint32_t *h = ghist + blockIdx.x * RADIX;
+  int t = threadIdx.x;
+  s[t] = h[t];
+  __syncthreads();
+  for (int off = 1; off < RADIX; off <<= 1) {
+    uint32_t v = t >= off ? s[t - off] : 0;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  h[t] = s[t] - h[t];  // exclusive
+}
+
+template <bool HAS_VALS>
+__global__ void __launch_bounds__(RS_THREADS) k_onesweep(
+    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ digit_start,
+    uint32_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
+  __shared__ uint32_t s_warp[RS_WARPS][RADIX];
+  __shared__ uint32_t s_excl[RADIX];
+  __shared__ uint32_t s_gbase[RADIX];
+  __shared__ uint32_t s_wsum[RS_WARPS];
+  __shared__ uint32_t s_tile;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(s_dyn);           // RS_TILE keys
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(s_dyn + 8 * RS_TILE);  // RS_TILE payloads
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_warp[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * RS_TILE;
+  const int64_t wbase = base + warp * (32 * RS_ITEMS);
+
+  uint64_t k[RS_ITEMS];
+  uint32_t v[RS_ITEMS];
+  uint32_t rank[RS_ITEMS];
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    int64_t idx = wbase + i * 32 + lane;
+    if (idx < n) {
+      k[i] = kin[idx];
+      if (HAS_VALS) v[i] = vin[idx];
+    } else {
+      k[i] = 0;
+      if (HAS_VALS) v[i] = 0;
+    }
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    int64_t idx = wbase + i * 32 + lane;
+    uint32_t dg = idx < n ? (uint32_t)((k[i] >> shift) & 255) : 256u;
+    uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (dg < 256 && lane == leader) {
+      b = s_warp[warp][dg];
+      s_warp[warp][dg] = b + __popc(peers);
+    }
+    b = __shfl_sync(0xffffffffu, b, leader);
+    rank[i] = b + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive offsets over warps, tile total
+  const int dgt = tid;  // RS_THREADS == RADIX
+  uint32_t run = 0;
+#pragma unroll
+  for (int w = 0; w < RS_WARPS; ++w) {
+    uint32_t c = s_warp[w][dgt];
+    s_warp[w][dgt] = run;
+    run += c;
+  }
+  const uint32_t total = run;
+  // decoupled look-back for this digit
+  uint32_t *st = status + tile * RADIX + dgt;
+  uint32_t excl = 0;
+  if (tile == 0) {
+    st_relaxed(st, FLAG_INC | total);
+  } else {
+    st_relaxed(st, FLAG_AGG | total);
+    int64_t j = tile - 1;
+    while (true) {
+      uint32_t s;
+      do {
+        s = ld_relaxed(status + j * RADIX + dgt);
+      } while ((s & ~VAL_MASK) == 0);
+      excl += s & VAL_MASK;
+      if ((s & ~VAL_MASK) == FLAG_INC) break;
+      --j;
+    }
+    st_relaxed(st, FLAG_INC | (excl + total));
+  }
+  s_gbase[dgt] = digit_start[dgt] + excl;
+  // block exclusive scan of tile totals over digits -> local staging offsets
+  uint32_t x = total;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+  s_excl[dgt] = wpre + x - total;
+  __syncthreads();
+  // stage in digit order
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    int64_t idx = wbase + i * 32 + lane;
+    if (idx < n) {
+      uint32_t dg = (uint32_t)((k[i] >> shift) & 255);
+      uint32_t pos = s_excl[dg] + s_warp[warp][dg] + rank[i];
+      s_keys[pos] = k[i];
+      if (HAS_VALS) s_vals[pos] = v[i];
+    }
+  }
+  __syncthreads();
+  const int tile_n = (int)min((int64_t)RS_TILE, n - base);
+  for (int j = tid; j < tile_n; j += RS_THREADS) {
+    uint64_t key = s_keys[j];
+    uint32_t dg = (uint32_t)((key >> shift) & 255);
+    uint32_t out = s_gbase[dg] + (j - s_excl[dg]);
+    kout[out] = key;
+    if (HAS_VALS) vout[out] = s_vals[j];
+  }
+}
+
+// ---------------------------------------------------------- compaction
+// Warp-striped blocks of COMPACT_TILE items.  Pred: bool(int64 i).
+constexpr int CP_THREADS = 256;
+constexpr int CP_ITEMS = 16;
+constexpr int CP_TILE = CP_THREADS * CP_ITEMS;
+
+template <class Pred>
+__global__ void __launch_bounds__(CP_THREADS) k_count(int64_t n, Pred pred, int64_t *block_counts) {
+  __shared__ int s_w[CP_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = (int64_t)blockIdx.x * CP_TILE + warp * (32 * CP_ITEMS);
+  int cnt = 0;
+#pragma unroll 4
+  for (int j = 0; j < CP_ITEMS; ++j) {
+    int64_t i = wbase + j * 32 + lane;
+    bool f = i < n && pred(i);
+    cnt += __popc(__ballot_sync(0xffffffffu, f));
+  }
+  if (lane == 0) s_w[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < CP_THREADS / 32; ++w) t += s_w[w];
+    block_counts[blockIdx.x] = t;
+  }
+}
+
+// emit(i, rank_excl, flag) is called for every i < n; rank_excl = number of
+// flagged items before i (global).
+template <class Pred, class Emit>
+__global__ void __launch_bounds__(CP_THREADS) k_emit(int64_t n, Pred pred, Emit emit,
+                                                     const int64_t *block_offsets) {
+  __shared__ int s_w[CP_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = (int64_t)blockIdx.x * CP_TILE + warp * (32 * CP_ITEMS);
+  // first: this warp's count (re-evaluate pred; cheap relative to a
+  // second smem round trip of flags)
+  uint32_t balls[CP_ITEMS];
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < CP_ITEMS; ++j) {
+    int64_t i = wbase + j * 32 + lane;
+    bool f = i < n && pred(i);
+    balls[j] = __ballot_sync(0xffffffffu, f);
+    cnt += __popc(balls[j]);
+  }
+  if (lane == 0) s_w[warp] = cnt;
+  __syncthreads();
+  int64_t run = block_offsets[blockIdx.x];
+  for (int w = 0; w < warp; ++w) run += s_w[w];
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < CP_ITEMS; ++j) {
+    int64_t i = wbase + j * 32 + lane;
+    bool f = (balls[j] >> lane) & 1u;
+    if (i < n) emit(i, run + __popc(balls[j] & lt), f);
+    run += __popc(balls[j]);
+  }
+}
+
+__global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total) {
+  // single block, 1024 threads, chunked exclusive scan
+  __shared__ int64_t s[1024];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += 1024) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < nb ? counts[i] : 0;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      int64_t y = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+      __syncthreads();
+      s[threadIdx.x] += y;
+      __syncthreads();
+    }
+    if (i < nb) counts[i] = carry + s[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += s[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+template <class Pred, class Emit>
+int compact(ftt_ctx *ctx, int64_t n, Pred pred, Emit emit, int64_t *block_counts,
+            int64_t *total_dev) {
+  if (n <= 0) return FTT_OK;
+  int64_t nb = ceil_div(n, CP_TILE);
+  k_count<Pred><<<(unsigned)nb, CP_THREADS, 0, ctx->stream>>>(n, pred, block_counts);
+  FTT_LAUNCHED(ctx);
+  k_scan_counts<<<1, 1024, 0, ctx->stream>>>(block_counts, nb, total_dev);
+  FTT_LAUNCHED(ctx);
+  k_emit<Pred, Emit><<<(unsigned)nb, CP_THREADS, 0, ctx->stream>>>(n, pred, emit, block_counts);
+  FTT_LAUNCHED(ctx);
+  return FTT_OK;
+}
+
+inline size_t compact_scratch_bytes(int64_t n) {
+  return align_up(sizeof(int64_t) * (ceil_div(n, CP_TILE) + 1)) + 256;
+}
+
+// ------------------------------------------------------------- functors
+struct AdjDiffPred {  // sorted keys: key/div differs from predecessor
+  const uint64_t *k;
+  uint64_t div;
+  __device__ bool operator()(int64_t i) const {
+    return i == 0 || (k[i] / div) != (k[i - 1] / div);
+  }
+};
+
+struct FiberEmit {
+  const uint64_t *k;
+  const uint32_t *perm;
+  const double *vals_in;
+  uint64_t np;
+  int64_t *fixed_lin, *indptr, *fiber_of, *pivot_index;
+  double *vals_out;
+  __device__ void operator()(int64_t i, int64_t r, bool f) const {
+    uint64_t key = k[i];
+    uint64_t fx = key / np;
+    if (f) {
+      indptr[r] = i;
+      fixed_lin[r] = (int64_t)fx;
+    }
+    if (fiber_of) fiber_of[i] = f ? r : r - 1;
+    pivot_index[i] = (int64_t)(key - fx * np);
+    vals_out[i] = vals_in[perm[i]];
+  }
+};
+
+struct FlagPred {
+  const uint32_t *present;
+  __device__ bool operator()(int64_t i) const { return present[i] != 0; }
+};
+
+struct KeptEmit {  // kept[r] = row, present[row] <- rank (overwrites the flag)
+  uint32_t *present;
+  int64_t *kept;
+  __device__ void operator()(int64_t i, int64_t r, bool f) const {
+    if (f) {
+      kept[r] = i;
+      present[i] = (uint32_t)r;
+    }
+  }
+};
+
+struct UniqEmit {  // sort path: sorted keys with fiber payload
+  const uint64_t *k;
+  const uint32_t *perm;
+  int64_t *kept, *map_out;
+  __device__ void operator()(int64_t i, int64_t r, bool f) const {
+    if (f) kept[r] = (int64_t)k[i];
+    map_out[perm[i]] = f ? r : r - 1;
+  }
+};
+
+struct SweepKey {
+  int32_t side;
+  const int64_t *fixed_lin;
+  int64_t stride, nk, r_other;
+  const int64_t *map_in;
+  __device__ int64_t operator()(int64_t f) const {
+    int64_t ik = (fixed_lin[f] / stride) % nk;
+    int64_t m = map_in ? map_in[f] : 0;
+    return side == 0 ? m * nk + ik : ik * r_other + m;
+  }
+};
+
+__global__ void k_sweep_mark(int64_t R, SweepKey key, uint32_t *present) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
+       f += (int64_t)gridDim.x * blockDim.x)
+    present[key(f)] = 1u;
+}
+
+__global__ void k_sweep_gather(int64_t R, SweepKey key, const uint32_t *present, int64_t *map_out) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
+       f += (int64_t)gridDim.x * blockDim.x)
+    map_out[f] = (int64_t)present[key(f)];
+}
+
+__global__ void k_sweep_keys(int64_t R, SweepKey key, uint64_t *keys) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
+       f += (int64_t)gridDim.x * blockDim.x)
+    keys[f] = (uint64_t)key(f);
+}
+
+__global__ void k_mark_rows(int64_t n, const int64_t *rows, uint32_t *present) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    present[rows[i]] = 1u;
+}
+
+__global__ void k_gather_rank(int64_t n, const int64_t *rows, const uint32_t *present, int64_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)present[rows[i]];
+}
+
+__global__ void k_copy_keys(int64_t n, const int64_t *in, uint64_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint64_t)in[i];
+}
+
+__global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
+
+__global__ void k_count_changes(const uint64_t *k, int64_t n, unsigned long long *out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += (i == 0 || k[i] != k[i - 1]) ? 1ull : 0ull;
+  for (int off = 16; off; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
+  __shared__ unsigned long long s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    atomicAdd(out, t);
+  }
+}
+
+__global__ void k_mode_index(const int64_t *fixed_lin, int64_t R, int64_t stride, int64_t n,
+                             int64_t *out) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
+       f += (int64_t)gridDim.x * blockDim.x)
+    out[f] = (fixed_lin[f] / stride) % n;
+}
+
+__global__ void k_pivot_scatter(int64_t nnz, const int64_t *__restrict__ fiber_of,
+                                const int64_t *__restrict__ pidx, const double *__restrict__ vals,
+                                const int64_t *__restrict__ t_map, const int64_t *__restrict__ s_map,
+                                int64_t np, int64_t r_next, double *__restrict__ core,
+                                double *__restrict__ partial) {
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t f = fiber_of[e];
+    int64_t row = t_map ? t_map[f] : 0;
+    int64_t col = s_map ? s_map[f] : 0;
+    double v = vals[e];
+    core[(row * np + pidx[e]) * r_next + col] = v;
+    acc += v * v;
+  }
+  if (partial) {
+    for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    __shared__ double s[32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+      partial[blockIdx.x] = t;
+    }
+  }
+}
+
+// deterministic final reduction of block partials
+__global__ void k_reduce_partials(const double *partial, int nb, double *out) {
+  __shared__ double s[1024];
+  double a = 0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) a += partial[i];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off; off >>= 1) {
+    if ((int)threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+__global__ void k_dot_partial(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
+                              double *partial) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += x[i] * (y ? y[i] : x[i]);
+  for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+  __shared__ double s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_side_core(int32_t side, const int64_t *kept, int64_t K, int64_t n, int64_t ro,
+                            double *core) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < K;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t kj = kept[j];
+    if (side == 0) {
+      // (ro, n, K): [kj / n, kj % n, j] -> ((kj/n)*n + kj%n)*K + j = kj*K + j
+      core[kj * K + j] = 1.0;
+    } else {
+      // (K, n, ro): [j, kj / ro, kj % ro] -> j*(n*ro) + kj
+      core[j * (n * ro) + kj] = 1.0;
+    }
+  }
+}
+
+__global__ void k_scatter_cols(int64_t rank, int64_t K, const int64_t *__restrict__ kept,
+                               const double *__restrict__ src, int64_t lds, int64_t ncols,
+                               double *__restrict__ dst) {
+  int64_t total = rank * K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = t / K, j = t - a * K;
+    dst[a * ncols + kept[j]] = src[a * lds + j];
+  }
+}
+
+__global__ void k_scatter_rows(int64_t K, int64_t rank, const int64_t *__restrict__ kept,
+                               const double *__restrict__ src, int64_t lds,
+                               double *__restrict__ dst) {
+  int64_t total = rank * K;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / rank, c = t - j * rank;
+    dst[kept[j] * rank + c] = src[j * lds + c];
+  }
+}
+
+int bit_length(uint64_t x) {
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+// Shared driver for the per-pass onesweep kernels once keys + histograms
+// exist.  keys[0]/vals[0] hold the input; the result pointer is returned in
+// *kres / *vres (one of the two ping-pong buffers).
+int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t n, int num_passes,
+                    uint32_t *ghist, uint32_t *status, uint32_t *counters, uint64_t **kres,
+                    uint32_t **vres) {
+  // decide which passes are needed (constant digit -> skip)
+  static thread_local std::vector<uint32_t> h;
+  h.assign((size_t)num_passes * RADIX, 0);
+  FTT_CHECK(copy_to_host(ctx, h.data(), ghist, sizeof(uint32_t) * num_passes * RADIX));
+  k_hist_scan<<<num_passes, RADIX, 0, ctx->stream>>>(ghist);
+  FTT_LAUNCHED(ctx);
+  int64_t ntiles = ceil_div(n, RS_TILE);
+  int cur = 0;
+  for (int p = 0; p < num_passes; ++p) {
+    bool trivial = false;
+    for (int b = 0; b < RADIX; ++b)
+      if ((int64_t)h[(size_t)p * RADIX + b] == n) trivial = true;
+    if (trivial) continue;
+    FTT_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * ntiles * RADIX, ctx->stream));
+    FTT_CUDA(cudaMemsetAsync(counters + p, 0, sizeof(uint32_t), ctx->stream));
+    static bool attr_set = false;
+    if (!attr_set) {
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    12 * RS_TILE));
+      attr_set = true;
+    }
+    if (vals[0]) {
+      k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
+          keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, ghist + p * RADIX, status,
+          counters + p);
+    } else {
+      k_onesweep<false><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
+          keys[cur], nullptr, keys[cur ^ 1], nullptr, n, 8 * p, ghist + p * RADIX, status,
+          counters + p);
+    }
+    FTT_LAUNCHED(ctx);
+    cur ^= 1;
+  }
+  *kres = keys[cur];
+  *vres = vals[cur];
+  return FTT_OK;
+}
+
+size_t onesweep_scratch(int64_t n) {
+  int64_t ntiles = ceil_div(n, RS_TILE);
+  return align_up(sizeof(uint32_t) * 8 * RADIX) + align_up(sizeof(uint32_t) * ntiles * RADIX) +
+         align_up(sizeof(uint32_t) * 8);
+}
+
+int check_dims(int32_t d, const int64_t *dims, int32_t pivot, bool need_pivot) {
+  if (d < 1 || d > 32) {
+    set_error("number of modes %d out of range 1..32", d);
+    return FTT_ERR_INVALID;
+  }
+  if (need_pivot && (pivot < 0 || pivot >= d)) {
+    set_error("pivot %d out of range for %d modes", pivot, d);
+    return FTT_ERR_INVALID;
+  }
+  __int128 size = 1;
+  for (int k = 0; k < d; ++k) {
+    if (dims[k] < 1) {
+      set_error("shape extents must be positive");
+      return FTT_ERR_INVALID;
+    }
+    size *= dims[k];
+    if (size >= ((__int128)1 << 63)) {
+      set_error("shape overflows 64-bit indexing");
+      return FTT_ERR_INVALID;
+    }
+  }
+  return FTT_OK;
+}
+
+// Key multipliers: mixed radix over the non-pivot modes in order, then the
+// pivot as the fastest digit (include_pivot) or dropped.
+void make_spec(int32_t d, const int64_t *dims, int32_t pivot, bool include_pivot, KeySpec *spec,
+               uint64_t *key_bound) {
+  spec->d = d;
+  uint64_t m = include_pivot ? (uint64_t)dims[pivot] : 1;
+  for (int k = d - 1; k >= 0; --k) {
+    if (k == pivot) continue;
+    spec->mult[k] = (int64_t)m;
+    m *= (uint64_t)dims[k];
+  }
+  spec->mult[pivot] = include_pivot ? 1 : 0;
+  *key_bound = m;  // keys < m
+}
+
+}  // namespace
+
+size_t radix_sort_scratch_bytes(int64_t n, bool with_vals) {
+  return onesweep_scratch(n) + 2 * align_up(sizeof(uint64_t) * n) +
+         (with_vals ? 2 * align_up(sizeof(uint32_t) * n) : 0);
+}
+
+// Sort keys_in (+vals_in) over bits [0, end_bit); outputs into keys_out /
+// vals_out (distinct from the inputs).  Arena must hold
+// radix_sort_scratch_bytes(n).
+int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
+               uint32_t *vals_out, int64_t n, int end_bit) {
+  if (n <= 0) return FTT_OK;
+  int num_passes = (end_bit + 7) / 8;
+  if (num_passes < 1) num_passes = 1;
+  uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, ceil_div(n, RS_TILE) * RADIX);
+  uint32_t *counters = take<uint32_t>(ctx, 8);
+  uint64_t *kb[2] = {take<uint64_t>(ctx, n), take<uint64_t>(ctx, n)};
+  uint32_t *vb[2] = {nullptr, nullptr};
+  if (vals_in) {
+    vb[0] = take<uint32_t>(ctx, n);
+    vb[1] = take<uint32_t>(ctx, n);
+  }
+  if (!ghist || !status || !counters || !kb[0] || !kb[1] || (vals_in && (!vb[0] || !vb[1]))) {
+    set_error("radix_sort: arena reservation too small");
+    return FTT_ERR_INVALID;
+  }
+  FTT_CUDA(cudaMemcpyAsync(kb[0], keys_in, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (vals_in)
+    FTT_CUDA(cudaMemcpyAsync(vb[0], vals_in, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  FTT_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
+  k_hist<<<grid_for(n, 256, 8), 256, 0, ctx->stream>>>(kb[0], n, num_passes, ghist, nullptr);
+  FTT_LAUNCHED(ctx);
+  uint64_t *kr;
+  uint32_t *vr;
+  FTT_CHECK(onesweep_passes(ctx, kb, vb, n, num_passes, ghist, status, counters, &kr, &vr));
+  FTT_CUDA(cudaMemcpyAsync(keys_out, kr, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (vals_out && vr)
+    FTT_CUDA(cudaMemcpyAsync(vals_out, vr, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  return FTT_OK;
+}
+
+int sum_squares(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_host) {
+  *out_host = 0.0;
+  if (n <= 0) return FTT_OK;
+  int nb = grid_for(n, 256, 4, kSumSqBlocks);
+  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, nullptr, partial);
+  FTT_LAUNCHED(ctx);
+  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, partial + nb);
+  FTT_LAUNCHED(ctx);
+  return copy_to_host(ctx, out_host, partial + nb, sizeof(double));
+}
+
+int scan_block_counts(ftt_ctx *ctx, int64_t *counts, int64_t nblocks, int64_t *total_dev) {
+  k_scan_counts<<<1, 1024, 0, ctx->stream>>>(counts, nblocks, total_dev);
+  FTT_LAUNCHED(ctx);
+  return FTT_OK;
+}
+
+// Internal: build keys from coords for one pivot and sort them.  With
+// include_pivot the key is the fiber key and a permutation payload rides
+// along; without, only the fixed-tuple keys are sorted (fiber count).
+static int sort_coords(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                       const int64_t *dims, int32_t pivot, bool include_pivot, uint64_t **kres,
+                       uint32_t **vres, uint64_t *key_bound) {
+  KeySpec spec;
+  make_spec(d, dims, pivot, include_pivot, &spec, key_bound);
+  int end_bit = bit_length(*key_bound > 0 ? *key_bound - 1 : 0);
+  int num_passes = (end_bit + 7) / 8;
+  if (num_passes < 1) num_passes = 1;
+  uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, ceil_div(nnz, RS_TILE) * RADIX);
+  uint32_t *counters = take<uint32_t>(ctx, 8);
+  uint64_t *kb[2] = {take<uint64_t>(ctx, nnz), take<uint64_t>(ctx, nnz)};
+  uint32_t *vb[2] = {nullptr, nullptr};
+  if (include_pivot) {
+    vb[0] = take<uint32_t>(ctx, nnz);
+    vb[1] = take<uint32_t>(ctx, nnz);
+  }
+  if (!ghist || !status || !counters || !kb[1] || (include_pivot && !vb[1])) {
+    set_error("sort_coords: arena reservation too small");
+    return FTT_ERR_INVALID;
+  }
+  FTT_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
+  k_keys_hist<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(coords, nnz, spec, num_passes, kb[0],
+                                                              vb[0], ghist);
+  FTT_LAUNCHED(ctx);
+  return onesweep_passes(ctx, kb, vb, nnz, num_passes, ghist, status, counters, kres, vres);
+}
+
+static size_t sort_coords_bytes(int64_t nnz, bool with_perm) {
+  return onesweep_scratch(nnz) + 2 * align_up(8 * nnz) + (with_perm ? 2 * align_up(4 * nnz) : 0);
+}
+
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" {
+
+int ftt_fiber_count(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                    const int64_t *dims_host, int32_t pivot, int64_t *count_out) {
+  if (!ctx || !count_out) return FTT_ERR_INVALID;
+  FTT_CHECK(check_dims(d, dims_host, pivot, true));
+  if (nnz >= ((int64_t)1 << 30)) {
+    set_error("nnz %lld exceeds the 2^30 sort limit", (long long)nnz);
+    return FTT_ERR_INVALID;
+  }
+  if (nnz == 0) {
+    *count_out = 0;
+    return FTT_OK;
+  }
+  FTT_CHECK(arena_reserve(ctx, sort_coords_bytes(nnz, false) + 1024));
+  uint64_t *kr;
+  uint32_t *vr;
+  uint64_t bound;
+  FTT_CHECK(sort_coords(ctx, coords, nnz, d, dims_host, pivot, false, &kr, &vr, &bound));
+  unsigned long long *cnt = take<unsigned long long>(ctx, 1);
+  FTT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+  k_count_changes<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(kr, nnz, cnt);
+  FTT_LAUNCHED(ctx);
+  unsigned long long h = 0;
+  FTT_CHECK(copy_to_host(ctx, &h, cnt, sizeof(h)));
+  *count_out = (int64_t)h;
+  return FTT_OK;
+}
+
+int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                         const int64_t *dims_host, int64_t *counts_host) {
+  if (!ctx || !counts_host) return FTT_ERR_INVALID;
+  FTT_CHECK(check_dims(d, dims_host, 0, false));
+  if (nnz >= ((int64_t)1 << 30)) {
+    set_error("nnz exceeds the 2^30 sort limit");
+    return FTT_ERR_INVALID;
+  }
+  if (nnz == 0) {
+    for (int p = 0; p < d; ++p) counts_host[p] = 0;
+    return FTT_OK;
+  }
+  FTT_CHECK(arena_reserve(ctx, sort_coords_bytes(nnz, false) + 4096));
+  unsigned long long *cnt = take<unsigned long long>(ctx, 32);
+  FTT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 32, ctx->stream));
+  size_t mark = ctx->arena.used;
+  for (int p = 0; p < d; ++p) {
+    ctx->arena.used = mark;
+    uint64_t *kr;
+    uint32_t *vr;
+    uint64_t bound;
+    FTT_CHECK(sort_coords(ctx, coords, nnz, d, dims_host, p, false, &kr, &vr, &bound));
+    k_count_changes<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(kr, nnz, cnt + p);
+    FTT_LAUNCHED(ctx);
+  }
+  unsigned long long h[32];
+  FTT_CHECK(copy_to_host(ctx, h, cnt, sizeof(unsigned long long) * d));
+  for (int p = 0; p < d; ++p) counts_host[p] = (int64_t)h[p];
+  return FTT_OK;
+}
+
+int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords, const double *values, int64_t nnz,
+                       int32_t d, const int64_t *dims_host, int32_t pivot, int64_t *fixed_lin,
+                       int64_t *indptr, int64_t *fiber_of, int64_t *pivot_index, double *values_out,
+                       int64_t *num_fibers_out) {
+  if (!ctx || !num_fibers_out) return FTT_ERR_INVALID;
+  FTT_CHECK(check_dims(d, dims_host, pivot, true));
+  if (nnz >= ((int64_t)1 << 30)) {
+    set_error("nnz exceeds the 2^30 sort limit");
+    return FTT_ERR_INVALID;
+  }
+  if (nnz == 0) {
+    *num_fibers_out = 0;
+    k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr, 0);
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
+  FTT_CHECK(arena_reserve(ctx, sort_coords_bytes(nnz, true) + compact_scratch_bytes(nnz) + 1024));
+  uint64_t *kr;
+  uint32_t *vr;
+  uint64_t bound;
+  FTT_CHECK(sort_coords(ctx, coords, nnz, d, dims_host, pivot, true, &kr, &vr, &bound));
+  int64_t *bc = take<int64_t>(ctx, ceil_div(nnz, CP_TILE) + 1);
+  int64_t *total = take<int64_t>(ctx, 1);
+  AdjDiffPred pred{kr, (uint64_t)dims_host[pivot]};
+  FiberEmit emit{kr, vr, values, (uint64_t)dims_host[pivot], fixed_lin, indptr, fiber_of,
+                 pivot_index, values_out};
+  FTT_CHECK(compact(ctx, nnz, pred, emit, bc, total));
+  int64_t R = 0;
+  FTT_CHECK(copy_to_host(ctx, &R, total, sizeof(R)));
+  k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr + R, nnz);
+  FTT_LAUNCHED(ctx);
+  *num_fibers_out = R;
+  return FTT_OK;
+}
+
+static int depar_from_keys(ftt_ctx *ctx, int64_t n_rows, int64_t R, const SweepKey *skey,
+                           const int64_t *rows, int64_t *kept, int64_t *map_out,
+                           int64_t *n_kept_out) {
+  // rows (explicit col_to_row) or skey (computed) gives key(f) for f < R
+  const bool flag_path = n_rows <= ((int64_t)1 << 31) - 1 &&
+                         (n_rows <= ((int64_t)1 << 24) || n_rows <= 8 * R);
+  if (flag_path) {
+    FTT_CHECK(arena_reserve(ctx, align_up(4 * n_rows) + compact_scratch_bytes(n_rows) + 1024));
+    uint32_t *present = take<uint32_t>(ctx, n_rows);
+    int64_t *bc = take<int64_t>(ctx, ceil_div(n_rows, CP_TILE) + 1);
+    int64_t *total = take<int64_t>(ctx, 1);
+    FTT_CUDA(cudaMemsetAsync(present, 0, 4 * n_rows, ctx->stream));
+    if (skey) {
+      k_sweep_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, *skey, present);
+    } else {
+      k_mark_rows<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, rows, present);
+    }
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(compact(ctx, n_rows, FlagPred{present}, KeptEmit{present, kept}, bc, total));
+    if (skey) {
+      k_sweep_gather<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, *skey, present, map_out);
+    } else {
+      k_gather_rank<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, rows, present, map_out);
+    }
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(copy_to_host(ctx, n_kept_out, total, sizeof(int64_t)));
+    return FTT_OK;
+  }
+  // sort path: unique over R keys
+  if (R >= ((int64_t)1 << 30)) {
+    set_error("fiber count exceeds the 2^30 sort limit");
+    return FTT_ERR_INVALID;
+  }
+  FTT_CHECK(arena_reserve(ctx, radix_sort_scratch_bytes(R, true) + 2 * align_up(8 * R) +
+                                   2 * align_up(4 * R) + compact_scratch_bytes(R) + 1024));
+  uint64_t *keys = take<uint64_t>(ctx, R);
+  uint64_t *skeys = take<uint64_t>(ctx, R);
+  uint32_t *perm = take<uint32_t>(ctx, R);
+  int64_t *bc = take<int64_t>(ctx, ceil_div(R, CP_TILE) + 1);
+  int64_t *total = take<int64_t>(ctx, 1);
+  if (skey) {
+    k_sweep_keys<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, *skey, keys);
+  } else {
+    k_copy_keys<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, rows, keys);
+  }
+  FTT_LAUNCHED(ctx);
+  // identity payload is produced by the histogram kernel inside radix_sort
+  // only for coords; build it here explicitly.
+  uint32_t *ident = take<uint32_t>(ctx, R);
+  if (!ident) {
+    set_error("depar: arena too small");
+    return FTT_ERR_INVALID;
+  }
+  {
+    // reuse k_hist's idx output to fill the identity permutation
+    uint32_t *dummy_hist = take<uint32_t>(ctx, 8 * RADIX);
+    FTT_CUDA(cudaMemsetAsync(dummy_hist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
+    k_hist<<<grid_for(R, 256, 8), 256, 0, ctx->stream>>>(keys, R, 0, dummy_hist, ident);
+    FTT_LAUNCHED(ctx);
+  }
+  FTT_CHECK(radix_sort(ctx, keys, ident, skeys, perm, R, bit_length((uint64_t)(n_rows - 1))));
+  FTT_CHECK(compact(ctx, R, AdjDiffPred{skeys, 1}, UniqEmit{skeys, perm, kept, map_out}, bc, total));
+  FTT_CHECK(copy_to_host(ctx, n_kept_out, total, sizeof(int64_t)));
+  return FTT_OK;
+}
+
+int ftt_depar_quasi_perm(ftt_ctx *ctx, int64_t n_rows, int64_t n_cols, const int64_t *col_to_row,
+                         int64_t *kept, int64_t *t_map, int64_t *n_kept_out) {
+  if (!ctx || !n_kept_out || n_rows < 0 || n_cols < 0) return FTT_ERR_INVALID;
+  if (n_cols == 0 || n_rows == 0) {
+    *n_kept_out = 0;
+    return FTT_OK;
+  }
+  return depar_from_keys(ctx, n_rows, n_cols, nullptr, col_to_row, kept, t_map, n_kept_out);
+}
+
+int ftt_index_sweep_step(ftt_ctx *ctx, int32_t side, const int64_t *fixed_lin, int64_t R,
+                         int64_t stride_k, int64_t n_k, const int64_t *map_in, int64_t r_other,
+                         int64_t *kept, int64_t *map_out, int64_t *n_kept_out) {
+  if (!ctx || !n_kept_out || (side != 0 && side != 1) || stride_k < 1 || n_k < 1 || r_other < 1) {
+    set_error("ftt_index_sweep_step: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  if (R == 0) {
+    *n_kept_out = 0;
+    return FTT_OK;
+  }
+  SweepKey sk{side, fixed_lin, stride_k, n_k, r_other, map_in};
+  return depar_from_keys(ctx, r_other * n_k, R, &sk, nullptr, kept, map_out, n_kept_out);
+}
+
+int ftt_mode_index(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R, int64_t stride, int64_t n,
+                   int64_t *out) {
+  if (!ctx || stride < 1 || n < 1) return FTT_ERR_INVALID;
+  if (R == 0) return FTT_OK;
+  k_mode_index<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(fixed_lin, R, stride, n, out);
+  FTT_LAUNCHED(ctx);
+  return FTT_OK;
+}
+
+int ftt_pivot_core_scatter(ftt_ctx *ctx, int64_t nnz, const int64_t *fiber_of,
+                           const int64_t *pivot_index, const double *values, const int64_t *t_map,
+                           const int64_t *s_map, int64_t r_prev, int64_t n_p, int64_t r_next,
+                           double *core, double *norm_out) {
+  if (!ctx) return FTT_ERR_INVALID;
+  size_t elems = (size_t)r_prev * n_p * r_next;
+  FTT_CUDA(cudaMemsetAsync(core, 0, elems * sizeof(double), ctx->stream));
+  int nb = grid_for(nnz, 256, 4, 148 * 8);
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * (nb + 1)) + 256));
+  double *partial = take<double>(ctx, nb + 1);
+  if (nnz > 0) {
+    k_pivot_scatter<<<nb, 256, 0, ctx->stream>>>(nnz, fiber_of, pivot_index, values, t_map, s_map,
+                                                 n_p, r_next, core, partial);
+    FTT_LAUNCHED(ctx);
+  }
+  if (norm_out) {
+    if (nnz == 0) {
+      *norm_out = 0.0;
+      return FTT_OK;
+    }
+    k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, partial + nb);
+    FTT_LAUNCHED(ctx);
+    double s2 = 0;
+    FTT_CHECK(copy_to_host(ctx, &s2, partial + nb, sizeof(double)));
+    *norm_out = sqrt(s2);
+  }
+  return FTT_OK;
+}
+
+int ftt_side_core_dense(ftt_ctx *ctx, int32_t side, const int64_t *kept, int64_t K, int64_t n,
+                        int64_t r_other, double *core) {
+  if (!ctx || (side != 0 && side != 1)) return FTT_ERR_INVALID;
+  FTT_CUDA(cudaMemsetAsync(core, 0, sizeof(double) * (size_t)K * n * r_other, ctx->stream));
+  if (K > 0) {
+    k_side_core<<<grid_for(K, 256, 4), 256, 0, ctx->stream>>>(side, kept, K, n, r_other, core);
+    FTT_LAUNCHED(ctx);
+  }
+  return FTT_OK;
+}
+
+int ftt_scatter_cols(ftt_ctx *ctx, int64_t rank, int64_t K, const int64_t *kept, const double *src,
+                     int64_t lds, int64_t ncols_new, double *dst) {
+  if (!ctx) return FTT_ERR_INVALID;
+  FTT_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * (size_t)rank * ncols_new, ctx->stream));
+  if (rank * K > 0) {
+    k_scatter_cols<<<grid_for(rank * K, 256, 4), 256, 0, ctx->stream>>>(rank, K, kept, src, lds,
+                                                                       ncols_new, dst);
+    FTT_LAUNCHED(ctx);
+  }
+  return FTT_OK;
+}
+
+int ftt_scatter_rows(ftt_ctx *ctx, int64_t K, int64_t rank, const int64_t *kept, const double *src,
+                     int64_t lds, int64_t nrows_new, double *dst) {
+  if (!ctx) return FTT_ERR_INVALID;
+  FTT_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * (size_t)nrows_new * rank, ctx->stream));
+  if (rank * K > 0) {
+    k_scatter_rows<<<grid_for(rank * K, 256, 4), 256, 0, ctx->stream>>>(K, rank, kept, src, lds,
+                                                                       dst);
+    FTT_LAUNCHED(ctx);
+  }
+  return FTT_OK;
+}
+
+int ftt_dot(ftt_ctx *ctx, int64_t n, const double *x, const double *y, double *out_host) {
+  if (!ctx || !out_host) return FTT_ERR_INVALID;
+  if (n == 0) {
+    *out_host = 0.0;
+    return FTT_OK;
+  }
+  int nb = grid_for(n, 256, 4, 148 * 8);
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * (nb + 1)) + 256));
+  double *partial = take<double>(ctx, nb + 1);
+  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, y, partial);
+  FTT_LAUNCHED(ctx);
+  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, partial + nb);
+  FTT_LAUNCHED(ctx);
+  return copy_to_host(ctx, out_host, partial + nb, sizeof(double));
+}
+
+}  // extern "C"

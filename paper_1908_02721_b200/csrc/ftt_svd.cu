@@ -1,0 +1,478 @@
+// Thin fp64 SVD for the truncation steps of the rounding sweeps
+// (svd_truncate_delta / svd_truncate_rank, linalg.py:75-125, whose
+// _full_svd is LAPACK gesdd, linalg.py:48-53).
+//
+// Backward-stable, no Gram-matrix shortcut:
+//   A (m_A x n_A, m_A >= n_A; the transpose is taken for wide inputs)
+//     = Q R                      blocked Householder QR (ftt_qr.cu)
+//   X = R^T,  X P = Y            one-sided block Jacobi: columns of X are
+//                                orthogonalised by right rotations P
+//   sigma_j = ||Y_j||,  A = (Q P) diag(sigma) (Y diag(1/sigma))^T
+// Block Jacobi: columns in blocks of 16; a round-robin tournament pairs the
+// blocks so every step processes nblk/2 disjoint 32-column pairs, one CTA
+// each.  A CTA forms the 32x32 Gram of its pair from the CURRENT columns
+// (fresh dot products, so each entry is accurate relative to its own column
+// norms), diagonalises it with cyclic two-sided Jacobi in shared memory
+// (Rutishauser rotation, relative threshold tol*sqrt(g_pp g_qq)), and applies
+// the accumulated 32x32 rotation to the pair's columns of X and P.  A sweep
+// with no rotation anywhere ends the iteration.
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "ftt_dense.cuh"
+
+namespace ftt {
+
+int launch_identity(ftt_ctx *ctx, int64_t m, int64_t k, double *Z, int64_t ldz);
+
+struct SvdState {
+  int64_t m = 0, n = 0;    // caller's shape
+  int64_t mA = 0, nA = 0;  // tall orientation
+  bool transposed = false;
+  double *Af = nullptr;    // factored A (mA x nA)
+  double *tau = nullptr;
+  double *Tb = nullptr;
+  double *Y = nullptr;     // nA x nA (X after Jacobi)
+  double *P = nullptr;     // nA x nA accumulated rotations
+  std::vector<double> sigma;  // sorted descending
+  std::vector<int64_t> perm;  // sorted position -> column of Y
+  int sweeps = 0;
+};
+
+void svd_state_free(ftt_ctx *ctx) {
+  if (!ctx->svd) return;
+  SvdState *s = ctx->svd;
+  owned_free(ctx, s->Af);
+  owned_free(ctx, s->tau);
+  owned_free(ctx, s->Tb);
+  owned_free(ctx, s->Y);
+  owned_free(ctx, s->P);
+  delete s;
+  ctx->svd = nullptr;
+}
+
+namespace {
+
+constexpr int JB = 16;
+constexpr int JP = 2 * JB;  // 32 columns per pair
+constexpr int JT = 256;
+constexpr int CH = 64;      // rows per staged chunk
+constexpr int MAX_INNER = 2;  // inner sweeps on the Gram before a fresh recompute
+
+__device__ __forceinline__ void pair_of(int nblk, int step, int c, int *a, int *b) {
+  // circle method, team nblk-1 fixed
+  const int L = nblk - 1;
+  if (c == 0) {
+    *a = step;
+    *b = L;
+  } else {
+    *a = (step + c) % L;
+    *b = (step - c + L) % L;
+  }
+}
+
+// One Jacobi step: CTA c handles block pair pair_of(nblk, step, c).
+// Convergence is decided on the FRESH Gram only (entries from the current
+// columns): pair (i, j) needs work iff both columns are above the noise
+// floor (|x|^2 > floor) and |g_ij| > tol sqrt(g_ii g_jj).  The inner
+// two-sided sweeps (at most MAX_INNER) use Rutishauser's diagonal update
+// g_pp -= t g_pq, g_qq += t g_pq; entries derived there are only used to
+// pick the next rotations, never to declare convergence, so rounding in
+// them (after cancellation between near-parallel columns) cannot stall the
+// iteration -- the next step recomputes them from the rotated columns.
+__global__ void __launch_bounds__(JT) k_jacobi_step(int64_t n, double *__restrict__ X,
+                                                    double *__restrict__ P, int64_t ld, int nblk,
+                                                    int step, double tol, double floor,
+                                                    unsigned long long *__restrict__ rotated) {
+  __shared__ double G[JP][JP + 1];
+  __shared__ double Z[JP][JP + 1];
+  __shared__ double S[CH][JP + 1];
+  __shared__ double rc[16], rs[16], rt[16], rpp[16], rqq[16], rpq[16];
+  __shared__ int col[JP];
+  __shared__ int s_round_any;
+  const int tid = threadIdx.x;
+  int ba, bb;
+  pair_of(nblk, step, blockIdx.x, &ba, &bb);
+  if (tid < JP) {
+    int blk = tid < JB ? ba : bb;
+    int cidx = blk * JB + (tid % JB);
+    col[tid] = cidx < n ? cidx : -1;
+  }
+  __syncthreads();
+  // ---- Gram of the pair's current columns
+  const int gi = tid >> 3;          // 0..31 row of G
+  const int gj = (tid & 7) * 4;     // 4 consecutive columns
+  double acc[4] = {0, 0, 0, 0};
+  for (int64_t r0 = 0; r0 < n; r0 += CH) {
+    for (int e = tid; e < CH * JP; e += JT) {
+      int c = e / CH, r = e % CH;
+      int64_t row = r0 + r;
+      int cc = col[c];
+      S[r][c] = (cc >= 0 && row < n) ? X[row + (int64_t)cc * ld] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < CH; ++r) {
+      double a = S[r][gi];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += a * S[r][gj + q];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) G[gi][gj + q] = acc[q];
+  for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = (e / JP == e % JP) ? 1.0 : 0.0;
+  __syncthreads();
+  // ---- fresh convergence test
+  int need = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int j = gj + q;
+    if (j > gi) {
+      double dii = G[gi][gi], djj = G[j][j], gij = G[gi][j];
+      if (dii > floor && djj > floor && fabs(gij) > tol * sqrt(dii * djj)) need = 1;
+    }
+  }
+  if (!__syncthreads_or(need)) return;
+  // ---- cyclic two-sided Jacobi on G (parallel: 16 disjoint pairs per round)
+  for (int sw = 0; sw < MAX_INNER; ++sw) {
+    int sweep_any = 0;
+    for (int round = 0; round < JP - 1; ++round) {
+      if (tid == 0) s_round_any = 0;
+      __syncthreads();
+      if (tid < 16) {
+        int p, q;
+        pair_of(JP, round, tid, &p, &q);
+        double gpp = G[p][p], gqq = G[q][q], gpq = G[p][q];
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (gpp > floor && gqq > floor && fabs(gpq) > tol * sqrt(gpp * gqq)) {
+          double zeta = (gqq - gpp) / (2.0 * gpq);
+          t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = c * t;
+          s_round_any = 1;
+        }
+        rc[tid] = c;
+        rs[tid] = s;
+        rt[tid] = t;
+        rpp[tid] = gpp;
+        rqq[tid] = gqq;
+        rpq[tid] = gpq;
+      }
+      __syncthreads();
+      if (s_round_any) {
+        // columns: G J and Z J  (16 pairs x 32 rows, 2 matrices)
+        for (int e = tid; e < 16 * JP; e += JT) {
+          int pr = e / JP, r = e % JP;
+          double c = rc[pr], s = rs[pr];
+          if (s == 0.0) continue;
+          int p, q;
+          pair_of(JP, round, pr, &p, &q);
+          double gp = G[r][p], gq = G[r][q];
+          G[r][p] = c * gp - s * gq;
+          G[r][q] = s * gp + c * gq;
+          double zp = Z[r][p], zq = Z[r][q];
+          Z[r][p] = c * zp - s * zq;
+          Z[r][q] = s * zp + c * zq;
+        }
+        __syncthreads();
+        // rows: J^T G
+        for (int e = tid; e < 16 * JP; e += JT) {
+          int pr = e / JP, r = e % JP;
+          double c = rc[pr], s = rs[pr];
+          if (s == 0.0) continue;
+          int p, q;
+          pair_of(JP, round, pr, &p, &q);
+          double gp = G[p][r], gq = G[q][r];
+          G[p][r] = c * gp - s * gq;
+          G[q][r] = s * gp + c * gq;
+        }
+        __syncthreads();
+        // the 2x2 block exactly (Rutishauser)
+        if (tid < 16 && rs[tid] != 0.0) {
+          int p, q;
+          pair_of(JP, round, tid, &p, &q);
+          G[p][q] = 0.0;
+          G[q][p] = 0.0;
+          G[p][p] = rpp[tid] - rt[tid] * rpq[tid];
+          G[q][q] = rqq[tid] + rt[tid] * rpq[tid];
+        }
+        sweep_any = 1;
+      }
+      __syncthreads();
+    }
+    if (!sweep_any) break;
+  }
+  __syncthreads();
+  if (tid == 0) atomicAdd(rotated, 1ull);
+  // ---- apply Z to the pair's columns of X and P
+  for (int mat = 0; mat < 2; ++mat) {
+    double *M = mat == 0 ? X : P;
+    for (int64_t r0 = 0; r0 < n; r0 += CH) {
+      for (int e = tid; e < CH * JP; e += JT) {
+        int c = e / CH, r = e % CH;
+        int64_t row = r0 + r;
+        int cc = col[c];
+        S[r][c] = (cc >= 0 && row < n) ? M[row + (int64_t)cc * ld] : 0.0;
+      }
+      __syncthreads();
+      // out[r][j] = sum_i S[r][i] Z[i][j]; thread -> (r = e % CH, j = e / CH)
+      double out[8];
+      for (int q = 0; q < 8; ++q) {
+        int e = q * JT + tid;
+        int r = e % CH, j = e / CH;
+        double v = 0.0;
+#pragma unroll 8
+        for (int i = 0; i < JP; ++i) v += S[r][i] * Z[i][j];
+        out[q] = v;
+      }
+      for (int q = 0; q < 8; ++q) {
+        int e = q * JT + tid;
+        int r = e % CH, j = e / CH;
+        int64_t row = r0 + r;
+        int cc = col[j];
+        if (cc >= 0 && row < n) M[row + (int64_t)cc * ld] = out[q];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// X = R^T from the factored A (upper triangle = R), n x n.
+__global__ void k_rt(int64_t n, const double *__restrict__ A, int64_t lda, double *__restrict__ X) {
+  int64_t total = n * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / n, i = t - j * n;  // X(i, j) = R(j, i) for j <= i
+    X[i + j * n] = j <= i ? A[j + i * lda] : 0.0;
+  }
+}
+
+__global__ void k_col_norms(int64_t n, int64_t ncol, const double *__restrict__ Y, int64_t ld,
+                            double *__restrict__ out) {
+  // one block per column, deterministic tree
+  __shared__ double s[256];
+  int64_t j = blockIdx.x;
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = Y[i + j * ld];
+    a += v * v;
+  }
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off; off >>= 1) {
+    if ((int)threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = sqrt(s[0]);
+}
+
+// out (rows x r): column j = src[:, sel[j]] * (scale ? 1/sig[j] : 1); rows beyond
+// src_rows are zero.
+__global__ void k_gather_cols(int64_t rows, int64_t src_rows, int64_t r, const double *__restrict__ src,
+                              int64_t lds, const int64_t *__restrict__ sel,
+                              const double *__restrict__ inv, double *__restrict__ out, int64_t ldo) {
+  int64_t total = rows * r;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = t / rows, i = t - j * rows;
+    double v = 0.0;
+    if (i < src_rows) {
+      v = src[i + sel[j] * lds];
+      if (inv) v *= inv[j];
+    }
+    out[i + j * ldo] = v;
+  }
+}
+
+// _fix_signs (linalg.py:56-63): first argmax |U[:, j]|; flip U[:, j] and
+// V[:, j] if that entry is negative; then optionally V[:, j] *= s[j].
+__global__ void k_fix_signs(int64_t mu, int64_t mv, double *__restrict__ U, int64_t ldu,
+                            double *__restrict__ V, int64_t ldv, const double *__restrict__ sig,
+                            int scale_v) {
+  const int64_t j = blockIdx.x;
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  double best = -1.0;
+  int64_t bi = 0;
+  for (int64_t i = threadIdx.x; i < mu; i += blockDim.x) {
+    double a = fabs(U[i + j * ldu]);
+    if (a > best) {
+      best = a;
+      bi = i;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      double o = sv[threadIdx.x + off];
+      int64_t oi = si[threadIdx.x + off];
+      if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = o;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  const bool flip = U[si[0] + j * ldu] < 0.0;
+  const double sc = scale_v ? sig[j] : 1.0;
+  if (flip)
+    for (int64_t i = threadIdx.x; i < mu; i += blockDim.x) U[i + j * ldu] = -U[i + j * ldu];
+  const double f = flip ? -sc : sc;
+  if (f != 1.0)
+    for (int64_t i = threadIdx.x; i < mv; i += blockDim.x) V[i + j * ldv] *= f;
+}
+
+}  // namespace
+
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
+                           int32_t a_row_major, double *s_host) {
+  if (!ctx || m < 0 || n < 0) return FTT_ERR_INVALID;
+  svd_state_free(ctx);
+  SvdState *st = new SvdState();
+  ctx->svd = st;
+  st->m = m;
+  st->n = n;
+  st->transposed = m < n;
+  st->mA = std::max(m, n);
+  st->nA = std::min(m, n);
+  const int64_t mA = st->mA, nA = st->nA;
+  if (nA == 0) return FTT_OK;
+  {
+    FTT_CHECK(arena_reserve(ctx, 1024));
+    bool ok = true;
+    if (a_row_major) FTT_CHECK(check_finite(ctx, n, m, A, lda, &ok));
+    else FTT_CHECK(check_finite(ctx, m, n, A, lda, &ok));
+    if (!ok) {
+      set_error("matrix entries must be finite");
+      return FTT_ERR_NONFINITE;
+    }
+  }
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->tau, 8 * (size_t)nA));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb, 8 * qr_tblk_elems(mA, nA)));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->P, 8 * (size_t)nA * nA));
+  // tall orientation A_tall (mA x nA, column-major): M itself when m >= n,
+  // else M^T.  A row-major M is the column-major M^T.
+  const bool need_t = a_row_major ? !st->transposed : st->transposed;
+  if (!need_t) {
+    FTT_CHECK(copy_matrix(ctx, mA, nA, A, lda, st->Af, mA));
+  } else {
+    FTT_CHECK(transpose(ctx, nA, mA, A, lda, st->Af, mA));
+  }
+  size_t wse = qr_workspace_elems(mA, nA);
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)nA) +
+                                   align_up(8 * (kSumSqBlocks + 1)) + 4096));
+  double *ws = take<double>(ctx, wse);
+  double *norms = take<double>(ctx, nA);
+  double *partial = take<double>(ctx, kSumSqBlocks + 1);
+  unsigned long long *rot = take<unsigned long long>(ctx, 64);
+  FTT_CHECK(qr_factor(ctx, mA, nA, st->Af, mA, st->tau, st->Tb, ws, wse));
+  k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->Y);
+  FTT_LAUNCHED(ctx);
+  FTT_CHECK(launch_identity(ctx, nA, nA, st->P, nA));
+  if (nA > 1) {
+    int nblk = (int)ceil_div(nA, JB);
+    if (nblk & 1) ++nblk;
+    const double tol = 2.220446049250313e-16 * sqrt((double)nA);
+    // noise floor: columns with |x|^2 <= (0.1 eps)^2 * nA * ||X||_F^2 are
+    // below the backward error of the QR and are not orthogonalised further
+    double fro2 = 0.0;
+    FTT_CHECK(sum_squares(ctx, nA * nA, st->Y, partial, &fro2));
+    const double floor = 0.01 * 2.220446049250313e-16 * 2.220446049250313e-16 * (double)nA * fro2;
+    const int max_sweeps = 60;
+    FTT_CUDA(cudaMemsetAsync(rot, 0, sizeof(unsigned long long) * 64, ctx->stream));
+    int sw = 0;
+    for (; sw < max_sweeps; ++sw) {
+      for (int step = 0; step < nblk - 1; ++step) {
+        k_jacobi_step<<<nblk / 2, JT, 0, ctx->stream>>>(nA, st->Y, st->P, nA, nblk, step, tol,
+                                                        floor, rot + (sw % 64));
+        FTT_LAUNCHED(ctx);
+      }
+      unsigned long long h = 0;
+      FTT_CHECK(copy_to_host(ctx, &h, rot + (sw % 64), sizeof(h)));
+      FTT_CUDA(cudaMemsetAsync(rot + (sw % 64), 0, sizeof(unsigned long long), ctx->stream));
+      if (h == 0) break;
+    }
+    st->sweeps = sw + 1;
+    if (sw == max_sweeps) {
+      set_error("Jacobi SVD did not converge in %d sweeps", max_sweeps);
+      return FTT_ERR_NOCONV;
+    }
+  }
+  k_col_norms<<<(unsigned)nA, 256, 0, ctx->stream>>>(nA, nA, st->Y, nA, norms);
+  FTT_LAUNCHED(ctx);
+  std::vector<double> raw(nA);
+  FTT_CHECK(copy_to_host(ctx, raw.data(), norms, 8 * nA));
+  st->perm.resize(nA);
+  std::iota(st->perm.begin(), st->perm.end(), 0);
+  std::stable_sort(st->perm.begin(), st->perm.end(),
+                   [&](int64_t a, int64_t b) { return raw[a] > raw[b]; });
+  st->sigma.resize(nA);
+  for (int64_t i = 0; i < nA; ++i) st->sigma[i] = raw[st->perm[i]];
+  if (s_host) memcpy(s_host, st->sigma.data(), 8 * nA);
+  return FTT_OK;
+}
+
+extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ldu,
+                               int32_t u_row_major, double *V, int64_t ldv, int32_t v_row_major,
+                               int32_t scale_v) {
+  if (!ctx || !ctx->svd) {
+    set_error("ftt_svd_vectors: no factorization in this context");
+    return FTT_ERR_INVALID;
+  }
+  SvdState *st = ctx->svd;
+  const int64_t mA = st->mA, nA = st->nA;
+  if (rank < 0 || rank > nA) {
+    set_error("rank %lld out of range", (long long)rank);
+    return FTT_ERR_INVALID;
+  }
+  if (rank == 0) return FTT_OK;
+  size_t wse = qr_apply_workspace_elems(mA, nA, rank);
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)mA * rank) +
+                                   align_up(8 * (size_t)nA * rank) + 3 * align_up(8 * rank) + 4096));
+  double *ws = take<double>(ctx, wse);
+  double *UA = take<double>(ctx, (size_t)mA * rank);
+  double *VA = take<double>(ctx, (size_t)nA * rank);
+  int64_t *sel = take<int64_t>(ctx, rank);
+  double *inv = take<double>(ctx, rank);
+  double *sig = take<double>(ctx, rank);
+  std::vector<double> hinv(rank);
+  for (int64_t j = 0; j < rank; ++j) hinv[j] = st->sigma[j] != 0.0 ? 1.0 / st->sigma[j] : 0.0;
+  FTT_CUDA(cudaMemcpyAsync(sel, st->perm.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+  FTT_CUDA(cudaMemcpyAsync(inv, hinv.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+  FTT_CUDA(cudaMemcpyAsync(sig, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+  // V_A = Y[:, sel] / sigma ;  U_A = Q [P[:, sel]; 0]
+  k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA, sel,
+                                                                      inv, VA, nA);
+  FTT_LAUNCHED(ctx);
+  k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, nA, rank, st->P, nA, sel,
+                                                                      nullptr, UA, mA);
+  FTT_LAUNCHED(ctx);
+  FTT_CHECK(qr_apply_q(ctx, mA, nA, st->Af, mA, st->Tb, rank, UA, mA, ws, wse));
+  double *UM = st->transposed ? VA : UA;
+  double *VM = st->transposed ? UA : VA;
+  const int64_t mu = st->transposed ? nA : mA;  // == caller m
+  const int64_t mv = st->transposed ? mA : nA;  // == caller n
+  k_fix_signs<<<(unsigned)rank, 256, 0, ctx->stream>>>(mu, mv, UM, mu, VM, mv, sig, scale_v);
+  FTT_LAUNCHED(ctx);
+  if (U) {
+    if (u_row_major) FTT_CHECK(transpose(ctx, mu, rank, UM, mu, U, ldu));
+    else FTT_CHECK(copy_matrix(ctx, mu, rank, UM, mu, U, ldu));
+  }
+  if (V) {
+    if (v_row_major) FTT_CHECK(transpose(ctx, mv, rank, VM, mv, V, ldv));
+    else FTT_CHECK(copy_matrix(ctx, mv, rank, VM, mv, V, ldv));
+  }
+  // keep the context stream-ordered for the host vectors we just copied from
+  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FTT_OK;
+}
