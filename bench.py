@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""FastTT benchmark on B200 (BASELINE.json metric: end-to-end FastTT
+nonzeros/sec in fp64 on one B200, plus the HBM roofline fraction of the
+sort/segment kernels).
+
+Workload (BASELINE.json configs[1]): 6-way 64^6 sparse tensor, sum of R=8
+rank-1 terms with s=6 seeded positions per factor, N(0,1) values
+(373,246 nnz at seed 0), eps = 1e-10, automatic pivot. One step = one full
+``fasttt`` decomposition (select_p -> fibers -> deparallelisation sweeps ->
+rounding sweeps -> error report).
+
+* ``value``: COO already in HBM (``fasttt_device``), cores left on the
+  device; per-step CUDA events on the launching stream, L2 flushed (256 MiB
+  write) between steps, summed over K steps, max over ranks.
+* ``e2e``: the public drop-in call ``fasttt(SparseTensor)`` from pinned host
+  buffers: H2D of coords+values, the decomposition, D2H of every core.
+* ``--impl reference``: the reference algorithm's CPU implementation (the
+  oracle port, oracle/fasttt_oracle.py -- the reference is pure Python and
+  cannot travel to the GPU box) on all host cores, rank 0 only.
+
+Multi-GPU: the decomposition is a chain of dependent factorisations, so N
+GPUs run N independent replicas ("replicas only", scaling "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "FastTT nonzeros/sec end-to-end (fp64) at 1 B200; % HBM roofline of sort/segment"
+UNIT = "nnz/s"
+TAGS = ["sort", "hist", "segment", "sweep", "scatter", "gemm", "qr_panel", "jacobi", "entries"]
+MEM_TAGS = {"sort", "hist", "segment", "sweep", "scatter", "entries"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, help="BASELINE config index (1-based)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(cfg):
+    from paper_1908_02721_b200 import generators as G
+
+    shape, coords, vals, eps = G.gen_config(cfg, seed=0)
+    return shape, coords, vals, eps, G.CONFIGS[cfg]["name"]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, val in zip(names, s[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_threads():
+    n = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(n)
+    except Exception:  # noqa: BLE001
+        pass
+    return n
+
+
+def oracle_step(shape, coords, vals, eps):
+    from oracle import fasttt_oracle as O
+
+    t0 = time.perf_counter()
+    cores, info = O.fasttt(shape, coords, vals, eps=eps, report=True)
+    return time.perf_counter() - t0, info
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    shape, coords, vals, eps, name = workload(args.config)
+    cores = cpu_threads()
+    for _ in range(max(args.warmup, 0)):
+        oracle_step(shape, coords, vals, eps)
+    times = [oracle_step(shape, coords, vals, eps)[0] for _ in range(args.steps)]
+    total = sum(times)
+    nnz = int(coords.shape[0])
+    value = nnz * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE.json configs[1])",
+        "config": {"workload": name, "nnz": nnz, "eps": eps, "seed": 0},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"full {name} decomposition incl. report per step "
+                                   "(oracle/fasttt_oracle.py: the reference algorithm restated in "
+                                   "numpy/LAPACK, index-form 0/1 cores)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def flush_l2(buf):
+    buf.fill_(1.0)  # 256 MiB > 126 MB L2
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch per kernel class from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import paper_1908_02721_b200 as ft
+    from paper_1908_02721_b200 import _native as nat
+
+    shape, coords, vals, eps, name = workload(args.config)
+    a = ft.SparseTensor(shape, coords, vals)
+    nnz = a.nnz
+    lib = nat.lib()
+    ctx = nat.context()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    cd, vd = a.device_arrays()
+    torch.cuda.synchronize()
+
+    def device_step():
+        return ft.fasttt_device(a, cd, vd, eps, None, "static", None, False, 1.0, report=True)
+
+    for _ in range(max(args.warmup, 1)):
+        res = device_step()
+    torch.cuda.synchronize()
+    ranks = res.ranks
+
+    # DMMA peak (fp64 tensor pipe) on this GPU, for the tensor-bound roofline
+    dmma = nat.ctypes.c_double(0.0)
+    nat.check(lib.ftt_bench_dmma(ctx, 20000, nat.ctypes.byref(dmma)), "ftt_bench_dmma")
+
+    # ---------------- timed: device resident
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = nat.kernel_launches()
+    nat.check(lib.ftt_profile_enable(ctx, 1), "profile")
+    stream = torch.cuda.current_stream()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            device_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = nat.kernel_launches() - launches0
+    prof = {}
+    for i, tag in enumerate(TAGS):
+        ms = nat.ctypes.c_double(0)
+        n = nat.ctypes.c_int64(0)
+        by = nat.ctypes.c_double(0)
+        fl = nat.ctypes.c_double(0)
+        nat.check(lib.ftt_profile_read(ctx, i, nat.ctypes.byref(ms), nat.ctypes.byref(n),
+                                       nat.ctypes.byref(by), nat.ctypes.byref(fl)), "profile_read")
+        prof[tag] = {"ms": ms.value, "launches": int(n.value), "bytes": by.value, "flops": fl.value}
+    nat.check(lib.ftt_profile_enable(ctx, 0), "profile")
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * nnz * args.steps / (total_ms * 1e-3)
+
+    # ---------------- e2e through the public API (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        h2d = a.coords.nbytes + a.values.nbytes
+        for _ in range(2):
+            a.drop_device_copy()
+            ft.fasttt(a, eps=eps)
+        e_times = []
+        d2h = 0
+        for _ in range(args.steps):
+            a.drop_device_copy()
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tt, rep = ft.fasttt(a, eps=eps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_times.append(e0.elapsed_time(e1))
+            d2h = sum(c.nbytes for c in tt.cores)
+        e_ms = sum(e_times)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * nnz * args.steps / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e_ms / args.steps}
+        a.device_arrays()
+
+    # ---------------- roofline of the dominant kernel class
+    pk, pk_src = peaks()
+    traffic = ncu_traffic()
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+
+    def roof(tag, rec):
+        if rec["ms"] <= 0 or rec["launches"] == 0:
+            return None
+        if tag in MEM_TAGS:
+            ach = rec["bytes"] / (rec["ms"] * 1e-3) / 1e9
+            peak = float(pk["hbm_gbs"])
+            tr = traffic.get(tag)
+            return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": tr, "kernel_class": tag,
+                    "launches": rec["launches"], "ms_total": rec["ms"],
+                    "alg_bytes_per_launch": rec["bytes"] / rec["launches"],
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_src})"}
+        ach = rec["flops"] / (rec["ms"] * 1e-3) / 1e12
+        peak = dmma.value
+        tr = traffic.get(tag)
+        return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak if peak else None, "traffic": tr, "kernel_class": tag,
+                "launches": rec["launches"], "ms_total": rec["ms"],
+                "alg_flops_per_launch": rec["flops"] / rec["launches"],
+                "peak_source": "fp64 DMMA (mma.sync m8n8k4) throughput measured in this run "
+                               "by ftt_bench_dmma; MEASURED_PEAKS.json has no fp64 figure"}
+
+    sortseg = {k: prof[k] for k in ("sort", "hist", "segment")}
+    agg = {"ms": sum(v["ms"] for v in sortseg.values()),
+           "launches": sum(v["launches"] for v in sortseg.values()),
+           "bytes": sum(v["bytes"] for v in sortseg.values()), "flops": 0.0}
+    roof_sort = roof("sort", agg)
+    if roof_sort:
+        roof_sort["kernel_class"] = "sort+hist+segment"
+        roof_sort["traffic"] = traffic.get("sort+hist+segment")
+
+    # ---------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = cpu_threads()
+        dt, _ = oracle_step(shape, coords, vals, eps)
+        cpu = {"value": nnz / dt, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"one full {name} decomposition incl. report "
+                         "(oracle/fasttt_oracle.py on the host cores)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 1), "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE.json configs[1]; no dataset involved)",
+            "config": {"workload": name, "nnz": nnz, "shape": list(shape), "eps": eps,
+                       "pivot": res.pivot, "ranks_lossless": list(res.ranks_lossless),
+                       "ranks": list(ranks), "seed": 0, "l2": "flushed (256 MiB write) between steps",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": roof(dom, d),
+            "roofline_sort_segment": roof_sort,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "dmma_peak_tflops": dmma.value,
+            "stages_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -49,6 +49,19 @@ int ftt_destroy(ftt_ctx *ctx);
 int ftt_set_stream(ftt_ctx *ctx, void *stream);
 /* Number of kernels this context launched since creation (instrumentation). */
 int64_t ftt_kernel_launches(const ftt_ctx *ctx);
+/* Live kernel timing for the roofline report: while enabled, every launch of
+ * an instrumented kernel is bracketed by CUDA events on the context stream
+ * and tagged with its class and algorithmic bytes / flops.  Enabling clears
+ * the records.  Classes: 0 sort passes, 1 key build + histogram, 2 segment,
+ * 3 deparallelisation sweep, 4 scatters, 5 DMMA GEMM, 6 QR panel,
+ * 7 Jacobi step, 8 tt_entries. */
+int ftt_profile_enable(ftt_ctx *ctx, int enable);
+int ftt_profile_read(ftt_ctx *ctx, int32_t tag, double *ms_out,
+                     int64_t *launches_out, double *bytes_out,
+                     double *flops_out);
+/* fp64 tensor-pipe (DMMA) peak microbenchmark: TFLOP/s over `iters`
+ * back-to-back mma.sync.m8n8k4.f64 per warp on every SM. */
+int ftt_bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops_out);
 
 /* ---------------------------------------------------- index path (int) */
 

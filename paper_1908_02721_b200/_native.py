@@ -39,6 +39,9 @@ SIGNATURES = {
     "ftt_destroy": [_c_p],
     "ftt_set_stream": [_c_p, _c_p],
     "ftt_kernel_launches": [_c_p],
+    "ftt_profile_enable": [_c_p, ctypes.c_int],
+    "ftt_profile_read": [_c_p, _c_i32, _P_d, _P_i64, _P_d, _P_d],
+    "ftt_bench_dmma": [_c_p, _c_i64, _P_d],
     "ftt_fiber_count": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, _P_i64],
     "ftt_fiber_counts_all": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _P_i64],
     "ftt_extract_fibers": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32,

@@ -19,6 +19,26 @@ void set_error(const char *fmt, ...);
 
 struct SvdState;  // ftt_svd.cu
 
+// Kernel classes for the live roofline measurement (ftt_profile_*).
+enum ProfTag {
+  PT_SORT = 0,     // onesweep radix passes
+  PT_HIST = 1,     // key build + digit histograms
+  PT_SEGMENT = 2,  // fiber segmentation / compaction
+  PT_SWEEP = 3,    // deparallelisation sweep kernels
+  PT_SCATTER = 4,  // pivot-core and carry scatters
+  PT_GEMM = 5,     // DMMA GEMM
+  PT_QR_PANEL = 6, // cooperative Householder panel
+  PT_JACOBI = 7,   // block Jacobi step
+  PT_ENTRIES = 8,  // tt_entries
+  PT_COUNT = 9
+};
+
+struct ProfRec {
+  int ev_a, ev_b;
+  int tag;
+  double bytes, flops;
+};
+
 // Grow-only device arena.  Every API call resets it; allocations are
 // 256-byte aligned bumps.  Growth frees the old block stream-ordered and
 // allocates a larger one (so pointers from before a growth in the same call
@@ -41,6 +61,11 @@ struct ftt_ctx {
   int64_t launches = 0;
   int num_sms = ftt::kNumSMs;
   void *pinned = nullptr;  // small pinned host scratch (64 KiB)
+  // live per-class kernel timing (off by default)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_used = 0;
+  std::vector<ftt::ProfRec> prof_recs;
 };
 
 namespace ftt {
@@ -71,6 +96,12 @@ namespace ftt {
       return FTT_ERR_CUDA;                                                 \
     }                                                                      \
   } while (0)
+
+// Profiling: prof_begin records an event before a launch (returns -1 when
+// profiling is off); prof_end records the closing event and the launch's
+// algorithmic bytes / flops under `tag`.
+int prof_begin(ftt_ctx *ctx);
+void prof_end(ftt_ctx *ctx, int begin, int tag, double bytes, double flops);
 
 // Reserve at least `bytes` of arena for this call (must be called before
 // taking pointers).  Resets `used`.

@@ -103,6 +103,30 @@ void owned_free(ftt_ctx *ctx, void *p) {
 
 void svd_state_free(ftt_ctx *ctx);  // ftt_svd.cu
 
+static int next_event(ftt_ctx *ctx) {
+  if (ctx->ev_used >= (int)ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_used++;
+}
+
+int prof_begin(ftt_ctx *ctx) {
+  if (!ctx->prof) return -1;
+  int i = next_event(ctx);
+  if (i >= 0) cudaEventRecord(ctx->ev_pool[i], ctx->stream);
+  return i;
+}
+
+void prof_end(ftt_ctx *ctx, int begin, int tag, double bytes, double flops) {
+  if (!ctx->prof || begin < 0) return;
+  int i = next_event(ctx);
+  if (i < 0) return;
+  cudaEventRecord(ctx->ev_pool[i], ctx->stream);
+  ctx->prof_recs.push_back({begin, i, tag, bytes, flops});
+}
+
 }  // namespace ftt
 
 using namespace ftt;
@@ -144,6 +168,7 @@ int ftt_destroy(ftt_ctx *ctx) {
   ctx->owned.clear();
   if (ctx->arena.base) cudaFreeAsync(ctx->arena.base, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   return FTT_OK;
@@ -156,5 +181,36 @@ int ftt_set_stream(ftt_ctx *ctx, void *stream) {
 }
 
 int64_t ftt_kernel_launches(const ftt_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int ftt_profile_enable(ftt_ctx *ctx, int enable) {
+  if (!ctx) return FTT_ERR_INVALID;
+  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->prof = enable != 0;
+  ctx->prof_recs.clear();
+  ctx->ev_used = 0;
+  return FTT_OK;
+}
+
+int ftt_profile_read(ftt_ctx *ctx, int32_t tag, double *ms_out, int64_t *launches_out,
+                     double *bytes_out, double *flops_out) {
+  if (!ctx || tag < 0 || tag >= PT_COUNT) return FTT_ERR_INVALID;
+  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  double ms = 0.0, bytes = 0.0, flops = 0.0;
+  int64_t n = 0;
+  for (const ProfRec &r : ctx->prof_recs) {
+    if (r.tag != tag) continue;
+    float t = 0.f;
+    FTT_CUDA(cudaEventElapsedTime(&t, ctx->ev_pool[r.ev_a], ctx->ev_pool[r.ev_b]));
+    ms += t;
+    bytes += r.bytes;
+    flops += r.flops;
+    ++n;
+  }
+  if (ms_out) *ms_out = ms;
+  if (launches_out) *launches_out = n;
+  if (bytes_out) *bytes_out = bytes;
+  if (flops_out) *flops_out = flops;
+  return FTT_OK;
+}
 
 }  // extern "C"

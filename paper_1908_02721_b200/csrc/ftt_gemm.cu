@@ -238,6 +238,7 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
   }
   dim3 grid((unsigned)tiles_m, (unsigned)tiles_n, (unsigned)splits);
   double *part = splits > 1 ? splitk_ws : nullptr;
+  const int pb = prof_begin(ctx);
 #define FTT_GEMM_LAUNCH(TA_, TB_)                                                          \
   k_dgemm<TA_, TB_><<<grid, GT, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, \
                                                   ldc, kps, part)
@@ -252,6 +253,49 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
                                                                      beta, C, ldc);
     FTT_LAUNCHED(ctx);
   }
+  prof_end(ctx, pb, PT_GEMM, 8.0 * ((double)m * k + (double)k * n + 2.0 * m * n),
+           2.0 * (double)m * n * k);
+  return FTT_OK;
+}
+
+namespace {
+__global__ void __launch_bounds__(256) k_dmma_peak(int64_t iters, double seed, double *out) {
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  double a = seed * (1 + (threadIdx.x & 7)), b = seed * (1 + (threadIdx.x >> 5));
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma(acc[j][0], acc[j][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += acc[j][0] + acc[j][1];
+  if (s == 1234.5678) out[0] = s;  // keep the chain alive
+}
+}  // namespace
+
+int bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops) {
+  FTT_CHECK(arena_reserve(ctx, 256));
+  double *sink = take<double>(ctx, 1);
+  cudaEvent_t e0, e1;
+  FTT_CUDA(cudaEventCreate(&e0));
+  FTT_CUDA(cudaEventCreate(&e1));
+  const int blocks = ctx->num_sms * 4;
+  k_dmma_peak<<<blocks, 256, 0, ctx->stream>>>(iters / 10 + 1, 1e-3, sink);  // warm-up
+  FTT_LAUNCHED(ctx);
+  FTT_CUDA(cudaEventRecord(e0, ctx->stream));
+  k_dmma_peak<<<blocks, 256, 0, ctx->stream>>>(iters, 1e-3, sink);
+  FTT_LAUNCHED(ctx);
+  FTT_CUDA(cudaEventRecord(e1, ctx->stream));
+  FTT_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  FTT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  // 8 warps x 8 chains x iters DMMAs, 512 flops each
+  double flops = (double)blocks * 8 * 8 * (double)iters * 512.0;
+  *tflops = flops / (ms * 1e-3) / 1e12;
   return FTT_OK;
 }
 
@@ -291,6 +335,11 @@ int ftt_dgemm(ftt_ctx *ctx, int32_t transa, int32_t transb, int64_t m, int64_t n
     part = take<double>(ctx, ws);
   }
   return gemm(ctx, transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, part, ws);
+}
+
+int ftt_bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops_out) {
+  if (!ctx || !tflops_out || iters < 1) return FTT_ERR_INVALID;
+  return bench_dmma(ctx, iters, tflops_out);
 }
 
 int ftt_orth_defect(ftt_ctx *ctx, int64_t n, const double *G, int64_t ldg, double *out_host) {

@@ -320,17 +320,22 @@ __global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total) {
   if (threadIdx.x == 0 && total) *total = carry;
 }
 
+// `tag`/`alg_bytes`: profiling class and algorithmic bytes of the whole
+// compaction (predicate reads + emitted outputs), charged to the emit pass
+// and the count pass together.
 template <class Pred, class Emit>
 int compact(ftt_ctx *ctx, int64_t n, Pred pred, Emit emit, int64_t *block_counts,
-            int64_t *total_dev) {
+            int64_t *total_dev, int tag = PT_SEGMENT, double alg_bytes = 0.0) {
   if (n <= 0) return FTT_OK;
   int64_t nb = ceil_div(n, CP_TILE);
+  const int pb = tag >= 0 ? prof_begin(ctx) : -1;
   k_count<Pred><<<(unsigned)nb, CP_THREADS, 0, ctx->stream>>>(n, pred, block_counts);
   FTT_LAUNCHED(ctx);
   k_scan_counts<<<1, 1024, 0, ctx->stream>>>(block_counts, nb, total_dev);
   FTT_LAUNCHED(ctx);
   k_emit<Pred, Emit><<<(unsigned)nb, CP_THREADS, 0, ctx->stream>>>(n, pred, emit, block_counts);
   FTT_LAUNCHED(ctx);
+  prof_end(ctx, pb, tag, alg_bytes, 0.0);
   return FTT_OK;
 }
 
@@ -600,6 +605,7 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
                                     12 * RS_TILE));
       attr_set = true;
     }
+    const int pb = prof_begin(ctx);
     if (vals[0]) {
       k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
           keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, ghist + p * RADIX, status,
@@ -610,6 +616,8 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
           counters + p);
     }
     FTT_LAUNCHED(ctx);
+    // algorithmic bytes: read + write every key (and payload) once
+    prof_end(ctx, pb, PT_SORT, (double)n * (vals[0] ? 24.0 : 16.0), 0.0);
     cur ^= 1;
   }
   *kres = keys[cur];
@@ -747,9 +755,12 @@ static int sort_coords(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t
     return FTT_ERR_INVALID;
   }
   FTT_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
+  const int pb = prof_begin(ctx);
   k_keys_hist<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(coords, nnz, spec, num_passes, kb[0],
                                                               vb[0], ghist);
   FTT_LAUNCHED(ctx);
+  // read the COO coordinates, write one key (+ identity payload) per nonzero
+  prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0 + (include_pivot ? 4.0 : 0.0)), 0.0);
   return onesweep_passes(ctx, kb, vb, nnz, num_passes, ghist, status, counters, kres, vres);
 }
 
@@ -847,7 +858,9 @@ int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords, const double *values
   AdjDiffPred pred{kr, (uint64_t)dims_host[pivot]};
   FiberEmit emit{kr, vr, values, (uint64_t)dims_host[pivot], fixed_lin, indptr, fiber_of,
                  pivot_index, values_out};
-  FTT_CHECK(compact(ctx, nnz, pred, emit, bc, total));
+  // per entry: sorted key + payload + gathered value in; pivot index, value,
+  // fiber id out (the per-fiber indptr / key writes are <= 16 bytes x R more)
+  FTT_CHECK(compact(ctx, nnz, pred, emit, bc, total, PT_SEGMENT, 44.0 * (double)nnz));
   int64_t R = 0;
   FTT_CHECK(copy_to_host(ctx, &R, total, sizeof(R)));
   k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr + R, nnz);
@@ -868,19 +881,24 @@ static int depar_from_keys(ftt_ctx *ctx, int64_t n_rows, int64_t R, const SweepK
     int64_t *bc = take<int64_t>(ctx, ceil_div(n_rows, CP_TILE) + 1);
     int64_t *total = take<int64_t>(ctx, 1);
     FTT_CUDA(cudaMemsetAsync(present, 0, 4 * n_rows, ctx->stream));
+    const int pb = prof_begin(ctx);
     if (skey) {
       k_sweep_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, *skey, present);
     } else {
       k_mark_rows<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, rows, present);
     }
     FTT_LAUNCHED(ctx);
-    FTT_CHECK(compact(ctx, n_rows, FlagPred{present}, KeptEmit{present, kept}, bc, total));
+    FTT_CHECK(compact(ctx, n_rows, FlagPred{present}, KeptEmit{present, kept}, bc, total, -1));
     if (skey) {
       k_sweep_gather<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, *skey, present, map_out);
     } else {
       k_gather_rank<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, rows, present, map_out);
     }
     FTT_LAUNCHED(ctx);
+    // mark: key inputs (16 B) per fiber + flag write; scan: flags; gather:
+    // key inputs again + rank read + map write (kept writes <= 8 B x R)
+    prof_end(ctx, pb, PT_SWEEP, (double)R * (16.0 + 4.0 + 16.0 + 4.0 + 8.0) + 8.0 * (double)n_rows,
+             0.0);
     FTT_CHECK(copy_to_host(ctx, n_kept_out, total, sizeof(int64_t)));
     return FTT_OK;
   }
@@ -967,9 +985,12 @@ int ftt_pivot_core_scatter(ftt_ctx *ctx, int64_t nnz, const int64_t *fiber_of,
   FTT_CHECK(arena_reserve(ctx, align_up(8 * (nb + 1)) + 256));
   double *partial = take<double>(ctx, nb + 1);
   if (nnz > 0) {
+    const int pb = prof_begin(ctx);
     k_pivot_scatter<<<nb, 256, 0, ctx->stream>>>(nnz, fiber_of, pivot_index, values, t_map, s_map,
                                                  n_p, r_next, core, partial);
     FTT_LAUNCHED(ctx);
+    // fiber id, pivot index, value, two map reads and the scattered write
+    prof_end(ctx, pb, PT_SCATTER, 48.0 * (double)nnz, 0.0);
   }
   if (norm_out) {
     if (nnz == 0) {

