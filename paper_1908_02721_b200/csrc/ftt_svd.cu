@@ -39,9 +39,13 @@ struct SvdState {
   double *Tb = nullptr;
   double *Y = nullptr;     // nA x nA (X after Jacobi)
   double *P = nullptr;     // nA x nA accumulated rotations
+  double *B = nullptr;     // nA x nA: QR of R^T (preconditioning), reflectors
+  double *tau2 = nullptr;
+  double *Tb2 = nullptr;
   std::vector<double> sigma;  // sorted descending
   std::vector<int64_t> perm;  // sorted position -> column of Y
   int sweeps = 0;
+  bool precond = false;  // Jacobi ran on R2^T (QR of R^T) instead of R^T
 };
 
 void svd_state_free(ftt_ctx *ctx) {
@@ -52,6 +56,9 @@ void svd_state_free(ftt_ctx *ctx) {
   owned_free(ctx, s->Tb);
   owned_free(ctx, s->Y);
   owned_free(ctx, s->P);
+  owned_free(ctx, s->B);
+  owned_free(ctx, s->tau2);
+  owned_free(ctx, s->Tb2);
   delete s;
   ctx->svd = nullptr;
 }
@@ -62,7 +69,40 @@ constexpr int JB = 16;
 constexpr int JP = 2 * JB;  // 32 columns per pair
 constexpr int JT = 256;
 constexpr int CH = 64;      // rows per staged chunk
-constexpr int MAX_INNER = 2;  // inner sweeps on the Gram before a fresh recompute
+constexpr int MAX_INNER = 3;  // inner sweeps on the Gram before a fresh recompute
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int LPT = 64 * 32 / 256;  // chunk elements per thread (CH * JP / JT)
+
+// One 64-row chunk of the pair's 32 columns: all LPT loads issued back to
+// back into registers (memory-level parallelism), stored to smem later so
+// the next chunk's loads overlap the current chunk's MMAs.
+__device__ __forceinline__ void chunk_load(double (&pre)[LPT], const double *__restrict__ M,
+                                           int64_t r0, int64_t n, int64_t ld, const int *col,
+                                           int tid) {
+#pragma unroll
+  for (int q = 0; q < LPT; ++q) {
+    const int e = q * 256 + tid;
+    const int c = e >> 6, r = e & 63;
+    const int64_t row = r0 + r;
+    const int cc = col[c];
+    pre[q] = (cc >= 0 && row < n) ? __ldcg(M + row + (int64_t)cc * ld) : 0.0;
+  }
+}
+
+template <int STRIDE>
+__device__ __forceinline__ void chunk_store(const double (&pre)[LPT], double (*S)[STRIDE], int tid) {
+#pragma unroll
+  for (int q = 0; q < LPT; ++q) {
+    const int e = q * 256 + tid;
+    S[e & 63][e >> 6] = pre[q];
+  }
+}
 
 __device__ __forceinline__ void pair_of(int nblk, int step, int c, int *a, int *b) {
   // circle method, team nblk-1 fixed
@@ -88,10 +128,11 @@ __device__ __forceinline__ void pair_of(int nblk, int step, int c, int *a, int *
 struct JacSmem {
   double G[JP][JP + 1];
   double Z[JP][JP + 1];
-  double S[CH][JP + 1];
+  double S[CH][JP + 4];  // row stride 36 doubles == 8 banks: conflict-free DMMA fragments
   double rc[16], rs[16], rt[16], rpp[16], rqq[16], rpq[16];
   int col[JP];
   int s_round_any;
+  unsigned char tp[JP - 1][16], tq[JP - 1][16];  // inner round-robin pairing table
 };
 
 __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restrict__ P, int64_t ld,
@@ -112,35 +153,57 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
   __syncthreads();  // the previous pair of this CTA is done with sm
   int ba, bb;
   pair_of(nblk, step, pc, &ba, &bb);
+  for (int e = tid; e < (JP - 1) * 16; e += JT) {
+    int p, q;
+    pair_of(JP, e / 16, e % 16, &p, &q);
+    sm.tp[e / 16][e % 16] = (unsigned char)p;
+    sm.tq[e / 16][e % 16] = (unsigned char)q;
+  }
   if (tid < JP) {
     int blk = tid < JB ? ba : bb;
     int cidx = blk * JB + (tid % JB);
     col[tid] = cidx < n ? cidx : -1;
   }
   __syncthreads();
-  // ---- Gram of the pair's current columns
-  const int gi = tid >> 3;          // 0..31 row of G
-  const int gj = (tid & 7) * 4;     // 4 consecutive columns
-  double acc[4] = {0, 0, 0, 0};
-  for (int64_t r0 = 0; r0 < n; r0 += CH) {
-    for (int e = tid; e < CH * JP; e += JT) {
-      int c = e / CH, r = e % CH;
-      int64_t row = r0 + r;
-      int cc = col[c];
-      S[r][c] = (cc >= 0 && row < n) ? X[row + (int64_t)cc * ld] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int r = 0; r < CH; ++r) {
-      double a = S[r][gi];
+  // ---- Gram of the pair's current columns on the DMMA pipe: 16 8x8 tiles,
+  // two per warp, K = the n rows streamed through shared memory in chunks
+  const int lane = tid & 31, warp = tid >> 5;
+  const int gi = tid >> 3;          // convergence test: row of G
+  const int gj = (tid & 7) * 4;     //   and 4 consecutive columns
+  {
+    double gacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double pre[LPT];
+    chunk_load(pre, X, 0, n, ld, col, tid);
+    for (int64_t r0 = 0; r0 < n; r0 += CH) {
+      chunk_store(pre, S, tid);
+      __syncthreads();
+      if (r0 + CH < n) chunk_load(pre, X, r0 + CH, n, ld, col, tid);  // in flight during the MMAs
+#pragma unroll 4
+      for (int k0 = 0; k0 < CH; k0 += 4) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] += a * S[r][gj + q];
+        for (int t = 0; t < 2; ++t) {
+          const int ti = (2 * warp + t) >> 2, tj = (2 * warp + t) & 3;
+          double a = S[k0 + (lane & 3)][ti * 8 + (lane >> 2)];
+          double b = S[k0 + (lane & 3)][tj * 8 + (lane >> 2)];
+          dmma(gacc[t][0], gacc[t][1], a, b);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int ti = (2 * warp + t) >> 2, tj = (2 * warp + t) & 3;
+      G[ti * 8 + (lane >> 2)][tj * 8 + 2 * (lane & 3)] = gacc[t][0];
+      G[ti * 8 + (lane >> 2)][tj * 8 + 2 * (lane & 3) + 1] = gacc[t][1];
+    }
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) G[gi][gj + q] = acc[q];
   for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = (e / JP == e % JP) ? 1.0 : 0.0;
+  __syncthreads();
+  // the two triangles come from different DMMA tiles; use the upper one for both
+  for (int e = tid; e < JP * JP; e += JT) {
+    int i = e / JP, j = e % JP;
+    if (j < i) G[i][j] = G[j][i];
+  }
   __syncthreads();
   // ---- fresh convergence test
   int need = 0;
@@ -157,11 +220,9 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
   for (int sw = 0; sw < MAX_INNER; ++sw) {
     int sweep_any = 0;
     for (int round = 0; round < JP - 1; ++round) {
-      if (tid == 0) s_round_any = 0;
-      __syncthreads();
+      int flag = 0;
       if (tid < 16) {
-        int p, q;
-        pair_of(JP, round, tid, &p, &q);
+        const int p = sm.tp[round][tid], q = sm.tq[round][tid];
         double gpp = G[p][p], gqq = G[q][q], gpq = G[p][q];
         double c = 1.0, s = 0.0, t = 0.0;
         if (gpp > floor && gqq > floor && fabs(gpq) > tol * sqrt(gpp * gqq)) {
@@ -169,7 +230,7 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
           t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           c = 1.0 / sqrt(1.0 + t * t);
           s = c * t;
-          s_round_any = 1;
+          flag = 1;
         }
         rc[tid] = c;
         rs[tid] = s;
@@ -178,47 +239,41 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
         rqq[tid] = gqq;
         rpq[tid] = gpq;
       }
-      __syncthreads();
-      if (s_round_any) {
-        // columns: G J and Z J  (16 pairs x 32 rows, 2 matrices)
-        for (int e = tid; e < 16 * JP; e += JT) {
-          int pr = e / JP, r = e % JP;
-          double c = rc[pr], s = rs[pr];
-          if (s == 0.0) continue;
-          int p, q;
-          pair_of(JP, round, pr, &p, &q);
-          double gp = G[r][p], gq = G[r][q];
-          G[r][p] = c * gp - s * gq;
-          G[r][q] = s * gp + c * gq;
-          double zp = Z[r][p], zq = Z[r][q];
-          Z[r][p] = c * zp - s * zq;
-          Z[r][q] = s * zp + c * zq;
-        }
-        __syncthreads();
-        // rows: J^T G
-        for (int e = tid; e < 16 * JP; e += JT) {
-          int pr = e / JP, r = e % JP;
-          double c = rc[pr], s = rs[pr];
-          if (s == 0.0) continue;
-          int p, q;
-          pair_of(JP, round, pr, &p, &q);
+      if (!__syncthreads_or(flag)) continue;  // barrier 1 (uniform)
+      sweep_any = 1;
+      // columns: G J and Z J  (16 pairs x 32 rows, 2 matrices)
+      for (int e = tid; e < 16 * JP; e += JT) {
+        const int pr = e / JP, r = e % JP;
+        const double c = rc[pr], s = rs[pr];
+        if (s == 0.0) continue;
+        const int p = sm.tp[round][pr], q = sm.tq[round][pr];
+        double gp = G[r][p], gq = G[r][q];
+        G[r][p] = c * gp - s * gq;
+        G[r][q] = s * gp + c * gq;
+        double zp = Z[r][p], zq = Z[r][q];
+        Z[r][p] = c * zp - s * zq;
+        Z[r][q] = s * zp + c * zq;
+      }
+      __syncthreads();  // barrier 2
+      // rows: J^T G; the pair's own 2x2 block exactly (Rutishauser)
+      for (int e = tid; e < 16 * JP; e += JT) {
+        const int pr = e / JP, r = e % JP;
+        const double c = rc[pr], s = rs[pr];
+        if (s == 0.0) continue;
+        const int p = sm.tp[round][pr], q = sm.tq[round][pr];
+        if (r == p) {
+          G[p][p] = rpp[pr] - rt[pr] * rpq[pr];
+          G[q][p] = 0.0;
+        } else if (r == q) {
+          G[p][q] = 0.0;
+          G[q][q] = rqq[pr] + rt[pr] * rpq[pr];
+        } else {
           double gp = G[p][r], gq = G[q][r];
           G[p][r] = c * gp - s * gq;
           G[q][r] = s * gp + c * gq;
         }
-        __syncthreads();
-        // the 2x2 block exactly (Rutishauser)
-        if (tid < 16 && rs[tid] != 0.0) {
-          int p, q;
-          pair_of(JP, round, tid, &p, &q);
-          G[p][q] = 0.0;
-          G[q][p] = 0.0;
-          G[p][p] = rpp[tid] - rt[tid] * rpq[tid];
-          G[q][q] = rqq[tid] + rt[tid] * rpq[tid];
-        }
-        sweep_any = 1;
       }
-      __syncthreads();
+      __syncthreads();  // barrier 3
     }
     if (!sweep_any) break;
   }
@@ -247,33 +302,41 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
   for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = S[e / JP][e % JP];
   __syncthreads();
   if (tid == 0) atomicAdd(rotated, 1ull);
-  // ---- apply Z to the pair's columns of X and P
+  // ---- apply Z to the pair's columns of X and P on the DMMA pipe: warp w
+  // owns rows 8w..8w+7 of every 64-row chunk (4 output tiles), the Z
+  // fragments stay in registers for the whole pair
+  double bz[4][8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) bz[j][ks] = Z[ks * 4 + (lane & 3)][j * 8 + (lane >> 2)];
   for (int mat = 0; mat < 2; ++mat) {
     double *M = mat == 0 ? X : P;
+    double pre[LPT];
+    chunk_load(pre, M, 0, n, ld, col, tid);
     for (int64_t r0 = 0; r0 < n; r0 += CH) {
+      chunk_store(pre, S, tid);
+      __syncthreads();
+      if (r0 + CH < n) chunk_load(pre, M, r0 + CH, n, ld, col, tid);
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        double a = S[warp * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[j][0], acc[j][1], a, bz[j][ks]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        S[warp * 8 + (lane >> 2)][j * 8 + 2 * (lane & 3)] = acc[j][0];
+        S[warp * 8 + (lane >> 2)][j * 8 + 2 * (lane & 3) + 1] = acc[j][1];
+      }
+      __syncthreads();
       for (int e = tid; e < CH * JP; e += JT) {
         int c = e / CH, r = e % CH;
         int64_t row = r0 + r;
         int cc = col[c];
-        S[r][c] = (cc >= 0 && row < n) ? M[row + (int64_t)cc * ld] : 0.0;
-      }
-      __syncthreads();
-      // out[r][j] = sum_i S[r][i] Z[i][j]; thread -> (r = e % CH, j = e / CH)
-      double out[8];
-      for (int q = 0; q < 8; ++q) {
-        int e = q * JT + tid;
-        int r = e % CH, j = e / CH;
-        double v = 0.0;
-#pragma unroll 8
-        for (int i = 0; i < JP; ++i) v += S[r][i] * Z[i][j];
-        out[q] = v;
-      }
-      for (int q = 0; q < 8; ++q) {
-        int e = q * JT + tid;
-        int r = e % CH, j = e / CH;
-        int64_t row = r0 + r;
-        int cc = col[j];
-        if (cc >= 0 && row < n) M[row + (int64_t)cc * ld] = out[q];
+        if (cc >= 0 && row < n) M[row + (int64_t)cc * ld] = S[r][c];
       }
       __syncthreads();
     }
@@ -437,6 +500,9 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb, 8 * qr_tblk_elems(mA, nA)));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->P, 8 * (size_t)nA * nA));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->B, 8 * (size_t)nA * nA));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->tau2, 8 * (size_t)nA));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb2, 8 * qr_tblk_elems(nA, nA)));
   // tall orientation A_tall (mA x nA, column-major): M itself when m >= n,
   // else M^T.  A row-major M is the column-major M^T.
   const bool need_t = a_row_major ? !st->transposed : st->transposed;
@@ -452,9 +518,32 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
   double *norms = take<double>(ctx, nA);
   double *partial = take<double>(ctx, kSumSqBlocks + 1);
   unsigned long long *rot = take<unsigned long long>(ctx, 64);
+  static const bool debug = getenv("FTT_DEBUG") != nullptr;
+  cudaEvent_t dbg_ev[3];
+  if (debug) {
+    for (auto &e : dbg_ev) cudaEventCreate(&e);
+    cudaEventRecord(dbg_ev[0], ctx->stream);
+  }
   FTT_CHECK(qr_factor(ctx, mA, nA, st->Af, mA, st->tau, st->Tb, ws, wse));
-  k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->Y);
-  FTT_LAUNCHED(ctx);
+  if (debug) cudaEventRecord(dbg_ev[1], ctx->stream);
+  // Preconditioning: one more QR, R^T = Q2 R2, and Jacobi on X = R2^T
+  // (each QR step moves the factor towards diagonal dominance; measured in
+  // emulation ~3 fewer sweeps, for (4/3) nA^3 flops ~ 1/9 of a sweep).
+  // Then A = (Q Yhat) Sigma (Q2 P)^T with Yhat = Y / sigma.
+  {
+    static const char *pc = getenv("FTT_PRECOND");
+    st->precond = nA > 1 && !(pc && pc[0] == '0');
+  }
+  if (st->precond) {
+    k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->B);
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(qr_factor(ctx, nA, nA, st->B, nA, st->tau2, st->Tb2, ws, wse));
+    k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->B, nA, st->Y);
+    FTT_LAUNCHED(ctx);
+  } else {
+    k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->Y);
+    FTT_LAUNCHED(ctx);
+  }
   FTT_CHECK(launch_identity(ctx, nA, nA, st->P, nA));
   if (nA > 1) {
     int nblk = (int)ceil_div(nA, JB);
@@ -500,6 +589,16 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
       return FTT_ERR_NOCONV;
     }
   }
+  if (debug) {
+    cudaEventRecord(dbg_ev[2], ctx->stream);
+    cudaEventSynchronize(dbg_ev[2]);
+    float qr_ms = 0, jac_ms = 0;
+    cudaEventElapsedTime(&qr_ms, dbg_ev[0], dbg_ev[1]);
+    cudaEventElapsedTime(&jac_ms, dbg_ev[1], dbg_ev[2]);
+    fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld) qr %.3f ms jacobi %.3f ms sweeps %d\n",
+            (long long)m, (long long)n, (long long)mA, (long long)nA, qr_ms, jac_ms, st->sweeps);
+    for (auto &e : dbg_ev) cudaEventDestroy(e);
+  }
   k_col_norms<<<(unsigned)nA, 256, 0, ctx->stream>>>(nA, nA, st->Y, nA, norms);
   FTT_LAUNCHED(ctx);
   std::vector<double> raw(nA);
@@ -542,13 +641,24 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
   FTT_CUDA(cudaMemcpyAsync(sel, st->perm.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
   FTT_CUDA(cudaMemcpyAsync(inv, hinv.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
   FTT_CUDA(cudaMemcpyAsync(sig, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
-  // V_A = Y[:, sel] / sigma ;  U_A = Q [P[:, sel]; 0]
-  k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA, sel,
-                                                                      inv, VA, nA);
-  FTT_LAUNCHED(ctx);
-  k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, nA, rank, st->P, nA, sel,
-                                                                      nullptr, UA, mA);
-  FTT_LAUNCHED(ctx);
+  if (st->precond) {
+    // preconditioned form: U_A = Q [Y[:, sel] / sigma; 0],  V_A = Q2 P[:, sel]
+    k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, nA, rank, st->Y, nA,
+                                                                        sel, inv, UA, mA);
+    FTT_LAUNCHED(ctx);
+    k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->P, nA,
+                                                                        sel, nullptr, VA, nA);
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(qr_apply_q(ctx, nA, nA, st->B, nA, st->Tb2, rank, VA, nA, ws, wse));
+  } else {
+    // V_A = Y[:, sel] / sigma ;  U_A = Q [P[:, sel]; 0]
+    k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA,
+                                                                        sel, inv, VA, nA);
+    FTT_LAUNCHED(ctx);
+    k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, nA, rank, st->P, nA,
+                                                                        sel, nullptr, UA, mA);
+    FTT_LAUNCHED(ctx);
+  }
   FTT_CHECK(qr_apply_q(ctx, mA, nA, st->Af, mA, st->Tb, rank, UA, mA, ws, wse));
   double *UM = st->transposed ? VA : UA;
   double *VM = st->transposed ? UA : VA;
