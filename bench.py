@@ -173,6 +173,25 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ replicas
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank float over the process group (identity when not
+    distributed). NCCL on the GPU box, gloo in the CPU tests."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(world: int, units_per_rank_step: int, steps: int, max_ms: float) -> float:
+    """Units all ranks processed / max-over-ranks time (weak scaling)."""
+    return world * units_per_rank_step * steps / (max_ms * 1e-3)
+
+
 # ------------------------------------------------------------------ GPU arm
 def flush_l2(buf):
     buf.fill_(1.0)  # 256 MiB > 126 MB L2
@@ -261,12 +280,8 @@ def run_ours(args):
                                        nat.ctypes.byref(by), nat.ctypes.byref(fl)), "profile_read")
         prof[tag] = {"ms": ms.value, "launches": int(n.value), "bytes": by.value, "flops": fl.value}
     nat.check(lib.ftt_profile_enable(ctx, 0), "profile")
-    total_ms = sum(times)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * nnz * args.steps / (total_ms * 1e-3)
+    total_ms = max_over_ranks(sum(times), device="cuda")
+    value = whole_job_rate(world, nnz, args.steps, total_ms)
 
     # ---------------- e2e through the public API (host buffers)
     e2e = None
@@ -289,12 +304,8 @@ def run_ours(args):
             torch.cuda.synchronize()
             e_times.append(e0.elapsed_time(e1))
             d2h = sum(c.nbytes for c in tt.cores)
-        e_ms = sum(e_times)
-        if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e2e = {"value": world * nnz * args.steps / (e_ms * 1e-3), "unit": UNIT,
+        e_ms = max_over_ranks(sum(e_times), device="cuda")
+        e2e = {"value": whole_job_rate(world, nnz, args.steps, e_ms), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e_ms / args.steps}
         a.device_arrays()

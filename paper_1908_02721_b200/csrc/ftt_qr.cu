@@ -27,6 +27,23 @@ constexpr int PT = 256;
 constexpr int PW = PT / 32;
 constexpr int PSLOTS = 34;  // alpha-row (32) + xx + spare
 
+// 32 per-lane accumulators -> lane l receives the warp-wide sum of slot l,
+// in 31 shuffles (halving exchange: at offset s each lane keeps the upper or
+// lower s slots by bit s of its lane id and adds the partner's copy).
+__device__ __forceinline__ double warp_reduce_scatter32(double (&acc)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      const double send = upper ? acc[j] : acc[j + s];
+      const double keep = upper ? acc[j + s] : acc[j];
+      acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return acc[0];
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
@@ -62,13 +79,7 @@ __global__ void __launch_bounds__(PT) k_panel(int64_t mp, int jb, double *__rest
       for (int j = 0; j < 32; ++j)
         if (j < nj) acc[j] += x * colc[i + (int64_t)j * lda];
     }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < nj) {
-        double v = warp_sum(acc[j]);
-        if (lane == 0) s_red[warp][j] = v;
-      }
-    }
+    s_red[warp][lane] = warp_reduce_scatter32(acc, lane);  // lane j <- warp total of slot j
     __syncthreads();
     if (tid < nj) {
       double t = 0.0;
@@ -313,13 +324,7 @@ __global__ void __launch_bounds__(PT) k_panel_res(int64_t mp, int jb, double *__
       for (int j = 0; j < 32; ++j)
         if (j < nj) acc[j] += x * colc[li + (int64_t)j * ld];
     }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < nj) {
-        double v = warp_sum(acc[j]);
-        if (lane == 0) s_red[warp][j] = v;
-      }
-    }
+    s_red[warp][lane] = warp_reduce_scatter32(acc, lane);  // lane j <- warp total of slot j
     __syncthreads();
     const bool owner = c >= r0 && c < r1;
     if (tid < nj) {
@@ -346,6 +351,7 @@ __global__ void __launch_bounds__(PT) k_panel_res(int64_t mp, int jb, double *__
       // computes bit-identical scalars
       double t = 0.0;
       if (lane < nj) {
+#pragma unroll 4
         for (int q = warp; q < nb; q += PW) {
           if (MODE == 0) {
             const double *rp = cg::this_cluster().map_shared_rank(&s_part[buf][0], q);

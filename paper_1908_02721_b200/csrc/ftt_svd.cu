@@ -135,9 +135,21 @@ struct JacSmem {
   unsigned char tp[JP - 1][16], tq[JP - 1][16];  // inner round-robin pairing table
 };
 
+// Exact work skipping (track != nullptr): last_mod[b] = global step at which
+// block b was last rotated, last_ok[a*nblk+b] = global step at which pair
+// (a, b) last passed the fresh convergence test.  If neither block changed
+// since that test, recomputing its Gram would reproduce the same data and
+// the same "no rotation" outcome, so the pair is skipped without reading X.
+struct JacTrack {
+  int *last_mod;
+  int *last_ok;
+  int t;  // global step index (sweep * (nblk - 1) + step)
+};
+
 __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restrict__ P, int64_t ld,
                             int nblk, int step, int pc, double tol, double floor,
-                            unsigned long long *__restrict__ rotated, JacSmem &sm) {
+                            unsigned long long *__restrict__ rotated, JacSmem &sm,
+                            const JacTrack *track = nullptr) {
   auto &G = sm.G;
   auto &Z = sm.Z;
   auto &S = sm.S;
@@ -153,6 +165,15 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
   __syncthreads();  // the previous pair of this CTA is done with sm
   int ba, bb;
   pair_of(nblk, step, pc, &ba, &bb);
+  const int pidx = min(ba, bb) * nblk + max(ba, bb);
+  if (track) {
+    int skip = 0;
+    if (tid == 0) {
+      const int ok = __ldcg(track->last_ok + pidx);
+      skip = ok > __ldcg(track->last_mod + ba) && ok > __ldcg(track->last_mod + bb);
+    }
+    if (__syncthreads_or(skip)) return;
+  }
   for (int e = tid; e < (JP - 1) * 16; e += JT) {
     int p, q;
     pair_of(JP, e / 16, e % 16, &p, &q);
@@ -215,7 +236,14 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
       if (dii > floor && djj > floor && fabs(gij) > tol * sqrt(dii * djj)) need = 1;
     }
   }
-  if (!__syncthreads_or(need)) return;
+  if (!__syncthreads_or(need)) {
+    if (track && tid == 0) track->last_ok[pidx] = track->t;
+    return;
+  }
+  if (track && tid == 0) {
+    track->last_mod[ba] = track->t;
+    track->last_mod[bb] = track->t;
+  }
   // ---- cyclic two-sided Jacobi on G (parallel: 16 disjoint pairs per round)
   for (int sw = 0; sw < MAX_INNER; ++sw) {
     int sweep_any = 0;
@@ -361,14 +389,17 @@ __global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, double *__r
                                                           int nblk, double tol, double floor,
                                                           int max_sweeps,
                                                           unsigned long long *__restrict__ counters,
-                                                          int *__restrict__ status) {
+                                                          int *__restrict__ status,
+                                                          int *__restrict__ last_mod,
+                                                          int *__restrict__ last_ok) {
   __shared__ JacSmem sm;
   cg::grid_group grid = cg::this_grid();
   const int npairs = nblk / 2;
   for (int sw = 0; sw < max_sweeps; ++sw) {
     for (int step = 0; step < nblk - 1; ++step) {
+      const JacTrack track{last_mod, last_ok, sw * (nblk - 1) + step};
       for (int pc = blockIdx.x; pc < npairs; pc += gridDim.x)
-        jacobi_pair(n, X, P, ld, nblk, step, pc, tol, floor, counters + sw, sm);
+        jacobi_pair(n, X, P, ld, nblk, step, pc, tol, floor, counters + sw, sm, &track);
       grid.sync();
     }
     const unsigned long long rot = *((volatile unsigned long long *)(counters + sw));
@@ -512,12 +543,15 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     FTT_CHECK(transpose(ctx, nA, mA, A, lda, st->Af, mA));
   }
   size_t wse = qr_workspace_elems(mA, nA);
+  const int64_t nblk_max = ceil_div(nA, JB) + 1;
   FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)nA) +
-                                   align_up(8 * (kSumSqBlocks + 1)) + 4096));
+                                   align_up(8 * (kSumSqBlocks + 1)) +
+                                   align_up(4 * nblk_max * (nblk_max + 1)) + 4096));
   double *ws = take<double>(ctx, wse);
   double *norms = take<double>(ctx, nA);
   double *partial = take<double>(ctx, kSumSqBlocks + 1);
   unsigned long long *rot = take<unsigned long long>(ctx, 64);
+  int *track_buf = take<int>(ctx, nblk_max * (nblk_max + 1));
   static const bool debug = getenv("FTT_DEBUG") != nullptr;
   cudaEvent_t dbg_ev[3];
   if (debug) {
@@ -532,7 +566,7 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
   // Then A = (Q Yhat) Sigma (Q2 P)^T with Yhat = Y / sigma.
   {
     static const char *pc = getenv("FTT_PRECOND");
-    st->precond = nA > 1 && !(pc && pc[0] == '0');
+    st->precond = nA > 1 && pc && pc[0] == '1';  // off by default: measured more sweeps on c3
   }
   if (st->precond) {
     k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->B);
@@ -548,7 +582,11 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
   if (nA > 1) {
     int nblk = (int)ceil_div(nA, JB);
     if (nblk & 1) ++nblk;
-    const double tol = 2.220446049250313e-16 * sqrt((double)nA);
+    // relative orthogonality target; the computed fresh dot products carry
+    // ~sqrt(n) eps relative rounding, so a target at that level keeps pairs
+    // rotating on noise -- FTT_JTOL scales it (tuning knob, default 1)
+    static const double jtol_scale = getenv("FTT_JTOL") ? atof(getenv("FTT_JTOL")) : 1.0;
+    const double tol = jtol_scale * 2.220446049250313e-16 * sqrt((double)nA);
     // noise floor: columns with |x|^2 <= (0.1 eps)^2 * nA * ||X||_F^2 are
     // below the backward error of the QR and are not orthogonalised further
     double fro2 = 0.0;
@@ -570,7 +608,12 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     int maxsw = max_sweeps;
     unsigned long long *cnt = rot;
     int *status = reinterpret_cast<int *>(rot + max_sweeps);
-    void *args[] = {&nA_, &Y, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &cnt, &status};
+    // last_mod[nblk] = -1 (0xff bytes), last_ok[nblk*nblk] = -1: nothing verified yet
+    int *last_mod = track_buf;
+    int *last_ok = track_buf + nblk;
+    FTT_CUDA(cudaMemsetAsync(track_buf, 0xff, sizeof(int) * (size_t)nblk * (nblk + 1), ctx->stream));
+    void *args[] = {&nA_, &Y, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &cnt, &status,
+                    &last_mod, &last_ok};
     const int pb = prof_begin(ctx);
     FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_persistent, dim3(G), dim3(JT), args,
                                          0, ctx->stream));
@@ -595,8 +638,15 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     float qr_ms = 0, jac_ms = 0;
     cudaEventElapsedTime(&qr_ms, dbg_ev[0], dbg_ev[1]);
     cudaEventElapsedTime(&jac_ms, dbg_ev[1], dbg_ev[2]);
-    fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld) qr %.3f ms jacobi %.3f ms sweeps %d\n",
+    fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld) qr %.3f ms jacobi %.3f ms sweeps %d",
             (long long)m, (long long)n, (long long)mA, (long long)nA, qr_ms, jac_ms, st->sweeps);
+    if (st->sweeps > 0) {
+      std::vector<unsigned long long> cnt(st->sweeps);
+      cudaMemcpy(cnt.data(), rot, 8 * st->sweeps, cudaMemcpyDeviceToHost);
+      fprintf(stderr, " rotated pairs/sweep:");
+      for (auto c : cnt) fprintf(stderr, " %llu", c);
+    }
+    fprintf(stderr, "\n");
     for (auto &e : dbg_ev) cudaEventDestroy(e);
   }
   k_col_norms<<<(unsigned)nA, 256, 0, ctx->stream>>>(nA, nA, st->Y, nA, norms);
