@@ -183,6 +183,23 @@ int ftt_qr_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
  * Factors stay in the context for phase 2.  A is not modified. */
 int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
                 int64_t lda, int32_t a_row_major, double *s_host);
+/* Certified low-rank phase 1 (an accelerator for svd_truncate_delta on
+ * numerically low-rank operands): A_tall ~= Q B with Q = orth(A_tall Omega)
+ * for a deterministic k-column test matrix Omega, B = Q^T A_tall, and the
+ * residual R = A_tall - Q B formed explicitly.  rest2_host = ||R||_F^2.
+ * Accepted when rest2 <= min(max(1e-8 delta2, nA eps^2 ||A||_F^2),
+ * 1e-6 delta2), i.e. below the rounding noise a full backward-stable SVD
+ * (the reference's gesdd) already has in its tail sums: then the k singular
+ * values of B go to s_host, *accepted = 1, and phase 2 (ftt_svd_vectors)
+ * returns Q U_B / V_B.  Since sigma_i(A)^2 - sigma_i(B)^2 <= ||R||_2^2 and
+ * the discarded tail is sum_{i>j} sigma_i(B)^2 + rest2 up to that error,
+ * the tail rule of linalg.py:97-99 decides the same rank as a full SVD
+ * except within ~rank*rest2 of a tie.  Otherwise *accepted = 0 and the
+ * caller runs ftt_svd_f64.  delta2 = delta^2 of the truncation step. */
+int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
+                        int64_t lda, int32_t a_row_major, int64_t k,
+                        double delta2, double *s_host, double *rest2_host,
+                        int32_t *accepted);
 /* Phase 2: the leading `rank` singular triplets of the last ftt_svd_f64, with
  * the sign convention of _fix_signs (linalg.py:56-63) applied to U: U (m x
  * rank) and V (n x rank, i.e. vt.T), each column- or row-major per its flag;

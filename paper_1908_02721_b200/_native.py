@@ -61,6 +61,8 @@ SIGNATURES = {
     "ftt_transpose": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64],
     "ftt_qr_f64": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64],
     "ftt_svd_f64": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i32, _P_d],
+    "ftt_svd_lowrank_f64": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i32, _c_i64, _c_d, _P_d, _P_d,
+                            ctypes.POINTER(ctypes.c_int32)],
     "ftt_svd_vectors": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_i32, _c_i32],
     "ftt_dot": [_c_p, _c_i64, _c_p, _c_p, _P_d],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],

@@ -46,22 +46,17 @@ struct SvdState {
   std::vector<int64_t> perm;  // sorted position -> column of Y
   int sweeps = 0;
   bool precond = false;  // Jacobi ran on R2^T (QR of R^T) instead of R^T
+  bool direct = false;   // Jacobi ran on A_tall itself (Y aliases Af)
+  // low-rank path (ftt_svd_lowrank_f64): A_tall ~= Qk Bk with a certified
+  // residual; the SVD of the small Bk lives in `inner`
+  bool lowrank = false;
+  double *Qk = nullptr;  // mA x k orthonormal range basis
+  double *Bk = nullptr;  // k x nA
+  SvdState *inner = nullptr;
 };
 
-void svd_state_free(ftt_ctx *ctx) {
-  if (!ctx->svd) return;
-  SvdState *s = ctx->svd;
-  owned_free(ctx, s->Af);
-  owned_free(ctx, s->tau);
-  owned_free(ctx, s->Tb);
-  owned_free(ctx, s->Y);
-  owned_free(ctx, s->P);
-  owned_free(ctx, s->B);
-  owned_free(ctx, s->tau2);
-  owned_free(ctx, s->Tb2);
-  delete s;
-  ctx->svd = nullptr;
-}
+void svd_state_free(ftt_ctx *ctx);
+void svd_state_release(ftt_ctx *ctx, SvdState *s);
 
 namespace {
 
@@ -146,7 +141,9 @@ struct JacTrack {
   int t;  // global step index (sweep * (nblk - 1) + step)
 };
 
-__device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restrict__ P, int64_t ld,
+// n columns; X is mX x n (ld ldx), P is n x n (ld ldp).
+__device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64_t ldx,
+                            double *__restrict__ P, int64_t ldp,
                             int nblk, int step, int pc, double tol, double floor,
                             unsigned long long *__restrict__ rotated, JacSmem &sm,
                             const JacTrack *track = nullptr) {
@@ -194,11 +191,11 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
   {
     double gacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     double pre[LPT];
-    chunk_load(pre, X, 0, n, ld, col, tid);
-    for (int64_t r0 = 0; r0 < n; r0 += CH) {
+    chunk_load(pre, X, 0, mX, ldx, col, tid);
+    for (int64_t r0 = 0; r0 < mX; r0 += CH) {
       chunk_store(pre, S, tid);
       __syncthreads();
-      if (r0 + CH < n) chunk_load(pre, X, r0 + CH, n, ld, col, tid);  // in flight during the MMAs
+      if (r0 + CH < mX) chunk_load(pre, X, r0 + CH, mX, ldx, col, tid);  // in flight during the MMAs
 #pragma unroll 4
       for (int k0 = 0; k0 < CH; k0 += 4) {
 #pragma unroll
@@ -340,12 +337,14 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
     for (int ks = 0; ks < 8; ++ks) bz[j][ks] = Z[ks * 4 + (lane & 3)][j * 8 + (lane >> 2)];
   for (int mat = 0; mat < 2; ++mat) {
     double *M = mat == 0 ? X : P;
+    const int64_t rows = mat == 0 ? mX : n;
+    const int64_t ld = mat == 0 ? ldx : ldp;
     double pre[LPT];
-    chunk_load(pre, M, 0, n, ld, col, tid);
-    for (int64_t r0 = 0; r0 < n; r0 += CH) {
+    chunk_load(pre, M, 0, rows, ld, col, tid);
+    for (int64_t r0 = 0; r0 < rows; r0 += CH) {
       chunk_store(pre, S, tid);
       __syncthreads();
-      if (r0 + CH < n) chunk_load(pre, M, r0 + CH, n, ld, col, tid);
+      if (r0 + CH < rows) chunk_load(pre, M, r0 + CH, rows, ld, col, tid);
       double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
@@ -364,7 +363,7 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
         int c = e / CH, r = e % CH;
         int64_t row = r0 + r;
         int cc = col[c];
-        if (cc >= 0 && row < n) M[row + (int64_t)cc * ld] = S[r][c];
+        if (cc >= 0 && row < rows) M[row + (int64_t)cc * ld] = S[r][c];
       }
       __syncthreads();
     }
@@ -372,20 +371,14 @@ __device__ void jacobi_pair(int64_t n, double *__restrict__ X, double *__restric
 }
 
 
-__global__ void __launch_bounds__(JT) k_jacobi_step(int64_t n, double *__restrict__ X,
-                                                    double *__restrict__ P, int64_t ld, int nblk,
-                                                    int step, double tol, double floor,
-                                                    unsigned long long *__restrict__ rotated) {
-  __shared__ JacSmem sm;
-  jacobi_pair(n, X, P, ld, nblk, step, blockIdx.x, tol, floor, rotated, sm);
-}
-
 // Whole Jacobi iteration in one cooperative launch: sweeps x steps x pairs
 // with a grid barrier between steps; the sweep's rotation count decides
 // convergence on the device (no host round trip per sweep).  counters
 // [max_sweeps] must be zero; status[0] receives the sweeps used (or -1).
-__global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, double *__restrict__ X,
-                                                          double *__restrict__ P, int64_t ld,
+// X is mX x n (ld ldx), P is n x n (ld ldp).
+__global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, int64_t mX,
+                                                          double *__restrict__ X, int64_t ldx,
+                                                          double *__restrict__ P, int64_t ldp,
                                                           int nblk, double tol, double floor,
                                                           int max_sweeps,
                                                           unsigned long long *__restrict__ counters,
@@ -399,7 +392,7 @@ __global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, double *__r
     for (int step = 0; step < nblk - 1; ++step) {
       const JacTrack track{last_mod, last_ok, sw * (nblk - 1) + step};
       for (int pc = blockIdx.x; pc < npairs; pc += gridDim.x)
-        jacobi_pair(n, X, P, ld, nblk, step, pc, tol, floor, counters + sw, sm, &track);
+        jacobi_pair(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, &track);
       grid.sync();
     }
     const unsigned long long rot = *((volatile unsigned long long *)(counters + sw));
@@ -501,14 +494,51 @@ __global__ void k_fix_signs(int64_t mu, int64_t mv, double *__restrict__ U, int6
 
 }  // namespace ftt
 
-using namespace ftt;
+namespace ftt {
+namespace {
 
-extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
-                           int32_t a_row_major, double *s_host) {
-  if (!ctx || m < 0 || n < 0) return FTT_ERR_INVALID;
-  svd_state_free(ctx);
-  SvdState *st = new SvdState();
-  ctx->svd = st;
+// Deterministic test matrix for the low-rank range finder: splitmix64 of the
+// element index, mapped to [-1, 1).
+__global__ void k_omega(int64_t total, double *__restrict__ O) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)t + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    O[t] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
+}
+
+}  // namespace
+
+void svd_state_release(ftt_ctx *ctx, SvdState *s) {
+  if (!s) return;
+  owned_free(ctx, s->Af);
+  owned_free(ctx, s->tau);
+  owned_free(ctx, s->Tb);
+  if (!s->direct) owned_free(ctx, s->Y);
+  owned_free(ctx, s->P);
+  owned_free(ctx, s->B);
+  owned_free(ctx, s->tau2);
+  owned_free(ctx, s->Tb2);
+  owned_free(ctx, s->Qk);
+  owned_free(ctx, s->Bk);
+  svd_state_release(ctx, s->inner);
+  delete s;
+}
+
+void svd_state_free(ftt_ctx *ctx) {
+  if (!ctx->svd) return;
+  svd_state_release(ctx, ctx->svd);
+  ctx->svd = nullptr;
+}
+
+namespace {
+
+// Phase 1 (QR + Jacobi) on a given state; see the file header.
+int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A, int64_t lda,
+               int32_t a_row_major) {
   st->m = m;
   st->n = n;
   st->transposed = m < n;
@@ -529,11 +559,25 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->tau, 8 * (size_t)nA));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb, 8 * qr_tblk_elems(mA, nA)));
-  FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
+  // Direct mode (opt-in, FTT_DIRECT=1): one-sided Jacobi on A_tall itself
+  // for nearly square operands.  Measured slower on the low-rank operands of
+  // the BASELINE configs (the QR concentrates the rank into a few rows of R,
+  // so most columns of R^T start near the noise floor), hence off by default.
+  {
+    static const char *dm = getenv("FTT_DIRECT");
+    st->direct = dm && dm[0] == '1' && nA > 1 && mA <= 3 * nA;
+  }
+  {
+    static const char *pc = getenv("FTT_PRECOND");
+    st->precond = !st->direct && nA > 1 && pc && pc[0] == '1';  // off by default
+  }
+  if (!st->direct) FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->P, 8 * (size_t)nA * nA));
-  FTT_CHECK(owned_alloc(ctx, (void **)&st->B, 8 * (size_t)nA * nA));
-  FTT_CHECK(owned_alloc(ctx, (void **)&st->tau2, 8 * (size_t)nA));
-  FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb2, 8 * qr_tblk_elems(nA, nA)));
+  if (st->precond) {
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->B, 8 * (size_t)nA * nA));
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->tau2, 8 * (size_t)nA));
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb2, 8 * qr_tblk_elems(nA, nA)));
+  }
   // tall orientation A_tall (mA x nA, column-major): M itself when m >= n,
   // else M^T.  A row-major M is the column-major M^T.
   const bool need_t = a_row_major ? !st->transposed : st->transposed;
@@ -558,17 +602,12 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     for (auto &e : dbg_ev) cudaEventCreate(&e);
     cudaEventRecord(dbg_ev[0], ctx->stream);
   }
-  FTT_CHECK(qr_factor(ctx, mA, nA, st->Af, mA, st->tau, st->Tb, ws, wse));
+  if (!st->direct) FTT_CHECK(qr_factor(ctx, mA, nA, st->Af, mA, st->tau, st->Tb, ws, wse));
   if (debug) cudaEventRecord(dbg_ev[1], ctx->stream);
-  // Preconditioning: one more QR, R^T = Q2 R2, and Jacobi on X = R2^T
-  // (each QR step moves the factor towards diagonal dominance; measured in
-  // emulation ~3 fewer sweeps, for (4/3) nA^3 flops ~ 1/9 of a sweep).
-  // Then A = (Q Yhat) Sigma (Q2 P)^T with Yhat = Y / sigma.
-  {
-    static const char *pc = getenv("FTT_PRECOND");
-    st->precond = nA > 1 && pc && pc[0] == '1';  // off by default: measured more sweeps on c3
-  }
-  if (st->precond) {
+  if (st->direct) {
+    st->Y = st->Af;  // Jacobi on A_tall (mA x nA) in place
+  } else if (st->precond) {
+    // R^T = Q2 R2, Jacobi on X = R2^T; A = (Q Yhat) Sigma (Q2 P)^T
     k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->B);
     FTT_LAUNCHED(ctx);
     FTT_CHECK(qr_factor(ctx, nA, nA, st->B, nA, st->tau2, st->Tb2, ws, wse));
@@ -579,19 +618,19 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     FTT_LAUNCHED(ctx);
   }
   FTT_CHECK(launch_identity(ctx, nA, nA, st->P, nA));
+  const int64_t mX = st->direct ? mA : nA;
   if (nA > 1) {
     int nblk = (int)ceil_div(nA, JB);
     if (nblk & 1) ++nblk;
-    // relative orthogonality target; the computed fresh dot products carry
-    // ~sqrt(n) eps relative rounding, so a target at that level keeps pairs
-    // rotating on noise -- FTT_JTOL scales it (tuning knob, default 1)
+    // relative orthogonality target sqrt(n) eps (LAPACK dgesvj's);
+    // FTT_JTOL scales it (measured: no effect on sweep counts up to 16x)
     static const double jtol_scale = getenv("FTT_JTOL") ? atof(getenv("FTT_JTOL")) : 1.0;
     const double tol = jtol_scale * 2.220446049250313e-16 * sqrt((double)nA);
-    // noise floor: columns with |x|^2 <= (0.1 eps)^2 * nA * ||X||_F^2 are
+    // noise floor: columns with |x|^2 <= (0.1 eps)^2 * rows * ||X||_F^2 are
     // below the backward error of the QR and are not orthogonalised further
     double fro2 = 0.0;
-    FTT_CHECK(sum_squares(ctx, nA * nA, st->Y, partial, &fro2));
-    const double floor = 0.01 * 2.220446049250313e-16 * 2.220446049250313e-16 * (double)nA * fro2;
+    FTT_CHECK(sum_squares(ctx, mX * nA, st->Y, partial, &fro2));
+    const double floor = 0.01 * 2.220446049250313e-16 * 2.220446049250313e-16 * (double)mX * fro2;
     const int max_sweeps = 60;
     FTT_CUDA(cudaMemsetAsync(rot, 0, sizeof(unsigned long long) * 64, ctx->stream));
     static int coresident = 0;
@@ -601,7 +640,7 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
       coresident = std::max(1, per_sm) * ctx->num_sms;
     }
     int G = std::min(nblk / 2, coresident);
-    int64_t nA_ = nA;
+    int64_t nA_ = nA, mX_ = mX;
     double *Y = st->Y, *Pm = st->P;
     int nblk_ = nblk;
     double tol_ = tol, floor_ = floor;
@@ -612,20 +651,19 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     int *last_mod = track_buf;
     int *last_ok = track_buf + nblk;
     FTT_CUDA(cudaMemsetAsync(track_buf, 0xff, sizeof(int) * (size_t)nblk * (nblk + 1), ctx->stream));
-    void *args[] = {&nA_, &Y, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &cnt, &status,
-                    &last_mod, &last_ok};
+    void *args[] = {&nA_, &mX_, &Y, &mX_, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &cnt,
+                    &status, &last_mod, &last_ok};
     const int pb = prof_begin(ctx);
     FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_persistent, dim3(G), dim3(JT), args,
                                          0, ctx->stream));
     FTT_LAUNCHED(ctx);
     int sw_used = 0;
     FTT_CHECK(copy_to_host(ctx, &sw_used, status, sizeof(int)));
-    // per sweep: every block pair forms its 32x32 Gram (2*32*32*nA flops)
-    // and applies the rotation to X and P (2 x 2*32*32*nA); X and P are
-    // read (and written) once per step
+    // per sweep and step: every block pair forms its 32x32 Gram from X
+    // (2*32^2*mX flops) and applies the rotation to X and P (2*32^2*(mX+n))
     const double sweeps_d = sw_used > 0 ? sw_used : max_sweeps;
-    prof_end(ctx, pb, PT_JACOBI, sweeps_d * (nblk - 1) * 4.0 * 8.0 * nA * nA,
-             sweeps_d * (nblk - 1) * (nblk / 2) * 6.0 * JP * JP * (double)nA);
+    prof_end(ctx, pb, PT_JACOBI, sweeps_d * (nblk - 1) * 8.0 * (3.0 * mX + 2.0 * nA) * nA,
+             sweeps_d * (nblk - 1) * (nblk / 2) * 2.0 * JP * JP * (2.0 * mX + (double)nA));
     st->sweeps = sw_used;
     if (sw_used < 0) {
       set_error("Jacobi SVD did not converge in %d sweeps", max_sweeps);
@@ -638,8 +676,9 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     float qr_ms = 0, jac_ms = 0;
     cudaEventElapsedTime(&qr_ms, dbg_ev[0], dbg_ev[1]);
     cudaEventElapsedTime(&jac_ms, dbg_ev[1], dbg_ev[2]);
-    fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld) qr %.3f ms jacobi %.3f ms sweeps %d",
-            (long long)m, (long long)n, (long long)mA, (long long)nA, qr_ms, jac_ms, st->sweeps);
+    fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld%s) qr %.3f ms jacobi %.3f ms sweeps %d",
+            (long long)m, (long long)n, (long long)mA, (long long)nA, st->direct ? " direct" : "",
+            qr_ms, jac_ms, st->sweeps);
     if (st->sweeps > 0) {
       std::vector<unsigned long long> cnt(st->sweeps);
       cudaMemcpy(cnt.data(), rot, 8 * st->sweeps, cudaMemcpyDeviceToHost);
@@ -649,7 +688,7 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
     fprintf(stderr, "\n");
     for (auto &e : dbg_ev) cudaEventDestroy(e);
   }
-  k_col_norms<<<(unsigned)nA, 256, 0, ctx->stream>>>(nA, nA, st->Y, nA, norms);
+  k_col_norms<<<(unsigned)nA, 256, 0, ctx->stream>>>(mX, nA, st->Y, mX, norms);
   FTT_LAUNCHED(ctx);
   std::vector<double> raw(nA);
   FTT_CHECK(copy_to_host(ctx, raw.data(), norms, 8 * nA));
@@ -659,40 +698,33 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
                    [&](int64_t a, int64_t b) { return raw[a] > raw[b]; });
   st->sigma.resize(nA);
   for (int64_t i = 0; i < nA; ++i) st->sigma[i] = raw[st->perm[i]];
-  if (s_host) memcpy(s_host, st->sigma.data(), 8 * nA);
   return FTT_OK;
 }
 
-extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ldu,
-                               int32_t u_row_major, double *V, int64_t ldv, int32_t v_row_major,
-                               int32_t scale_v) {
-  if (!ctx || !ctx->svd) {
-    set_error("ftt_svd_vectors: no factorization in this context");
-    return FTT_ERR_INVALID;
-  }
-  SvdState *st = ctx->svd;
+// The leading `rank` triplets of a full (non-low-rank) state in its tall
+// orientation: UA (mA x rank), VA (nA x rank), column-major, unscaled and
+// without the sign rule.
+int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double *VA) {
   const int64_t mA = st->mA, nA = st->nA;
-  if (rank < 0 || rank > nA) {
-    set_error("rank %lld out of range", (long long)rank);
-    return FTT_ERR_INVALID;
-  }
-  if (rank == 0) return FTT_OK;
   size_t wse = qr_apply_workspace_elems(mA, nA, rank);
-  FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)mA * rank) +
-                                   align_up(8 * (size_t)nA * rank) + 3 * align_up(8 * rank) + 4096));
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + 2 * align_up(8 * rank) + 4096));
   double *ws = take<double>(ctx, wse);
-  double *UA = take<double>(ctx, (size_t)mA * rank);
-  double *VA = take<double>(ctx, (size_t)nA * rank);
   int64_t *sel = take<int64_t>(ctx, rank);
   double *inv = take<double>(ctx, rank);
-  double *sig = take<double>(ctx, rank);
   std::vector<double> hinv(rank);
   for (int64_t j = 0; j < rank; ++j) hinv[j] = st->sigma[j] != 0.0 ? 1.0 / st->sigma[j] : 0.0;
   FTT_CUDA(cudaMemcpyAsync(sel, st->perm.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
   FTT_CUDA(cudaMemcpyAsync(inv, hinv.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
-  FTT_CUDA(cudaMemcpyAsync(sig, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
-  if (st->precond) {
-    // preconditioned form: U_A = Q [Y[:, sel] / sigma; 0],  V_A = Q2 P[:, sel]
+  if (st->direct) {
+    // U_A = Y[:, sel] / sigma (Y = A P, mA x nA),  V_A = P[:, sel]
+    k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, mA, rank, st->Y, mA,
+                                                                        sel, inv, UA, mA);
+    FTT_LAUNCHED(ctx);
+    k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->P, nA,
+                                                                        sel, nullptr, VA, nA);
+    FTT_LAUNCHED(ctx);
+  } else if (st->precond) {
+    // U_A = Q [Y[:, sel] / sigma; 0],  V_A = Q2 P[:, sel]
     k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, nA, rank, st->Y, nA,
                                                                         sel, inv, UA, mA);
     FTT_LAUNCHED(ctx);
@@ -709,7 +741,156 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
                                                                         sel, nullptr, UA, mA);
     FTT_LAUNCHED(ctx);
   }
-  FTT_CHECK(qr_apply_q(ctx, mA, nA, st->Af, mA, st->Tb, rank, UA, mA, ws, wse));
+  if (!st->direct) FTT_CHECK(qr_apply_q(ctx, mA, nA, st->Af, mA, st->Tb, rank, UA, mA, ws, wse));
+  // the host vectors above must outlive the async copies
+  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FTT_OK;
+}
+
+}  // namespace
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
+                           int32_t a_row_major, double *s_host) {
+  if (!ctx || m < 0 || n < 0) return FTT_ERR_INVALID;
+  svd_state_free(ctx);
+  SvdState *st = new SvdState();
+  ctx->svd = st;
+  FTT_CHECK(svd_factor(ctx, st, m, n, A, lda, a_row_major));
+  if (s_host && st->nA) memcpy(s_host, st->sigma.data(), 8 * st->nA);
+  return FTT_OK;
+}
+
+extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
+                                   int64_t lda, int32_t a_row_major, int64_t k, double delta2,
+                                   double *s_host, double *rest2_host, int32_t *accepted) {
+  if (!ctx || m < 0 || n < 0 || !accepted || !rest2_host) return FTT_ERR_INVALID;
+  svd_state_free(ctx);
+  SvdState *st = new SvdState();
+  ctx->svd = st;
+  st->lowrank = true;
+  st->m = m;
+  st->n = n;
+  st->transposed = m < n;
+  st->mA = std::max(m, n);
+  st->nA = std::min(m, n);
+  const int64_t mA = st->mA, nA = st->nA;
+  *accepted = 0;
+  *rest2_host = -1.0;
+  if (nA == 0 || k <= 0 || k >= nA) return FTT_OK;
+  {
+    FTT_CHECK(arena_reserve(ctx, 1024));
+    bool ok = true;
+    if (a_row_major) FTT_CHECK(check_finite(ctx, n, m, A, lda, &ok));
+    else FTT_CHECK(check_finite(ctx, m, n, A, lda, &ok));
+    if (!ok) {
+      set_error("matrix entries must be finite");
+      return FTT_ERR_NONFINITE;
+    }
+  }
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
+  const bool need_t = a_row_major ? !st->transposed : st->transposed;
+  if (!need_t) {
+    FTT_CHECK(copy_matrix(ctx, mA, nA, A, lda, st->Af, mA));
+  } else {
+    FTT_CHECK(transpose(ctx, nA, mA, A, lda, st->Af, mA));
+  }
+  double *Om = nullptr, *Yk = nullptr, *sk = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&Om, 8 * (size_t)nA * k));
+  FTT_CHECK(owned_alloc(ctx, (void **)&Yk, 8 * (size_t)mA * k));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Qk, 8 * (size_t)mA * k));
+  FTT_CHECK(owned_alloc(ctx, (void **)&st->Bk, 8 * (size_t)k * nA));
+  const size_t ske = std::max({gemm_splitk_elems(mA, k, nA), gemm_splitk_elems(k, nA, mA),
+                               gemm_splitk_elems(mA, nA, k), (size_t)1});
+  FTT_CHECK(owned_alloc(ctx, (void **)&sk, 8 * ske));
+  k_omega<<<grid_for(nA * k, 256, 4), 256, 0, ctx->stream>>>(nA * k, Om);
+  FTT_LAUNCHED(ctx);
+  // range finder: Y = A Omega, Q = qr(Y), B = Q^T A, residual A - Q B (in place)
+  FTT_CHECK(gemm(ctx, 0, 0, mA, k, nA, 1.0, st->Af, mA, Om, nA, 0.0, Yk, mA, sk, ske));
+  {
+    size_t wse = qr_workspace_elems(mA, k);
+    FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)k) +
+                                     align_up(8 * qr_tblk_elems(mA, k)) + 4096));
+    double *ws = take<double>(ctx, wse);
+    double *tau = take<double>(ctx, k);
+    double *Tb = take<double>(ctx, qr_tblk_elems(mA, k));
+    FTT_CHECK(qr_factor(ctx, mA, k, Yk, mA, tau, Tb, ws, wse));
+    FTT_CHECK(launch_identity(ctx, mA, k, st->Qk, mA));
+    FTT_CHECK(qr_apply_q(ctx, mA, k, Yk, mA, Tb, k, st->Qk, mA, ws, wse));
+  }
+  double fro2 = 0.0, rest2 = 0.0;
+  {
+    FTT_CHECK(arena_reserve(ctx, align_up(8 * (kSumSqBlocks + 1)) + 256));
+    double *partial = take<double>(ctx, kSumSqBlocks + 1);
+    FTT_CHECK(sum_squares(ctx, mA * nA, st->Af, partial, &fro2));
+    FTT_CHECK(gemm(ctx, 1, 0, k, nA, mA, 1.0, st->Qk, mA, st->Af, mA, 0.0, st->Bk, k, sk, ske));
+    FTT_CHECK(gemm(ctx, 0, 0, mA, nA, k, -1.0, st->Qk, mA, st->Bk, k, 1.0, st->Af, mA, sk, ske));
+    FTT_CHECK(sum_squares(ctx, mA * nA, st->Af, partial, &rest2));
+  }
+  owned_free(ctx, Om);
+  owned_free(ctx, Yk);
+  owned_free(ctx, sk);
+  *rest2_host = rest2;
+  // Acceptance: the residual energy must sit below the rounding noise a
+  // backward-stable full SVD already carries in the tail sums
+  // (~ nA (eps ||A||_F)^2, the reference's own gesdd), or below 1e-8 delta^2,
+  // and never above 1e-6 delta^2 (so tail(k) <= delta^2 and the rank <= k).
+  const double eps = 2.220446049250313e-16;
+  const double noise2 = (double)nA * eps * eps * fro2;
+  const double thr = std::min(std::max(1e-8 * delta2, noise2), 1e-6 * delta2);
+  static const bool debug = getenv("FTT_DEBUG") != nullptr;
+  if (debug)
+    fprintf(stderr, "[ftt] lowrank m=%lld n=%lld k=%lld rest2=%.3e thr=%.3e -> %s\n",
+            (long long)m, (long long)n, (long long)k, rest2, thr,
+            rest2 <= thr ? "accepted" : "rejected");
+  if (!(rest2 <= thr)) return FTT_OK;
+  st->inner = new SvdState();
+  FTT_CHECK(svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0));
+  st->sigma = st->inner->sigma;
+  if (s_host) memcpy(s_host, st->sigma.data(), 8 * st->sigma.size());
+  *accepted = 1;
+  return FTT_OK;
+}
+
+extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ldu,
+                               int32_t u_row_major, double *V, int64_t ldv, int32_t v_row_major,
+                               int32_t scale_v) {
+  if (!ctx || !ctx->svd) {
+    set_error("ftt_svd_vectors: no factorization in this context");
+    return FTT_ERR_INVALID;
+  }
+  SvdState *st = ctx->svd;
+  const int64_t mA = st->mA, nA = st->nA;
+  if (rank < 0 || rank > (int64_t)st->sigma.size()) {
+    set_error("rank %lld out of range", (long long)rank);
+    return FTT_ERR_INVALID;
+  }
+  if (rank == 0) return FTT_OK;
+  double *UA = nullptr, *VA = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&UA, 8 * (size_t)mA * rank));
+  FTT_CHECK(owned_alloc(ctx, (void **)&VA, 8 * (size_t)nA * rank));
+  if (st->lowrank) {
+    // A_tall ~= Qk B with B = U_B S V_B^T  =>  U_A = Qk U_B, V_A = V_B
+    SvdState *in = st->inner;
+    double *UAi = nullptr, *VAi = nullptr;
+    FTT_CHECK(owned_alloc(ctx, (void **)&UAi, 8 * (size_t)in->mA * rank));
+    FTT_CHECK(owned_alloc(ctx, (void **)&VAi, 8 * (size_t)in->nA * rank));
+    FTT_CHECK(svd_raw_vectors(ctx, in, rank, UAi, VAi));
+    const int64_t k = in->m;  // B is k x nA
+    double *UB = in->transposed ? VAi : UAi;  // k x rank
+    double *VB = in->transposed ? UAi : VAi;  // nA x rank
+    FTT_CHECK(gemm(ctx, 0, 0, mA, rank, k, 1.0, st->Qk, mA, UB, k, 0.0, UA, mA, nullptr, 0));
+    FTT_CHECK(copy_matrix(ctx, nA, rank, VB, nA, VA, nA));
+    owned_free(ctx, UAi);
+    owned_free(ctx, VAi);
+  } else {
+    FTT_CHECK(svd_raw_vectors(ctx, st, rank, UA, VA));
+  }
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * rank) + 256));
+  double *sig = take<double>(ctx, rank);
+  FTT_CUDA(cudaMemcpyAsync(sig, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
   double *UM = st->transposed ? VA : UA;
   double *VM = st->transposed ? UA : VA;
   const int64_t mu = st->transposed ? nA : mA;  // == caller m
@@ -724,6 +905,8 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
     if (v_row_major) FTT_CHECK(transpose(ctx, mv, rank, VM, mv, V, ldv));
     else FTT_CHECK(copy_matrix(ctx, mv, rank, VM, mv, V, ldv));
   }
+  owned_free(ctx, UA);
+  owned_free(ctx, VA);
   // keep the context stream-ordered for the host vectors we just copied from
   FTT_CUDA(cudaStreamSynchronize(ctx->stream));
   return FTT_OK;

@@ -39,21 +39,62 @@ class QRResult:
     r: np.ndarray
 
 
-def tail_rank(s: np.ndarray, delta: float, shape) -> int:
+def tail_rank(s: np.ndarray, delta: float, shape, rest2: float = 0.0) -> int:
     """Smallest kept rank whose discarded tail has ``sum(s[r:]**2) <= delta**2``;
-    ``delta == 0`` keeps ``s >= max(shape) * eps * s[0]`` (linalg.py:89-99)."""
+    ``delta == 0`` keeps ``s >= max(shape) * eps * s[0]`` (linalg.py:89-99).
+    ``rest2`` is the certified energy beyond the returned values (low-rank
+    path; 0 for a full SVD, which makes this the reference rule verbatim)."""
     if delta == 0.0:
         if s.size == 0 or s[0] == 0.0:
             return 0
         return int(np.count_nonzero(s >= max(shape) * _EPS * s[0]))
     sq = s * s
     tails = np.concatenate([np.cumsum(sq[::-1])[::-1], [0.0]])
+    if rest2:
+        tails = tails + rest2
     return int(np.argmax(tails <= delta * delta))
 
 
-def tail_error(s: np.ndarray, rank: int) -> float:
+def tail_error(s: np.ndarray, rank: int, rest2: float = 0.0) -> float:
     sq = s * s
-    return float(np.sqrt(max(float(np.sum(sq[rank:])), 0.0)))
+    return float(np.sqrt(max(float(np.sum(sq[rank:])) + rest2, 0.0)))
+
+
+LOWRANK_MIN = 48        # smaller operands: the full SVD is already cheap
+
+
+def lowrank_k(min_dim: int, hint) -> int:
+    """Sketch width for the certified low-rank path (0 = do not try)."""
+    if min_dim < LOWRANK_MIN:
+        return 0
+    k = 32 if hint is None else max(16, 2 * int(hint) + 8)
+    k = (k + 7) // 8 * 8
+    return k if 2 * k <= min_dim else 0
+
+
+def dev_svd_values_lowrank(buf, m: int, n: int, ld: int, row_major: bool, k: int,
+                           delta2: float):
+    """Phase 1 of the certified low-rank path: (s[k], rest2, accepted)."""
+    s = np.zeros(k)
+    rest2 = nat.ctypes.c_double(0.0)
+    acc = nat.ctypes.c_int32(0)
+    nat.check(nat.lib().ftt_svd_lowrank_f64(
+        nat.context(), int(m), int(n), nat.ptr(buf), int(ld), int(bool(row_major)), int(k),
+        float(delta2), s.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_double)),
+        nat.ctypes.byref(rest2), nat.ctypes.byref(acc)), "ftt_svd_lowrank_f64")
+    return s, float(rest2.value), bool(acc.value)
+
+
+def dev_svd_truncate(buf, m: int, n: int, ld: int, row_major: bool, delta, hint=None):
+    """Phase 1 for a truncation step: (s, rest2). Tries the certified
+    low-rank path when delta > 0, else (or on rejection) the full SVD."""
+    if delta is not None and delta > 0.0:
+        k = lowrank_k(min(m, n), hint)
+        if k:
+            s, rest2, ok = dev_svd_values_lowrank(buf, m, n, ld, row_major, k, delta * delta)
+            if ok:
+                return s, rest2
+    return dev_svd_values(buf, m, n, ld, row_major), 0.0
 
 
 def _check_matrix(m) -> np.ndarray:

@@ -37,7 +37,7 @@ from .coo import (
     device_dot,
     fibers_device,
 )
-from .dense import dev_svd_values, dev_svd_vectors, tail_error, tail_rank
+from .dense import dev_svd_truncate, dev_svd_values, dev_svd_vectors, tail_error, tail_rank
 from .trains import (
     QuasiPermMatrix,
     StructuredTT,
@@ -441,32 +441,51 @@ class TruncationBudget:
 
 
 class _Trunc:
-    """Per-step truncation policy (static / dynamic / fixed-rank)."""
+    """Per-step truncation policy (static / dynamic / fixed-rank).
+
+    ``delta_first/second`` give the step's tolerance before the SVD (None in
+    fixed-rank mode); ``first/second`` turn the singular values (plus the
+    certified remainder ``rest2`` of the low-rank path) into the kept rank and
+    update the dynamic budget (fasttt.py:416-426)."""
 
     def __init__(self, kind, d, delta=0.0, left=0.0, right=0.0, targets=None):
         self.kind, self.d = kind, d
         self.delta, self.left, self.right = delta, left, right
         self.targets = targets
 
-    def first(self, k, s, shape):
+    def delta_first(self, k):
         if self.kind == "static":
-            r = tail_rank(s, self.delta, shape)
-            return r, tail_error(s, r)
+            return self.delta
         if self.kind == "dynamic":
-            r = tail_rank(s, self.right / math.sqrt(self.d - 1 - k), shape)
-            err = tail_error(s, r)
+            return self.right / math.sqrt(self.d - 1 - k)
+        return None
+
+    def delta_second(self, k):
+        if self.kind == "static":
+            return self.delta
+        if self.kind == "dynamic":
+            return self.left / math.sqrt(k)
+        return None
+
+    def first(self, k, s, shape, rest2=0.0):
+        if self.kind == "static":
+            r = tail_rank(s, self.delta, shape, rest2)
+            return r, tail_error(s, r, rest2)
+        if self.kind == "dynamic":
+            r = tail_rank(s, self.right / math.sqrt(self.d - 1 - k), shape, rest2)
+            err = tail_error(s, r, rest2)
             self.right = math.sqrt(max(self.right ** 2 - err ** 2, 0.0))
             return r, err
         r = int(min(self.targets[k + 1], min(shape)))
         return r, tail_error(s, r)
 
-    def second(self, k, s, shape):
+    def second(self, k, s, shape, rest2=0.0):
         if self.kind == "static":
-            r = tail_rank(s, self.delta, shape)
-            return r, tail_error(s, r)
+            r = tail_rank(s, self.delta, shape, rest2)
+            return r, tail_error(s, r, rest2)
         if self.kind == "dynamic":
-            r = tail_rank(s, self.left / math.sqrt(k), shape)
-            err = tail_error(s, r)
+            r = tail_rank(s, self.left / math.sqrt(k), shape, rest2)
+            err = tail_error(s, r, rest2)
             self.left = math.sqrt(max(self.left ** 2 - err ** 2, 0.0))
             return r, err
         r = int(min(self.targets[k], min(shape)))
@@ -481,12 +500,14 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
     lib, ctx = nat.lib(), nat.context()
     cs = list(cores)
     d = len(cs)
+    hint = None  # previous step's rank: sketch width of the low-rank path
     for k in range(pivot, d - 1):  # :334-341
         C = cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
         m = r0 * n
-        s = dev_svd_values(C, m, r1, r1, True)
-        rank, _ = policy.first(k, s, (m, r1))
+        s, rest2 = dev_svd_truncate(C, m, r1, r1, True, policy.delta_first(k), hint)
+        rank, _ = policy.first(k, s, (m, r1), rest2)
+        hint = rank
         if rank == 0:
             return None
         U, V = dev_svd_vectors(m, r1, rank, True, False, True)  # V: carry (r1 x rank) col-major
@@ -518,8 +539,9 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
     for k in range(pivot, 0, -1):  # :348-355
         C = cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
-        s = dev_svd_values(C, n * r1, r0, n * r1, False)
-        rank, _ = policy.second(k, s, (n * r1, r0))
+        s, rest2 = dev_svd_truncate(C, n * r1, r0, n * r1, False, policy.delta_second(k), hint)
+        rank, _ = policy.second(k, s, (n * r1, r0), rest2)
+        hint = rank
         if rank == 0:
             return None
         U, V = dev_svd_vectors(n * r1, r0, rank, False, True, True)  # V: carry (r0 x rank) row-major
