@@ -448,6 +448,55 @@ __global__ void k_copy_keys(int64_t n, const int64_t *in, uint64_t *out) {
 
 __global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
 
+constexpr int HS_MAXP = 32;
+struct HashSpec {
+  int d, np, lg;
+  int64_t mult[HS_MAXP][32];  // key multipliers per pivot of the group (pivot -> 0)
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Insert the np fixed-tuple keys of every nonzero into np hash sets (empty
+// slot = ~0, keys < 2^63); count first insertions per set.
+__global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict__ coords, int64_t n,
+                                                       HashSpec hs,
+                                                       unsigned long long *__restrict__ tables,
+                                                       unsigned long long *__restrict__ counts) {
+  const int64_t T = (int64_t)1 << hs.lg;
+  const uint64_t mask = (uint64_t)T - 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    int64_t c[32];
+    if (i < n)
+      for (int k = 0; k < hs.d; ++k) c[k] = coords[i * hs.d + k];
+    for (int q = 0; q < hs.np; ++q) {
+      int fresh = 0;
+      if (i < n) {
+        uint64_t key = 0;
+        for (int k = 0; k < hs.d; ++k) key += (uint64_t)c[k] * (uint64_t)hs.mult[q][k];
+        unsigned long long *tab = tables + (int64_t)q * T;
+        uint64_t h = mix64(key) & mask;
+        while (true) {
+          unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)key);
+          if (old == ~0ull) {
+            fresh = 1;
+            break;
+          }
+          if (old == key) break;
+          h = (h + 1) & mask;
+        }
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, fresh);
+      if (lane == 0 && b) atomicAdd(counts + q, (unsigned long long)__popc(b));
+    }
+  }
+}
+
 __global__ void k_count_changes(const uint64_t *k, int64_t n, unsigned long long *out) {
   unsigned long long c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -813,19 +862,41 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
     for (int p = 0; p < d; ++p) counts_host[p] = 0;
     return FTT_OK;
   }
-  FTT_CHECK(arena_reserve(ctx, sort_coords_bytes(nnz, false) + 4096));
+  // One pass over the COO: every nonzero inserts its d fixed-tuple keys into
+  // d open-addressing hash sets (table size 2^ceil(log2(2 nnz))); a CAS that
+  // claims an empty slot is a new distinct key.  Exact (insertion order does
+  // not change the count) and reads the coordinates once instead of d
+  // radix sorts.  Tables for all d pivots at once when they fit in 4 GiB,
+  // else pivot groups.
+  int lg = 1;
+  while (((int64_t)1 << lg) < 2 * nnz) ++lg;
+  const int64_t T = (int64_t)1 << lg;
+  int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));  // 4 GiB
+  uint64_t *tables = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&tables, 8 * (size_t)T * group));
+  FTT_CHECK(arena_reserve(ctx, 4096));
   unsigned long long *cnt = take<unsigned long long>(ctx, 32);
   FTT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 32, ctx->stream));
-  size_t mark = ctx->arena.used;
-  for (int p = 0; p < d; ++p) {
-    ctx->arena.used = mark;
-    uint64_t *kr;
-    uint32_t *vr;
-    uint64_t bound;
-    FTT_CHECK(sort_coords(ctx, coords, nnz, d, dims_host, p, false, &kr, &vr, &bound));
-    k_count_changes<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(kr, nnz, cnt + p);
+  for (int p0 = 0; p0 < d; p0 += group) {
+    const int np = std::min(group, d - p0);
+    HashSpec hs;
+    hs.d = d;
+    hs.np = np;
+    hs.lg = lg;
+    for (int q = 0; q < np; ++q) {
+      KeySpec ks;
+      uint64_t bound;
+      make_spec(d, dims_host, p0 + q, false, &ks, &bound);
+      for (int k = 0; k < d; ++k) hs.mult[q][k] = ks.mult[k];
+    }
+    FTT_CUDA(cudaMemsetAsync(tables, 0xff, 8 * (size_t)T * np, ctx->stream));
+    const int pb = prof_begin(ctx);
+    k_distinct_hash<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(coords, nnz, hs, tables, cnt + p0);
     FTT_LAUNCHED(ctx);
+    // coordinates read once + one 8-byte CAS per pivot and nonzero
+    prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0 * np), 0.0);
   }
+  owned_free(ctx, tables);
   unsigned long long h[32];
   FTT_CHECK(copy_to_host(ctx, h, cnt, sizeof(unsigned long long) * d));
   for (int p = 0; p < d; ++p) counts_host[p] = (int64_t)h[p];

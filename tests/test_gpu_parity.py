@@ -342,3 +342,17 @@ def test_config_parity(cfg):
 @pytest.mark.parametrize("cfg", [3, 5])
 def test_config_parity_large(cfg):
     _config_case(cfg, n_zero=100_000)
+
+
+@pytest.mark.parametrize("dims,ranks,n", [((4, 5, 6, 7, 3), (5, 9, 12, 4), 100_000),
+                                          ((16,) * 8, (10, 46, 60, 64, 50, 33, 9), 70_000)])
+def test_tt_entries_meet_in_the_middle(dims, ranks, n):
+    """The split (prefix x suffix) evaluation path (n >= 65536, ranks <= 64)
+    against the chained oracle evaluator, relative error <= 1e-12."""
+    rng = np.random.default_rng(n)
+    full = (1,) + ranks + (1,)
+    cores = [rng.standard_normal((full[k], m, full[k + 1])) for k, m in enumerate(dims)]
+    coords = np.stack([rng.integers(0, m, n) for m in dims], 1)
+    coords = coords[np.lexsort(coords.T[::-1])]  # sorted like SparseTensor input
+    got = ft.tt_entries(ft.TTTensor(cores), coords)
+    assert rel_err(got, O.tt_entries(cores, coords)) < 1e-12
