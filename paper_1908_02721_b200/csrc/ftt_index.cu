@@ -891,7 +891,8 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
     }
     FTT_CUDA(cudaMemsetAsync(tables, 0xff, 8 * (size_t)T * np, ctx->stream));
     const int pb = prof_begin(ctx);
-    k_distinct_hash<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(coords, nnz, hs, tables, cnt + p0);
+    k_distinct_hash<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(
+        coords, nnz, hs, reinterpret_cast<unsigned long long *>(tables), cnt + p0);
     FTT_LAUNCHED(ctx);
     // coordinates read once + one 8-byte CAS per pivot and nonzero
     prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0 * np), 0.0);
