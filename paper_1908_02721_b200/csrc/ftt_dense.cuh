@@ -10,6 +10,11 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
          const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
          int64_t ldc, double *splitk_ws, size_t splitk_ws_elems);
 size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k);
+// ||R0 - op(A) op(B)||_F^2 without materialising the residual (R0 stored
+// transposed when r_trans).
+int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k,
+                     const double *A, int64_t lda, const double *B, int64_t ldb, const double *R0,
+                     int64_t ldr, int r_trans, double *out_host);
 int transpose(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *src, int64_t lds,
               double *dst, int64_t ldd);
 

@@ -24,12 +24,19 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <bool TA, bool TB>
+// EPI 0: C = alpha op(A) op(B) + beta C (or split-K partials).
+// EPI 1: residual norm -- no C write; each CTA writes
+//   npart[tile] = sum over its tile of (R0(row, col) - op(A) op(B))^2,
+// R0 = C read-only, stored transposed when c_trans (R0(row, col) at
+// C[col + row * ldc]).  Used by the certified low-rank SVD to form
+// ||A - Q B||_F without materialising the residual.
+template <bool TA, bool TB, int EPI = 0>
 __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, double alpha,
                                               const double *__restrict__ A, int64_t lda,
                                               const double *__restrict__ B, int64_t ldb, double beta,
                                               double *__restrict__ C, int64_t ldc, int64_t kps,
-                                              double *__restrict__ partial) {
+                                              double *__restrict__ partial, int c_trans = 0,
+                                              double *__restrict__ npart = nullptr) {
   __shared__ double As[2][BK][BM + PAD];
   __shared__ double Bs[2][BK][BN + PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -126,6 +133,7 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
     buf ^= 1;
   }
   // epilogue
+  double ss = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int64_t row = tm + wm + i * 8 + (lane >> 2);
@@ -136,7 +144,11 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
       for (int h = 0; h < 2; ++h) {
         int64_t col = tn + wn + j * 8 + 2 * (lane & 3) + h;
         if (col >= n) continue;
-        if (partial) {
+        if (EPI == 1) {
+          const double r0 = c_trans ? C[col + row * ldc] : C[row + col * ldc];
+          const double v = r0 - acc[i][j][h];
+          ss += v * v;
+        } else if (partial) {
           partial[((int64_t)blockIdx.z * n + col) * m + row] = acc[i][j][h];
         } else {
           double v = alpha * acc[i][j][h];
@@ -146,6 +158,31 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
       }
     }
   }
+  if (EPI == 1) {
+    __shared__ double s_ss[GT / 32];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, off);
+    if (lane == 0) s_ss[warp] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < GT / 32; ++w) t += s_ss[w];
+      npart[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = t;
+    }
+  }
+}
+
+__global__ void k_sum_partials(const double *__restrict__ p, int64_t n, double *__restrict__ out) {
+  __shared__ double s[1024];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += p[i];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off; off >>= 1) {
+    if ((int)threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
 }
 
 __global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *__restrict__ partial,
@@ -296,6 +333,40 @@ int bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops) {
   // 8 warps x 8 chains x iters DMMAs, 512 flops each
   double flops = (double)blocks * 8 * 8 * (double)iters * 512.0;
   *tflops = flops / (ms * 1e-3) / 1e12;
+  return FTT_OK;
+}
+
+// ||R0 - op(A) op(B)||_F^2 (m x n, inner k) without writing the residual;
+// deterministic (fixed tile grid, fixed-order reduction).
+int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k,
+                     const double *A, int64_t lda, const double *B, int64_t ldb, const double *R0,
+                     int64_t ldr, int r_trans, double *out_host) {
+  *out_host = 0.0;
+  if (m <= 0 || n <= 0) return FTT_OK;
+  const int64_t tiles_m = ceil_div(m, BM), tiles_n = ceil_div(n, BN);
+  if (tiles_n > 65535) {
+    set_error("gemm_resid_sumsq: too many column tiles");
+    return FTT_ERR_INVALID;
+  }
+  const int64_t nt = tiles_m * tiles_n;
+  double *npart = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&npart, 8 * (size_t)(nt + 1)));
+  dim3 grid((unsigned)tiles_m, (unsigned)tiles_n, 1);
+  const int64_t kps = ceil_div(std::max<int64_t>(k, 1), BK) * BK;
+  double *C = const_cast<double *>(R0);
+#define FTT_RESID_LAUNCH(TA_, TB_)                                                              \
+  k_dgemm<TA_, TB_, 1><<<grid, GT, 0, ctx->stream>>>(m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldr, \
+                                                     kps, nullptr, r_trans, npart)
+  if (!ta && !tb) FTT_RESID_LAUNCH(false, false);
+  else if (!ta && tb) FTT_RESID_LAUNCH(false, true);
+  else if (ta && !tb) FTT_RESID_LAUNCH(true, false);
+  else FTT_RESID_LAUNCH(true, true);
+#undef FTT_RESID_LAUNCH
+  FTT_LAUNCHED(ctx);
+  k_sum_partials<<<1, 1024, 0, ctx->stream>>>(npart, nt, npart + nt);
+  FTT_LAUNCHED(ctx);
+  FTT_CHECK(copy_to_host(ctx, out_host, npart + nt, sizeof(double)));
+  owned_free(ctx, npart);
   return FTT_OK;
 }
 

@@ -867,10 +867,17 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
   // claims an empty slot is a new distinct key.  Exact (insertion order does
   // not change the count) and reads the coordinates once instead of d
   // radix sorts.  Tables for all d pivots at once when they fit in 4 GiB,
-  // else pivot groups.
+  // else pivot groups.  Once one table outgrows a slice of L2 the random CAS
+  // traffic goes to HBM and d onesweep sorts (streaming, coalesced) win, so
+  // large inputs take the sort route (measured crossover ~2-4M nonzeros).
   int lg = 1;
   while (((int64_t)1 << lg) < 2 * nnz) ++lg;
   const int64_t T = (int64_t)1 << lg;
+  if (8 * T > ((int64_t)32 << 20)) {
+    for (int p = 0; p < d; ++p)
+      FTT_CHECK(ftt_fiber_count(ctx, coords, nnz, d, dims_host, p, &counts_host[p]));
+    return FTT_OK;
+  }
   int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));  // 4 GiB
   uint64_t *tables = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&tables, 8 * (size_t)T * group));

@@ -780,22 +780,34 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   *accepted = 0;
   *rest2_host = -1.0;
   if (nA == 0 || k <= 0 || k >= nA) return FTT_OK;
-  {
-    FTT_CHECK(arena_reserve(ctx, 1024));
-    bool ok = true;
-    if (a_row_major) FTT_CHECK(check_finite(ctx, n, m, A, lda, &ok));
-    else FTT_CHECK(check_finite(ctx, m, n, A, lda, &ok));
-    if (!ok) {
-      set_error("matrix entries must be finite");
-      return FTT_ERR_NONFINITE;
-    }
-  }
-  FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
+  // The tall view A_tall (mA x nA) is read straight from the caller's buffer:
+  // `buf` col-major with leading dimension `ld`, stored transposed when
+  // `need_t`.  A strided (non-packed) input is packed once first.
   const bool need_t = a_row_major ? !st->transposed : st->transposed;
-  if (!need_t) {
-    FTT_CHECK(copy_matrix(ctx, mA, nA, A, lda, st->Af, mA));
-  } else {
-    FTT_CHECK(transpose(ctx, nA, mA, A, lda, st->Af, mA));
+  const double *buf = A;
+  int64_t ld = lda;
+  double fro2 = 0.0, rest2 = 0.0;
+  {
+    FTT_CHECK(arena_reserve(ctx, align_up(8 * (kSumSqBlocks + 1)) + 256));
+    double *partial = take<double>(ctx, kSumSqBlocks + 1);
+    const int64_t inner = need_t ? nA : mA;
+    if (lda != inner) {
+      FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
+      FTT_CHECK(copy_matrix(ctx, inner, mA * nA / inner, A, lda, st->Af, inner));
+      buf = st->Af;
+      ld = inner;
+    }
+    FTT_CHECK(sum_squares(ctx, mA * nA, buf, partial, &fro2));
+    if (!std::isfinite(fro2)) {
+      // either a non-finite entry or an overflowing (but finite) energy
+      bool ok = true;
+      FTT_CHECK(check_finite(ctx, need_t ? nA : mA, need_t ? mA : nA, buf, ld, &ok));
+      if (!ok) {
+        set_error("matrix entries must be finite");
+        return FTT_ERR_NONFINITE;
+      }
+      return FTT_OK;  // not accepted: the caller takes the full SVD
+    }
   }
   double *Om = nullptr, *Yk = nullptr, *sk = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&Om, 8 * (size_t)nA * k));
@@ -808,7 +820,7 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   k_omega<<<grid_for(nA * k, 256, 4), 256, 0, ctx->stream>>>(nA * k, Om);
   FTT_LAUNCHED(ctx);
   // range finder: Y = A Omega, Q = qr(Y), B = Q^T A, residual A - Q B (in place)
-  FTT_CHECK(gemm(ctx, 0, 0, mA, k, nA, 1.0, st->Af, mA, Om, nA, 0.0, Yk, mA, sk, ske));
+  FTT_CHECK(gemm(ctx, need_t, 0, mA, k, nA, 1.0, buf, ld, Om, nA, 0.0, Yk, mA, sk, ske));
   {
     size_t wse = qr_workspace_elems(mA, k);
     FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)k) +
@@ -820,15 +832,8 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
     FTT_CHECK(launch_identity(ctx, mA, k, st->Qk, mA));
     FTT_CHECK(qr_apply_q(ctx, mA, k, Yk, mA, Tb, k, st->Qk, mA, ws, wse));
   }
-  double fro2 = 0.0, rest2 = 0.0;
-  {
-    FTT_CHECK(arena_reserve(ctx, align_up(8 * (kSumSqBlocks + 1)) + 256));
-    double *partial = take<double>(ctx, kSumSqBlocks + 1);
-    FTT_CHECK(sum_squares(ctx, mA * nA, st->Af, partial, &fro2));
-    FTT_CHECK(gemm(ctx, 1, 0, k, nA, mA, 1.0, st->Qk, mA, st->Af, mA, 0.0, st->Bk, k, sk, ske));
-    FTT_CHECK(gemm(ctx, 0, 0, mA, nA, k, -1.0, st->Qk, mA, st->Bk, k, 1.0, st->Af, mA, sk, ske));
-    FTT_CHECK(sum_squares(ctx, mA * nA, st->Af, partial, &rest2));
-  }
+  FTT_CHECK(gemm(ctx, 1, need_t, k, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, k, sk, ske));
+  FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t, &rest2));
   owned_free(ctx, Om);
   owned_free(ctx, Yk);
   owned_free(ctx, sk);
