@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "ftt_dense.cuh"
+#include "ftt_small.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -655,6 +656,15 @@ extern "C" int ftt_qr_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, i
   if (!ctx || m < 0 || n < 0) return FTT_ERR_INVALID;
   const int64_t k = std::min(m, n);
   if (k == 0) return FTT_OK;
+  static const bool no_small = getenv("FTT_NO_SMALL") != nullptr;
+  if (!no_small && tsqr_ok(m, n)) {
+    // narrow: TSQR tree of CTA-local Householder QRs (ftt_small.cu)
+    double *Qt = Q;
+    if (!Qt) FTT_CHECK(owned_alloc(ctx, (void **)&Qt, 8 * (size_t)m * n));
+    const int rc = tsqr_q(ctx, m, n, A, lda, 0, Qt, Q ? ldq : m, R, ldr);
+    if (!Q) owned_free(ctx, Qt);
+    return rc;
+  }
   size_t wse = qr_workspace_elems(m, std::max(n, k));
   size_t need = align_up(8 * (size_t)m * n) + align_up(8 * (size_t)k) +
                 align_up(8 * qr_tblk_elems(m, n)) + align_up(8 * wse) + 1024;

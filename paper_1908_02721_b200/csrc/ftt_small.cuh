@@ -1,0 +1,19 @@
+// Narrow (n <= 64) QR / SVD without grid barriers (ftt_small.cu).
+#pragma once
+#include "ftt_common.cuh"
+
+namespace ftt {
+
+// A_tall (M x n) is `A` column-major (ld lda) or its transpose (trans).
+bool tsqr_ok(int64_t m, int64_t n);
+
+// Q (M x n, ld ldq) and R (n x n, ld ldr, diag >= 0; may be NULL) of A_tall.
+int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int trans, double *Q,
+           int64_t ldq, double *R, int64_t ldr);
+
+// Thin SVD core: U = Q P (M x n, ld ldu), Y = R^T P (n x n), norms_host[j] =
+// ||Y_j|| (unsorted; sigma up to the caller's permutation).
+int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int trans, double *U,
+             int64_t ldu, double *Y, double *norms_host, int *sweeps);
+
+}  // namespace ftt

@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include "ftt_dense.cuh"
+#include "ftt_small.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -47,6 +48,7 @@ struct SvdState {
   int sweeps = 0;
   bool precond = false;  // Jacobi ran on R2^T (QR of R^T) instead of R^T
   bool direct = false;   // Jacobi ran on A_tall itself (Y aliases Af)
+  bool small = false;    // narrow path (ftt_small.cu): Af holds U = Q P, Y = R^T P
   // low-rank path (ftt_svd_lowrank_f64): A_tall ~= Qk Bk with a certified
   // residual; the SVD of the small Bk lives in `inner`
   bool lowrank = false;
@@ -546,6 +548,34 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
   st->nA = std::min(m, n);
   const int64_t mA = st->mA, nA = st->nA;
   if (nA == 0) return FTT_OK;
+  static const bool no_small = getenv("FTT_NO_SMALL") != nullptr;
+  if (!no_small && tsqr_ok(mA, nA)) {
+    // narrow operand: CTA-local QR (+ TSQR tree) and CTA-local Jacobi, one
+    // host round trip for the whole factorisation
+    st->small = true;
+    const bool need_t = a_row_major ? !st->transposed : st->transposed;
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
+    std::vector<double> raw(nA);
+    const int pb = prof_begin(ctx);
+    FTT_CHECK(tsqr_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, mA, st->Y, raw.data(),
+                       &st->sweeps));
+    // QR (4 m n^2 / 3) + Q formation + Q P, plus sweeps x n^2/2 pairs x 10 n
+    prof_end(ctx, pb, PT_JACOBI, 8.0 * ((double)mA * nA * 3 + (double)nA * nA * 2),
+             (double)mA * nA * nA * (8.0 / 3.0 + 2.0) + 5.0 * std::max(st->sweeps, 1) *
+                                                           (double)nA * nA * nA);
+    static const bool debug = getenv("FTT_DEBUG") != nullptr;
+    if (debug)
+      fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld small) sweeps %d\n", (long long)m,
+              (long long)n, (long long)mA, (long long)nA, st->sweeps);
+    st->perm.resize(nA);
+    std::iota(st->perm.begin(), st->perm.end(), 0);
+    std::stable_sort(st->perm.begin(), st->perm.end(),
+                     [&](int64_t a, int64_t b) { return raw[a] > raw[b]; });
+    st->sigma.resize(nA);
+    for (int64_t i = 0; i < nA; ++i) st->sigma[i] = raw[st->perm[i]];
+    return FTT_OK;
+  }
   {
     FTT_CHECK(arena_reserve(ctx, 1024));
     bool ok = true;
@@ -715,6 +745,17 @@ int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double
   for (int64_t j = 0; j < rank; ++j) hinv[j] = st->sigma[j] != 0.0 ? 1.0 / st->sigma[j] : 0.0;
   FTT_CUDA(cudaMemcpyAsync(sel, st->perm.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
   FTT_CUDA(cudaMemcpyAsync(inv, hinv.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+  if (st->small) {
+    // U_A = (Q P)[:, sel],  V_A = Y[:, sel] / sigma
+    k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, mA, rank, st->Af, mA,
+                                                                        sel, nullptr, UA, mA);
+    FTT_LAUNCHED(ctx);
+    k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA,
+                                                                        sel, inv, VA, nA);
+    FTT_LAUNCHED(ctx);
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return FTT_OK;
+  }
   if (st->direct) {
     // U_A = Y[:, sel] / sigma (Y = A P, mA x nA),  V_A = P[:, sel]
     k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, mA, rank, st->Y, mA,
@@ -821,7 +862,10 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   FTT_LAUNCHED(ctx);
   // range finder: Y = A Omega, Q = qr(Y), B = Q^T A, residual A - Q B (in place)
   FTT_CHECK(gemm(ctx, need_t, 0, mA, k, nA, 1.0, buf, ld, Om, nA, 0.0, Yk, mA, sk, ske));
-  {
+  static const bool no_small = getenv("FTT_NO_SMALL") != nullptr;
+  if (!no_small && tsqr_ok(mA, k)) {
+    FTT_CHECK(tsqr_q(ctx, mA, k, Yk, mA, 0, st->Qk, mA, nullptr, 0));
+  } else {
     size_t wse = qr_workspace_elems(mA, k);
     FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)k) +
                                      align_up(8 * qr_tblk_elems(mA, k)) + 4096));

@@ -129,7 +129,7 @@ def test_dgemm_matches_blas(m, n, k):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 3), (3, 5), (100, 37), (129, 300), (5000, 260),
-                                 (70000, 40)])
+                                 (70000, 40), (64, 64), (2000, 64), (300000, 32), (881, 1)])
 def test_qr_economic(m, n):
     """Householder QR: Q R = A to 1e-11, Q^T Q = I to 1e-12, diag(R) >= 0,
     R equal to LAPACK's sign-fixed R to 1e-10 (full column rank)."""
@@ -146,7 +146,8 @@ def test_qr_economic(m, n):
 
 @pytest.mark.parametrize("m,n,rk", [(1, 1, 1), (6, 4, 4), (100, 37, 5), (37, 100, 5),
                                     (300, 300, 300), (4096, 200, 16), (200, 3000, 200),
-                                    (1000, 700, 300)])
+                                    (1000, 700, 300), (512, 37, 37), (10366, 24, 8),
+                                    (62206, 64, 8), (300000, 32, 16), (24, 512, 24)])
 def test_svd_matches_lapack(m, n, rk):
     """Jacobi SVD: singular values within 1e-13*s_max of gesdd; truncated
     reconstruction and tail rank identical to the reference rule."""
@@ -177,6 +178,24 @@ def test_svd_graded_spectrum():
     A = (U * s_true) @ V.T
     res = ft.svd_truncate_rank(A, 100)
     assert np.abs(res.s - np.linalg.svd(A, compute_uv=False)).max() < 1e-14
+
+
+def test_narrow_rank_deficient_and_graded():
+    """Narrow operands (the CTA-local / TSQR path): rank-deficient QR stays
+    exact (Q orthonormal, QR = A) and a 15-decade spectrum keeps LAPACK's
+    absolute accuracy."""
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((3000, 5)) @ rng.standard_normal((5, 40))
+    res = ft.qr_economic(A)
+    assert np.abs(res.q @ res.r - A).max() < 1e-11
+    assert np.abs(res.q.T @ res.q - np.eye(40)).max() < 1e-12
+    U, _ = np.linalg.qr(rng.standard_normal((5000, 60)))
+    V, _ = np.linalg.qr(rng.standard_normal((60, 60)))
+    s_true = np.logspace(0, -15, 60)
+    A = (U * s_true) @ V.T
+    res = ft.svd_truncate_rank(A, 60)
+    assert np.abs(res.s - np.linalg.svd(A, compute_uv=False)).max() < 1e-14
+    assert np.abs((res.u * res.s) @ res.vt - A).max() < 1e-13
 
 
 def test_svd_errors():
