@@ -184,18 +184,20 @@ int ftt_qr_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
 int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
                 int64_t lda, int32_t a_row_major, double *s_host);
 /* Certified low-rank phase 1 (an accelerator for svd_truncate_delta on
- * numerically low-rank operands): A_tall ~= Q B with Q = orth(A_tall Omega)
- * for a deterministic k-column test matrix Omega, B = Q^T A_tall, and the
- * residual R = A_tall - Q B formed explicitly.  rest2_host = ||R||_F^2.
- * Accepted when rest2 <= min(max(1e-8 delta2, nA eps^2 ||A||_F^2),
- * 1e-6 delta2), i.e. below the rounding noise a full backward-stable SVD
- * (the reference's gesdd) already has in its tail sums: then the k singular
- * values of B go to s_host, *accepted = 1, and phase 2 (ftt_svd_vectors)
- * returns Q U_B / V_B.  Since sigma_i(A)^2 - sigma_i(B)^2 <= ||R||_2^2 and
- * the discarded tail is sum_{i>j} sigma_i(B)^2 + rest2 up to that error,
- * the tail rule of linalg.py:97-99 decides the same rank as a full SVD
- * except within ~rank*rest2 of a tie.  Otherwise *accepted = 0 and the
- * caller runs ftt_svd_f64.  delta2 = delta^2 of the truncation step. */
+ * numerically low-rank operands): A_tall ~= Q B with Q an orthonormal basis
+ * of the numerically spanning columns of the sketch A_tall Omega (Omega a
+ * deterministic k-column test matrix, k <= min(m,n) / 2), B = Q^T A_tall,
+ * and the residual R = A_tall - Q B evaluated explicitly:
+ * rest2_host = ||R||_F^2.  The singular values of B go to s_host (at most k;
+ * the rest stay untouched) and phase 2 (ftt_svd_vectors) returns Q U_B /
+ * V_B.  Every true tail sum of A_tall lies in [tail_B, tail_B + rest2]
+ * (A^T A = B^T B + R^T R).  *accepted = 2 when rest2 <=
+ * min(max(1e-8 delta2, nA eps^2 ||A||_F^2), 1e-6 delta2) -- below the
+ * rounding noise of a full backward-stable SVD's tails (the reference's
+ * gesdd); = 1 when only rest2 <= 1e-6 delta2 (the caller may use it when
+ * the tail rule of linalg.py:97-99 decides the same rank at both ends of
+ * the interval); = 0 otherwise, and the caller runs ftt_svd_f64.
+ * delta2 = delta^2 of the truncation step. */
 int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
                         int64_t lda, int32_t a_row_major, int64_t k,
                         double delta2, double *s_host, double *rest2_host,

@@ -33,6 +33,12 @@ int qr_apply_q(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
                int64_t r, double *Z, int64_t ldz, double *ws, size_t ws_elems);
 size_t qr_apply_workspace_elems(int64_t m, int64_t n, int64_t r);
 
+// Numerical rank r of the sketch Y (mA x k <= 64) and its pivot order
+// (sel_dev, k entries; the first r span Y) from a pivoted Cholesky of the
+// Gram (ftt_cholqr.cu).
+int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau, int64_t *sel_dev,
+                int64_t *rank);
+
 int check_finite(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, bool *ok);
 int copy_matrix(ftt_ctx *ctx, int64_t m, int64_t n, const double *src, int64_t lds, double *dst,
                 int64_t ldd);

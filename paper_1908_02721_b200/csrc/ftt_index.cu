@@ -497,6 +497,177 @@ __global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict
   }
 }
 
+// ---- partitioned distinct counts (select_p on large inputs) --------------
+// Exact number of distinct fixed tuples per pivot p without sorting:
+//   lin   = C-order linear index of each nonzero (< 2^63, one pass over COO)
+//   key_p = lin with the mode-p digit removed = (lin / T_p) S_p + lin mod S_p
+//           (S_p = prod of the dims after p, T_p = n_p S_p; division by
+//           run-time constants via exact 64-bit magic multipliers)
+//   bucket = top `bits` bits of mix64(key_p): equal keys share a bucket
+//   pass 1 per-block bucket histograms, pass 2 scatter into bucket segments,
+//   pass 3 one CTA per bucket counts distinct keys in a shared-memory hash
+//   set (slot = low bits of the same mix).  Counting is insertion-order
+//   independent, so the result is exact and deterministic; a bucket too large
+//   for the shared table flags its pivot, which is then counted by sorting.
+constexpr int PC_MAXG = 8;
+constexpr int PC_TMAX = 8192;  // shared hash-set slots (64 KB)
+struct PartSpec {
+  int g, bits;
+  int64_t chunk;  // nonzeros per block
+  uint64_t S[PC_MAXG], mS[PC_MAXG], mT[PC_MAXG];
+  int shS[PC_MAXG], shT[PC_MAXG];  // -1: divisor 1
+};
+
+__device__ __forceinline__ uint64_t udiv_magic(uint64_t x, uint64_t m, int sh) {
+  return sh < 0 ? x : (__umul64hi(x, m) >> sh);
+}
+
+__device__ __forceinline__ uint64_t drop_digit(uint64_t lin, const PartSpec &ps, int q) {
+  const uint64_t hi = udiv_magic(lin, ps.mT[q], ps.shT[q]);
+  const uint64_t lo = lin - udiv_magic(lin, ps.mS[q], ps.shS[q]) * ps.S[q];
+  return hi * ps.S[q] + lo;
+}
+
+struct LinSpec {
+  int d;
+  int64_t stride[32];
+};
+
+__global__ void __launch_bounds__(256) k_linearize(const int64_t *__restrict__ coords, int64_t n,
+                                                   LinSpec ls, uint64_t *__restrict__ lin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t *c = coords + i * ls.d;
+    uint64_t x = 0;
+    for (int k = 0; k < ls.d; ++k) x += (uint64_t)c[k] * (uint64_t)ls.stride[k];
+    lin[i] = x;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_part_hist(const uint64_t *__restrict__ lin, int64_t n,
+                                                   PartSpec ps, uint32_t *__restrict__ bh) {
+  extern __shared__ uint32_t hsm[];
+  const int nbk = 1 << ps.bits, tot = ps.g * nbk;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) hsm[e] = 0;
+  __syncthreads();
+  const int64_t i0 = blockIdx.x * ps.chunk, i1 = min(n, i0 + ps.chunk);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint64_t x = lin[i];
+    for (int q = 0; q < ps.g; ++q) {
+      const uint32_t b = (uint32_t)(mix64(drop_digit(x, ps, q)) >> (64 - ps.bits));
+      atomicAdd(&hsm[q * nbk + b], 1u);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) bh[(int64_t)blockIdx.x * tot + e] = hsm[e];
+}
+
+// Per (pivot, bucket) slot: exclusive prefix over blocks in place, totals out.
+__global__ void k_part_scan_blocks(uint32_t *__restrict__ bh, int nb, int tot,
+                                   uint32_t *__restrict__ total) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  uint32_t run = 0;
+  for (int b = 0; b < nb; ++b) {
+    const uint32_t c = bh[(int64_t)b * tot + e];
+    bh[(int64_t)b * tot + e] = run;
+    run += c;
+  }
+  total[e] = run;
+}
+
+// Bucket start offsets per pivot (exclusive scan of totals, one CTA per
+// pivot), plus q * n so that every pivot has its own n-slot region.
+__global__ void __launch_bounds__(1024) k_part_scan_buckets(const uint32_t *__restrict__ total,
+                                                            int nbk, int64_t n,
+                                                            int64_t *__restrict__ base) {
+  __shared__ int64_t s[1024];
+  const int q = blockIdx.x;
+  const int per = (nbk + 1023) / 1024;
+  const int b0 = threadIdx.x * per;
+  int64_t loc = 0;
+  for (int j = 0; j < per; ++j)
+    if (b0 + j < nbk) loc += total[q * nbk + b0 + j];
+  s[threadIdx.x] = loc;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int64_t v = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = s[threadIdx.x] - loc + (int64_t)q * n;
+  for (int j = 0; j < per; ++j)
+    if (b0 + j < nbk) {
+      base[q * nbk + b0 + j] = run;
+      run += total[q * nbk + b0 + j];
+    }
+}
+
+__global__ void __launch_bounds__(512) k_part_scatter(const uint64_t *__restrict__ lin, int64_t n,
+                                                      PartSpec ps, const uint32_t *__restrict__ bh,
+                                                      const int64_t *__restrict__ base,
+                                                      uint64_t *__restrict__ keys) {
+  extern __shared__ unsigned long long cur[];
+  const int nbk = 1 << ps.bits, tot = ps.g * nbk;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x)
+    cur[e] = (unsigned long long)(base[e] + bh[(int64_t)blockIdx.x * tot + e]);
+  __syncthreads();
+  const int64_t i0 = blockIdx.x * ps.chunk, i1 = min(n, i0 + ps.chunk);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint64_t x = lin[i];
+    for (int q = 0; q < ps.g; ++q) {
+      const uint64_t key = drop_digit(x, ps, q);
+      const uint32_t b = (uint32_t)(mix64(key) >> (64 - ps.bits));
+      const unsigned long long pos = atomicAdd(&cur[q * nbk + b], 1ull);
+      keys[pos] = key;
+    }
+  }
+}
+
+// One CTA per (bucket, pivot): distinct keys of the bucket via a shared
+// open-addressing set.  flags[q] = 1 if a bucket exceeded the table.
+__global__ void __launch_bounds__(256) k_part_count(const uint64_t *__restrict__ keys,
+                                                    const int64_t *__restrict__ base,
+                                                    const uint32_t *__restrict__ total, int nbk,
+                                                    unsigned long long *__restrict__ counts,
+                                                    int *__restrict__ flags) {
+  extern __shared__ unsigned long long tab[];
+  __shared__ unsigned long long s_cnt;
+  const int b = blockIdx.x, q = blockIdx.y;
+  const int64_t start = base[q * nbk + b];
+  const int len = (int)total[q * nbk + b];
+  if (len == 0) return;
+  int T = 64;
+  while (T < 2 * len) T <<= 1;
+  if (T > PC_TMAX) {
+    if (threadIdx.x == 0) flags[q] = 1;
+    return;
+  }
+  for (int e = threadIdx.x; e < T; e += blockDim.x) tab[e] = ~0ull;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const uint64_t mask = (uint64_t)T - 1;
+  unsigned long long fresh = 0;
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {
+    const uint64_t key = keys[start + j];
+    uint64_t h = mix64(key) & mask;
+    while (true) {
+      const unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)key);
+      if (old == ~0ull) {
+        ++fresh;
+        break;
+      }
+      if (old == key) break;
+      h = (h + 1) & mask;
+    }
+  }
+  for (int off = 16; off; off >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, off);
+  if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(&s_cnt, fresh);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(counts + q, s_cnt);
+}
+
 __global__ void k_count_changes(const uint64_t *k, int64_t n, unsigned long long *out) {
   unsigned long long c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -821,6 +992,117 @@ static size_t sort_coords_bytes(int64_t nnz, bool with_perm) {
 
 using namespace ftt;
 
+namespace {
+
+void magic_u63(uint64_t D, uint64_t *m, int *sh) {
+  // floor(x / D) = mulhi(x, m) >> sh for all x < 2^63 (Granlund-Montgomery,
+  // N = 63: m = floor(2^(63+l) / D) + 1 < 2^64, l = ceil(log2 D)); D = 1 -> sh = -1
+  if (D <= 1) {
+    *m = 0;
+    *sh = -1;
+    return;
+  }
+  int l = 0;
+  while (((unsigned __int128)1 << l) < D) ++l;
+  const unsigned __int128 num = (unsigned __int128)1 << (63 + l);
+  *m = (uint64_t)(num / D + 1);
+  *sh = l - 1;
+}
+
+int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                           const int64_t *dims, int64_t *counts_host) {
+  // bucket bits: ~2048 keys per bucket on average
+  int bits = 4;
+  while (bits < 12 && (nnz >> bits) > 2048) ++bits;
+  const int nbk = 1 << bits;
+  const int G = std::max(1, std::min(std::min((int)d, PC_MAXG), 16384 / nbk));
+  const int nb = 2 * kNumSMs;
+  LinSpec ls;
+  ls.d = d;
+  {
+    int64_t st = 1;
+    for (int k = d - 1; k >= 0; --k) {
+      ls.stride[k] = st;
+      st *= dims[k];
+    }
+  }
+  uint64_t *lin = nullptr, *keys = nullptr;
+  uint32_t *bh = nullptr, *total = nullptr;
+  int64_t *base = nullptr;
+  unsigned long long *cnt = nullptr;
+  int *flags = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&lin, 8 * (size_t)nnz));
+  FTT_CHECK(owned_alloc(ctx, (void **)&keys, 8 * (size_t)nnz * G));
+  FTT_CHECK(owned_alloc(ctx, (void **)&bh, 4 * (size_t)nb * G * nbk));
+  FTT_CHECK(owned_alloc(ctx, (void **)&total, 4 * (size_t)G * nbk));
+  FTT_CHECK(owned_alloc(ctx, (void **)&base, 8 * (size_t)G * nbk));
+  FTT_CHECK(owned_alloc(ctx, (void **)&cnt, 8 * 32 + 4 * 32));
+  flags = reinterpret_cast<int *>(cnt + 32);
+  FTT_CUDA(cudaMemsetAsync(cnt, 0, 8 * 32 + 4 * 32, ctx->stream));
+  static bool attrs = false;
+  if (!attrs) {
+    FTT_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    FTT_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  131072));
+    FTT_CUDA(cudaFuncSetAttribute(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  8 * PC_TMAX));
+    attrs = true;
+  }
+  int pb = prof_begin(ctx);
+  k_linearize<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(coords, nnz, ls, lin);
+  FTT_LAUNCHED(ctx);
+  prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0), 0.0);
+  for (int p0 = 0; p0 < d; p0 += G) {
+    PartSpec ps;
+    ps.g = std::min(G, d - p0);
+    ps.bits = bits;
+    ps.chunk = ceil_div(nnz, nb);
+    for (int q = 0; q < ps.g; ++q) {
+      const int p = p0 + q;
+      const uint64_t S = (uint64_t)ls.stride[p];
+      ps.S[q] = S;
+      magic_u63(S, &ps.mS[q], &ps.shS[q]);
+      magic_u63(S * (uint64_t)dims[p], &ps.mT[q], &ps.shT[q]);
+    }
+    const int tot = ps.g * nbk;
+    pb = prof_begin(ctx);
+    k_part_hist<<<nb, 512, 4 * (size_t)tot, ctx->stream>>>(lin, nnz, ps, bh);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb, PT_HIST, 8.0 * (double)nnz + 4.0 * nb * tot, 0.0);
+    k_part_scan_blocks<<<(unsigned)ceil_div(tot, 256), 256, 0, ctx->stream>>>(bh, nb, tot, total);
+    FTT_LAUNCHED(ctx);
+    k_part_scan_buckets<<<ps.g, 1024, 0, ctx->stream>>>(total, nbk, nnz, base);
+    FTT_LAUNCHED(ctx);
+    pb = prof_begin(ctx);
+    k_part_scatter<<<nb, 512, 8 * (size_t)tot, ctx->stream>>>(lin, nnz, ps, bh, base, keys);
+    FTT_LAUNCHED(ctx);
+    // read lin, write one key per pivot
+    prof_end(ctx, pb, PT_SORT, (double)nnz * (8.0 + 8.0 * ps.g), 0.0);
+    pb = prof_begin(ctx);
+    k_part_count<<<dim3(nbk, ps.g), 256, 8 * PC_TMAX, ctx->stream>>>(keys, base, total, nbk,
+                                                                      cnt + p0, flags + p0);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz * ps.g, 0.0);
+  }
+  unsigned long long h[32];
+  int hf[32];
+  FTT_CHECK(copy_to_host(ctx, h, cnt, 8 * 32));
+  FTT_CHECK(copy_to_host(ctx, hf, flags, 4 * 32));
+  owned_free(ctx, lin);
+  owned_free(ctx, keys);
+  owned_free(ctx, bh);
+  owned_free(ctx, total);
+  owned_free(ctx, base);
+  owned_free(ctx, cnt);
+  for (int p = 0; p < d; ++p) {
+    if (hf[p]) FTT_CHECK(ftt_fiber_count(ctx, coords, nnz, d, dims, p, &counts_host[p]));
+    else counts_host[p] = (int64_t)h[p];
+  }
+  return FTT_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int ftt_fiber_count(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
@@ -873,11 +1155,17 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
   int lg = 1;
   while (((int64_t)1 << lg) < 2 * nnz) ++lg;
   const int64_t T = (int64_t)1 << lg;
-  if (8 * T > ((int64_t)32 << 20)) {
+  const char *path = getenv("FTT_COUNT_PATH");  // test override: hash | part | sort
+  const bool force_part = path && !strcmp(path, "part");
+  const bool force_sort = path && !strcmp(path, "sort");
+  const bool force_hash = path && !strcmp(path, "hash");
+  if (force_sort) {
     for (int p = 0; p < d; ++p)
       FTT_CHECK(ftt_fiber_count(ctx, coords, nnz, d, dims_host, p, &counts_host[p]));
     return FTT_OK;
   }
+  if (force_part || (!force_hash && 8 * T > ((int64_t)32 << 20)))
+    return fiber_counts_partition(ctx, coords, nnz, d, dims_host, counts_host);
   int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));  // 4 GiB
   uint64_t *tables = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&tables, 8 * (size_t)T * group));

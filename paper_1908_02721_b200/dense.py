@@ -74,7 +74,9 @@ def lowrank_k(min_dim: int, hint) -> int:
 
 def dev_svd_values_lowrank(buf, m: int, n: int, ld: int, row_major: bool, k: int,
                            delta2: float):
-    """Phase 1 of the certified low-rank path: (s[k], rest2, accepted)."""
+    """Phase 1 of the certified low-rank path: (s[k], rest2, accepted) with
+    accepted 2 = residual below full-SVD noise, 1 = rest2 <= 1e-6 delta^2
+    (interval-certified use only), 0 = rejected."""
     s = np.zeros(k)
     rest2 = nat.ctypes.c_double(0.0)
     acc = nat.ctypes.c_int32(0)
@@ -82,18 +84,30 @@ def dev_svd_values_lowrank(buf, m: int, n: int, ld: int, row_major: bool, k: int
         nat.context(), int(m), int(n), nat.ptr(buf), int(ld), int(bool(row_major)), int(k),
         float(delta2), s.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_double)),
         nat.ctypes.byref(rest2), nat.ctypes.byref(acc)), "ftt_svd_lowrank_f64")
-    return s, float(rest2.value), bool(acc.value)
+    return s, float(rest2.value), int(acc.value)
 
 
-def dev_svd_truncate(buf, m: int, n: int, ld: int, row_major: bool, delta, hint=None):
+def dev_svd_truncate(buf, m: int, n: int, ld: int, row_major: bool, delta, hint=None,
+                     interval_ok: bool = False):
     """Phase 1 for a truncation step: (s, rest2). Tries the certified
-    low-rank path when delta > 0, else (or on rejection) the full SVD."""
+    low-rank path when delta > 0, else (or on rejection) the full SVD.
+
+    The low-rank values bound every true tail sum of the operand inside
+    [tail_B(r), tail_B(r) + rest2] (Ky Fan: A^T A = B^T B + E^T E with
+    ||E||_F^2 = rest2).  A residual above the full-SVD noise level is still
+    used (``interval_ok``, static budgets) when the rank rule gives the same
+    answer at both ends of that interval -- then the decision is the exact
+    arithmetic one, like the reference's."""
     if delta is not None and delta > 0.0:
         k = lowrank_k(min(m, n), hint)
         if k:
-            s, rest2, ok = dev_svd_values_lowrank(buf, m, n, ld, row_major, k, delta * delta)
-            if ok:
+            s, rest2, acc = dev_svd_values_lowrank(buf, m, n, ld, row_major, k, delta * delta)
+            if acc == 2:
                 return s, rest2
+            if acc == 1 and interval_ok:
+                shape = (m, n)
+                if tail_rank(s, delta, shape, 0.0) == tail_rank(s, delta, shape, rest2):
+                    return s, rest2
     return dev_svd_values(buf, m, n, ld, row_major), 0.0
 
 

@@ -505,7 +505,8 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
         C = cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
         m = r0 * n
-        s, rest2 = dev_svd_truncate(C, m, r1, r1, True, policy.delta_first(k), hint)
+        s, rest2 = dev_svd_truncate(C, m, r1, r1, True, policy.delta_first(k), hint,
+                                    policy.kind == "static")
         rank, _ = policy.first(k, s, (m, r1), rest2)
         hint = rank
         if rank == 0:
@@ -539,7 +540,8 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
     for k in range(pivot, 0, -1):  # :348-355
         C = cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
-        s, rest2 = dev_svd_truncate(C, n * r1, r0, n * r1, False, policy.delta_second(k), hint)
+        s, rest2 = dev_svd_truncate(C, n * r1, r0, n * r1, False, policy.delta_second(k), hint,
+                                    policy.kind == "static")
         rank, _ = policy.second(k, s, (n * r1, r0), rest2)
         hint = rank
         if rank == 0:

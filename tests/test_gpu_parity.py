@@ -375,3 +375,28 @@ def test_tt_entries_meet_in_the_middle(dims, ranks, n):
     coords = coords[np.lexsort(coords.T[::-1])]  # sorted like SparseTensor input
     got = ft.tt_entries(ft.TTTensor(cores), coords)
     assert rel_err(got, O.tt_entries(cores, coords)) < 1e-12
+
+
+@pytest.mark.parametrize("path", ["hash", "part", "sort"])
+def test_fiber_counts_all_paths(path, monkeypatch):
+    """Exact distinct fixed-tuple counts per pivot through every device path
+    (shared hash set, bucket partition + shared hash sets, radix sort),
+    including a pivot whose fibers are so long that one partition bucket
+    overflows its shared table (falls back to the sort)."""
+    rng = np.random.default_rng(5)
+    dims = (40, 3, 50, 7, 64, 9)
+    base = np.stack([rng.integers(0, n, 60000) for n in dims], axis=1)
+    reps = base[rng.integers(0, 60000, 250000)]
+    reps[:, 2] = rng.integers(0, 50, reps.shape[0])  # long fibers along mode 2
+    coords = np.unique(reps, axis=0)
+    long = np.zeros((20000, 3), dtype=np.int64)
+    long[:, 0] = np.arange(20000)  # one fiber of 20000 nonzeros along mode 0
+    cases = [(dims, coords), ((20000, 2, 2), long)]
+    monkeypatch.setenv("FTT_COUNT_PATH", path)
+    for shape, c in cases:
+        t = ft.SparseTensor(shape, c, np.ones(c.shape[0]))
+        want = []
+        for p in range(len(shape)):
+            rest = np.delete(c, p, axis=1)
+            want.append(int(np.unique(rest, axis=0).shape[0]))
+        assert P._fiber_counts_device(t) == want
