@@ -135,7 +135,7 @@ constexpr size_t CQ_SMEM = 3 * sizeof(double) * CQ_MAX * (CQ_MAX + 1);
 // of Y^T Y (relative pivot cutoff tau) and the pivot order (sel_dev[0..r)
 // are the columns of a well-conditioned spanning subset).
 int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau, int64_t *sel_dev,
-                int64_t *rank) {
+                int64_t *rank, const double *aux_dev, double *aux_host) {
   *rank = 0;
   if (k <= 0 || k > CQ_MAX) {
     set_error("sketch_rank: k out of range");
@@ -157,8 +157,14 @@ int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau
   FTT_CHECK(gemm(ctx, 1, 0, k, k, mA, 1.0, Y, mA, Y, mA, 0.0, G, k, sk, ske));
   k_chol_inv<<<1, 256, CQ_SMEM, ctx->stream>>>((int)k, G, k, tau, M, dev_r, sel_dev);
   FTT_LAUNCHED(ctx);
-  int r = 0;
-  FTT_CHECK(copy_to_host(ctx, &r, dev_r, sizeof(int)));
+  // one round trip for the rank and the caller's device scalar
+  if (aux_dev)
+    FTT_CUDA(cudaMemcpyAsync(dev_r + 2, aux_dev, sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  int hb[4] = {0, 0, 0, 0};
+  FTT_CHECK(copy_to_host(ctx, hb, dev_r, aux_dev ? 16 : 4));
+  const int r = hb[0];
+  if (aux_dev && aux_host) memcpy(aux_host, hb + 2, sizeof(double));
   owned_free(ctx, G);
   owned_free(ctx, M);
   owned_free(ctx, sk);

@@ -11,10 +11,11 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
          int64_t ldc, double *splitk_ws, size_t splitk_ws_elems);
 size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k);
 // ||R0 - op(A) op(B)||_F^2 without materialising the residual (R0 stored
-// transposed when r_trans).
+// transposed when r_trans), to the host (out_host) and/or left in device
+// memory (out_dev).
 int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k,
                      const double *A, int64_t lda, const double *B, int64_t ldb, const double *R0,
-                     int64_t ldr, int r_trans, double *out_host);
+                     int64_t ldr, int r_trans, double *out_host, double *out_dev = nullptr);
 int transpose(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *src, int64_t lds,
               double *dst, int64_t ldd);
 
@@ -36,8 +37,9 @@ size_t qr_apply_workspace_elems(int64_t m, int64_t n, int64_t r);
 // Numerical rank r of the sketch Y (mA x k <= 64) and its pivot order
 // (sel_dev, k entries; the first r span Y) from a pivoted Cholesky of the
 // Gram (ftt_cholqr.cu).
+// aux_dev (optional): one device double fetched in the same round trip.
 int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau, int64_t *sel_dev,
-                int64_t *rank);
+                int64_t *rank, const double *aux_dev = nullptr, double *aux_host = nullptr);
 
 int check_finite(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, bool *ok);
 int copy_matrix(ftt_ctx *ctx, int64_t m, int64_t n, const double *src, int64_t lds, double *dst,

@@ -340,9 +340,12 @@ int bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops) {
 // deterministic (fixed tile grid, fixed-order reduction).
 int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k,
                      const double *A, int64_t lda, const double *B, int64_t ldb, const double *R0,
-                     int64_t ldr, int r_trans, double *out_host) {
-  *out_host = 0.0;
-  if (m <= 0 || n <= 0) return FTT_OK;
+                     int64_t ldr, int r_trans, double *out_host, double *out_dev) {
+  if (out_host) *out_host = 0.0;
+  if (m <= 0 || n <= 0) {
+    if (out_dev) FTT_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), ctx->stream));
+    return FTT_OK;
+  }
   const int64_t tiles_m = ceil_div(m, BM), tiles_n = ceil_div(n, BN);
   if (tiles_n > 65535) {
     set_error("gemm_resid_sumsq: too many column tiles");
@@ -363,9 +366,9 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
   else FTT_RESID_LAUNCH(true, true);
 #undef FTT_RESID_LAUNCH
   FTT_LAUNCHED(ctx);
-  k_sum_partials<<<1, 1024, 0, ctx->stream>>>(npart, nt, npart + nt);
+  k_sum_partials<<<1, 1024, 0, ctx->stream>>>(npart, nt, out_dev ? out_dev : npart + nt);
   FTT_LAUNCHED(ctx);
-  FTT_CHECK(copy_to_host(ctx, out_host, npart + nt, sizeof(double)));
+  if (out_host) FTT_CHECK(copy_to_host(ctx, out_host, npart + nt, sizeof(double)));
   owned_free(ctx, npart);
   return FTT_OK;
 }

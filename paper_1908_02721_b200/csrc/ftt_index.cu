@@ -934,14 +934,22 @@ int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in, u
 }
 
 int sum_squares(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_host) {
-  *out_host = 0.0;
-  if (n <= 0) return FTT_OK;
+  FTT_CHECK(sum_squares_dev(ctx, n, x, partial, partial + kSumSqBlocks));
+  return copy_to_host(ctx, out_host, partial + kSumSqBlocks, sizeof(double));
+}
+
+// The same, leaving the total in device memory (*out_dev; 0 for n <= 0).
+int sum_squares_dev(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_dev) {
+  if (n <= 0) {
+    FTT_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), ctx->stream));
+    return FTT_OK;
+  }
   int nb = grid_for(n, 256, 4, kSumSqBlocks);
   k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, nullptr, partial);
   FTT_LAUNCHED(ctx);
-  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, partial + nb);
+  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, out_dev);
   FTT_LAUNCHED(ctx);
-  return copy_to_host(ctx, out_host, partial + nb, sizeof(double));
+  return FTT_OK;
 }
 
 int scan_block_counts(ftt_ctx *ctx, int64_t *counts, int64_t nblocks, int64_t *total_dev) {

@@ -51,12 +51,18 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// 32 per-lane slots -> lane l receives the warp-wide sum of slot l (31
-// shuffles: at offset s each lane keeps the upper or lower s slots by bit s
-// of its lane id and adds the partner's copy).
-__device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
+// W per-lane slots (W = 8, 16, 32) -> lane l receives the warp-wide sum of
+// slot l mod W: lanes differing in the bits >= log2(W) are folded first,
+// then a halving exchange (at offset s each lane keeps the upper or lower s
+// slots by bit s of its lane id and adds the partner's copy).
+template <int W>
+__device__ __forceinline__ double reduce_scatter(double (&v)[32], int lane) {
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
+  for (int o = 16; o >= W; o >>= 1)
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+#pragma unroll
+  for (int s = W / 2; s >= 1; s >>= 1) {
     const bool upper = (lane & s) != 0;
 #pragma unroll
     for (int j = 0; j < s; ++j) {
@@ -79,19 +85,25 @@ struct Scratch {
 };
 
 // Column sums over the CTA of x * b[t] (t < NMAX) -> red[warp][t], in chunks
-// of 32 slots (warp reduce-scatter: lane l ends with the warp sum of slot l).
+// of up to 32 slots (warp reduce-scatter: lane l ends with the warp sum of
+// slot l).
+template <int NMAX, int H, int W>
+__device__ __forceinline__ void chunk_partials(double (*red)[NMAX], double x, const double (&b)[NMAX],
+                                               int lane, int warp) {
+  double p[32];
+#pragma unroll
+  for (int t = 0; t < 32; ++t) p[t] = (t < W && H + t < NMAX) ? x * b[H + t] : 0.0;
+  const double tot = reduce_scatter<W>(p, lane);
+  if (lane < W && H + lane < NMAX) red[warp][H + lane] = tot;
+}
+
 template <int NMAX>
 __device__ __forceinline__ void block_partials(double (*red)[NMAX], double x,
                                                const double (&b)[NMAX]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int h = 0; h < NMAX; h += 32) {
-    double p[32];
-#pragma unroll
-    for (int t = 0; t < 32; ++t) p[t] = h + t < NMAX ? x * b[h + t] : 0.0;
-    const double tot = reduce_scatter32(p, lane);
-    if (h + lane < NMAX) red[warp][h + lane] = tot;
-  }
+  constexpr int W0 = NMAX >= 24 ? 32 : (NMAX > 8 ? 16 : 8);
+  chunk_partials<NMAX, 0, W0>(red, x, b, lane, warp);
+  if constexpr (NMAX > 32) chunk_partials<NMAX, 32, (NMAX - 32 > 16 ? 32 : 16)>(red, x, b, lane, warp);
 }
 
 template <int NMAX>
@@ -420,7 +432,7 @@ __global__ void __launch_bounds__(256) k_tsqr_expand(int64_t M, int n, int r, in
 constexpr size_t kSmemCapBytes = 200 * 1024;
 constexpr int kCapElems = (int)(kSmemCapBytes / 8);
 
-int nmax_for(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64; }
+int nmax_for(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : n <= 24 ? 24 : n <= 32 ? 32 : n <= 48 ? 48 : 64; }
 
 bool attrs_set = false;
 int set_attrs() {
@@ -430,6 +442,8 @@ int set_attrs() {
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<8>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<16>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<32>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<24>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<48>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<64>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_jacobi_small, a, cap));
   attrs_set = true;
@@ -451,6 +465,14 @@ void launch_level(ftt_ctx *ctx, int n, unsigned grid, int64_t M, const double *A
       break;
     case 32:
       k_tsqr_level<32><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+                                                          status);
+      break;
+    case 24:
+      k_tsqr_level<24><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+                                                          status);
+      break;
+    case 48:
+      k_tsqr_level<48><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                           status);
       break;
     default:
@@ -535,7 +557,7 @@ static int tsqr_expand(ftt_ctx *ctx, const Tree &t, int n, int r, const std::vec
 }
 
 int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, int trans,
-           double *Q, int64_t ldq, double *R, int64_t ldr) {
+           double *Q, int64_t ldq, double *R, int64_t ldr, bool check) {
   const int n = (int)n64;
   FTT_CHECK(set_attrs());
   int *status = nullptr;
@@ -560,7 +582,7 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, i
   }
   for (double *p : qs) owned_free(ctx, p);
   int h = 0;
-  FTT_CHECK(copy_to_host(ctx, &h, status, sizeof(int)));
+  if (check) FTT_CHECK(copy_to_host(ctx, &h, status, sizeof(int)));
   owned_free(ctx, status);
   if (h & 1) {
     set_error("matrix entries must be finite");

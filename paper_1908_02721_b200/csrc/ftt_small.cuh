@@ -8,8 +8,10 @@ namespace ftt {
 bool tsqr_ok(int64_t m, int64_t n);
 
 // Q (M x n, ld ldq) and R (n x n, ld ldr, diag >= 0; may be NULL) of A_tall.
+// check = false skips the finite-input check (no host round trip) when the
+// caller already knows the input is finite.
 int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int trans, double *Q,
-           int64_t ldq, double *R, int64_t ldr);
+           int64_t ldq, double *R, int64_t ldr, bool check = true);
 
 // Thin SVD core: U = Q P (M x n, ld ldu), Y = R^T P (n x n), norms_host[j] =
 // ||Y_j|| (unsorted; sigma up to the caller's permutation).

@@ -454,9 +454,10 @@ __global__ void k_gather_cols(int64_t rows, int64_t src_rows, int64_t r, const d
 
 // _fix_signs (linalg.py:56-63): first argmax |U[:, j]|; flip U[:, j] and
 // V[:, j] if that entry is negative; then optionally V[:, j] *= s[j].
-__global__ void k_fix_signs(int64_t mu, int64_t mv, double *__restrict__ U, int64_t ldu,
-                            double *__restrict__ V, int64_t ldv, const double *__restrict__ sig,
-                            int scale_v) {
+// k_sign_pick: one CTA per column decides the sign (fixed-order tree);
+// k_sign_apply: grid (rank, chunks) rescales the rows.
+__global__ void k_sign_pick(int64_t mu, const double *__restrict__ U, int64_t ldu,
+                            double *__restrict__ fac) {
   const int64_t j = blockIdx.x;
   __shared__ double sv[256];
   __shared__ int64_t si[256];
@@ -483,13 +484,22 @@ __global__ void k_fix_signs(int64_t mu, int64_t mv, double *__restrict__ U, int6
     }
     __syncthreads();
   }
-  const bool flip = U[si[0] + j * ldu] < 0.0;
-  const double sc = scale_v ? sig[j] : 1.0;
-  if (flip)
-    for (int64_t i = threadIdx.x; i < mu; i += blockDim.x) U[i + j * ldu] = -U[i + j * ldu];
-  const double f = flip ? -sc : sc;
-  if (f != 1.0)
-    for (int64_t i = threadIdx.x; i < mv; i += blockDim.x) V[i + j * ldv] *= f;
+  if (threadIdx.x == 0) fac[j] = U[si[0] + j * ldu] < 0.0 ? -1.0 : 1.0;
+}
+
+__global__ void k_sign_apply(int64_t mu, int64_t mv, double *__restrict__ U, int64_t ldu,
+                             double *__restrict__ V, int64_t ldv, const double *__restrict__ fac,
+                             const double *__restrict__ sig, int scale_v) {
+  const int64_t j = blockIdx.x;
+  const double fu = fac[j];
+  const double fv = fu * (scale_v ? sig[j] : 1.0);
+  const int64_t nch = gridDim.y, c = blockIdx.y;
+  const int64_t u0 = mu * c / nch, u1 = mu * (c + 1) / nch;
+  const int64_t v0 = mv * c / nch, v1 = mv * (c + 1) / nch;
+  if (fu != 1.0)
+    for (int64_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) U[i + j * ldu] = -U[i + j * ldu];
+  if (fv != 1.0)
+    for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) V[i + j * ldv] *= fv;
 }
 
 }  // namespace
@@ -828,9 +838,11 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   const double *buf = A;
   int64_t ld = lda;
   double fro2 = 0.0, rest2 = 0.0;
+  // ||A||_F^2 stays on the device until the sketch rank comes back (one host
+  // round trip for both); a non-finite entry is diagnosed there
+  double *fro2_dev = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 2)));
   {
-    FTT_CHECK(arena_reserve(ctx, align_up(8 * (kSumSqBlocks + 1)) + 256));
-    double *partial = take<double>(ctx, kSumSqBlocks + 1);
     const int64_t inner = need_t ? nA : mA;
     if (lda != inner) {
       FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
@@ -838,18 +850,18 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
       buf = st->Af;
       ld = inner;
     }
-    FTT_CHECK(sum_squares(ctx, mA * nA, buf, partial, &fro2));
-    if (!std::isfinite(fro2)) {
-      // either a non-finite entry or an overflowing (but finite) energy
-      bool ok = true;
-      FTT_CHECK(check_finite(ctx, need_t ? nA : mA, need_t ? mA : nA, buf, ld, &ok));
-      if (!ok) {
-        set_error("matrix entries must be finite");
-        return FTT_ERR_NONFINITE;
-      }
-      return FTT_OK;  // not accepted: the caller takes the full SVD
-    }
+    FTT_CHECK(sum_squares_dev(ctx, mA * nA, buf, fro2_dev + 1, fro2_dev));
   }
+  auto finite_or_decline = [&]() -> int {
+    // non-finite energy: either a non-finite entry (error) or an overflow
+    bool ok = true;
+    FTT_CHECK(check_finite(ctx, need_t ? nA : mA, need_t ? mA : nA, buf, ld, &ok));
+    if (!ok) {
+      set_error("matrix entries must be finite");
+      return FTT_ERR_NONFINITE;
+    }
+    return FTT_OK;  // not accepted: the caller takes the full SVD
+  };
   double *Om = nullptr, *Yk = nullptr, *sk = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&Om, 8 * (size_t)nA * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&Yk, 8 * (size_t)mA * k));
@@ -871,24 +883,33 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
     int64_t kr = 0;
     int64_t *sel = nullptr;
     FTT_CHECK(owned_alloc(ctx, (void **)&sel, 8 * (size_t)k));
-    FTT_CHECK(sketch_rank(ctx, mA, k, Yk, 1e-11, sel, &kr));
-    if (kr == 0) {
+    FTT_CHECK(sketch_rank(ctx, mA, k, Yk, 1e-11, sel, &kr, fro2_dev, &fro2));
+    if (kr == 0 || !std::isfinite(fro2)) {
       owned_free(ctx, sel);
       owned_free(ctx, Om);
       owned_free(ctx, Yk);
       owned_free(ctx, sk);
-      return FTT_OK;  // no usable basis: the caller takes the full SVD
+      owned_free(ctx, fro2_dev);
+      return std::isfinite(fro2) ? FTT_OK : finite_or_decline();  // full SVD instead
     }
     double *Ys = nullptr;
     FTT_CHECK(owned_alloc(ctx, (void **)&Ys, 8 * (size_t)mA * kr));
     k_gather_cols<<<grid_for(mA * kr, 256, 4), 256, 0, ctx->stream>>>(mA, mA, kr, Yk, mA, sel,
                                                                       nullptr, Ys, mA);
     FTT_LAUNCHED(ctx);
-    FTT_CHECK(tsqr_q(ctx, mA, kr, Ys, mA, 0, st->Qk, mA, nullptr, 0));
+    FTT_CHECK(tsqr_q(ctx, mA, kr, Ys, mA, 0, st->Qk, mA, nullptr, 0, false));
     owned_free(ctx, Ys);
     owned_free(ctx, sel);
     k = kr;
   } else {
+    FTT_CHECK(copy_to_host(ctx, &fro2, fro2_dev, sizeof(double)));
+    if (!std::isfinite(fro2)) {
+      owned_free(ctx, Om);
+      owned_free(ctx, Yk);
+      owned_free(ctx, sk);
+      owned_free(ctx, fro2_dev);
+      return finite_or_decline();
+    }
     size_t wse = qr_workspace_elems(mA, k);
     FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * (size_t)k) +
                                      align_up(8 * qr_tblk_elems(mA, k)) + 4096));
@@ -904,6 +925,7 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   owned_free(ctx, Om);
   owned_free(ctx, Yk);
   owned_free(ctx, sk);
+  owned_free(ctx, fro2_dev);
   *rest2_host = rest2;
   // Acceptance: the residual energy must sit below the rounding noise a
   // backward-stable full SVD already carries in the tail sums
@@ -965,14 +987,21 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
   } else {
     FTT_CHECK(svd_raw_vectors(ctx, st, rank, UA, VA));
   }
-  FTT_CHECK(arena_reserve(ctx, align_up(8 * rank) + 256));
-  double *sig = take<double>(ctx, rank);
-  FTT_CUDA(cudaMemcpyAsync(sig, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
   double *UM = st->transposed ? VA : UA;
   double *VM = st->transposed ? UA : VA;
   const int64_t mu = st->transposed ? nA : mA;  // == caller m
   const int64_t mv = st->transposed ? mA : nA;  // == caller n
-  k_fix_signs<<<(unsigned)rank, 256, 0, ctx->stream>>>(mu, mv, UM, mu, VM, mv, sig, scale_v);
+  {
+    FTT_CHECK(arena_reserve(ctx, 2 * align_up(8 * rank) + 256));
+    double *sig2 = take<double>(ctx, rank);
+    double *fac = take<double>(ctx, rank);
+    FTT_CUDA(cudaMemcpyAsync(sig2, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+    k_sign_pick<<<(unsigned)rank, 256, 0, ctx->stream>>>(mu, UM, mu, fac);
+    FTT_LAUNCHED(ctx);
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(std::max(mu, mv), 4096)));
+    k_sign_apply<<<dim3((unsigned)rank, (unsigned)nch), 256, 0, ctx->stream>>>(mu, mv, UM, mu, VM, mv,
+                                                                              fac, sig2, scale_v);
+  }
   FTT_LAUNCHED(ctx);
   if (U) {
     if (u_row_major) FTT_CHECK(transpose(ctx, mu, rank, UM, mu, U, ldu));
