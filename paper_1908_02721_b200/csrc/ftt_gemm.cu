@@ -18,6 +18,8 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16, GT = 128;
 constexpr int PAD = 4;  // (64+4) doubles = 136 words == 8 banks: conflict-free fragment loads
 
+__device__ __forceinline__ int64_t ceil_div_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
@@ -30,18 +32,24 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 // R0 = C read-only, stored transposed when c_trans (R0(row, col) at
 // C[col + row * ldc]).  Used by the certified low-rank SVD to form
 // ||A - Q B||_F without materialising the residual.
-template <bool TA, bool TB, int EPI = 0>
+// Tile TBM x TBN (64x64, 128x32 for narrow outputs, 32x128 for short ones),
+// 4 warps of 32x32 each (4x4 DMMA 8x8 tiles), BK = 16, register prefetch of
+// the next k-tile into the second shared buffer.
+template <bool TA, bool TB, int EPI = 0, int TBM = 64, int TBN = 64>
 __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, double alpha,
                                               const double *__restrict__ A, int64_t lda,
                                               const double *__restrict__ B, int64_t ldb, double beta,
                                               double *__restrict__ C, int64_t ldc, int64_t kps,
                                               double *__restrict__ partial, int c_trans = 0,
                                               double *__restrict__ npart = nullptr) {
-  __shared__ double As[2][BK][BM + PAD];
-  __shared__ double Bs[2][BK][BN + PAD];
+  constexpr int WM = TBM / 32;           // warps along M
+  constexpr int RA = TBM * BK / GT;      // A-tile elements per thread
+  constexpr int RB = TBN * BK / GT;      // B-tile elements per thread
+  __shared__ double As[2][BK][TBM + PAD];
+  __shared__ double Bs[2][BK][TBN + PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
-  const int64_t tm = (int64_t)blockIdx.x * BM, tn = (int64_t)blockIdx.y * BN;
+  const int wm = (warp % WM) * 32, wn = (warp / WM) * 32;
+  const int64_t tm = (int64_t)blockIdx.x * TBM, tn = (int64_t)blockIdx.y * TBN;
   const int64_t kb = (int64_t)blockIdx.z * kps;
   const int64_t ke = min(k, kb + kps);
 
@@ -51,33 +59,36 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double ra[8], rb[8];
+  double ra[RA], rb[RB];
   auto load = [&](int64_t k0) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      int e = r * GT + tid;
+    for (int r = 0; r < RA; ++r) {
+      const int e = r * GT + tid;
       int i, kk;
       if (!TA) {
-        i = e % BM;
-        kk = e / BM;
+        i = e % TBM;
+        kk = e / TBM;
       } else {
         kk = e % BK;
         i = e / BK;
       }
-      int64_t gi = tm + i, gk = k0 + kk;
+      const int64_t gi = tm + i, gk = k0 + kk;
       double v = 0.0;
       if (gi < m && gk < ke) v = TA ? A[gk + gi * lda] : A[gi + gk * lda];
       ra[r] = v;
-      int j;
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int e = r * GT + tid;
+      int j, kk;
       if (!TB) {
         kk = e % BK;
         j = e / BK;
       } else {
-        j = e % BN;
-        kk = e / BN;
+        j = e % TBN;
+        kk = e / TBN;
       }
-      int64_t gj = tn + j;
-      gk = k0 + kk;
+      const int64_t gj = tn + j, gk = k0 + kk;
       double w = 0.0;
       if (gj < n && gk < ke) w = TB ? B[gj + gk * ldb] : B[gk + gj * ldb];
       rb[r] = w;
@@ -85,23 +96,28 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      int e = r * GT + tid;
-      int i, kk, j;
+    for (int r = 0; r < RA; ++r) {
+      const int e = r * GT + tid;
+      int i, kk;
       if (!TA) {
-        i = e % BM;
-        kk = e / BM;
+        i = e % TBM;
+        kk = e / TBM;
       } else {
         kk = e % BK;
         i = e / BK;
       }
       As[buf][kk][i] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int e = r * GT + tid;
+      int j, kk;
       if (!TB) {
         kk = e % BK;
         j = e / BK;
       } else {
-        j = e % BN;
-        kk = e / BN;
+        j = e % TBN;
+        kk = e / TBN;
       }
       Bs[buf][kk][j] = rb[r];
     }
@@ -171,6 +187,165 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
     }
   }
 }
+
+// ||R0 - Q B||_F^2 partials for a short inner dimension (k <= 64): a CTA
+// owns 128 rows, keeps its Q rows in shared memory for the whole sweep over
+// the column tiles (64 columns each, B tile staged per step), forms Q B on
+// the DMMA pipe and reads every R0 element exactly once (RT: R0 stored
+// transposed, R0(row, col) at R0[col + row * ldr]).  The general GEMM
+// epilogue path re-read the Q tile for every 64x64 output tile, i.e.
+// ~65x for the 314,928 x 4,160 operand of config 5.
+template <bool RT>
+__global__ void __launch_bounds__(128) k_resid_rows(int64_t m, int64_t n, int k, int kp,
+                                                    const double *__restrict__ Q, int64_t ldq,
+                                                    const double *__restrict__ B, int64_t ldb,
+                                                    const double *__restrict__ R0, int64_t ldr,
+                                                    int64_t tiles_per_cta,
+                                                    double *__restrict__ npart) {
+  extern __shared__ double rs_smem[];
+  double(*Qs)[128 + PAD] = reinterpret_cast<double(*)[128 + PAD]>(rs_smem);       // [kp][128]
+  double(*Bs)[64 + PAD] = reinterpret_cast<double(*)[64 + PAD]>(rs_smem + (size_t)kp * (128 + PAD));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t tm = (int64_t)blockIdx.x * 128;
+  for (int e = tid; e < kp * 128; e += 128) {
+    const int i = e % 128, kk = e / 128;
+    const int64_t gi = tm + i;
+    Qs[kk][i] = (gi < m && kk < k) ? Q[gi + (int64_t)kk * ldq] : 0.0;
+  }
+  double ss = 0.0;
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_cta;
+  const int64_t t1 = min(ceil_div_dev(n, 64), t0 + tiles_per_cta);
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t tn = t * 64;
+    __syncthreads();  // previous tile's Bs reads are done (and Qs is ready)
+    for (int e = tid; e < kp * 64; e += 128) {
+      const int kk = e % kp, j = e / kp;
+      const int64_t gj = tn + j;
+      Bs[kk][j] = (gj < n && kk < k) ? B[kk + gj * ldb] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][8][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int ks = 0; ks < kp; ks += 4) {
+      double a[4], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Qs[ks + (lane & 3)][warp * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Bs[ks + (lane & 3)][j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = tm + warp * 32 + i * 8 + (lane >> 2);
+      if (row >= m) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = tn + j * 8 + 2 * (lane & 3) + h;
+          if (col >= n) continue;
+          const double r0 = RT ? R0[col + row * ldr] : R0[row + col * ldr];
+          const double v = r0 - acc[i][j][h];
+          ss += v * v;
+        }
+    }
+  }
+  __shared__ double s_ss[4];
+#pragma unroll
+  for (int off = 16; off; off >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, off);
+  if (lane == 0) s_ss[warp] = ss;
+  __syncthreads();
+  if (tid == 0) npart[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = (s_ss[0] + s_ss[1]) + (s_ss[2] + s_ss[3]);
+}
+
+// Column-block variant for a column-major R0 (rows contiguous): a CTA owns
+// 64 columns and a chunk of `rows_per_cta` rows, keeps its B tile in shared
+// memory and steps down the rows 128 at a time (Q rows staged per step from
+// L2), so every CTA streams 64 contiguous column segments -- the row-block
+// order touched a new 2 MB page per 1 KB read on the 10.5 GB operand.
+__global__ void __launch_bounds__(128) k_resid_cols(int64_t m, int64_t n, int k, int kp,
+                                                    const double *__restrict__ Q, int64_t ldq,
+                                                    const double *__restrict__ B, int64_t ldb,
+                                                    const double *__restrict__ R0, int64_t ldr,
+                                                    int64_t rows_per_cta,
+                                                    double *__restrict__ npart) {
+  extern __shared__ double rs_smem[];
+  double(*Qs)[128 + PAD] = reinterpret_cast<double(*)[128 + PAD]>(rs_smem);       // [kp][128]
+  double(*Bs)[64 + PAD] = reinterpret_cast<double(*)[64 + PAD]>(rs_smem + (size_t)kp * (128 + PAD));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t tn = (int64_t)blockIdx.x * 64;
+  for (int e = tid; e < kp * 64; e += 128) {
+    const int kk = e % kp, j = e / kp;
+    const int64_t gj = tn + j;
+    Bs[kk][j] = (gj < n && kk < k) ? B[kk + gj * ldb] : 0.0;
+  }
+  double ss = 0.0;
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_cta;
+  const int64_t r_end = min(m, r_begin + rows_per_cta);
+  for (int64_t tm = r_begin; tm < r_end; tm += 128) {
+    __syncthreads();
+    for (int e = tid; e < kp * 128; e += 128) {
+      const int i = e % 128, kk = e / 128;
+      const int64_t gi = tm + i;
+      Qs[kk][i] = (gi < r_end && kk < k) ? Q[gi + (int64_t)kk * ldq] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][8][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int ks = 0; ks < kp; ks += 4) {
+      double a[4], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Qs[ks + (lane & 3)][warp * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Bs[ks + (lane & 3)][j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = tm + warp * 32 + i * 8 + (lane >> 2);
+      if (row >= r_end) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = tn + j * 8 + 2 * (lane & 3) + h;
+          if (col >= n) continue;
+          const double v = R0[row + col * ldr] - acc[i][j][h];
+          ss += v * v;
+        }
+    }
+  }
+  __shared__ double s_ss[4];
+#pragma unroll
+  for (int off = 16; off; off >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, off);
+  if (lane == 0) s_ss[warp] = ss;
+  __syncthreads();
+  if (tid == 0) npart[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = (s_ss[0] + s_ss[1]) + (s_ss[2] + s_ss[3]);
+}
+
+// Tile shape for an m x n output: narrow outputs (n <= 32) use 128x32,
+// short ones (m <= 32) 32x128 -- a 64x64 tile would spend half or more of
+// its DMMAs on padding.
+enum TileShape { T64x64 = 0, T128x32 = 1, T32x128 = 2 };
+inline TileShape pick_tile(int64_t m, int64_t n) {
+  if (n <= 32 && m > 32) return T128x32;
+  if (m <= 32 && n > 32) return T32x128;
+  return T64x64;
+}
+inline int tile_m(TileShape t) { return t == T128x32 ? 128 : (t == T32x128 ? 32 : 64); }
+inline int tile_n(TileShape t) { return t == T128x32 ? 32 : (t == T32x128 ? 128 : 64); }
 
 __global__ void k_sum_partials(const double *__restrict__ p, int64_t n, double *__restrict__ out) {
   __shared__ double s[1024];
@@ -256,13 +431,16 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
     FTT_LAUNCHED(ctx);
     return FTT_OK;
   }
-  int64_t tiles_m = ceil_div(m, BM), tiles_n = ceil_div(n, BN);
+  const TileShape ts = pick_tile(m, n);
+  int64_t tiles_m = ceil_div(m, tile_m(ts)), tiles_n = ceil_div(n, tile_n(ts));
   int64_t tiles = tiles_m * tiles_n;
   int splits = 1;
   if (tiles < 2 * ctx->num_sms && k >= 4 * 256) {
-    int64_t s = ceil_div(2 * ctx->num_sms, tiles);
+    // enough CTAs for ~8 per SM: long-K products with a small output (Gram
+    // matrices, B = Q^T A) are otherwise a handful of CTAs streaming all of K
+    int64_t s = ceil_div(8 * ctx->num_sms, tiles);
     s = std::min<int64_t>(s, k / 256);
-    s = std::min<int64_t>(s, 64);
+    s = std::min<int64_t>(s, 1024);
     if (splitk_ws) s = std::min<int64_t>(s, (int64_t)(splitk_ws_elems / (size_t)(m * n)));
     else s = 1;
     if (s > 1) splits = (int)s;
@@ -276,13 +454,20 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
   dim3 grid((unsigned)tiles_m, (unsigned)tiles_n, (unsigned)splits);
   double *part = splits > 1 ? splitk_ws : nullptr;
   const int pb = prof_begin(ctx);
-#define FTT_GEMM_LAUNCH(TA_, TB_)                                                          \
-  k_dgemm<TA_, TB_><<<grid, GT, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, \
-                                                  ldc, kps, part)
-  if (!ta && !tb) FTT_GEMM_LAUNCH(false, false);
-  else if (!ta && tb) FTT_GEMM_LAUNCH(false, true);
-  else if (ta && !tb) FTT_GEMM_LAUNCH(true, false);
-  else FTT_GEMM_LAUNCH(true, true);
+#define FTT_GEMM_LAUNCH(TA_, TB_, M_, N_)                                                     \
+  k_dgemm<TA_, TB_, 0, M_, N_><<<grid, GT, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, \
+                                                            beta, C, ldc, kps, part)
+#define FTT_GEMM_TILES(TA_, TB_)                                  \
+  do {                                                            \
+    if (ts == T128x32) FTT_GEMM_LAUNCH(TA_, TB_, 128, 32);        \
+    else if (ts == T32x128) FTT_GEMM_LAUNCH(TA_, TB_, 32, 128);   \
+    else FTT_GEMM_LAUNCH(TA_, TB_, 64, 64);                       \
+  } while (0)
+  if (!ta && !tb) FTT_GEMM_TILES(false, false);
+  else if (!ta && tb) FTT_GEMM_TILES(false, true);
+  else if (ta && !tb) FTT_GEMM_TILES(true, false);
+  else FTT_GEMM_TILES(true, true);
+#undef FTT_GEMM_TILES
 #undef FTT_GEMM_LAUNCH
   FTT_LAUNCHED(ctx);
   if (splits > 1) {
@@ -346,6 +531,52 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
     if (out_dev) FTT_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), ctx->stream));
     return FTT_OK;
   }
+  if (!ta && !tb && k >= 1 && k <= 64) {
+    // short inner dimension: Q / B tiles resident in shared memory, R0 read
+    // once in its contiguous direction (rows for a transposed R0, columns
+    // otherwise)
+    const int kp = (int)ceil_div(k, 4) * 4;
+    static bool attr = false;
+    if (!attr) {
+      const int mx = 8 * 64 * (128 + PAD + 64 + PAD);
+      FTT_CUDA(cudaFuncSetAttribute(k_resid_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      FTT_CUDA(cudaFuncSetAttribute(k_resid_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      attr = true;
+    }
+    const size_t smem = 8 * (size_t)kp * (128 + PAD + 64 + PAD);
+    dim3 grid;
+    int64_t per = 0;
+    if (r_trans) {
+      const int64_t rb = ceil_div(m, 128), ct = ceil_div(n, 64);
+      const int64_t chunks = std::min<int64_t>(ct, std::max<int64_t>(1, ceil_div(4 * ctx->num_sms, rb)));
+      per = ceil_div(ct, chunks);
+      grid = dim3((unsigned)rb, (unsigned)ceil_div(ct, per));
+    } else {
+      const int64_t cb = ceil_div(n, 64);
+      // row chunks: >= 8 CTAs per SM overall, >= 128 rows each
+      const int64_t want = std::max<int64_t>(1, ceil_div(8 * ctx->num_sms, cb));
+      per = std::max<int64_t>(128, ceil_div(ceil_div(m, want), 128) * 128);
+      grid = dim3((unsigned)cb, (unsigned)ceil_div(m, per));
+    }
+    const int64_t nt = (int64_t)grid.x * grid.y;
+    double *npart = nullptr;
+    FTT_CHECK(owned_alloc(ctx, (void **)&npart, 8 * (size_t)(nt + 1)));
+    const int pb = prof_begin(ctx);
+    if (r_trans)
+      k_resid_rows<true><<<grid, 128, smem, ctx->stream>>>(m, n, (int)k, kp, A, lda, B, ldb, R0, ldr,
+                                                           per, npart);
+    else
+      k_resid_cols<<<grid, 128, smem, ctx->stream>>>(m, n, (int)k, kp, A, lda, B, ldb, R0, ldr, per,
+                                                     npart);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb, PT_GEMM, 8.0 * ((double)m * n + (double)m * k + (double)k * n),
+             2.0 * (double)m * n * k);
+    k_sum_partials<<<1, 1024, 0, ctx->stream>>>(npart, nt, out_dev ? out_dev : npart + nt);
+    FTT_LAUNCHED(ctx);
+    if (out_host) FTT_CHECK(copy_to_host(ctx, out_host, npart + nt, sizeof(double)));
+    owned_free(ctx, npart);
+    return FTT_OK;
+  }
   const int64_t tiles_m = ceil_div(m, BM), tiles_n = ceil_div(n, BN);
   if (tiles_n > 65535) {
     set_error("gemm_resid_sumsq: too many column tiles");
@@ -374,9 +605,10 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
 }
 
 size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k) {
-  int64_t tiles = ceil_div(m, BM) * ceil_div(n, BN);
+  const TileShape ts = pick_tile(m, n);
+  int64_t tiles = ceil_div(m, tile_m(ts)) * ceil_div(n, tile_n(ts));
   if (tiles >= 2 * kNumSMs || k < 4 * 256) return 0;
-  int64_t s = std::min<int64_t>(std::min<int64_t>(ceil_div(2 * kNumSMs, tiles), k / 256), 64);
+  int64_t s = std::min<int64_t>(std::min<int64_t>(ceil_div(8 * kNumSMs, tiles), k / 256), 1024);
   return s > 1 ? (size_t)(s * m * n) : 0;
 }
 
