@@ -10,7 +10,9 @@ What comes from where:
 
 * ``small``: 24 seeded small tensors x every pivot x 3 modes, run through the
   reference ``fasttt`` -- cores, ranks, report fields, fiber arrays.
-* c1, c3: the reference ``fasttt(a, eps)`` at its own auto pivot.
+* c1: the reference ``fasttt(a, eps)`` at its own auto pivot.
+* c3: index goldens from the reference, train from the oracle (the reference's
+  own run at the auto pivot did not finish in > 3 h here; ``REF_C3=1`` runs it).
 * c2, c4, c5: the reference raises MemoryError at the auto pivot (it
   densifies the 0/1 cores, fasttt.py:246-255). Their integer goldens (pivot,
   per-pivot fiber counts, FiberSet, kept arrays, maps, lossless ranks) come
@@ -125,7 +127,12 @@ def config(cfg: int):
     meta["select_p_s"] = time.time() - t0
     meta["auto_pivot"] = int(p)
     meta["index"] = index_goldens(t, p)
-    if cfg in (1, 3):
+    # c3: the reference fasttt() at its auto pivot densifies two 0/1 cores and
+    # ran > 3 h in the 16-core build container without finishing; its train is
+    # taken from the oracle restatement (bit-identical to the reference where
+    # both run, c1 and the small suite) -- set REF_C3=1 to run the reference.
+    ref_full = cfg == 1 or (cfg == 3 and os.environ.get("REF_C3") == "1")
+    if ref_full:
         t0 = time.time()
         tt, rep = sparsett.fasttt(t, eps=eps)
         meta["ref_fasttt_s"] = time.time() - t0
@@ -153,7 +160,8 @@ def config(cfg: int):
         t0 = time.time()
         cores, info = O.fasttt(t.shape, t.coords, t.values, eps=eps, pivot=p, report=False)
         meta["oracle_s"] = time.time() - t0
-        meta["source"] = "oracle restatement at auto pivot (reference OOM there); index goldens from reference"
+        meta["source"] = ("oracle restatement at auto pivot (reference OOM or > 3 h there); "
+                          "index goldens from reference")
         assert list(info["ranks_lossless"]) == meta["index"]["ranks_lossless"]
     save_config(f"c{cfg}", t, eps, cores, meta)
 
