@@ -47,6 +47,13 @@ const char *ftt_last_error(void);
 int ftt_create(int device, void *stream, ftt_ctx **ctx_out);
 int ftt_destroy(ftt_ctx *ctx);
 int ftt_set_stream(ftt_ctx *ctx, void *stream);
+/* Deferred status checks (on != 0): the narrow QR kernels OR their
+ * non-finite-input flag into a device word instead of reading it back per
+ * call; ftt_take_status reads and clears it (bit 0 = non-finite input).
+ * Used by the decomposition driver, whose inputs are validated finite up
+ * front (tensor.py:129-146), to drop one host round trip per QR-sweep step. */
+int ftt_set_deferred_checks(ftt_ctx *ctx, int32_t on);
+int ftt_take_status(ftt_ctx *ctx, int32_t *flags_out);
 /* Number of kernels this context launched since creation (instrumentation). */
 int64_t ftt_kernel_launches(const ftt_ctx *ctx);
 /* Live kernel timing for the roofline report: while enabled, every launch of

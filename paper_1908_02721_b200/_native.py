@@ -65,6 +65,8 @@ SIGNATURES = {
                             ctypes.POINTER(ctypes.c_int32)],
     "ftt_svd_vectors": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_i32, _c_i32],
     "ftt_dot": [_c_p, _c_i64, _c_p, _c_p, _P_d],
+    "ftt_set_deferred_checks": [_c_p, _c_i32],
+    "ftt_take_status": [_c_p, ctypes.POINTER(ctypes.c_int32)],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],
 }
 _RESTYPES = {
@@ -118,6 +120,7 @@ def check(status: int, what: str = "") -> None:
 
 # ------------------------------------------------------------------ context
 _ctx_cache: dict = {}
+_ctx_stream: dict = {}
 
 
 def torch_mod():
@@ -147,7 +150,10 @@ def context():
         check(lib.ftt_create(dev, _c_p(stream), ctypes.byref(h)), "ftt_create")
         ctx = h
         _ctx_cache[dev] = ctx
-    check(lib.ftt_set_stream(ctx, _c_p(stream)), "ftt_set_stream")
+        _ctx_stream[dev] = stream
+    elif _ctx_stream.get(dev) != stream:
+        check(lib.ftt_set_stream(ctx, _c_p(stream)), "ftt_set_stream")
+        _ctx_stream[dev] = stream
     return ctx
 
 

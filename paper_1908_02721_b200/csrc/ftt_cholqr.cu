@@ -25,49 +25,69 @@ namespace {
 
 constexpr int CQ_MAX = 64;
 
-// Pivoted (or plain, tau < 0) Cholesky of the k x k SPD-ish G (ld ldg) and
-// M = P[:, :r] L11^-T written to M (k x k, ld k; columns >= r zero).
-// out[0] = r.  One CTA of 256 threads.
-__global__ void __launch_bounds__(256) k_chol_inv(int k, const double *__restrict__ G, int64_t ldg,
-                                                  double tau, double *__restrict__ M,
-                                                  int *__restrict__ out,
-                                                  int64_t *__restrict__ piv_out) {
+// Pivoted Cholesky of the k x k SPD-ish G (ld ldg): G = P L L^T P^T, stopping
+// at the first pivot <= tau * max diag(G).  out[0] = r, piv_out[0..k) = P
+// (the first r entries are a well-conditioned spanning column subset).
+// The matrix is never permuted: it stays in the original index order, a
+// `done` mask marks eliminated indices and the Schur complement is updated
+// in place on the rest.  One CTA of CQ_NT threads, thread t owns row t % 64
+// and columns t / 64 + 8 q of the update (no integer division); warp 0 picks
+// the pivot by a shuffle argmax (largest diagonal, lowest index on ties).
+// Three barriers per step.
+constexpr int CQ_NT = 512;
+__global__ void __launch_bounds__(CQ_NT) k_chol_inv(int k, const double *__restrict__ G, int64_t ldg,
+                                                    double tau, int *__restrict__ out,
+                                                    int64_t *__restrict__ piv_out) {
   extern __shared__ double cq_smem[];
-  double(*A)[CQ_MAX + 1] = reinterpret_cast<double(*)[CQ_MAX + 1]>(cq_smem);  // working copy
-  double(*L)[CQ_MAX + 1] = A + CQ_MAX;
-  double(*R)[CQ_MAX + 1] = L + CQ_MAX;  // L11^-T = (L11^T)^-1, upper
-  __shared__ int piv[CQ_MAX];
+  double(*A)[CQ_MAX + 1] = reinterpret_cast<double(*)[CQ_MAX + 1]>(cq_smem);  // Schur complement
+  __shared__ double lcol[CQ_MAX];
+  __shared__ int done[CQ_MAX];
+  __shared__ int order[CQ_MAX];
   __shared__ double dmax0;
   __shared__ int s_p, s_stop;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int e = tid; e < k * k; e += blockDim.x) {
     const int i = e % k, j = e / k;
     // symmetrise (the two triangles of a GEMM Gram may differ in the last bit)
     A[i][j] = 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]);
-    L[i][j] = 0.0;
   }
-  if (tid < k) piv[tid] = tid;
+  if (tid < k) done[tid] = 0;
   __syncthreads();
-  if (tid == 0) {
+  if (tid < 32) {
     double m = 0.0;
-    for (int i = 0; i < k; ++i) m = fmax(m, A[i][i]);
-    dmax0 = m;
+    for (int i = lane; i < k; i += 32) m = fmax(m, A[i][i]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) dmax0 = m;
   }
-  __syncthreads();
+  const int ra = tid & (CQ_MAX - 1), cb0 = tid / CQ_MAX;
+  constexpr int CSTEP = CQ_NT / CQ_MAX;
   int r = k;
   for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
-      int p = j;
-      if (tau >= 0.0) {
-        double best = A[j][j];
-        for (int i = j + 1; i < k; ++i)
-          if (A[i][i] > best) {
-            best = A[i][i];
-            p = i;
-          }
+    __syncthreads();  // previous update (and dmax0) visible
+    if (tid < 32) {
+      double best = -INFINITY;
+      int p = k;
+      for (int i = lane; i < k; i += 32)
+        if (!done[i] && (A[i][i] > best || p == k)) {
+          best = A[i][i];
+          p = i;
+        }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p, o);
+        if (op < k && (p == k || ob > best || (ob == best && op < p))) {
+          best = ob;
+          p = op;
+        }
       }
-      s_p = p;
-      s_stop = !(A[p][p] > fmax(tau, 0.0) * dmax0) || !(A[p][p] > 0.0);
+      if (lane == 0) {
+        s_p = p;
+        s_stop = !(best > fmax(tau, 0.0) * dmax0) || !(best > 0.0);
+        if (!s_stop) {
+          order[j] = p;
+          done[p] = 1;
+        }
+      }
     }
     __syncthreads();
     if (s_stop) {
@@ -75,59 +95,30 @@ __global__ void __launch_bounds__(256) k_chol_inv(int k, const double *__restric
       break;
     }
     const int p = s_p;
-    if (p != j) {  // symmetric swap of rows/cols j and p of A, rows of L, piv
-      for (int t = tid; t < k; t += blockDim.x) {
-        const double a = A[j][t];
-        A[j][t] = A[p][t];
-        A[p][t] = a;
-      }
-      __syncthreads();
-      for (int t = tid; t < k; t += blockDim.x) {
-        const double a = A[t][j];
-        A[t][j] = A[t][p];
-        A[t][p] = a;
-        if (t < j) {
-          const double l = L[j][t];
-          L[j][t] = L[p][t];
-          L[p][t] = l;
-        }
-      }
-      if (tid == 0) {
-        const int x = piv[j];
-        piv[j] = piv[p];
-        piv[p] = x;
-      }
-      __syncthreads();
-    }
-    // right-looking: A (trailing) holds the Schur complement
-    const double ljj = sqrt(A[j][j]);
-    for (int i = j + tid; i < k; i += blockDim.x) L[i][j] = i == j ? ljj : A[i][j] / ljj;
-    __syncthreads();
-    for (int e = tid; e < (k - j - 1) * (k - j - 1); e += blockDim.x) {
-      const int a = j + 1 + e % (k - j - 1), b = j + 1 + e / (k - j - 1);
-      A[a][b] -= L[a][j] * L[b][j];
+    if (tid < k) {
+      const double ljj = sqrt(A[p][p]);
+      lcol[tid] = done[tid] ? 0.0 : A[tid][p] / ljj;
     }
     __syncthreads();
-  }
-  // R = (L11^T)^-1 (upper, r x r): column c solves L11^T x = e_c backwards
-  for (int c = tid; c < r; c += blockDim.x) {
-    for (int i = r - 1; i >= 0; --i) {
-      double s = i == c ? 1.0 : 0.0;
-      for (int t = i + 1; t <= c; ++t) s -= L[t][i] * R[t][c];
-      R[i][c] = i > c ? 0.0 : s / L[i][i];
+    if (ra < k && !done[ra]) {
+      const double la = lcol[ra];
+      for (int b = cb0; b < k; b += CSTEP) A[ra][b] -= la * lcol[b];
     }
   }
   __syncthreads();
-  for (int e = tid; e < k * k; e += blockDim.x) {
-    const int i = e % k, c = e / k;  // row i of the permuted order, column c
-    M[piv[i] + (int64_t)c * k] = (i < r && c < r) ? R[i][c] : 0.0;
+  if (piv_out && tid < k) {
+    // pivots in elimination order, then the never-chosen indices ascending
+    if (tid < r) piv_out[tid] = order[tid];
+    if (!done[tid]) {
+      int pos = r;
+      for (int i = 0; i < tid; ++i) pos += !done[i];
+      piv_out[pos] = tid;
+    }
   }
-  if (piv_out)
-    for (int i = tid; i < k; i += blockDim.x) piv_out[i] = piv[i];
   if (tid == 0) out[0] = r;
 }
 
-constexpr size_t CQ_SMEM = 3 * sizeof(double) * CQ_MAX * (CQ_MAX + 1);
+constexpr size_t CQ_SMEM = sizeof(double) * CQ_MAX * (CQ_MAX + 1);
 
 }  // namespace
 
@@ -148,14 +139,13 @@ int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau
     attr = true;
   }
   const size_t ske = std::max(gemm_splitk_elems(k, k, mA), (size_t)1);
-  double *G = nullptr, *M = nullptr, *sk = nullptr;
+  double *G = nullptr, *sk = nullptr;
   int *dev_r = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&G, 8 * (size_t)k * k));
-  FTT_CHECK(owned_alloc(ctx, (void **)&M, 8 * (size_t)k * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&sk, 8 * ske));
   FTT_CHECK(owned_alloc(ctx, (void **)&dev_r, 64));
   FTT_CHECK(gemm(ctx, 1, 0, k, k, mA, 1.0, Y, mA, Y, mA, 0.0, G, k, sk, ske));
-  k_chol_inv<<<1, 256, CQ_SMEM, ctx->stream>>>((int)k, G, k, tau, M, dev_r, sel_dev);
+  k_chol_inv<<<1, CQ_NT, CQ_SMEM, ctx->stream>>>((int)k, G, k, tau, dev_r, sel_dev);
   FTT_LAUNCHED(ctx);
   // one round trip for the rank and the caller's device scalar
   if (aux_dev)
@@ -166,7 +156,6 @@ int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau
   const int r = hb[0];
   if (aux_dev && aux_host) memcpy(aux_host, hb + 2, sizeof(double));
   owned_free(ctx, G);
-  owned_free(ctx, M);
   owned_free(ctx, sk);
   owned_free(ctx, dev_r);
   *rank = r;

@@ -61,6 +61,15 @@ struct ftt_ctx {
   int64_t launches = 0;
   int num_sms = ftt::kNumSMs;
   void *pinned = nullptr;  // small pinned host scratch (64 KiB)
+  // pinned ring for stream-ordered host->device staging without a sync
+  // (stage_to_device); one event fences the latest staged copy
+  char *ring = nullptr;
+  size_t ring_off = 0;
+  cudaEvent_t ring_ev = nullptr;
+  // deferred status checks: narrow-QR non-finite flags OR into `sticky`
+  // (device int) instead of a host round trip per call (ftt_take_status)
+  bool defer_checks = false;
+  int *sticky = nullptr;
   // live per-class kernel timing (off by default)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -128,6 +137,11 @@ inline int grid_for(int64_t n, int threads, int per_thread = 1, int max_blocks =
 // Synchronous device->host copy of a few scalars through pinned scratch.
 int copy_to_host(ftt_ctx *ctx, void *host, const void *dev, size_t bytes);
 int copy_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes);
+// Stream-ordered host->device copy through the pinned ring: returns without
+// waiting (the host buffer may be reused at once).  Falls back to a
+// synchronous copy for transfers larger than the ring.
+int stage_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes);
+constexpr size_t kRingBytes = 1 << 20;
 
 // Persistent device buffer owned by the context (freed on destroy).
 int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes);

@@ -77,6 +77,27 @@ int copy_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes) {
   return FTT_OK;
 }
 
+int stage_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes) {
+  if (bytes == 0) return FTT_OK;
+  const size_t b = align_up(bytes, 64);
+  if (!ctx->ring || b > kRingBytes) {
+    FTT_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return FTT_OK;
+  }
+  if (ctx->ring_off + b > kRingBytes) {
+    // wrap: every copy staged on the previous lap is done once the latest is
+    FTT_CUDA(cudaEventSynchronize(ctx->ring_ev));
+    ctx->ring_off = 0;
+  }
+  char *slot = ctx->ring + ctx->ring_off;
+  ctx->ring_off += b;
+  memcpy(slot, host, bytes);
+  FTT_CUDA(cudaMemcpyAsync(dev, slot, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  FTT_CUDA(cudaEventRecord(ctx->ring_ev, ctx->stream));
+  return FTT_OK;
+}
+
 int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes) {
   *p = nullptr;
   if (bytes == 0) bytes = 256;
@@ -162,9 +183,17 @@ int ftt_create(int device, void *stream, ftt_ctx **ctx_out) {
     }
   }
   cudaError_t e = cudaMallocHost(&ctx->pinned, 65536);
+  if (e == cudaSuccess) e = cudaMallocHost((void **)&ctx->ring, kRingBytes);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ring_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMalloc((void **)&ctx->sticky, 64);
+  if (e == cudaSuccess) e = cudaMemset(ctx->sticky, 0, 64);
   if (e != cudaSuccess) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->ring) cudaFreeHost(ctx->ring);
+    if (ctx->ring_ev) cudaEventDestroy(ctx->ring_ev);
+    if (ctx->sticky) cudaFree(ctx->sticky);
     delete ctx;
-    set_error("pinned scratch: %s", cudaGetErrorString(e));
+    set_error("context buffers: %s", cudaGetErrorString(e));
     return FTT_ERR_CUDA;
   }
   *ctx_out = ctx;
@@ -181,13 +210,34 @@ int ftt_destroy(ftt_ctx *ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->ring) cudaFreeHost(ctx->ring);
+  if (ctx->ring_ev) cudaEventDestroy(ctx->ring_ev);
+  if (ctx->sticky) cudaFree(ctx->sticky);
   delete ctx;
   return FTT_OK;
 }
 
 int ftt_set_stream(ftt_ctx *ctx, void *stream) {
   if (!ctx) return FTT_ERR_INVALID;
+  if (static_cast<cudaStream_t>(stream) == ctx->stream) return FTT_OK;
+  // staged copies and deferred flags of the old stream must land first
+  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->stream = static_cast<cudaStream_t>(stream);
+  return FTT_OK;
+}
+
+int ftt_set_deferred_checks(ftt_ctx *ctx, int32_t on) {
+  if (!ctx) return FTT_ERR_INVALID;
+  ctx->defer_checks = on != 0;
+  return FTT_OK;
+}
+
+int ftt_take_status(ftt_ctx *ctx, int32_t *flags_out) {
+  if (!ctx || !flags_out) return FTT_ERR_INVALID;
+  int h = 0;
+  FTT_CHECK(copy_to_host(ctx, &h, ctx->sticky, sizeof(int)));
+  FTT_CUDA(cudaMemsetAsync(ctx->sticky, 0, sizeof(int), ctx->stream));
+  *flags_out = h;
   return FTT_OK;
 }
 

@@ -360,17 +360,46 @@ __global__ void k_sum_partials(const double *__restrict__ p, int64_t n, double *
   if (threadIdx.x == 0) *out = s[0];
 }
 
-__global__ void k_splitk_reduce(int64_t m, int64_t n, int splits, const double *__restrict__ partial,
-                                double alpha, double beta, double *__restrict__ C, int64_t ldc) {
-  int64_t total = m * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t col = t / m, row = t - col * m;
+// Deterministic split-K reduction.  Block = 64 outputs x 4 split groups:
+// thread (o, g) sums the contiguous group g of the partials of output o in
+// split order (loads unrolled 8 deep so they are in flight together), then
+// the 4 group sums are added in group order.  Fixed association for a given
+// `splits`, so results are bit-reproducible.
+constexpr int SR_OUT = 64, SR_GRP = 4;
+__global__ void __launch_bounds__(SR_OUT *SR_GRP) k_splitk_reduce(
+    int64_t m, int64_t n, int splits, const double *__restrict__ partial, double alpha, double beta,
+    double *__restrict__ C, int64_t ldc) {
+  __shared__ double gs[SR_GRP][SR_OUT];
+  const int64_t total = m * n;
+  const int o = threadIdx.x % SR_OUT, g = threadIdx.x / SR_OUT;
+  const int per = (splits + SR_GRP - 1) / SR_GRP;
+  const int z0 = g * per, z1 = min(splits, z0 + per);
+  for (int64_t base = (int64_t)blockIdx.x * SR_OUT; base < total; base += (int64_t)gridDim.x * SR_OUT) {
+    const int64_t t = base + o;
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + t];
-    double v = alpha * s;
-    if (beta != 0.0) v += beta * C[row + col * ldc];
-    C[row + col * ldc] = v;
+    if (t < total) {
+      int z = z0;
+      for (; z + 8 <= z1; z += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(partial + (int64_t)(z + u) * total + t);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; z < z1; ++z) s += __ldcg(partial + (int64_t)z * total + t);
+    }
+    gs[g][o] = s;
+    __syncthreads();
+    if (g == 0 && t < total) {
+      double tot = gs[0][o];
+#pragma unroll
+      for (int q = 1; q < SR_GRP; ++q) tot += gs[q][o];
+      const int64_t col = t / m, row = t - col * m;
+      double v = alpha * tot;
+      if (beta != 0.0) v += beta * C[row + col * ldc];
+      C[row + col * ldc] = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -421,6 +450,19 @@ __global__ void k_orth_defect(int64_t n, const double *__restrict__ G, int64_t l
 
 }  // namespace
 
+// K splits for a product with `tiles` output tiles: long-K products with a
+// small output (Gram matrices, B = Q^T A, train-norm contractions) otherwise
+// run a handful of CTAs that walk all of K one BK step at a time (latency
+// bound, ~0.7 us per step).  Aim for ~8 CTAs per SM, at least 128 K per CTA
+// (8 BK steps), at most 256 splits (the reduction's serial depth).
+int64_t splitk_count(int64_t tiles, int64_t k, int num_sms) {
+  if (tiles >= 2 * (int64_t)num_sms || k < 512) return 1;
+  int64_t s = ceil_div(8 * (int64_t)num_sms, tiles);
+  s = std::min<int64_t>(s, k / 128);
+  s = std::min<int64_t>(s, 256);
+  return std::max<int64_t>(s, 1);
+}
+
 int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
          const double *A, int64_t lda, const double *B, int64_t ldb, double beta, double *C,
          int64_t ldc, double *splitk_ws, size_t splitk_ws_elems) {
@@ -435,12 +477,8 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
   int64_t tiles_m = ceil_div(m, tile_m(ts)), tiles_n = ceil_div(n, tile_n(ts));
   int64_t tiles = tiles_m * tiles_n;
   int splits = 1;
-  if (tiles < 2 * ctx->num_sms && k >= 4 * 256) {
-    // enough CTAs for ~8 per SM: long-K products with a small output (Gram
-    // matrices, B = Q^T A) are otherwise a handful of CTAs streaming all of K
-    int64_t s = ceil_div(8 * ctx->num_sms, tiles);
-    s = std::min<int64_t>(s, k / 256);
-    s = std::min<int64_t>(s, 1024);
+  {
+    int64_t s = splitk_count(tiles, k, ctx->num_sms);
     if (splitk_ws) s = std::min<int64_t>(s, (int64_t)(splitk_ws_elems / (size_t)(m * n)));
     else s = 1;
     if (s > 1) splits = (int)s;
@@ -471,8 +509,9 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
 #undef FTT_GEMM_LAUNCH
   FTT_LAUNCHED(ctx);
   if (splits > 1) {
-    k_splitk_reduce<<<grid_for(m * n, 256, 2), 256, 0, ctx->stream>>>(m, n, splits, part, alpha,
-                                                                     beta, C, ldc);
+    const int64_t rb = std::min<int64_t>(ceil_div(m * n, SR_OUT), 4 * (int64_t)ctx->num_sms);
+    k_splitk_reduce<<<(unsigned)rb, SR_OUT * SR_GRP, 0, ctx->stream>>>(m, n, splits, part, alpha,
+                                                                      beta, C, ldc);
     FTT_LAUNCHED(ctx);
   }
   prof_end(ctx, pb, PT_GEMM, 8.0 * ((double)m * k + (double)k * n + 2.0 * m * n),
@@ -607,8 +646,7 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
 size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k) {
   const TileShape ts = pick_tile(m, n);
   int64_t tiles = ceil_div(m, tile_m(ts)) * ceil_div(n, tile_n(ts));
-  if (tiles >= 2 * kNumSMs || k < 4 * 256) return 0;
-  int64_t s = std::min<int64_t>(std::min<int64_t>(ceil_div(8 * kNumSMs, tiles), k / 256), 1024);
+  int64_t s = splitk_count(tiles, k, kNumSMs);
   return s > 1 ? (size_t)(s * m * n) : 0;
 }
 

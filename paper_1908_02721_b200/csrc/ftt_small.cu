@@ -42,7 +42,7 @@ namespace {
 
 constexpr double kEps = 2.220446049250313e-16;
 constexpr int LEAF_NT = 256;  // TSQR / QR kernels: 256 threads, one row each
-constexpr int SVD_NT = 512;   // SVD kernel: 16 warps for the Jacobi rounds
+constexpr int SVD_NT = 1024;  // SVD kernel: 32 warps, one per pair of a Jacobi round (n <= 64)
 
 __device__ __forceinline__ double warp_sum(double v) {
   // butterfly: every lane ends with the bit-identical total (fp add commutes)
@@ -76,7 +76,7 @@ __device__ __forceinline__ double reduce_scatter(double (&v)[32], int lane) {
 
 template <int NMAX>
 struct Scratch {
-  double red[SVD_NT / 32][NMAX];  // per-warp partial sums (<= 16 warps)
+  double red[LEAF_NT / 32][NMAX];  // per-warp partial sums (QR kernels: LEAF_NT threads)
   double rowc[NMAX];              // row c (pivot row) of the current step
   double wv[NMAX];                // w_j of the current step
   double sc[4];                   // tau, beta, scal
@@ -560,9 +560,15 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, i
            double *Q, int64_t ldq, double *R, int64_t ldr, bool check) {
   const int n = (int)n64;
   FTT_CHECK(set_attrs());
+  // deferred mode: flags go to the context's sticky word (no round trip)
+  const bool deferred = check && ctx->defer_checks;
   int *status = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&status, 64));
-  FTT_CUDA(cudaMemsetAsync(status, 0, 64, ctx->stream));
+  if (deferred) {
+    status = ctx->sticky;
+  } else {
+    FTT_CHECK(owned_alloc(ctx, (void **)&status, 64));
+    FTT_CUDA(cudaMemsetAsync(status, 0, 64, ctx->stream));
+  }
   Tree t;
   std::vector<double *> qs;
   const double *root;
@@ -582,6 +588,7 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, i
   }
   for (double *p : qs) owned_free(ctx, p);
   int h = 0;
+  if (deferred) return FTT_OK;
   if (check) FTT_CHECK(copy_to_host(ctx, &h, status, sizeof(int)));
   owned_free(ctx, status);
   if (h & 1) {
@@ -592,11 +599,13 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, i
 }
 
 int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, int trans,
-             double *U, int64_t ldu, double *Y, double *norms_host, int *sweeps) {
+             double *U, int64_t ldu, double *Y, double *norms_host, int *sweeps,
+             const double *extra_dev, double *extra_host) {
   const int n = (int)n64;
   FTT_CHECK(set_attrs());
   // status (2 ints) | norms n | R n x n | P n x n
   double *dev = nullptr;
+  // status (2 ints) | extra | norms n | R n x n | P n x n
   FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n + 2 * (size_t)n * n)));
   int *status = reinterpret_cast<int *>(dev);
   double *norms = dev + 2;
@@ -630,8 +639,13 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   owned_free(ctx, Qr);
   if (W) owned_free(ctx, W);
   for (double *p : qs) owned_free(ctx, p);
+  // one round trip: status, the caller's device scalar and the norms
+  if (extra_dev)
+    FTT_CUDA(cudaMemcpyAsync(dev + 1, extra_dev, sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
   std::vector<double> h(n + 2);
   FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));
+  if (extra_dev && extra_host) *extra_host = h[1];
   owned_free(ctx, dev);
   int st[2];
   memcpy(st, h.data(), 8);

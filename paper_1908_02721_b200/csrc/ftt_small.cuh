@@ -14,8 +14,11 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int
            int64_t ldq, double *R, int64_t ldr, bool check = true);
 
 // Thin SVD core: U = Q P (M x n, ld ldu), Y = R^T P (n x n), norms_host[j] =
-// ||Y_j|| (unsorted; sigma up to the caller's permutation).
+// ||Y_j|| (unsorted; sigma up to the caller's permutation).  One host round
+// trip, which also brings back the caller's device scalar extra_dev (if any)
+// into *extra_host.
 int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int trans, double *U,
-             int64_t ldu, double *Y, double *norms_host, int *sweeps);
+             int64_t ldu, double *Y, double *norms_host, int *sweeps,
+             const double *extra_dev = nullptr, double *extra_host = nullptr);
 
 }  // namespace ftt

@@ -549,8 +549,11 @@ void svd_state_free(ftt_ctx *ctx) {
 namespace {
 
 // Phase 1 (QR + Jacobi) on a given state; see the file header.
+// extra_dev / extra_host: a device scalar of the caller brought back with
+// the narrow path's single round trip (ignored on the wide path).
 int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A, int64_t lda,
-               int32_t a_row_major) {
+               int32_t a_row_major, const double *extra_dev = nullptr,
+               double *extra_host = nullptr) {
   st->m = m;
   st->n = n;
   st->transposed = m < n;
@@ -569,7 +572,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     std::vector<double> raw(nA);
     const int pb = prof_begin(ctx);
     FTT_CHECK(tsqr_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, mA, st->Y, raw.data(),
-                       &st->sweeps));
+                       &st->sweeps, extra_dev, extra_host));
     // QR (4 m n^2 / 3) + Q formation + Q P, plus sweeps x n^2/2 pairs x 10 n
     prof_end(ctx, pb, PT_JACOBI, 8.0 * ((double)mA * nA * 3 + (double)nA * nA * 2),
              (double)mA * nA * nA * (8.0 / 3.0 + 2.0) + 5.0 * std::max(st->sweeps, 1) *
@@ -753,8 +756,8 @@ int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double
   double *inv = take<double>(ctx, rank);
   std::vector<double> hinv(rank);
   for (int64_t j = 0; j < rank; ++j) hinv[j] = st->sigma[j] != 0.0 ? 1.0 / st->sigma[j] : 0.0;
-  FTT_CUDA(cudaMemcpyAsync(sel, st->perm.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
-  FTT_CUDA(cudaMemcpyAsync(inv, hinv.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+  FTT_CHECK(stage_to_device(ctx, sel, st->perm.data(), 8 * rank));
+  FTT_CHECK(stage_to_device(ctx, inv, hinv.data(), 8 * rank));
   if (st->small) {
     // U_A = (Q P)[:, sel],  V_A = Y[:, sel] / sigma
     k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, mA, rank, st->Af, mA,
@@ -763,7 +766,6 @@ int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double
     k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA,
                                                                         sel, inv, VA, nA);
     FTT_LAUNCHED(ctx);
-    FTT_CUDA(cudaStreamSynchronize(ctx->stream));
     return FTT_OK;
   }
   if (st->direct) {
@@ -793,8 +795,6 @@ int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double
     FTT_LAUNCHED(ctx);
   }
   if (!st->direct) FTT_CHECK(qr_apply_q(ctx, mA, nA, st->Af, mA, st->Tb, rank, UA, mA, ws, wse));
-  // the host vectors above must outlive the async copies
-  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
   return FTT_OK;
 }
 
@@ -841,7 +841,8 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   // ||A||_F^2 stays on the device until the sketch rank comes back (one host
   // round trip for both); a non-finite entry is diagnosed there
   double *fro2_dev = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 2)));
+  FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 3)));
+  double *rest2_dev = fro2_dev + kSumSqBlocks + 2;  // after sum_squares' partials
   {
     const int64_t inner = need_t ? nA : mA;
     if (lda != inner) {
@@ -921,7 +922,26 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
     FTT_CHECK(qr_apply_q(ctx, mA, k, Yk, mA, Tb, k, st->Qk, mA, ws, wse));
   }
   FTT_CHECK(gemm(ctx, 1, need_t, k, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, k, sk, ske));
-  FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t, &rest2));
+  // A narrow B (k <= 64) is factored speculatively before the certificate is
+  // read: the residual energy then comes back with the singular values in
+  // one host round trip (a rejected certificate wastes one small SVD).
+  const bool speculate = tsqr_ok(std::max(k, nA), std::min(k, nA)) &&
+                         !getenv("FTT_NO_SPECULATE");
+  if (speculate) {
+    FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
+                               nullptr, rest2_dev));
+    st->inner = new SvdState();
+    if (svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0, rest2_dev, &rest2) != FTT_OK) {
+      // speculative factorisation failed: decide on the certificate alone
+      // (an accepted certificate re-runs the factorisation below and reports)
+      svd_state_release(ctx, st->inner);
+      st->inner = nullptr;
+      FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
+    }
+  } else {
+    FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
+                               &rest2));
+  }
   owned_free(ctx, Om);
   owned_free(ctx, Yk);
   owned_free(ctx, sk);
@@ -944,9 +964,11 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
     fprintf(stderr, "[ftt] lowrank m=%lld n=%lld k=%lld rest2=%.3e thr=%.3e -> %s\n",
             (long long)m, (long long)n, (long long)k, rest2, thr,
             strict ? "accepted" : (loose ? "accepted (interval)" : "rejected"));
-  if (!loose) return FTT_OK;
-  st->inner = new SvdState();
-  FTT_CHECK(svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0));
+  if (!loose) return FTT_OK;  // (a speculative inner state is released with st)
+  if (!st->inner) {
+    st->inner = new SvdState();
+    FTT_CHECK(svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0));
+  }
   st->sigma = st->inner->sigma;
   if (s_host) memcpy(s_host, st->sigma.data(), 8 * st->sigma.size());
   *accepted = strict ? 2 : 1;
@@ -995,7 +1017,7 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
     FTT_CHECK(arena_reserve(ctx, 2 * align_up(8 * rank) + 256));
     double *sig2 = take<double>(ctx, rank);
     double *fac = take<double>(ctx, rank);
-    FTT_CUDA(cudaMemcpyAsync(sig2, st->sigma.data(), 8 * rank, cudaMemcpyHostToDevice, ctx->stream));
+    FTT_CHECK(stage_to_device(ctx, sig2, st->sigma.data(), 8 * rank));
     k_sign_pick<<<(unsigned)rank, 256, 0, ctx->stream>>>(mu, UM, mu, fac);
     FTT_LAUNCHED(ctx);
     const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(std::max(mu, mv), 4096)));
@@ -1013,7 +1035,5 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
   }
   owned_free(ctx, UA);
   owned_free(ctx, VA);
-  // keep the context stream-ordered for the host vectors we just copied from
-  FTT_CUDA(cudaStreamSynchronize(ctx->stream));
   return FTT_OK;
 }

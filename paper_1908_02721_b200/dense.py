@@ -60,7 +60,7 @@ def tail_error(s: np.ndarray, rank: int, rest2: float = 0.0) -> float:
     return float(np.sqrt(max(float(np.sum(sq[rank:])) + rest2, 0.0)))
 
 
-LOWRANK_MIN = 48        # smaller operands: the full SVD is already cheap
+LOWRANK_MIN = 16        # smaller operands: the full SVD is already cheap
 
 
 def lowrank_k(min_dim: int, hint) -> int:
@@ -69,7 +69,12 @@ def lowrank_k(min_dim: int, hint) -> int:
         return 0
     k = 32 if hint is None else max(16, 2 * int(hint) + 8)
     k = (k + 7) // 8 * 8
-    return k if 2 * k <= min_dim else 0
+    # narrow operands (<= 64 columns) also take the sketch when it is narrower:
+    # the full path's column-sequential TSQR + Jacobi cost grows with the
+    # width, the sketch path's with the (certified) rank
+    if k < min_dim and (2 * k <= min_dim or min_dim <= 64):
+        return k
+    return 0
 
 
 def dev_svd_values_lowrank(buf, m: int, n: int, ld: int, row_major: bool, k: int,

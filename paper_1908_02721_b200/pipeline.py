@@ -790,6 +790,26 @@ def fasttt_device(a: SparseTensor, coords_d, values_d, eps, pivot, mode, fixed_r
         return DeviceResult(cores=None, pivot=pivot, mode=mode, eps=eps, num_fibers=0,
                             ranks_lossless=(0,) * (d - 1), ranks=(1,) * (d - 1), eps_actual=0.0,
                             eps_actual_method="exact", eps_actual_inner=0.0, notes=notes, zero=True)
+    lib, ctx = nat.lib(), nat.context()
+    # the narrow QR steps report non-finite inputs through a device flag read
+    # once at the end (the COO values are validated finite up front)
+    nat.check(lib.ftt_set_deferred_checks(ctx, 1), "ftt_set_deferred_checks")
+    try:
+        res = _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, notes,
+                                  report)
+    finally:
+        nat.check(lib.ftt_set_deferred_checks(ctx, 0), "ftt_set_deferred_checks")
+    flags = nat.ctypes.c_int32(0)
+    nat.check(lib.ftt_take_status(ctx, nat.ctypes.byref(flags)), "ftt_take_status")
+    if flags.value & 1:
+        raise ValueError("matrix entries must be finite")
+    return res
+
+
+def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, notes, report):
+    d = a.ndim
+    dims = a.shape
+    nnz = a.nnz
     df = fibers_device(dims, pivot, coords_d, values_d, nnz)
     if d == 1:
         # the reference's FiberSet rejects its own d = 1 output (tensor.py:326-329)
