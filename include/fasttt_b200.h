@@ -54,6 +54,9 @@ int ftt_set_stream(ftt_ctx *ctx, void *stream);
  * front (tensor.py:129-146), to drop one host round trip per QR-sweep step. */
 int ftt_set_deferred_checks(ftt_ctx *ctx, int32_t on);
 int ftt_take_status(ftt_ctx *ctx, int32_t *flags_out);
+/* Host round trips (device->host reads that wait on the stream) since
+ * creation and the host milliseconds spent blocked in them (instrumentation). */
+int ftt_sync_stats(const ftt_ctx *ctx, int64_t *syncs_out, double *wait_ms_out);
 /* Number of kernels this context launched since creation (instrumentation). */
 int64_t ftt_kernel_launches(const ftt_ctx *ctx);
 /* Live kernel timing for the roofline report: while enabled, every launch of

@@ -67,6 +67,7 @@ SIGNATURES = {
     "ftt_dot": [_c_p, _c_i64, _c_p, _c_p, _P_d],
     "ftt_set_deferred_checks": [_c_p, _c_i32],
     "ftt_take_status": [_c_p, ctypes.POINTER(ctypes.c_int32)],
+    "ftt_sync_stats": [_c_p, ctypes.POINTER(ctypes.c_int64), _P_d],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],
 }
 _RESTYPES = {

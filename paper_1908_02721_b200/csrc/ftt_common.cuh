@@ -69,6 +69,9 @@ struct ftt_ctx {
   // deferred status checks: narrow-QR non-finite flags OR into `sticky`
   // (device int) instead of a host round trip per call (ftt_take_status)
   bool defer_checks = false;
+  // host round trips (copy_to_host) and the host time spent blocked in them
+  int64_t syncs = 0;
+  double sync_wait_ms = 0.0;
   int *sticky = nullptr;
   // live per-class kernel timing (off by default)
   bool prof = false;

@@ -1,6 +1,8 @@
 // Context, arena and error plumbing of the C ABI.
 #include <stdarg.h>
 
+#include <chrono>
+
 #include "ftt_common.cuh"
 
 namespace ftt {
@@ -51,6 +53,15 @@ void *arena_take(ftt_ctx *ctx, size_t bytes) {
 
 int copy_to_host(ftt_ctx *ctx, void *host, const void *dev, size_t bytes) {
   if (bytes == 0) return FTT_OK;
+  struct Wait {
+    ftt_ctx *c;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~Wait() {
+      c->syncs++;
+      c->sync_wait_ms +=
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  } wait{ctx};
   if (bytes <= 65536) {
     FTT_CUDA(cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     FTT_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -238,6 +249,13 @@ int ftt_take_status(ftt_ctx *ctx, int32_t *flags_out) {
   FTT_CHECK(copy_to_host(ctx, &h, ctx->sticky, sizeof(int)));
   FTT_CUDA(cudaMemsetAsync(ctx->sticky, 0, sizeof(int), ctx->stream));
   *flags_out = h;
+  return FTT_OK;
+}
+
+int ftt_sync_stats(const ftt_ctx *ctx, int64_t *syncs_out, double *wait_ms_out) {
+  if (!ctx) return FTT_ERR_INVALID;
+  if (syncs_out) *syncs_out = ctx->syncs;
+  if (wait_ms_out) *wait_ms_out = ctx->sync_wait_ms;
   return FTT_OK;
 }
 

@@ -544,113 +544,82 @@ __global__ void __launch_bounds__(256) k_linearize(const int64_t *__restrict__ c
   }
 }
 
-__global__ void __launch_bounds__(512) k_part_hist(const uint64_t *__restrict__ lin, int64_t n,
-                                                   PartSpec ps, uint32_t *__restrict__ bh) {
-  extern __shared__ uint32_t hsm[];
+// One pass per pivot group: each block histograms its chunk of `lin` per
+// (pivot, bucket) in shared memory, reserves that many slots of the bucket's
+// fixed-capacity region with one global atomic per non-empty counter, then
+// re-reads the chunk (L2-resident) and scatters the keys into its reserved
+// runs.  Bucket order inside a region is arbitrary -- the distinct count is
+// order independent -- so no global histogram / scan pass is needed.  A
+// bucket that outgrows its capacity flags its pivot (sort-path fallback).
+__global__ void __launch_bounds__(1024) k_part_scatter(const uint64_t *__restrict__ lin, int64_t n,
+                                                       PartSpec ps, int64_t cap,
+                                                       unsigned int *__restrict__ fill,
+                                                       uint64_t *__restrict__ keys,
+                                                       int *__restrict__ flags) {
+  extern __shared__ unsigned int cur[];
   const int nbk = 1 << ps.bits, tot = ps.g * nbk;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) hsm[e] = 0;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) cur[e] = 0;
   __syncthreads();
   const int64_t i0 = blockIdx.x * ps.chunk, i1 = min(n, i0 + ps.chunk);
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const uint64_t x = lin[i];
+#pragma unroll 4
     for (int q = 0; q < ps.g; ++q) {
       const uint32_t b = (uint32_t)(mix64(drop_digit(x, ps, q)) >> (64 - ps.bits));
-      atomicAdd(&hsm[q * nbk + b], 1u);
+      atomicAdd(&cur[q * nbk + b], 1u);
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) bh[(int64_t)blockIdx.x * tot + e] = hsm[e];
-}
-
-// Per (pivot, bucket) slot: exclusive prefix over blocks in place, totals out.
-__global__ void k_part_scan_blocks(uint32_t *__restrict__ bh, int nb, int tot,
-                                   uint32_t *__restrict__ total) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= tot) return;
-  uint32_t run = 0;
-  for (int b = 0; b < nb; ++b) {
-    const uint32_t c = bh[(int64_t)b * tot + e];
-    bh[(int64_t)b * tot + e] = run;
-    run += c;
-  }
-  total[e] = run;
-}
-
-// Bucket start offsets per pivot (exclusive scan of totals, one CTA per
-// pivot), plus q * n so that every pivot has its own n-slot region.
-__global__ void __launch_bounds__(1024) k_part_scan_buckets(const uint32_t *__restrict__ total,
-                                                            int nbk, int64_t n,
-                                                            int64_t *__restrict__ base) {
-  __shared__ int64_t s[1024];
-  const int q = blockIdx.x;
-  const int per = (nbk + 1023) / 1024;
-  const int b0 = threadIdx.x * per;
-  int64_t loc = 0;
-  for (int j = 0; j < per; ++j)
-    if (b0 + j < nbk) loc += total[q * nbk + b0 + j];
-  s[threadIdx.x] = loc;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const int64_t v = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
-    __syncthreads();
-    s[threadIdx.x] += v;
-    __syncthreads();
-  }
-  int64_t run = s[threadIdx.x] - loc + (int64_t)q * n;
-  for (int j = 0; j < per; ++j)
-    if (b0 + j < nbk) {
-      base[q * nbk + b0 + j] = run;
-      run += total[q * nbk + b0 + j];
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const unsigned int c = cur[e];
+    if (c) {
+      const unsigned int off = atomicAdd(&fill[e], c);
+      if ((int64_t)off + c > cap) flags[e / nbk] = 1;
+      cur[e] = off;
     }
-}
-
-__global__ void __launch_bounds__(512) k_part_scatter(const uint64_t *__restrict__ lin, int64_t n,
-                                                      PartSpec ps, const uint32_t *__restrict__ bh,
-                                                      const int64_t *__restrict__ base,
-                                                      uint64_t *__restrict__ keys) {
-  extern __shared__ unsigned long long cur[];
-  const int nbk = 1 << ps.bits, tot = ps.g * nbk;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x)
-    cur[e] = (unsigned long long)(base[e] + bh[(int64_t)blockIdx.x * tot + e]);
+  }
   __syncthreads();
-  const int64_t i0 = blockIdx.x * ps.chunk, i1 = min(n, i0 + ps.chunk);
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const uint64_t x = lin[i];
+#pragma unroll 4
     for (int q = 0; q < ps.g; ++q) {
       const uint64_t key = drop_digit(x, ps, q);
       const uint32_t b = (uint32_t)(mix64(key) >> (64 - ps.bits));
-      const unsigned long long pos = atomicAdd(&cur[q * nbk + b], 1ull);
-      keys[pos] = key;
+      const int e = q * nbk + b;
+      const unsigned int pos = atomicAdd(&cur[e], 1u);
+      if (pos < cap) keys[(int64_t)e * cap + pos] = key;
     }
   }
 }
 
 // One CTA per (bucket, pivot): distinct keys of the bucket via a shared
-// open-addressing set.  flags[q] = 1 if a bucket exceeded the table.
-__global__ void __launch_bounds__(256) k_part_count(const uint64_t *__restrict__ keys,
-                                                    const int64_t *__restrict__ base,
-                                                    const uint32_t *__restrict__ total, int nbk,
+// open-addressing set (slot = low bits of the same mix; the bucket fixed its
+// top bits).  Counts are exact and independent of the insertion order.
+__global__ void __launch_bounds__(256) k_part_count(const uint64_t *__restrict__ keys, int64_t cap,
+                                                    const unsigned int *__restrict__ fill, int nbk,
                                                     unsigned long long *__restrict__ counts,
                                                     int *__restrict__ flags) {
   extern __shared__ unsigned long long tab[];
   __shared__ unsigned long long s_cnt;
   const int b = blockIdx.x, q = blockIdx.y;
-  const int64_t start = base[q * nbk + b];
-  const int len = (int)total[q * nbk + b];
+  const int e = q * nbk + b;
+  const int64_t len = fill[e];
   if (len == 0) return;
+  if (len > cap) return;  // flagged by the scatter
   int T = 64;
   while (T < 2 * len) T <<= 1;
   if (T > PC_TMAX) {
     if (threadIdx.x == 0) flags[q] = 1;
     return;
   }
-  for (int e = threadIdx.x; e < T; e += blockDim.x) tab[e] = ~0ull;
+  for (int j = threadIdx.x; j < T; j += blockDim.x) tab[j] = ~0ull;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   const uint64_t mask = (uint64_t)T - 1;
+  const uint64_t *src = keys + (int64_t)e * cap;
   unsigned long long fresh = 0;
   for (int j = threadIdx.x; j < len; j += blockDim.x) {
-    const uint64_t key = keys[start + j];
+    const uint64_t key = __ldcs(src + j);
     uint64_t h = mix64(key) & mask;
     while (true) {
       const unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)key);
@@ -1019,12 +988,22 @@ void magic_u63(uint64_t D, uint64_t *m, int *sh) {
 
 int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
                            const int64_t *dims, int64_t *counts_host) {
-  // bucket bits: ~2048 keys per bucket on average
+  // One pivot per pass: the bucketed key array (~1.2 x 8 B x nnz) then stays
+  // resident in L2 between the scatter and the count, so the scattered 8-byte
+  // writes merge in L2 instead of reaching DRAM as partial sectors (measured
+  // with 4 pivots per pass: 3.3x write and 6x read amplification).
+  // Bucket bits: ~2048 keys per bucket on average; fixed capacity mean +
+  // 8 sigma (+64): overflow (duplicate-heavy pivots) falls back to sorting
   int bits = 4;
   while (bits < 12 && (nnz >> bits) > 2048) ++bits;
   const int nbk = 1 << bits;
-  const int G = std::max(1, std::min(std::min((int)d, PC_MAXG), 16384 / nbk));
-  const int nb = 2 * kNumSMs;
+  const int64_t mean = ceil_div(nnz, nbk);
+  // (fibers with several nonzeros land whole in one bucket: the variance of a
+  // bucket's fill is ~mean x (average fiber size), hence the wide margin)
+  const int64_t cap = std::min<int64_t>(nnz, mean + 16 * (int64_t)std::sqrt((double)mean) + 256);
+  static const char *gs = getenv("FTT_PART_GROUP");  // A/B knob: pivots per pass
+  const int G = std::max(1, std::min(std::min((int)d, PC_MAXG), gs ? atoi(gs) : 1));
+  const int nb = kNumSMs;
   LinSpec ls;
   ls.d = d;
   {
@@ -1035,23 +1014,20 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
     }
   }
   uint64_t *lin = nullptr, *keys = nullptr;
-  uint32_t *bh = nullptr, *total = nullptr;
-  int64_t *base = nullptr;
+  unsigned int *fill = nullptr;
   unsigned long long *cnt = nullptr;
   int *flags = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&lin, 8 * (size_t)nnz));
-  FTT_CHECK(owned_alloc(ctx, (void **)&keys, 8 * (size_t)nnz * G));
-  FTT_CHECK(owned_alloc(ctx, (void **)&bh, 4 * (size_t)nb * G * nbk));
-  FTT_CHECK(owned_alloc(ctx, (void **)&total, 4 * (size_t)G * nbk));
-  FTT_CHECK(owned_alloc(ctx, (void **)&base, 8 * (size_t)G * nbk));
+  FTT_CHECK(owned_alloc(ctx, (void **)&keys, 8 * (size_t)cap * nbk * G));
+  FTT_CHECK(owned_alloc(ctx, (void **)&fill, 4 * (size_t)G * nbk * ceil_div(d, G)));
   FTT_CHECK(owned_alloc(ctx, (void **)&cnt, 8 * 32 + 4 * 32));
   flags = reinterpret_cast<int *>(cnt + 32);
   FTT_CUDA(cudaMemsetAsync(cnt, 0, 8 * 32 + 4 * 32, ctx->stream));
+  FTT_CUDA(cudaMemsetAsync(fill, 0, 4 * (size_t)G * nbk * ceil_div(d, G), ctx->stream));
   static bool attrs = false;
   if (!attrs) {
-    FTT_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     FTT_CUDA(cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  131072));
+                                  65536));
     FTT_CUDA(cudaFuncSetAttribute(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   8 * PC_TMAX));
     attrs = true;
@@ -1060,7 +1036,7 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
   k_linearize<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(coords, nnz, ls, lin);
   FTT_LAUNCHED(ctx);
   prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0), 0.0);
-  for (int p0 = 0; p0 < d; p0 += G) {
+  for (int p0 = 0, grp = 0; p0 < d; p0 += G, ++grp) {
     PartSpec ps;
     ps.g = std::min(G, d - p0);
     ps.bits = bits;
@@ -1073,21 +1049,15 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
       magic_u63(S * (uint64_t)dims[p], &ps.mT[q], &ps.shT[q]);
     }
     const int tot = ps.g * nbk;
+    unsigned int *gfill = fill + (size_t)grp * G * nbk;
     pb = prof_begin(ctx);
-    k_part_hist<<<nb, 512, 4 * (size_t)tot, ctx->stream>>>(lin, nnz, ps, bh);
+    k_part_scatter<<<nb, 1024, 4 * (size_t)tot, ctx->stream>>>(lin, nnz, ps, cap, gfill, keys,
+                                                               flags + p0);
     FTT_LAUNCHED(ctx);
-    prof_end(ctx, pb, PT_HIST, 8.0 * (double)nnz + 4.0 * nb * tot, 0.0);
-    k_part_scan_blocks<<<(unsigned)ceil_div(tot, 256), 256, 0, ctx->stream>>>(bh, nb, tot, total);
-    FTT_LAUNCHED(ctx);
-    k_part_scan_buckets<<<ps.g, 1024, 0, ctx->stream>>>(total, nbk, nnz, base);
-    FTT_LAUNCHED(ctx);
-    pb = prof_begin(ctx);
-    k_part_scatter<<<nb, 512, 8 * (size_t)tot, ctx->stream>>>(lin, nnz, ps, bh, base, keys);
-    FTT_LAUNCHED(ctx);
-    // read lin, write one key per pivot
+    // read lin (the second read of each chunk hits L2), write one key per pivot
     prof_end(ctx, pb, PT_SORT, (double)nnz * (8.0 + 8.0 * ps.g), 0.0);
     pb = prof_begin(ctx);
-    k_part_count<<<dim3(nbk, ps.g), 256, 8 * PC_TMAX, ctx->stream>>>(keys, base, total, nbk,
+    k_part_count<<<dim3(nbk, ps.g), 256, 8 * PC_TMAX, ctx->stream>>>(keys, cap, gfill, nbk,
                                                                       cnt + p0, flags + p0);
     FTT_LAUNCHED(ctx);
     prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz * ps.g, 0.0);
@@ -1098,11 +1068,11 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
   FTT_CHECK(copy_to_host(ctx, hf, flags, 4 * 32));
   owned_free(ctx, lin);
   owned_free(ctx, keys);
-  owned_free(ctx, bh);
-  owned_free(ctx, total);
-  owned_free(ctx, base);
+  owned_free(ctx, fill);
   owned_free(ctx, cnt);
+  static const bool debug = getenv("FTT_DEBUG") != nullptr;
   for (int p = 0; p < d; ++p) {
+    if (debug && hf[p]) fprintf(stderr, "[ftt] select_p partition overflow at pivot %d\n", p);
     if (hf[p]) FTT_CHECK(ftt_fiber_count(ctx, coords, nnz, d, dims, p, &counts_host[p]));
     else counts_host[p] = (int64_t)h[p];
   }

@@ -41,6 +41,28 @@ for _ in range(5):
     walls.append((time.perf_counter() - t0) * 1e3)
     devs.append(e0.elapsed_time(e1))
 print(f"wall ms {[round(x, 3) for x in walls]}\ndevice ms {[round(x, 3) for x in devs]}")
+from paper_1908_02721_b200 import _native as nat  # noqa: E402
+
+lib, ctx = nat.lib(), nat.context()
+
+
+def stats():
+    n = nat.ctypes.c_int64(0)
+    w = nat.ctypes.c_double(0)
+    lib.ftt_sync_stats(ctx, nat.ctypes.byref(n), nat.ctypes.byref(w))
+    return n.value, w.value, nat.kernel_launches()
+
+
+s0 = stats()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(5):
+    step()
+torch.cuda.synchronize()
+wall = (time.perf_counter() - t0) * 1e3 / 5
+s1 = stats()
+print(f"per step: wall {wall:.3f} ms, native round trips {(s1[0] - s0[0]) / 5:.1f}, "
+      f"blocked {(s1[1] - s0[1]) / 5:.3f} ms, launches {(s1[2] - s0[2]) / 5:.1f}")
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(5):
