@@ -26,6 +26,7 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys
+constexpr int RS_MIN_TILE = RS_THREADS * 8;     // smallest tile variant (status sizing)
 constexpr int RADIX = 256;
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;
@@ -117,7 +118,7 @@ __global__ void k_hist_scan(uint32_t *ghist) {
   h[t] = s[t] - h[t];  // exclusive
 }
 
-template <bool HAS_VALS>
+template <bool HAS_VALS, int ITEMS = RS_ITEMS>
 __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ digit_start,
@@ -128,22 +129,22 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
   __shared__ uint32_t s_wsum[RS_WARPS];
   __shared__ uint32_t s_tile;
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  uint64_t *s_keys = reinterpret_cast<uint64_t *>(s_dyn);           // RS_TILE keys
-  uint32_t *s_vals = reinterpret_cast<uint32_t *>(s_dyn + 8 * RS_TILE);  // RS_TILE payloads
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(s_dyn);           // (RS_THREADS * ITEMS) keys
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(s_dyn + 8 * (RS_THREADS * ITEMS));  // (RS_THREADS * ITEMS) payloads
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_warp[0][0])[i] = 0;
   __syncthreads();
   const int64_t tile = s_tile;
-  const int64_t base = tile * RS_TILE;
-  const int64_t wbase = base + warp * (32 * RS_ITEMS);
+  const int64_t base = tile * (RS_THREADS * ITEMS);
+  const int64_t wbase = base + warp * (32 * ITEMS);
 
-  uint64_t k[RS_ITEMS];
-  uint32_t v[RS_ITEMS];
-  uint32_t rank[RS_ITEMS];
+  uint64_t k[ITEMS];
+  uint32_t v[ITEMS];
+  uint32_t rank[ITEMS];
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     int64_t idx = wbase + i * 32 + lane;
     if (idx < n) {
       k[i] = kin[idx];
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
   }
   const uint32_t lt = lanemask_lt();
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     int64_t idx = wbase + i * 32 + lane;
     uint32_t dg = idx < n ? (uint32_t)((k[i] >> shift) & 255) : 256u;
     uint32_t peers = __match_any_sync(0xffffffffu, dg);
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
   __syncthreads();
   // stage in digit order
 #pragma unroll
-  for (int i = 0; i < RS_ITEMS; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     int64_t idx = wbase + i * 32 + lane;
     if (idx < n) {
       uint32_t dg = (uint32_t)((k[i] >> shift) & 255);
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
     }
   }
   __syncthreads();
-  const int tile_n = (int)min((int64_t)RS_TILE, n - base);
+  const int tile_n = (int)min((int64_t)(RS_THREADS * ITEMS), n - base);
   for (int j = tid; j < tile_n; j += RS_THREADS) {
     uint64_t key = s_keys[j];
     uint32_t dg = (uint32_t)((key >> shift) & 255);
@@ -344,11 +345,37 @@ inline size_t compact_scratch_bytes(int64_t n) {
 }
 
 // ------------------------------------------------------------- functors
+// Exact division of x < 2^63 by a run-time constant D: floor(x / D) =
+// mulhi(x, m) >> sh (Granlund-Montgomery with N = 63; D = 1 -> sh = -1).
+// 64-bit integer division is a ~70-instruction software routine on the GPU;
+// the segment and sweep kernels divide every element.
+struct Div63 {
+  uint64_t d, m;
+  int sh;
+  __device__ __forceinline__ uint64_t quo(uint64_t x) const { return sh < 0 ? x : (__umul64hi(x, m) >> sh); }
+};
+
+Div63 make_div63(uint64_t D) {
+  Div63 r;
+  r.d = D;
+  if (D <= 1) {
+    r.m = 0;
+    r.sh = -1;
+    return r;
+  }
+  int l = 0;
+  while (((unsigned __int128)1 << l) < D) ++l;
+  const unsigned __int128 num = (unsigned __int128)1 << (63 + l);
+  r.m = (uint64_t)(num / D + 1);
+  r.sh = l - 1;
+  return r;
+}
+
 struct AdjDiffPred {  // sorted keys: key/div differs from predecessor
   const uint64_t *k;
-  uint64_t div;
+  Div63 div;
   __device__ bool operator()(int64_t i) const {
-    return i == 0 || (k[i] / div) != (k[i - 1] / div);
+    return i == 0 || div.quo(k[i]) != div.quo(k[i - 1]);
   }
 };
 
@@ -356,18 +383,18 @@ struct FiberEmit {
   const uint64_t *k;
   const uint32_t *perm;
   const double *vals_in;
-  uint64_t np;
+  Div63 np;
   int64_t *fixed_lin, *indptr, *fiber_of, *pivot_index;
   double *vals_out;
   __device__ void operator()(int64_t i, int64_t r, bool f) const {
     uint64_t key = k[i];
-    uint64_t fx = key / np;
+    uint64_t fx = np.quo(key);
     if (f) {
       indptr[r] = i;
       fixed_lin[r] = (int64_t)fx;
     }
     if (fiber_of) fiber_of[i] = f ? r : r - 1;
-    pivot_index[i] = (int64_t)(key - fx * np);
+    pivot_index[i] = (int64_t)(key - fx * np.d);
     vals_out[i] = vals_in[perm[i]];
   }
 };
@@ -403,8 +430,10 @@ struct SweepKey {
   const int64_t *fixed_lin;
   int64_t stride, nk, r_other;
   const int64_t *map_in;
+  Div63 dstride, dnk;
   __device__ int64_t operator()(int64_t f) const {
-    int64_t ik = (fixed_lin[f] / stride) % nk;
+    const uint64_t q = dstride.quo((uint64_t)fixed_lin[f]);
+    int64_t ik = (int64_t)(q - dnk.quo(q) * (uint64_t)nk);
     int64_t m = map_in ? map_in[f] : 0;
     return side == 0 ? m * nk + ik : ik * r_other + m;
   }
@@ -777,7 +806,14 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
   FTT_CHECK(copy_to_host(ctx, h.data(), ghist, sizeof(uint32_t) * num_passes * RADIX));
   k_hist_scan<<<num_passes, RADIX, 0, ctx->stream>>>(ghist);
   FTT_LAUNCHED(ctx);
-  int64_t ntiles = ceil_div(n, RS_TILE);
+  // tile size: RS_ITEMS (16) or 24 keys per thread (A/B knob FTT_RS_ITEMS)
+  static const int items = [] {
+    const char *e = getenv("FTT_RS_ITEMS");
+    const int v = e ? atoi(e) : RS_ITEMS;
+    return (v == 8 || v == 12 || v == 24) ? v : RS_ITEMS;
+  }();
+  const int tile = RS_THREADS * items;
+  int64_t ntiles = ceil_div(n, tile);
   int cur = 0;
   for (int p = 0; p < num_passes; ++p) {
     bool trivial = false;
@@ -788,22 +824,35 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
     FTT_CUDA(cudaMemsetAsync(counters + p, 0, sizeof(uint32_t), ctx->stream));
     static bool attr_set = false;
     if (!attr_set) {
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    12 * RS_TILE));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    12 * RS_TILE));
+      const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, RS_ITEMS>, a, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, RS_ITEMS>, a, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, 24>, a, 12 * RS_THREADS * 24));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, 24>, a, 12 * RS_THREADS * 24));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, 12>, a, 12 * RS_THREADS * 12));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, 12>, a, 12 * RS_THREADS * 12));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, 8>, a, 12 * RS_THREADS * 8));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, 8>, a, 12 * RS_THREADS * 8));
       attr_set = true;
     }
     const int pb = prof_begin(ctx);
+#define FTT_ONESWEEP(V_, I_)                                                                  \
+  k_onesweep<V_, I_><<<(unsigned)ntiles, RS_THREADS, (V_ ? 12 : 8) * RS_THREADS * I_,         \
+                       ctx->stream>>>(keys[cur], V_ ? vals[cur] : nullptr, keys[cur ^ 1],      \
+                                      V_ ? vals[cur ^ 1] : nullptr, n, 8 * p,                 \
+                                      ghist + p * RADIX, status, counters + p)
     if (vals[0]) {
-      k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
-          keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, ghist + p * RADIX, status,
-          counters + p);
+      if (items == 24) FTT_ONESWEEP(true, 24);
+      else if (items == 12) FTT_ONESWEEP(true, 12);
+      else if (items == 8) FTT_ONESWEEP(true, 8);
+      else FTT_ONESWEEP(true, RS_ITEMS);
     } else {
-      k_onesweep<false><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
-          keys[cur], nullptr, keys[cur ^ 1], nullptr, n, 8 * p, ghist + p * RADIX, status,
-          counters + p);
+      if (items == 24) FTT_ONESWEEP(false, 24);
+      else if (items == 12) FTT_ONESWEEP(false, 12);
+      else if (items == 8) FTT_ONESWEEP(false, 8);
+      else FTT_ONESWEEP(false, RS_ITEMS);
     }
+#undef FTT_ONESWEEP
     FTT_LAUNCHED(ctx);
     // algorithmic bytes: read + write every key (and payload) once
     prof_end(ctx, pb, PT_SORT, (double)n * (vals[0] ? 24.0 : 16.0), 0.0);
@@ -815,7 +864,7 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
 }
 
 size_t onesweep_scratch(int64_t n) {
-  int64_t ntiles = ceil_div(n, RS_TILE);
+  int64_t ntiles = ceil_div(n, RS_MIN_TILE);
   return align_up(sizeof(uint32_t) * 8 * RADIX) + align_up(sizeof(uint32_t) * ntiles * RADIX) +
          align_up(sizeof(uint32_t) * 8);
 }
@@ -875,7 +924,7 @@ int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in, u
   int num_passes = (end_bit + 7) / 8;
   if (num_passes < 1) num_passes = 1;
   uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
-  uint32_t *status = take<uint32_t>(ctx, ceil_div(n, RS_TILE) * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, ceil_div(n, RS_MIN_TILE) * RADIX);
   uint32_t *counters = take<uint32_t>(ctx, 8);
   uint64_t *kb[2] = {take<uint64_t>(ctx, n), take<uint64_t>(ctx, n)};
   uint32_t *vb[2] = {nullptr, nullptr};
@@ -939,7 +988,7 @@ static int sort_coords(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t
   int num_passes = (end_bit + 7) / 8;
   if (num_passes < 1) num_passes = 1;
   uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
-  uint32_t *status = take<uint32_t>(ctx, ceil_div(nnz, RS_TILE) * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, ceil_div(nnz, RS_MIN_TILE) * RADIX);
   uint32_t *counters = take<uint32_t>(ctx, 8);
   uint64_t *kb[2] = {take<uint64_t>(ctx, nnz), take<uint64_t>(ctx, nnz)};
   uint32_t *vb[2] = {nullptr, nullptr};
@@ -1200,8 +1249,8 @@ int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords, const double *values
   FTT_CHECK(sort_coords(ctx, coords, nnz, d, dims_host, pivot, true, &kr, &vr, &bound));
   int64_t *bc = take<int64_t>(ctx, ceil_div(nnz, CP_TILE) + 1);
   int64_t *total = take<int64_t>(ctx, 1);
-  AdjDiffPred pred{kr, (uint64_t)dims_host[pivot]};
-  FiberEmit emit{kr, vr, values, (uint64_t)dims_host[pivot], fixed_lin, indptr, fiber_of,
+  AdjDiffPred pred{kr, make_div63((uint64_t)dims_host[pivot])};
+  FiberEmit emit{kr, vr, values, make_div63((uint64_t)dims_host[pivot]), fixed_lin, indptr, fiber_of,
                  pivot_index, values_out};
   // per entry: sorted key + payload + gathered value in; pivot index, value,
   // fiber id out (the per-fiber indptr / key writes are <= 16 bytes x R more)
@@ -1280,7 +1329,7 @@ static int depar_from_keys(ftt_ctx *ctx, int64_t n_rows, int64_t R, const SweepK
     FTT_LAUNCHED(ctx);
   }
   FTT_CHECK(radix_sort(ctx, keys, ident, skeys, perm, R, bit_length((uint64_t)(n_rows - 1))));
-  FTT_CHECK(compact(ctx, R, AdjDiffPred{skeys, 1}, UniqEmit{skeys, perm, kept, map_out}, bc, total));
+  FTT_CHECK(compact(ctx, R, AdjDiffPred{skeys, make_div63(1)}, UniqEmit{skeys, perm, kept, map_out}, bc, total));
   FTT_CHECK(copy_to_host(ctx, n_kept_out, total, sizeof(int64_t)));
   return FTT_OK;
 }
@@ -1306,7 +1355,8 @@ int ftt_index_sweep_step(ftt_ctx *ctx, int32_t side, const int64_t *fixed_lin, i
     *n_kept_out = 0;
     return FTT_OK;
   }
-  SweepKey sk{side, fixed_lin, stride_k, n_k, r_other, map_in};
+  SweepKey sk{side, fixed_lin, stride_k, n_k, r_other, map_in, make_div63((uint64_t)stride_k),
+              make_div63((uint64_t)n_k)};
   return depar_from_keys(ctx, r_other * n_k, R, &sk, nullptr, kept, map_out, n_kept_out);
 }
 

@@ -39,7 +39,9 @@ pivot = P.select_p(a)
 print(f"config {cfg}: nnz {nnz}, d {d}, pivot {pivot}, counts {counts}")
 b = nnz * (8 * d + 8) + d * nnz * 16
 print(f"select_p counts   {ms:8.3f} ms  {b / ms / 1e6:8.0f} GB/s (alg {b / 1e6:.0f} MB: COO + 16 B/nnz/pivot)")
-ms, df = timed(lambda: ft.coo.fibers_device(a.shape, pivot, cd, vd, nnz))
+for _ in range(3):
+    ms, df = timed(lambda: ft.coo.fibers_device(a.shape, pivot, cd, vd, nnz))
+    print(f"  (extract fibers {ms:.3f} ms)")
 b = nnz * (8 * d + 8) + 16 * nnz + 8 * d * df.R
 print(f"extract fibers    {ms:8.3f} ms  {b / ms / 1e6:8.0f} GB/s (alg {b / 1e6:.0f} MB), R {df.R}")
 ms, sw = timed(lambda: P.index_sweeps_device(df))
