@@ -212,6 +212,24 @@ int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
                         int64_t lda, int32_t a_row_major, int64_t k,
                         double delta2, double *s_host, double *rest2_host,
                         int32_t *accepted);
+/* The same certified low-rank phase 1 on the pivot core of
+ * parallel_vector_round (fasttt.py:256-259) given by its entries instead of
+ * the dense core: the operand is M = core.reshape(r_prev * n_p, r_next)
+ * (m = r_prev * n_p, n = r_next), entry e at row t_map[f] * n_p +
+ * pivot_index[e], column s_map[f] (f = fiber_of[e]; t_map / s_map NULL for
+ * r_prev / r_next = 1), value values[e] -- the FiberSet arrays of
+ * ftt_extract_fibers and the maps of ftt_index_sweep_step.  Y, B and the
+ * residual energy (over every element of M, zeros included) are computed
+ * from the entries; k <= 64.  Phase 2 is ftt_svd_vectors as above.  A
+ * rejected certificate (accepted = 0) leaves the caller to densify the core
+ * (ftt_pivot_core_scatter) for ftt_svd_f64. */
+int ftt_svd_lowrank_sparse_f64(ftt_ctx *ctx, int64_t m, int64_t n, int64_t nnz,
+                               const int64_t *fiber_of,
+                               const int64_t *pivot_index,
+                               const double *values, const int64_t *t_map,
+                               const int64_t *s_map, int64_t n_p, int64_t k,
+                               double delta2, double *s_host,
+                               double *rest2_host, int32_t *accepted);
 /* Phase 2: the leading `rank` singular triplets of the last ftt_svd_f64, with
  * the sign convention of _fix_signs (linalg.py:56-63) applied to U: U (m x
  * rank) and V (n x rank, i.e. vt.T), each column- or row-major per its flag;

@@ -15,7 +15,9 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfasttt_b200.so")
+# FTT_LIB: load another build of the same library (A/B timing of two builds in
+# one process environment); the default is the in-tree build.
+LIB_PATH = os.environ.get("FTT_LIB") or os.path.join(_HERE, "libfasttt_b200.so")
 
 FTT_OK = 0
 FTT_ERR_INVALID = 1
@@ -63,6 +65,8 @@ SIGNATURES = {
     "ftt_svd_f64": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i32, _P_d],
     "ftt_svd_lowrank_f64": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i32, _c_i64, _c_d, _P_d, _P_d,
                             ctypes.POINTER(ctypes.c_int32)],
+    "ftt_svd_lowrank_sparse_f64": [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                   _c_i64, _c_i64, _c_d, _P_d, _P_d, ctypes.POINTER(ctypes.c_int32)],
     "ftt_svd_vectors": [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_i32, _c_i32],
     "ftt_dot": [_c_p, _c_i64, _c_p, _c_p, _P_d],
     "ftt_set_deferred_checks": [_c_p, _c_i32],

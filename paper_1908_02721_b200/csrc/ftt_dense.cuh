@@ -41,6 +41,40 @@ size_t qr_apply_workspace_elems(int64_t m, int64_t n, int64_t r);
 int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau, int64_t *sel_dev,
                 int64_t *rank, const double *aux_dev = nullptr, double *aux_host = nullptr);
 
+// Sparse operand of the first truncation step (ftt_sparse.cu): the entries
+// of the pivot core as A_tall (mA x nA = M or M^T) in CSR (by row) and CSC
+// (by column, rows ascending) order.
+struct SparseOperand {
+  int64_t nnz = 0, mA = 0, nA = 0;
+  bool transposed = false;
+  int64_t *rptr = nullptr;   // mA + 1
+  int32_t *cidx_r = nullptr; // CSR column per entry
+  double *v_r = nullptr;     // CSR values
+  int64_t *cptr = nullptr;   // nA + 1
+  uint64_t *keyc = nullptr;  // CSC keys: col * mA + row (sorted)
+  int32_t *ridx_c = nullptr; // CSC row per entry
+  int32_t *cidx_c = nullptr; // CSC column per entry
+  double *v_c = nullptr;     // CSC values
+  int64_t *seg_base = nullptr;  // nA + 1: first B segment of each column
+  int64_t max_segs = 0;
+  double *Qr = nullptr;      // row-major copy of the range basis (sparse_qt_a)
+  int64_t ldq = 0;           // its row stride (kr rounded up to even)
+};
+// M (m x n): entry e at row t_map[f] * np + pidx[e], column s_map[f]
+// (f = fiber_of[e]; a NULL map means 0).
+int sparse_operand_build(ftt_ctx *ctx, SparseOperand *op, int64_t nnz, const int64_t *fiber_of,
+                         const int64_t *pidx, const double *vals, const int64_t *tmap,
+                         const int64_t *smap, int64_t np, int64_t m, int64_t n);
+void sparse_operand_free(ftt_ctx *ctx, SparseOperand *op);
+// Y (mA x k col-major) = A_tall Omega with the range finder's test matrix.
+int sparse_sketch(ftt_ctx *ctx, const SparseOperand &op, int64_t k, double *Y);
+// B (kr x nA col-major) = Q^T A_tall, Q mA x kr col-major.
+int sparse_qt_a(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, double *B);
+// ||A_tall - Q B||_F^2 over every element (deterministic) -> out_dev.
+// (after sparse_qt_a with the same Q)
+int sparse_resid(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, const double *B,
+                 double *out_dev);
+
 int check_finite(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, bool *ok);
 int copy_matrix(ftt_ctx *ctx, int64_t m, int64_t n, const double *src, int64_t lds, double *dst,
                 int64_t ldd);

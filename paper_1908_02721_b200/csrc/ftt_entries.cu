@@ -45,6 +45,48 @@ __global__ void k_entries_small(TrainDesc t, const int64_t *__restrict__ coords,
   }
 }
 
+// Ranks <= L (L = 4, 8, 16, 32): a group of L lanes per coordinate (32 / L
+// coordinates per warp), the running row vector one register per lane,
+// broadcasts by width-L shuffles.
+template <int L>
+__global__ void k_entries_grp(TrainDesc t, const int64_t *__restrict__ coords, int64_t n,
+                              double *__restrict__ out) {
+  const int lane = threadIdx.x & 31, sub = lane & (L - 1);
+  constexpr int PER_WARP = 32 / L;
+  const int64_t slots = (int64_t)gridDim.x * (blockDim.x >> 5) * PER_WARP;
+  const int64_t first = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * PER_WARP +
+                        (lane / L);
+  // every lane of a warp runs the same trip count (shuffles need the full warp)
+  const int64_t trips = (n + slots - 1) / slots;
+  for (int64_t it = 0; it < trips; ++it) {
+    const int64_t i = first + it * slots;
+    const bool live = i < n;
+    double v = sub == 0 ? 1.0 : 0.0;
+    for (int k = 0; k < t.d; ++k) {
+      const int64_t r0 = t.ranks[k], r1 = t.ranks[k + 1], nk = t.dims[k];
+      const int64_t idx = live ? coords[i * t.d + k] : 0;
+      const double *G = t.cores[k] + idx * r1;
+      const int64_t rowst = nk * r1;
+      // slice loads issued 8 at a time ahead of the shuffles/FMAs (the slices
+      // come from L2: a dependent load per step made this latency bound)
+      double acc = 0.0;
+      const bool act = live && sub < r1;
+      for (int a0 = 0; a0 < (int)r0; a0 += 8) {
+        double g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g[u] = (act && a0 + u < r0) ? __ldg(G + (a0 + u) * rowst + sub) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double va = __shfl_sync(0xffffffffu, v, (a0 + u) & (L - 1), L);
+          acc += va * g[u];
+        }
+      }
+      v = acc;
+    }
+    if (live && sub == 0) out[i] = v;
+  }
+}
+
 __global__ void k_first_rows(int64_t n, const int64_t *__restrict__ coords, int d, const double *core0,
                              int64_t r1, const int64_t *__restrict__ idx, double *__restrict__ V) {
   int64_t total = n * r1;
@@ -318,7 +360,23 @@ extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
     set_error("edge ranks must be 1");
     return FTT_ERR_INVALID;
   }
-  if (rmax <= 64 && d >= 4 && n >= 65536 && n < ((int64_t)1 << 31)) return entries_mitm(ctx, t, coords, n, out);
+  // direct evaluation costs ~n * sum_k r_k shuffle-FMA steps per lane group;
+  // the meet-in-the-middle path a fixed ~0.2 ms of sorts: it only pays for
+  // large n * sum_k r_k (config 5: 8.5M coordinates x 176)
+  double steps = 0.0;
+  for (int k = 0; k < d; ++k) steps += (double)ranks_host[k];
+  if (rmax <= 64 && d >= 4 && (double)n * steps > 4e8 && n < ((int64_t)1 << 31))
+    return entries_mitm(ctx, t, coords, n, out);
+  if (rmax <= 32) {
+    const int L = rmax <= 4 ? 4 : rmax <= 8 ? 8 : rmax <= 16 ? 16 : 32;
+    const int grid = grid_for(n, 8 * (32 / L), 1, 148 * 64);
+    if (L == 4) k_entries_grp<4><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
+    else if (L == 8) k_entries_grp<8><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
+    else if (L == 16) k_entries_grp<16><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
+    else k_entries_grp<32><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
   if (rmax <= 64) {
     k_entries_small<<<grid_for(n, 8, 1, 148 * 64), 256, 0, ctx->stream>>>(t, coords, n, out);
     FTT_LAUNCHED(ctx);

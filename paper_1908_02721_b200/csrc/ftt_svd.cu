@@ -814,9 +814,11 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
   return FTT_OK;
 }
 
-extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
-                                   int64_t lda, int32_t a_row_major, int64_t k, double delta2,
-                                   double *s_host, double *rest2_host, int32_t *accepted) {
+// The certified low-rank path on a dense operand (A, lda, a_row_major) or on
+// the entries of a sparse one (sp != nullptr, ftt_sparse.cu).
+static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
+                       int32_t a_row_major, SparseOperand *sp, int64_t k, double delta2,
+                       double *s_host, double *rest2_host, int32_t *accepted) {
   if (!ctx || m < 0 || n < 0 || !accepted || !rest2_host) return FTT_ERR_INVALID;
   svd_state_free(ctx);
   SvdState *st = new SvdState();
@@ -831,6 +833,7 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   *accepted = 0;
   *rest2_host = -1.0;
   if (nA == 0 || k <= 0 || k >= nA) return FTT_OK;
+  if (sp && k > 64) return FTT_OK;  // sparse products handle sketches <= 64 wide
   // The tall view A_tall (mA x nA) is read straight from the caller's buffer:
   // `buf` col-major with leading dimension `ld`, stored transposed when
   // `need_t`.  A strided (non-packed) input is packed once first.
@@ -843,7 +846,9 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   double *fro2_dev = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 3)));
   double *rest2_dev = fro2_dev + kSumSqBlocks + 2;  // after sum_squares' partials
-  {
+  if (sp) {
+    FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->v_r, fro2_dev + 1, fro2_dev));
+  } else {
     const int64_t inner = need_t ? nA : mA;
     if (lda != inner) {
       FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
@@ -855,6 +860,7 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   }
   auto finite_or_decline = [&]() -> int {
     // non-finite energy: either a non-finite entry (error) or an overflow
+    if (sp) return FTT_OK;  // entries are validated finite: overflow, full SVD decides
     bool ok = true;
     FTT_CHECK(check_finite(ctx, need_t ? nA : mA, need_t ? mA : nA, buf, ld, &ok));
     if (!ok) {
@@ -864,17 +870,21 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
     return FTT_OK;  // not accepted: the caller takes the full SVD
   };
   double *Om = nullptr, *Yk = nullptr, *sk = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&Om, 8 * (size_t)nA * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&Yk, 8 * (size_t)mA * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Qk, 8 * (size_t)mA * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Bk, 8 * (size_t)k * nA));
-  const size_t ske = std::max({gemm_splitk_elems(mA, k, nA), gemm_splitk_elems(k, nA, mA),
-                               gemm_splitk_elems(mA, nA, k), (size_t)1});
+  const size_t ske = sp ? 1 : std::max({gemm_splitk_elems(mA, k, nA), gemm_splitk_elems(k, nA, mA),
+                                        gemm_splitk_elems(mA, nA, k), (size_t)1});
   FTT_CHECK(owned_alloc(ctx, (void **)&sk, 8 * ske));
-  k_omega<<<grid_for(nA * k, 256, 4), 256, 0, ctx->stream>>>(nA * k, Om);
-  FTT_LAUNCHED(ctx);
   // range finder: Y = A Omega, Q = qr(Y), B = Q^T A, residual A - Q B (in place)
-  FTT_CHECK(gemm(ctx, need_t, 0, mA, k, nA, 1.0, buf, ld, Om, nA, 0.0, Yk, mA, sk, ske));
+  if (sp) {
+    FTT_CHECK(sparse_sketch(ctx, *sp, k, Yk));
+  } else {
+    FTT_CHECK(owned_alloc(ctx, (void **)&Om, 8 * (size_t)nA * k));
+    k_omega<<<grid_for(nA * k, 256, 4), 256, 0, ctx->stream>>>(nA * k, Om);
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(gemm(ctx, need_t, 0, mA, k, nA, 1.0, buf, ld, Om, nA, 0.0, Yk, mA, sk, ske));
+  }
   static const char *qr_mode = getenv("FTT_SKETCH_QR");  // test override: householder
   if (k <= 64 && !(qr_mode && !strcmp(qr_mode, "householder"))) {
     // numerical rank of the sketch (pivoted Cholesky of its Gram, directions
@@ -921,15 +931,17 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
     FTT_CHECK(launch_identity(ctx, mA, k, st->Qk, mA));
     FTT_CHECK(qr_apply_q(ctx, mA, k, Yk, mA, Tb, k, st->Qk, mA, ws, wse));
   }
-  FTT_CHECK(gemm(ctx, 1, need_t, k, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, k, sk, ske));
+  if (sp) FTT_CHECK(sparse_qt_a(ctx, *sp, k, st->Qk, st->Bk));
+  else FTT_CHECK(gemm(ctx, 1, need_t, k, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, k, sk, ske));
   // A narrow B (k <= 64) is factored speculatively before the certificate is
   // read: the residual energy then comes back with the singular values in
   // one host round trip (a rejected certificate wastes one small SVD).
   const bool speculate = tsqr_ok(std::max(k, nA), std::min(k, nA)) &&
                          !getenv("FTT_NO_SPECULATE");
   if (speculate) {
-    FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
-                               nullptr, rest2_dev));
+    if (sp) FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
+    else FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
+                                    nullptr, rest2_dev));
     st->inner = new SvdState();
     if (svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0, rest2_dev, &rest2) != FTT_OK) {
       // speculative factorisation failed: decide on the certificate alone
@@ -938,6 +950,9 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
       st->inner = nullptr;
       FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
     }
+  } else if (sp) {
+    FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
+    FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
   } else {
     FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
                                &rest2));
@@ -973,6 +988,38 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   if (s_host) memcpy(s_host, st->sigma.data(), 8 * st->sigma.size());
   *accepted = strict ? 2 : 1;
   return FTT_OK;
+}
+
+extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A,
+                                   int64_t lda, int32_t a_row_major, int64_t k, double delta2,
+                                   double *s_host, double *rest2_host, int32_t *accepted) {
+  return lowrank_run(ctx, m, n, A, lda, a_row_major, nullptr, k, delta2, s_host, rest2_host,
+                     accepted);
+}
+
+extern "C" int ftt_svd_lowrank_sparse_f64(ftt_ctx *ctx, int64_t m, int64_t n, int64_t nnz,
+                                          const int64_t *fiber_of, const int64_t *pivot_index,
+                                          const double *values, const int64_t *t_map,
+                                          const int64_t *s_map, int64_t n_p, int64_t k,
+                                          double delta2, double *s_host, double *rest2_host,
+                                          int32_t *accepted) {
+  if (!ctx || m < 1 || n < 1 || nnz < 1 || n_p < 1 || !fiber_of || !pivot_index || !values ||
+      !accepted || !rest2_host) {
+    set_error("ftt_svd_lowrank_sparse_f64: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  if (m > 0x7fffffffLL || n > 0x7fffffffLL || nnz >= ((int64_t)1 << 30)) {
+    set_error("ftt_svd_lowrank_sparse_f64: operand too large for 32-bit entry indices");
+    return FTT_ERR_INVALID;
+  }
+  *accepted = 0;
+  *rest2_host = -1.0;
+  SparseOperand op;
+  FTT_CHECK(sparse_operand_build(ctx, &op, nnz, fiber_of, pivot_index, values, t_map, s_map, n_p, m,
+                                 n));
+  const int rc = lowrank_run(ctx, m, n, nullptr, 0, 1, &op, k, delta2, s_host, rest2_host, accepted);
+  sparse_operand_free(ctx, &op);
+  return rc;
 }
 
 extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ldu,

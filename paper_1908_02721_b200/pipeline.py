@@ -37,7 +37,14 @@ from .coo import (
     device_dot,
     fibers_device,
 )
-from .dense import dev_svd_truncate, dev_svd_values, dev_svd_vectors, tail_error, tail_rank
+from .dense import (
+    dev_svd_truncate,
+    dev_svd_values,
+    dev_svd_vectors,
+    lowrank_k,
+    tail_error,
+    tail_rank,
+)
 from .trains import (
     QuasiPermMatrix,
     StructuredTT,
@@ -385,7 +392,56 @@ def _pivot_core(df, sw: DeviceSweeps):
     return core, float(norm.value)
 
 
-def _structured_train(df, sw: DeviceSweeps):
+class SparsePivotCore:
+    """The pivot core of parallel_vector_round (fasttt.py:256-259) kept as its
+    entries -- value at (t_map[f], i_p, s_map[f]) -- until a dense copy is
+    needed.  The first truncation step runs the certified low-rank range
+    finder on the entries (ftt_svd_lowrank_sparse_f64); config 5's core is
+    0.65 % dense and 10.5 GB when materialised."""
+
+    __slots__ = ("df", "sw", "shape", "_dense")
+
+    def __init__(self, df, sw: DeviceSweeps):
+        self.df, self.sw = df, sw
+        self.shape = (sw.r_prev, df.dims[df.pivot], sw.r_next)
+        self._dense = None
+
+    @property
+    def density(self) -> float:
+        return self.df.nnz / float(max(math.prod(self.shape), 1))
+
+    def dense(self):
+        if self._dense is None:
+            self._dense, _ = _pivot_core(self.df, self.sw)
+        return self._dense
+
+    def svd_lowrank(self, k: int, delta: float):
+        """(s, rest2, accepted) of the first sweep step's operand
+        core.reshape(r_prev n_p, r_next) (see dense.dev_svd_values_lowrank)."""
+        r0, n, r1 = self.shape
+        df, sw = self.df, self.sw
+        s = np.zeros(k)
+        rest2 = nat.ctypes.c_double(0.0)
+        acc = nat.ctypes.c_int32(0)
+        nat.check(nat.lib().ftt_svd_lowrank_sparse_f64(
+            nat.context(), r0 * n, r1, df.nnz, nat.ptr(df.fiber_of), nat.ptr(df.pivot_index),
+            nat.ptr(df.values), nat.ptr(sw.t_map), nat.ptr(sw.s_map), n, int(k),
+            float(delta * delta), s.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_double)),
+            nat.ctypes.byref(rest2), nat.ctypes.byref(acc)), "ftt_svd_lowrank_sparse_f64")
+        return s, float(rest2.value), int(acc.value)
+
+
+# below this density the first truncation step works on the pivot core's
+# entries (sorting them twice costs about as much as one pass over a dense
+# core of ~20x the entry count)
+_SPARSE_PIVOT_DENSITY = 0.02
+
+
+def _as_dense(c):
+    return c.dense() if isinstance(c, (SideCore, SparsePivotCore)) else c
+
+
+def _structured_train(df, sw: DeviceSweeps, lazy_pivot: bool = False):
     d = len(df.dims)
     cores = [None] * d
     for k, (kept, rp) in enumerate(sw.left):
@@ -393,6 +449,12 @@ def _structured_train(df, sw: DeviceSweeps):
     for step, (kept, rn) in enumerate(sw.right):
         k = d - 1 - step
         cores[k] = SideCore("R", kept, rn, df.dims[k])
+    if lazy_pivot:
+        spc = SparsePivotCore(df, sw)
+        if spc.density < _SPARSE_PIVOT_DENSITY and df.pivot < d - 1:
+            # ||pivot core||_F = ||values||_2 (fasttt.py:359-361)
+            cores[df.pivot] = spc
+            return cores, math.sqrt(device_dot(df.values, None))
     pc, norm = _pivot_core(df, sw)
     cores[df.pivot] = pc
     return cores, norm
@@ -409,7 +471,7 @@ def parallel_vector_round(s: StructuredTT) -> TTTensor:
     df = _device_fibers_of(s)
     sw = index_sweeps_device(df)
     cores, _ = _structured_train(df, sw)
-    out = [c.dense() if isinstance(c, SideCore) else c for c in cores]
+    out = [_as_dense(c) for c in cores]
     return TTTensor([c.cpu().numpy() for c in out], copy=False)
 
 
@@ -505,8 +567,16 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
         C = cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
         m = r0 * n
-        s, rest2 = dev_svd_truncate(C, m, r1, r1, True, policy.delta_first(k), hint,
-                                    policy.kind == "static")
+        s = None
+        if isinstance(C, SparsePivotCore):
+            s, rest2 = _sparse_first_step(C, m, r1, policy.delta_first(k), hint,
+                                          policy.kind == "static")
+            if s is None:  # certificate rejected (or not applicable): dense operand
+                C = cs[k] = C.dense()
+                s, rest2 = dev_svd_values(C, m, r1, r1, True), 0.0
+        if s is None:
+            s, rest2 = dev_svd_truncate(C, m, r1, r1, True, policy.delta_first(k), hint,
+                                        policy.kind == "static")
         rank, _ = policy.first(k, s, (m, r1), rest2)
         hint = rank
         if rank == 0:
@@ -525,7 +595,7 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
             dgemm(0, 0, nn * c, rank, r1, 1.0, nxt, nn * c, V, r1, 0.0, new, nn * c)
             cs[k + 1] = new.reshape(rank, nn, c)
     for k in range(d - 1, pivot, -1):  # :342-347
-        C = cs[k]
+        C = cs[k] = _as_dense(cs[k]) if isinstance(cs[k], SparsePivotCore) else cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
         Q, R = dev_qr(C, n * r1, r0, n * r1)
         q = int(Q.shape[0])
@@ -538,7 +608,7 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
         dgemm(0, 0, q, a * b, c, 1.0, R, q, P, c, 0.0, Y, q)
         cs[k - 1] = Y.reshape(a, b, q)
     for k in range(pivot, 0, -1):  # :348-355
-        C = cs[k]
+        C = cs[k] = _as_dense(cs[k]) if isinstance(cs[k], SparsePivotCore) else cs[k]
         r0, n, r1 = (int(x) for x in C.shape)
         s, rest2 = dev_svd_truncate(C, n * r1, r0, n * r1, False, policy.delta_second(k), hint,
                                     policy.kind == "static")
@@ -559,11 +629,27 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
             Y = _empty((a * b, rank))
             dgemm(0, 0, rank, a * b, c, 1.0, V, rank, prv, c, 0.0, Y, rank)
             cs[k - 1] = Y.reshape(a, b, rank)
-    out = []
-    for c in cs:
-        out.append(c.dense() if isinstance(c, SideCore) else c)
+    out = [_as_dense(c) for c in cs]
     del torch
     return out
+
+
+def _sparse_first_step(spc: SparsePivotCore, m: int, n: int, delta, hint, interval_ok: bool):
+    """dev_svd_truncate's low-rank branch on the entries of the pivot core;
+    (None, 0) when it does not apply or its certificate is rejected."""
+    if delta is None or not delta > 0.0:
+        return None, 0.0
+    k = lowrank_k(min(m, n), hint)
+    if not k or k > 64:
+        return None, 0.0
+    s, rest2, acc = spc.svd_lowrank(k, delta)
+    if acc == 2:
+        return s, rest2
+    if acc == 1 and interval_ok:
+        shape = (m, n)
+        if tail_rank(s, delta, shape, 0.0) == tail_rank(s, delta, shape, rest2):
+            return s, rest2
+    return None, 0.0
 
 
 def _make_policy(budget: TruncationBudget, d: int, norm: float):
@@ -816,7 +902,7 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
         raise ValueError("inconsistent fiber index pointers")
     sw = index_sweeps_device(df)
     ranks_lossless = _lossless_ranks_from(sw, d)
-    cores, pnorm = _structured_train(df, sw)
+    cores, pnorm = _structured_train(df, sw, lazy_pivot=mode != "fixed_rank")
     budget = TruncationBudget(eps=eps, pivot=pivot, mode=mode, fixed_ranks=fixed_ranks)
     if mode == "fixed_rank":
         policy = _Trunc("fixed", d, targets=_fixed_targets(budget, dims))
@@ -833,10 +919,10 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
     if report:
         norm_a = math.sqrt(device_dot(values_d, None))
         inner = _inner_error_device(coords_d, values_d, nnz, out)
-        exact_shapes = [c.shape if isinstance(c, SideCore) else tuple(c.shape) for c in cores]
+        exact_shapes = [tuple(c.shape) for c in cores]
         total = _diff_total(exact_shapes, [tuple(c.shape) for c in out])
         if total <= _ERROR_MEASURE_CAP:
-            exact_d = [c.dense() if isinstance(c, SideCore) else c for c in cores]
+            exact_d = [_as_dense(c) for c in cores]
             res.eps_actual = _dev_relative_error(exact_d, out, norm_a)
             res.eps_actual_method = "tt_difference"
         else:

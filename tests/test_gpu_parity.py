@@ -400,3 +400,64 @@ def test_fiber_counts_all_paths(path, monkeypatch):
             rest = np.delete(c, p, axis=1)
             want.append(int(np.unique(rest, axis=0).shape[0]))
         assert P._fiber_counts_device(t) == want
+
+
+def _rank_r_sparse(dims, R, s, seed):
+    """Sum of R sparse rank-1 terms (s seeded positions per mode), coalesced."""
+    rng = np.random.default_rng(seed)
+    lins, vals = [], []
+    for _ in range(R):
+        pos = [rng.choice(n, s, replace=False) for n in dims]
+        fac = [rng.standard_normal(s) for _ in dims]
+        grid = np.stack(np.meshgrid(*pos, indexing="ij"), -1).reshape(-1, len(dims))
+        val = np.ones(1)
+        for f in fac:
+            val = np.multiply.outer(val, f).reshape(-1)
+        lins.append(np.ravel_multi_index(grid.T, dims))
+        vals.append(val)
+    lin = np.concatenate(lins)
+    v = np.concatenate(vals)
+    u, inv = np.unique(lin, return_inverse=True)
+    vsum = np.zeros(u.size)
+    np.add.at(vsum, inv, v)
+    keep = vsum != 0.0
+    coords = np.stack(np.unravel_index(u[keep], dims), 1).astype(np.int64)
+    return ft.SparseTensor(dims, coords, vsum[keep])
+
+
+@pytest.mark.parametrize("dims,R,s,pivot", [((40,) * 6, 6, 3, 2), ((16,) * 5, 4, 4, 1),
+                                             ((40, 9, 40, 9), 5, 5, 0)])
+def test_sparse_pivot_core_lowrank_matches_dense(dims, R, s, pivot, monkeypatch):
+    """The low-rank range finder on the pivot core's entries
+    (ftt_svd_lowrank_sparse_f64) against the same path on the densified core:
+    singular values within 1e-12 relative, both certificates accepted, the
+    sparse residual energy within rounding of the dense one; and the full
+    decomposition through the sparse path reproduces the oracle's ranks and
+    entries within 1e-10."""
+    t = _rank_r_sparse(dims, R, s, seed=sum(dims) + R)
+    fs = ft.extract_nonzero_fibers(t, pivot)
+    df = fs._dev
+    sw = P.index_sweeps_device(df)
+    spc = P.SparsePivotCore(df, sw)
+    r0, n, r1 = spc.shape
+    m = r0 * n
+    norm = math.sqrt(float(np.sum(t.values ** 2)))
+    delta = 1e-10 * norm / (math.sqrt(pivot) + math.sqrt(len(dims) - 1 - pivot))
+    k = 2 * R + 8
+    assert k < min(m, r1)
+    s_sp, rest_sp, acc_sp = spc.svd_lowrank(k, delta)
+    dense = spc.dense()
+    from paper_1908_02721_b200 import dense as D
+    s_de, rest_de, acc_de = D.dev_svd_values_lowrank(dense, m, r1, r1, True, k, delta * delta)
+    assert acc_sp >= 1 and acc_de >= 1
+    kk = min(len(s_sp), len(s_de))
+    assert np.max(np.abs(s_sp[:kk] - s_de[:kk])) <= 1e-12 * s_de[0]
+    assert rest_sp <= 1e-6 * delta * delta and rest_de <= 1e-6 * delta * delta
+    # end to end through the sparse first step (forced for the denser cases)
+    monkeypatch.setattr(P, "_SPARSE_PIVOT_DENSITY", 1.0)
+    tt, rep = ft.fasttt(t, eps=1e-10, pivot=pivot)
+    cores, info = O.fasttt(t.shape, t.coords, t.values, eps=1e-10, pivot=pivot, report=False)
+    assert tuple(rep.ranks) == info["ranks"]
+    rng = np.random.default_rng(3)
+    probe = np.concatenate([t.coords, np.stack([rng.integers(0, d, 20000) for d in dims], 1)])
+    assert rel_err(ft.tt_entries(tt, probe), O.tt_entries(cores, probe)) <= RECON_TOL
