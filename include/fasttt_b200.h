@@ -252,6 +252,11 @@ int ftt_dot(ftt_ctx *ctx, int64_t n, const double *x, const double *y,
 int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
                    const int64_t *ranks_host, const double *const *cores_host,
                    const int64_t *coords, int64_t n, double *out);
+/* Frobenius norm of the same train description (tt_norm, ttformat.py:198-203):
+ * the train contracted with itself core by core (two DMMA GEMMs per core). */
+int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
+                const int64_t *ranks_host, const double *const *cores_host,
+                double *norm_out);
 
 #ifdef __cplusplus
 }

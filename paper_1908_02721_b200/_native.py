@@ -72,6 +72,7 @@ SIGNATURES = {
     "ftt_set_deferred_checks": [_c_p, _c_i32],
     "ftt_take_status": [_c_p, ctypes.POINTER(ctypes.c_int32)],
     "ftt_sync_stats": [_c_p, ctypes.POINTER(ctypes.c_int64), _P_d],
+    "ftt_tt_norm": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _P_d],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],
 }
 _RESTYPES = {
@@ -141,14 +142,30 @@ def device_ready() -> bool:
         return False
 
 
+def _current_device_stream():
+    """(device, raw cudaStream_t) of torch's current stream; the private C
+    entry points skip torch.cuda's Python layers (this runs ~50 times per
+    decomposition)."""
+    C = torch_mod()._C
+    try:
+        dev = C._cuda_getDevice()
+        return dev, C._cuda_getCurrentRawStream(dev)
+    except AttributeError:  # pragma: no cover - older torch
+        torch = torch_mod()
+        dev = torch.cuda.current_device()
+        return dev, torch.cuda.current_stream(dev).cuda_stream
+
+
 def context():
     """The per-device native context, bound to torch's current stream."""
-    torch = torch_mod()
-    if not torch.cuda.is_available():
-        raise RuntimeError("a CUDA device is required: the B200 FastTT path has no CPU fallback")
-    lib = load_library()
-    dev = torch.cuda.current_device()
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    if not _ctx_cache:
+        torch = torch_mod()
+        if not torch.cuda.is_available():
+            raise RuntimeError("a CUDA device is required: the B200 FastTT path has no CPU "
+                               "fallback")
+        torch.cuda.init()
+    lib = _lib if _lib is not None else load_library()
+    dev, stream = _current_device_stream()
     ctx = _ctx_cache.get(dev)
     if ctx is None:
         h = _c_p()
@@ -163,7 +180,7 @@ def context():
 
 
 def lib():
-    return load_library()
+    return _lib if _lib is not None else load_library()
 
 
 def kernel_launches() -> int:

@@ -47,10 +47,27 @@ __global__ void k_entries_small(TrainDesc t, const int64_t *__restrict__ coords,
 
 // Ranks <= L (L = 4, 8, 16, 32): a group of L lanes per coordinate (32 / L
 // coordinates per warp), the running row vector one register per lane,
-// broadcasts by width-L shuffles.
+// broadcasts by width-L shuffles.  Latency hiding: the point's coordinates
+// are loaded once up front (lane s of the group holds modes s, s + L, ...),
+// and the core slice of step k + 1 is loaded before the FMAs of step k.
 template <int L>
-__global__ void k_entries_grp(TrainDesc t, const int64_t *__restrict__ coords, int64_t n,
-                              double *__restrict__ out) {
+__device__ __forceinline__ void load_slice(const TrainDesc &t, int k, int64_t idx, int sub, bool act,
+                                           double (&g)[L]) {
+  const int r0 = (int)t.ranks[k], r1 = (int)t.ranks[k + 1];
+  const int rowst = (int)t.dims[k] * r1;  // < 2^31 for the ranks <= 32 of this path
+  const double *G = t.cores[k] + (idx * r1 + sub);
+  const bool on = act && sub < r1;
+#pragma unroll
+  for (int a = 0; a < L; ++a) {
+    g[a] = (on && a < r0) ? __ldg(G) : 0.0;
+    G += rowst;
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) k_entries_grp(TrainDesc t, const int64_t *__restrict__ coords,
+                                                     int64_t n, double *__restrict__ out) {
+  constexpr int CW = (32 + L - 1) / L;  // coordinate registers per lane (d <= 32)
   const int lane = threadIdx.x & 31, sub = lane & (L - 1);
   constexpr int PER_WARP = 32 / L;
   const int64_t slots = (int64_t)gridDim.x * (blockDim.x >> 5) * PER_WARP;
@@ -58,30 +75,38 @@ __global__ void k_entries_grp(TrainDesc t, const int64_t *__restrict__ coords, i
                         (lane / L);
   // every lane of a warp runs the same trip count (shuffles need the full warp)
   const int64_t trips = (n + slots - 1) / slots;
+  const int d = t.d;
   for (int64_t it = 0; it < trips; ++it) {
     const int64_t i = first + it * slots;
     const bool live = i < n;
+    int64_t cw[CW];
+#pragma unroll
+    for (int u = 0; u < CW; ++u) {
+      const int k = sub + u * L;
+      cw[u] = (live && k < d) ? coords[i * d + k] : 0;
+    }
+    auto coord = [&](int k) -> int64_t {  // mode-k index of this group's point
+      int64_t x = cw[0];
+#pragma unroll
+      for (int u = 1; u < CW; ++u)
+        if (k / L == u) x = cw[u];
+      return __shfl_sync(0xffffffffu, x, k & (L - 1), L);
+    };
     double v = sub == 0 ? 1.0 : 0.0;
-    for (int k = 0; k < t.d; ++k) {
-      const int64_t r0 = t.ranks[k], r1 = t.ranks[k + 1], nk = t.dims[k];
-      const int64_t idx = live ? coords[i * t.d + k] : 0;
-      const double *G = t.cores[k] + idx * r1;
-      const int64_t rowst = nk * r1;
-      // slice loads issued 8 at a time ahead of the shuffles/FMAs (the slices
-      // come from L2: a dependent load per step made this latency bound)
+    double g[L], gn[L];
+    load_slice<L>(t, 0, coord(0), sub, live, g);
+    for (int k = 0; k < d; ++k) {
+      if (k + 1 < d) load_slice<L>(t, k + 1, coord(k + 1), sub, live, gn);
+      const int r0 = (int)t.ranks[k];
       double acc = 0.0;
-      const bool act = live && sub < r1;
-      for (int a0 = 0; a0 < (int)r0; a0 += 8) {
-        double g[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) g[u] = (act && a0 + u < r0) ? __ldg(G + (a0 + u) * rowst + sub) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double va = __shfl_sync(0xffffffffu, v, (a0 + u) & (L - 1), L);
-          acc += va * g[u];
-        }
+      for (int a = 0; a < L; ++a) {
+        const double va = __shfl_sync(0xffffffffu, v, a, L);
+        if (a < r0) acc += va * g[a];
       }
       v = acc;
+#pragma unroll
+      for (int a = 0; a < L; ++a) g[a] = gn[a];
     }
     if (live && sub == 0) out[i] = v;
   }
@@ -370,11 +395,16 @@ extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
   if (rmax <= 32) {
     const int L = rmax <= 4 ? 4 : rmax <= 8 ? 8 : rmax <= 16 ? 16 : 32;
     const int grid = grid_for(n, 8 * (32 / L), 1, 148 * 64);
+    double steps_sum = 0.0;
+    for (int k = 0; k < d; ++k) steps_sum += (double)ranks_host[k] * ranks_host[k + 1];
+    const int pb = prof_begin(ctx);
     if (L == 4) k_entries_grp<4><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
     else if (L == 8) k_entries_grp<8><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
     else if (L == 16) k_entries_grp<16><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
     else k_entries_grp<32><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out);
     FTT_LAUNCHED(ctx);
+    // coordinates + output per point; 2 sum_k r_k r_{k+1} flops per point
+    prof_end(ctx, pb, PT_ENTRIES, (double)n * (8.0 * d + 8.0), 2.0 * steps_sum * (double)n);
     return FTT_OK;
   }
   if (rmax <= 64) {
@@ -440,3 +470,50 @@ extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
   }
   return FTT_OK;
 }
+
+// Frobenius norm of a train by contracting it with itself (ttformat.py:
+// 198-203): W_0 = [1]; per core G (a x n x b): T = W G (a x n b), W' = G^T T
+// over the (a n) rows (b x b); ||t||^2 = W_d.  Two DMMA GEMMs per core, one
+// host round trip.
+extern "C" int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
+                           const int64_t *ranks_host, const double *const *cores_host,
+                           double *norm_out) {
+  if (!ctx || !norm_out || d < 1 || d > 32) {
+    set_error("ftt_tt_norm: invalid train");
+    return FTT_ERR_INVALID;
+  }
+  int64_t wmax = 1, tmax = 1;
+  size_t ske = 1;
+  for (int k = 0; k < d; ++k) {
+    const int64_t a = ranks_host[k], n = dims_host[k], b = ranks_host[k + 1];
+    wmax = std::max(wmax, b * b);
+    tmax = std::max(tmax, a * n * b);
+    ske = std::max({ske, gemm_splitk_elems(n * b, a, a), gemm_splitk_elems(b, b, a * n)});
+  }
+  double *W[2] = {nullptr, nullptr}, *T = nullptr, *sk = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&W[0], 8 * (size_t)wmax));
+  FTT_CHECK(owned_alloc(ctx, (void **)&W[1], 8 * (size_t)wmax));
+  FTT_CHECK(owned_alloc(ctx, (void **)&T, 8 * (size_t)tmax));
+  FTT_CHECK(owned_alloc(ctx, (void **)&sk, 8 * ske));
+  const double one = 1.0;
+  FTT_CHECK(stage_to_device(ctx, W[0], &one, sizeof(double)));
+  int cur = 0;
+  for (int k = 0; k < d; ++k) {
+    const int64_t a = ranks_host[k], n = dims_host[k], b = ranks_host[k + 1];
+    // row-major T (a x n b) = W (a x a) G (a x n b)  <=>  col-major T^T = G^T W^T
+    FTT_CHECK(gemm(ctx, 0, 0, n * b, a, a, 1.0, cores_host[k], n * b, W[cur], a, 0.0, T, n * b, sk,
+                   ske));
+    // W' (b x b) = G(a n x b)^T T(a n x b)  <=>  col-major W'^T = T^T G  (row-major views)
+    FTT_CHECK(gemm(ctx, 0, 1, b, b, a * n, 1.0, T, b, cores_host[k], b, 0.0, W[cur ^ 1], b, sk, ske));
+    cur ^= 1;
+  }
+  double v = 0.0;
+  FTT_CHECK(copy_to_host(ctx, &v, W[cur], sizeof(double)));
+  owned_free(ctx, W[0]);
+  owned_free(ctx, W[1]);
+  owned_free(ctx, T);
+  owned_free(ctx, sk);
+  *norm_out = std::sqrt(std::max(v, 0.0));
+  return FTT_OK;
+}
+

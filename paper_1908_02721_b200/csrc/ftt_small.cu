@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_small(int n, const double *__
   double *P = S + (size_t)n * n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double f = 0.0;
-  for (int e = tid; e < n * n; e += SVD_NT) {
+  for (int e = tid; e < n * n; e += (int)blockDim.x) {
     const int j = e / n, i = e - j * n;  // X(i, j) = R(j, i)
     const double v = j <= i ? R[j + (int64_t)i * ldr] : 0.0;
     X[e] = v;
@@ -389,13 +389,13 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_small(int n, const double *__
     status[1] = sweeps;
     if (sweeps < 0) atomicOr(status, 2);
   }
-  for (int j = warp; j < n; j += SVD_NT / 32) {
+  for (int j = warp; j < n; j += (int)(blockDim.x >> 5)) {
     double s2 = 0.0;
     for (int i = lane; i < n; i += 32) s2 += X[i + (size_t)j * n] * X[i + (size_t)j * n];
     s2 = warp_sum(s2);
     if (lane == 0) norms[j] = sqrt(s2);
   }
-  for (int e = tid; e < n * n; e += SVD_NT) {
+  for (int e = tid; e < n * n; e += (int)blockDim.x) {
     Yo[e] = X[e];
     Po[e] = P[e];
   }
@@ -454,29 +454,36 @@ void launch_level(ftt_ctx *ctx, int n, unsigned grid, int64_t M, const double *A
                   int trans, double *Rs, int64_t ldr, double *Qo, int64_t ldq, int root,
                   int *status) {
   const size_t smem = 8 * (size_t)std::min<int64_t>(M, LEAF_NT) * n;
+  // a single short block (tree roots, 16..64 rows) runs with just enough
+  // warps for its rows and columns: fewer warps per barrier and reduction
+  unsigned nt = LEAF_NT;
+  if (grid == 1) {
+    const int64_t need = std::max<int64_t>(std::min<int64_t>(M, LEAF_NT), n);
+    nt = (unsigned)std::min<int64_t>(LEAF_NT, ceil_div(need, 32) * 32);
+  }
   switch (nmax_for(n)) {
     case 8:
-      k_tsqr_level<8><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+      k_tsqr_level<8><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                          status);
       break;
     case 16:
-      k_tsqr_level<16><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+      k_tsqr_level<16><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                           status);
       break;
     case 32:
-      k_tsqr_level<32><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+      k_tsqr_level<32><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                           status);
       break;
     case 24:
-      k_tsqr_level<24><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+      k_tsqr_level<24><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                           status);
       break;
     case 48:
-      k_tsqr_level<48><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+      k_tsqr_level<48><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                           status);
       break;
     default:
-      k_tsqr_level<64><<<grid, LEAF_NT, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
+      k_tsqr_level<64><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
                                                           status);
   }
 }
@@ -624,8 +631,11 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   launch_level(ctx, n, 1, Mr, root, root_ld, single ? trans : 0, R, n, Qr, Mr, 1, status);
   FTT_LAUNCHED(ctx);
   const int max_sweeps = 60;
-  k_jacobi_small<<<1, SVD_NT, 16 * (size_t)n * n, ctx->stream>>>(n, R, n, Y, P, norms, max_sweeps,
-                                                                  status);
+  // one warp per column pair of a round: small n needs few warps (and gets
+  // cheaper barriers)
+  const int jt = 32 * std::max(1, std::min(SVD_NT / 32, (n + 1) / 2));
+  k_jacobi_small<<<1, jt, 16 * (size_t)n * n, ctx->stream>>>(n, R, n, Y, P, norms, max_sweeps,
+                                                              status);
   FTT_LAUNCHED(ctx);
   // W = Q_root P, then down the tree
   if (!single) FTT_CHECK(owned_alloc(ctx, (void **)&W, 8 * (size_t)Mr * n));

@@ -793,8 +793,9 @@ def tt_relative_error(reference: TTTensor, approx: TTTensor, norm: float | None 
                                [to_device(c) for c in approx.cores], norm)
 
 
-def _inner_error_device(coords_d, values_d, nnz, approx_d):
-    na2 = device_dot(values_d, None)
+def _inner_error_device(coords_d, values_d, nnz, approx_d, na2=None):
+    if na2 is None:
+        na2 = device_dot(values_d, None)
     if na2 == 0.0:
         return 0.0 if dev_tt_norm(approx_d) == 0.0 else math.inf
     ent = dev_tt_entries(approx_d, coords_d)
@@ -917,8 +918,9 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
     res = DeviceResult(cores=out, pivot=pivot, mode=mode, eps=eps, num_fibers=df.R,
                        ranks_lossless=ranks_lossless, ranks=ranks, notes=notes, zero=zero)
     if report:
-        norm_a = math.sqrt(device_dot(values_d, None))
-        inner = _inner_error_device(coords_d, values_d, nnz, out)
+        na2 = device_dot(values_d, None)
+        norm_a = math.sqrt(na2)
+        inner = _inner_error_device(coords_d, values_d, nnz, out, na2)
         exact_shapes = [tuple(c.shape) for c in cores]
         total = _diff_total(exact_shapes, [tuple(c.shape) for c in out])
         if total <= _ERROR_MEASURE_CAP:

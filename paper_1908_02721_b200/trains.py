@@ -357,21 +357,17 @@ def dev_tt_entries(cores_d, coords_d):
 
 
 def dev_tt_norm(cores_d) -> float:
-    """Train Frobenius norm by contracting with itself (ttformat.py:198-203),
-    two DMMA GEMMs per core."""
-    torch = nat.torch_mod()
-    w = torch.ones((1, 1), dtype=torch.float64, device="cuda")
-    for c in cores_d:
-        a, n, r = (int(x) for x in c.shape)
-        # tmp (a, n r) = w @ c  <=>  col-major tmp^T = c^T w^T
-        tmp = torch.empty((a, n * r), dtype=torch.float64, device="cuda")
-        dgemm(0, 0, n * r, a, a, 1.0, c, n * r, w, a, 0.0, tmp, n * r)
-        # w' (r x r) = c(an x r)^T tmp(an x r)  <=>  col-major w'^T = tmp^T c
-        w2 = torch.empty((r, r), dtype=torch.float64, device="cuda")
-        dgemm(0, 1, r, r, a * n, 1.0, tmp, r, c, r, 0.0, w2, r)
-        w = w2
-    val = float(w.reshape(-1)[0].item())
-    return math.sqrt(max(val, 0.0))
+    """Train Frobenius norm by contracting it with itself (ttformat.py:198-203):
+    ftt_tt_norm, two DMMA GEMMs per core and one host round trip."""
+    d = len(cores_d)
+    dims = [int(c.shape[1]) for c in cores_d]
+    ranks = [int(cores_d[0].shape[0])] + [int(c.shape[2]) for c in cores_d]
+    cs = [c.contiguous() for c in cores_d]
+    ptrs = (nat.ctypes.c_void_p * d)(*[c.data_ptr() for c in cs])
+    out = nat.ctypes.c_double(0.0)
+    nat.check(nat.lib().ftt_tt_norm(nat.context(), d, nat.i64_array(dims), nat.i64_array(ranks),
+                                    ptrs, nat.ctypes.byref(out)), "ftt_tt_norm")
+    return float(out.value)
 
 
 def dev_right_orthogonalize(cores_d):

@@ -14,14 +14,18 @@ import json
 import sys
 
 CLASSES = [
-    ("sort", ("k_onesweep",)),
-    ("hist", ("k_keys_hist", "k_hist", "k_distinct_hash", "k_part_")),
-    ("segment", ("k_count", "k_emit", "k_scan_counts", "k_count_changes", "k_distinct_")),
+    ("sort", ("k_onesweep", "k_part_scatter")),
+    ("hist", ("k_keys_hist", "k_hist", "k_distinct_hash", "k_linearize")),
+    ("segment", ("k_count", "k_emit", "k_scan_counts", "k_count_changes", "k_distinct_",
+                 "k_part_count")),
     ("sweep", ("k_sweep",)),
-    ("scatter", ("k_pivot_scatter", "k_side_core", "k_scatter_")),
-    ("gemm", ("k_dgemm", "k_splitk_reduce", "k_sum_partials")),
+    ("scatter", ("k_pivot_scatter", "k_side_core", "k_scatter_", "k_sp_entries", "k_sp_gather",
+                 "k_gather_i32", "k_sp_bitmap", "k_lower_bounds", "k_scan_blocks", "k_scan_fix",
+                 "k_seg_counts")),
+    ("gemm", ("k_dgemm", "k_splitk_reduce", "k_sum_partials", "k_spmm_", "k_sp_resid",
+              "k_seg_reduce", "k_sp_sum", "k_resid_")),
     ("qr_panel", ("k_panel", "k_larft", "k_extract_v")),
-    ("jacobi", ("k_jacobi", "k_svd_small", "k_tsqr", "k_qr_root")),
+    ("jacobi", ("k_jacobi", "k_svd_small", "k_tsqr", "k_qr_root", "k_chol")),
     ("entries", ("k_entries", "k_mitm", "k_half_", "k_seg_")),
 ]
 
