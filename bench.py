@@ -473,7 +473,11 @@ def index_leg_c5(ft, nat, lib, ctx, roof, reps):
     r = roof("sort", agg)
     if r:
         r["kernel_class"] = "sort+hist+segment"
-        r["traffic"] = None
+        try:  # DRAM bytes per launch of the committed config-5 ncu capture
+            with open(os.path.join(ROOT, "profiles", "r01", "traffic_c5.json")) as fh:
+                r["traffic"] = json.load(fh).get("sort+hist+segment")
+        except Exception:  # noqa: BLE001
+            r["traffic"] = None
     per_class = {}
     for k in ("sort", "hist", "segment", "sweep"):
         rk = roof(k, prof[k])
