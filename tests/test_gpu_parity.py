@@ -129,7 +129,9 @@ def test_dgemm_matches_blas(m, n, k):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 3), (3, 5), (100, 37), (129, 300), (5000, 260),
-                                 (70000, 40), (64, 64), (2000, 64), (300000, 32), (881, 1)])
+                                 (70000, 40), (64, 64), (2000, 64), (300000, 32), (881, 1),
+                                 (62206, 8), (300, 16), (257, 13), (40, 11), (12, 9), (100000, 16),
+                                 (33, 7)])
 def test_qr_economic(m, n):
     """Householder QR: Q R = A to 1e-11, Q^T Q = I to 1e-12, diag(R) >= 0,
     R equal to LAPACK's sign-fixed R to 1e-10 (full column rank)."""
@@ -178,6 +180,19 @@ def test_svd_graded_spectrum():
     A = (U * s_true) @ V.T
     res = ft.svd_truncate_rank(A, 100)
     assert np.abs(res.s - np.linalg.svd(A, compute_uv=False)).max() < 1e-14
+
+
+@pytest.mark.parametrize("m,n,rk", [(3000, 16, 5), (700, 8, 3), (65000, 12, 12), (250, 16, 1)])
+def test_narrow_two_stage_qr_rank_deficient(m, n, rk):
+    """The two-stage warp QR (n <= 16) on rank-deficient and graded inputs:
+    Q R = A, Q^T Q = I, diag(R) >= 0."""
+    rng = np.random.default_rng(m + 7 * n + rk)
+    A = rng.standard_normal((m, rk)) @ rng.standard_normal((rk, n))
+    A[:, -1] *= 1e-12
+    res = ft.qr_economic(A)
+    assert np.abs(res.q @ res.r - A).max() < 1e-11 * max(1.0, np.abs(A).max())
+    assert np.abs(res.q.T @ res.q - np.eye(n)).max() < 1e-12
+    assert np.all(np.diag(res.r) >= 0)
 
 
 def test_narrow_rank_deficient_and_graded():
