@@ -73,6 +73,19 @@ int ftt_profile_read(ftt_ctx *ctx, int32_t tag, double *ms_out,
  * back-to-back mma.sync.m8n8k4.f64 per warp on every SM. */
 int ftt_bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops_out);
 
+/* ---------------------------------------------------- input side (host) */
+/* COO text reader (formats.py:47-100, ingest_coo): header "# shape n1 ...
+ * nd", then d 1-based indices and a value per nonempty line.  Host memory
+ * only (no context, no GPU).  On success *coords_out (nnz x d, 0-based) and
+ * *vals_out are malloc'd -- release them with ftt_free_host.  Any line the
+ * strict fast path does not accept returns FTT_ERR_INVALID with *bad_line
+ * set (1 = header, 0 = empty or unreadable file); the Python mirror then
+ * re-reads the file with the reference loop for the exact FormatError. */
+int ftt_parse_coo_text(const char *path, int32_t *d_out, int64_t *dims_out,
+                       int64_t *nnz_out, int64_t **coords_out, double **vals_out,
+                       int64_t *bad_line);
+void ftt_free_host(void *p);
+
 /* ---------------------------------------------------- index path (int) */
 
 /* Distinct fixed tuples for one pivot mode: the fiber count R_p computed
@@ -103,6 +116,18 @@ int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords,
                        int64_t *fixed_lin, int64_t *indptr, int64_t *fiber_of,
                        int64_t *pivot_index, double *values_out,
                        int64_t *num_fibers_out);
+/* tensorize_matrix (ttformat.py:414-433) on the device: matrix entries
+ * (rows[e], cols[e], vals[e]) -> the fused d-way tensor with f_i = x_i *
+ * col_dims[i] + y_i (x, y the row / column digits over row_dims / col_dims),
+ * in canonical form: C-order sorted, duplicates summed in input order (the
+ * reference's tocsr() coalescing), zero sums dropped (tensor.py:147-153).
+ * coords_out (nnz x d int64 row-major) and vals_out hold nnz entries;
+ * *nnz_out = entries kept.  FTT_ERR_INVALID for an entry outside the
+ * factored extents. */
+int ftt_tensorize_matrix(ftt_ctx *ctx, int64_t nnz, const int64_t *rows,
+                         const int64_t *cols, const double *vals, int32_t d,
+                         const int64_t *row_dims, const int64_t *col_dims,
+                         int64_t *coords_out, double *vals_out, int64_t *nnz_out);
 
 /* depar_quasi_perm (fasttt.py:148-167): kept = ascending distinct rows of
  * col_to_row, t_map[j] = rank of col_to_row[j] among kept.  kept capacity
@@ -110,6 +135,18 @@ int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords,
 int ftt_depar_quasi_perm(ftt_ctx *ctx, int64_t n_rows, int64_t n_cols,
                          const int64_t *col_to_row, int64_t *kept,
                          int64_t *t_map, int64_t *n_kept_out);
+/* depar_general (fasttt.py:96-145): floating-point deparallelisation of the
+ * rows x cols column-major M (ld ldm).  Columns in order; column j is
+ * parallel to kept basis column i when |u - c b_i|^2 <= tol^2 |u|^2 with
+ * c = (b_i . u) / |b_i|^2, the lowest such i wins; zero columns are dropped
+ * (t_row = -1).  Outputs: kept[0..width) = basis columns of M
+ * (first-occurrence order), t_row / t_coeff per column (the single nonzero
+ * of t's column j), width_at[j] = basis width when column j was visited
+ * (the reference's float_ops accounting), *width_out.  Device arrays of
+ * cols entries each. */
+int ftt_depar_general(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *M,
+                      int64_t ldm, double tol, int64_t *kept, int64_t *t_row,
+                      double *t_coeff, int64_t *width_at, int64_t *width_out);
 
 /* One step of _index_sweeps (fasttt.py:192-210) fused with its key build:
  *   side 0 (left of pivot):  key[f] = map_in[f] * n_k + i_k(f)
@@ -122,6 +159,18 @@ int ftt_index_sweep_step(ftt_ctx *ctx, int32_t side, const int64_t *fixed_lin,
                          int64_t R, int64_t stride_k, int64_t n_k,
                          const int64_t *map_in, int64_t r_other,
                          int64_t *kept, int64_t *map_out,
+                         int64_t *n_kept_out);
+/* Every deparallelisation step of _index_sweeps (fasttt.py:181-211) in one
+ * call and one host round trip: steps s = left modes 0..p-1, then right modes
+ * d-1..p+1; each step's kept count stays on the device and feeds the next
+ * step's key.  kept[s] (device, min(R, bound_s) entries with bound_s =
+ * min(R, product of the modes already swept on that side) * n_k) and maps[s]
+ * (device, R entries) are the same arrays ftt_index_sweep_step produces;
+ * n_kept_out[s] the kept counts.  FTT_ERR_INVALID when a bound exceeds the
+ * flag path's limits (the caller then steps with ftt_index_sweep_step). */
+int ftt_index_sweeps_all(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R,
+                         int32_t d, const int64_t *dims, int32_t pivot,
+                         int64_t *const *kept, int64_t *const *maps,
                          int64_t *n_kept_out);
 
 /* Per-fiber coordinate of one rest mode: (fixed_lin / stride) % n

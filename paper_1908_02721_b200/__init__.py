@@ -28,6 +28,7 @@ from .pipeline import (
     DecompositionReport,
     TruncationBudget,
     build_structured_tt,
+    depar_general,
     depar_quasi_perm,
     dynamic_tt_rounding,
     efficient_tt_rounding,
@@ -60,9 +61,12 @@ from .trains import (
 
 __version__ = "0.1.0"
 
+from .formats import ingest_coo, ingest_matrix_market, write_coo  # noqa: E402
+
 __all__ = [
+    "ingest_coo", "ingest_matrix_market", "write_coo",
     "ContractViolationError", "FormatError", "DecompositionReport", "TruncationBudget",
-    "build_structured_tt", "depar_quasi_perm", "dynamic_tt_rounding", "efficient_tt_rounding",
+    "build_structured_tt", "depar_general", "depar_quasi_perm", "dynamic_tt_rounding", "efficient_tt_rounding",
     "fasttt", "fasttt_device", "fixed_rank_rounding", "float_ops", "flops_fasttt",
     "parallel_vector_round", "select_p", "sparse_inner_error", "tt_relative_error",
     "QRResult", "SVDResult", "qr_economic", "svd_truncate_delta", "svd_truncate_rank",

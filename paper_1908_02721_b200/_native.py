@@ -71,6 +71,18 @@ SIGNATURES = {
     "ftt_dot": [_c_p, _c_i64, _c_p, _c_p, _P_d],
     "ftt_set_deferred_checks": [_c_p, _c_i32],
     "ftt_take_status": [_c_p, ctypes.POINTER(ctypes.c_int32)],
+    "ftt_depar_general": [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_d, _c_p, _c_p, _c_p, _c_p,
+                          ctypes.POINTER(ctypes.c_int64)],
+    "ftt_tensorize_matrix": [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_i32, _P_i64, _P_i64, _c_p, _c_p,
+                             ctypes.POINTER(ctypes.c_int64)],
+    "ftt_parse_coo_text": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
+                           ctypes.POINTER(ctypes.c_int64),
+                           ctypes.POINTER(ctypes.POINTER(ctypes.c_int64)),
+                           ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
+                           ctypes.POINTER(ctypes.c_int64)],
+    "ftt_free_host": [_c_p],
+    "ftt_index_sweeps_all": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, ctypes.POINTER(_c_p),
+                             ctypes.POINTER(_c_p), ctypes.POINTER(ctypes.c_int64)],
     "ftt_sync_stats": [_c_p, ctypes.POINTER(ctypes.c_int64), _P_d],
     "ftt_tt_norm": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _P_d],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],
@@ -79,6 +91,7 @@ _RESTYPES = {
     "ftt_version": ctypes.c_char_p,
     "ftt_last_error": ctypes.c_char_p,
     "ftt_kernel_launches": ctypes.c_int64,
+    "ftt_free_host": None,
 }
 
 _lib = None

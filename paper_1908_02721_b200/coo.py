@@ -145,6 +145,24 @@ class SparseTensor:
     def __setattr__(self, name, value):
         raise AttributeError("SparseTensor is immutable")
 
+    @classmethod
+    def _from_canonical_device(cls, shape, coords_d, values_d) -> "SparseTensor":
+        """A tensor whose canonical form (nonzero, C-order sorted, unique) was
+        produced on the device (ftt_tensorize_matrix): the host arrays are a
+        D2H copy and the device arrays stay cached -- no re-upload."""
+        dims = check_shape(shape)
+        c = np.ascontiguousarray(coords_d.cpu().numpy(), dtype=np.int64).reshape(-1, len(dims))
+        v = np.ascontiguousarray(values_d.cpu().numpy(), dtype=np.float64)
+        c.setflags(write=False)
+        v.setflags(write=False)
+        t = cls.__new__(cls)
+        object.__setattr__(t, "shape", dims)
+        object.__setattr__(t, "coords", c)
+        object.__setattr__(t, "values", v)
+        object.__setattr__(t, "_dev", (coords_d, values_d))
+        object.__setattr__(t, "_pin", None)
+        return t
+
     @property
     def ndim(self) -> int:
         return len(self.shape)

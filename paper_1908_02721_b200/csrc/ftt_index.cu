@@ -431,13 +431,24 @@ struct SweepKey {
   int64_t stride, nk, r_other;
   const int64_t *map_in;
   Div63 dstride, dnk;
+  const int64_t *r_other_dev = nullptr;  // device-resident r_other (batched sweeps)
   __device__ int64_t operator()(int64_t f) const {
     const uint64_t q = dstride.quo((uint64_t)fixed_lin[f]);
     int64_t ik = (int64_t)(q - dnk.quo(q) * (uint64_t)nk);
     int64_t m = map_in ? map_in[f] : 0;
-    return side == 0 ? m * nk + ik : ik * r_other + m;
+    const int64_t ro = r_other_dev ? *r_other_dev : r_other;
+    return side == 0 ? m * nk + ik : ik * ro + m;
   }
 };
+
+// present[kept[r]] = 0 for r < *count (undo one step's marks / ranks).
+__global__ void k_unmark(const int64_t *__restrict__ kept, const int64_t *__restrict__ count,
+                         int64_t bound, uint32_t *__restrict__ present) {
+  const int64_t n = min(*count, bound);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    present[kept[r]] = 0u;
+}
 
 __global__ void k_sweep_mark(int64_t R, SweepKey key, uint32_t *present) {
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
@@ -784,6 +795,72 @@ __global__ void k_scatter_rows(int64_t K, int64_t rank, const int64_t *__restric
     dst[kept[j] * rank + c] = src[j * lds + c];
   }
 }
+
+// ---- tensorize_matrix on the device (ttformat.py:414-433) ------------------
+struct FuseSpec {
+  int d;
+  int64_t rdims[32], cdims[32], stride[32];  // stride: C order over fused dims
+};
+
+// fused C-order key of matrix entry (row, col): digits x_i of row over
+// row_dims, y_i of col over col_dims, f_i = x_i * c_i + y_i.
+__global__ void k_fuse_keys(int64_t nnz, const int64_t *__restrict__ rows,
+                            const int64_t *__restrict__ cols, FuseSpec fs,
+                            uint64_t *__restrict__ keys, uint32_t *__restrict__ ident,
+                            int *__restrict__ bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = rows[e], c = cols[e];
+    uint64_t key = 0;
+    bool ok = r >= 0 && c >= 0;
+    for (int i = fs.d - 1; i >= 0; --i) {
+      const int64_t x = r % fs.rdims[i], y = c % fs.cdims[i];
+      r /= fs.rdims[i];
+      c /= fs.cdims[i];
+      key += (uint64_t)(x * fs.cdims[i] + y) * (uint64_t)fs.stride[i];
+    }
+    if (r != 0 || c != 0) ok = false;  // outside the matrix extents
+    if (!ok) atomicOr(bad, 1);
+    keys[e] = key;
+    ident[e] = (uint32_t)e;
+  }
+}
+
+// Run of equal keys starting at a head: values summed in input (stable sort)
+// order, the scipy tocsr() coalescing; zero sums are dropped like the
+// SparseTensor constructor does (tensor.py:147-153).
+struct CoalescePred {
+  const uint64_t *k;
+  const uint32_t *perm;
+  const double *v;
+  int64_t n;
+  __device__ double run_sum(int64_t i) const {
+    double s = v[perm[i]];
+    for (int64_t j = i + 1; j < n && k[j] == k[i]; ++j) s += v[perm[j]];
+    return s;
+  }
+  __device__ bool operator()(int64_t i) const {
+    if (i > 0 && k[i] == k[i - 1]) return false;
+    return run_sum(i) != 0.0;
+  }
+};
+
+struct CoalesceEmit {
+  CoalescePred p;
+  FuseSpec fs;
+  int64_t *coords;
+  double *vals;
+  __device__ void operator()(int64_t i, int64_t r, bool f) const {
+    if (!f) return;
+    uint64_t key = p.k[i];
+    for (int q = 0; q < fs.d; ++q) {
+      const uint64_t st = (uint64_t)fs.stride[q];
+      coords[r * fs.d + q] = (int64_t)(key / st);
+      key %= st;
+    }
+    vals[r] = p.run_sum(i);
+  }
+};
 
 int bit_length(uint64_t x) {
   int b = 0;
@@ -1360,6 +1437,94 @@ int ftt_index_sweep_step(ftt_ctx *ctx, int32_t side, const int64_t *fixed_lin, i
   return depar_from_keys(ctx, r_other * n_k, R, &sk, nullptr, kept, map_out, n_kept_out);
 }
 
+// All deparallelisation steps of _index_sweeps (fasttt.py:181-211) in one
+// call with one host round trip: each step's kept count stays on the device
+// and feeds the next step's key (right side: i_k * r_next + s_map) directly.
+// The flag array is sized by a host-side bound of r_other * n_k (min(R,
+// product of the dims already swept)) and cleaned after each step by
+// unmarking the step's kept rows, so no per-step memset or count read-back
+// is needed.  Returns FTT_ERR_INVALID (nothing launched) when a bound is too
+// large for the flag path -- the caller then runs ftt_index_sweep_step per
+// step.  kept[s] / maps[s] (step s: left k = 0..p-1, then right k =
+// d-1..p+1) hold min(R, bound_s) / R entries; n_kept_out[s] gets the counts.
+int ftt_index_sweeps_all(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R, int32_t d,
+                         const int64_t *dims, int32_t pivot, int64_t *const *kept,
+                         int64_t *const *maps, int64_t *n_kept_out) {
+  if (!ctx || !n_kept_out || d < 2 || d > 32 || pivot < 0 || pivot >= d || R < 1) {
+    set_error("ftt_index_sweeps_all: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  const int nsteps = d - 1;
+  std::vector<int64_t> bound(nsteps), nk(nsteps), stride(nsteps);
+  std::vector<int> side(nsteps);
+  {
+    // rest strides: C order over the modes != pivot
+    std::vector<int64_t> rest_stride(d, 0);
+    int64_t st = 1;
+    for (int k = d - 1; k >= 0; --k) {
+      if (k == pivot) continue;
+      rest_stride[k] = st;
+      st *= dims[k];
+    }
+    int s = 0;
+    int64_t prod = 1;
+    for (int k = 0; k < pivot; ++k, ++s) {
+      side[s] = 0;
+      nk[s] = dims[k];
+      stride[s] = rest_stride[k];
+      bound[s] = std::min<int64_t>(R, prod) * dims[k];
+      prod = std::min<int64_t>(prod * dims[k], (int64_t)1 << 40);
+    }
+    prod = 1;
+    for (int k = d - 1; k > pivot; --k, ++s) {
+      side[s] = 1;
+      nk[s] = dims[k];
+      stride[s] = rest_stride[k];
+      bound[s] = std::min<int64_t>(R, prod) * dims[k];
+      prod = std::min<int64_t>(prod * dims[k], (int64_t)1 << 40);
+    }
+  }
+  int64_t bmax = 1;
+  for (int s = 0; s < nsteps; ++s) {
+    // the per-step flag path's own condition (depar_from_keys), on the bound
+    const bool flag_ok = bound[s] <= ((int64_t)1 << 31) - 1 &&
+                         (bound[s] <= ((int64_t)1 << 24) || bound[s] <= 8 * R);
+    if (!flag_ok) {
+      set_error("ftt_index_sweeps_all: flag bound too large");
+      return FTT_ERR_INVALID;
+    }
+    bmax = std::max(bmax, bound[s]);
+  }
+  FTT_CHECK(arena_reserve(ctx, align_up(4 * bmax) + compact_scratch_bytes(bmax) +
+                                   align_up(8 * (size_t)(nsteps + 1)) + 4096));
+  uint32_t *present = take<uint32_t>(ctx, bmax);
+  int64_t *bc = take<int64_t>(ctx, ceil_div(bmax, CP_TILE) + 1);
+  int64_t *counts = take<int64_t>(ctx, nsteps + 1);
+  FTT_CUDA(cudaMemsetAsync(present, 0, 4 * (size_t)bmax, ctx->stream));
+  const int pb = prof_begin(ctx);
+  double alg = 0.0;
+  for (int s = 0; s < nsteps; ++s) {
+    // previous step of the same side: its map and (right side) its count
+    const bool first_of_side = (s == 0) || side[s - 1] != side[s];
+    SweepKey sk{side[s], fixed_lin, stride[s], nk[s], 1, first_of_side ? nullptr : maps[s - 1],
+                make_div63((uint64_t)stride[s]), make_div63((uint64_t)nk[s])};
+    if (side[s] == 1 && !first_of_side) sk.r_other_dev = counts + (s - 1);
+    k_sweep_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present);
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(compact(ctx, bound[s], FlagPred{present}, KeptEmit{present, kept[s]}, bc, counts + s,
+                      -1));
+    k_sweep_gather<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present, maps[s]);
+    FTT_LAUNCHED(ctx);
+    k_unmark<<<grid_for(std::min(R, bound[s]), 256, 4), 256, 0, ctx->stream>>>(
+        kept[s], counts + s, std::min(R, bound[s]), present);
+    FTT_LAUNCHED(ctx);
+    alg += (double)R * (16.0 + 4.0 + 16.0 + 4.0 + 8.0) + 4.0 * (double)bound[s];
+  }
+  prof_end(ctx, pb, PT_SWEEP, alg, 0.0);
+  FTT_CHECK(copy_to_host(ctx, n_kept_out, counts, sizeof(int64_t) * nsteps));
+  return FTT_OK;
+}
+
 int ftt_mode_index(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R, int64_t stride, int64_t n,
                    int64_t *out) {
   if (!ctx || stride < 1 || n < 1) return FTT_ERR_INVALID;
@@ -1450,6 +1615,58 @@ int ftt_dot(ftt_ctx *ctx, int64_t n, const double *x, const double *y, double *o
   k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, partial + nb);
   FTT_LAUNCHED(ctx);
   return copy_to_host(ctx, out_host, partial + nb, sizeof(double));
+}
+
+
+int ftt_tensorize_matrix(ftt_ctx *ctx, int64_t nnz, const int64_t *rows, const int64_t *cols,
+                         const double *vals, int32_t d, const int64_t *row_dims,
+                         const int64_t *col_dims, int64_t *coords_out, double *vals_out,
+                         int64_t *nnz_out) {
+  if (!ctx || !nnz_out || d < 1 || d > 32 || nnz < 0) {
+    set_error("ftt_tensorize_matrix: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  FuseSpec fs;
+  fs.d = d;
+  int64_t fused[32];
+  for (int i = 0; i < d; ++i) {
+    fs.rdims[i] = row_dims[i];
+    fs.cdims[i] = col_dims[i];
+    fused[i] = row_dims[i] * col_dims[i];
+  }
+  FTT_CHECK(check_dims(d, fused, 0, false));
+  unsigned __int128 prod = 1;
+  for (int i = d - 1; i >= 0; --i) {
+    fs.stride[i] = (int64_t)prod;
+    prod *= (unsigned __int128)fused[i];
+  }
+  *nnz_out = 0;
+  if (nnz == 0) return FTT_OK;
+  if (nnz >= ((int64_t)1 << 30)) {
+    set_error("nnz exceeds the 2^30 sort limit");
+    return FTT_ERR_INVALID;
+  }
+  FTT_CHECK(arena_reserve(ctx, radix_sort_scratch_bytes(nnz, true) + 2 * align_up(8 * nnz) +
+                                   2 * align_up(4 * nnz) + compact_scratch_bytes(nnz) + 4096));
+  uint64_t *keys = take<uint64_t>(ctx, nnz), *skeys = take<uint64_t>(ctx, nnz);
+  uint32_t *ident = take<uint32_t>(ctx, nnz), *perm = take<uint32_t>(ctx, nnz);
+  int64_t *bc = take<int64_t>(ctx, ceil_div(nnz, CP_TILE) + 1);
+  int64_t *total = take<int64_t>(ctx, 2);  // [0] kept entries, [1] out-of-range flag
+  int *bad = reinterpret_cast<int *>(total + 1);
+  FTT_CUDA(cudaMemsetAsync(total + 1, 0, sizeof(int64_t), ctx->stream));
+  k_fuse_keys<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(nnz, rows, cols, fs, keys, ident, bad);
+  FTT_LAUNCHED(ctx);
+  FTT_CHECK(radix_sort(ctx, keys, ident, skeys, perm, nnz, bit_length((uint64_t)(prod - 1))));
+  CoalescePred pred{skeys, perm, vals, nnz};
+  FTT_CHECK(compact(ctx, nnz, pred, CoalesceEmit{pred, fs, coords_out, vals_out}, bc, total));
+  int64_t h[2] = {0, 0};
+  FTT_CHECK(copy_to_host(ctx, h, total, 2 * sizeof(int64_t)));
+  if ((int)h[1]) {
+    set_error("matrix entry outside the factored extents");
+    return FTT_ERR_INVALID;
+  }
+  *nnz_out = h[0];
+  return FTT_OK;
 }
 
 }  // extern "C"

@@ -594,3 +594,114 @@ int sparse_resid(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, c
 }
 
 }  // namespace ftt
+
+// ---------------------------------------------------------------------------
+// depar_general (fasttt.py:96-145): the floating-point deparallelisation.
+// Columns are visited in order (first-occurrence classes, as the
+// reference's loop); for column u the kept basis columns b_i are tested in
+// parallel (one warp per basis column): coeff_i = (b_i . u) / |b_i|^2, the
+// residual |u - coeff_i b_i|^2 evaluated explicitly, hit_i = rnorm2 <= tol^2
+// |u|^2; the lowest hit index wins, else u joins the basis.  One CTA walks the
+// columns (the kept set depends on every earlier decision).
+namespace ftt {
+namespace {
+
+__global__ void __launch_bounds__(1024) k_depar_general(int64_t rows, int64_t cols,
+                                                        const double *__restrict__ M, int64_t ldm,
+                                                        double tol, int64_t *__restrict__ kept,
+                                                        double *__restrict__ bnorm2,
+                                                        int64_t *__restrict__ t_row,
+                                                        double *__restrict__ t_coeff,
+                                                        int64_t *__restrict__ width_at,
+                                                        int64_t *__restrict__ width_out) {
+  __shared__ double red[32];
+  __shared__ int s_hit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int64_t width = 0;
+  for (int64_t j = 0; j < cols; ++j) {
+    const double *u = M + j * ldm;
+    double a = 0.0;
+    for (int64_t r = tid; r < rows; r += blockDim.x) a += u[r] * u[r];
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) red[warp] = a;
+    if (tid == 0) s_hit = 0x7fffffff;
+    __syncthreads();
+    double unorm2 = 0.0;
+    for (int w = 0; w < nw; ++w) unorm2 += red[w];
+    if (tid == 0) width_at[j] = width;
+    if (unorm2 == 0.0) {
+      if (tid == 0) {
+        t_row[j] = -1;
+        t_coeff[j] = 0.0;
+      }
+      __syncthreads();
+      continue;
+    }
+    const double thr = tol * tol * unorm2;
+    for (int64_t i = warp; i < width; i += nw) {
+      const double *b = M + kept[i] * ldm;
+      double dot = 0.0;
+      for (int64_t r = lane; r < rows; r += 32) dot += b[r] * u[r];
+      for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const double coeff = dot / bnorm2[i];
+      double rn = 0.0;
+      for (int64_t r = lane; r < rows; r += 32) {
+        const double e = u[r] - b[r] * coeff;
+        rn += e * e;
+      }
+      for (int o = 16; o; o >>= 1) rn += __shfl_xor_sync(0xffffffffu, rn, o);
+      if (lane == 0 && rn <= thr) atomicMin(&s_hit, (int)i);
+      (void)coeff;
+    }
+    __syncthreads();
+    const int hit = s_hit;
+    if (hit != 0x7fffffff) {
+      // the winner's coefficient (recomputed by one warp: same arithmetic)
+      if (warp == 0) {
+        const double *b = M + kept[hit] * ldm;
+        double dot = 0.0;
+        for (int64_t r = lane; r < rows; r += 32) dot += b[r] * u[r];
+        for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) {
+          t_row[j] = hit;
+          t_coeff[j] = dot / bnorm2[hit];
+        }
+      }
+    } else if (tid == 0) {
+      kept[width] = j;
+      bnorm2[width] = unorm2;
+      t_row[j] = width;
+      t_coeff[j] = 1.0;
+    }
+    if (hit == 0x7fffffff) ++width;
+    __syncthreads();
+  }
+  if (tid == 0) *width_out = width;
+}
+
+}  // namespace
+}  // namespace ftt
+
+using namespace ftt;
+
+extern "C" int ftt_depar_general(ftt_ctx *ctx, int64_t rows, int64_t cols, const double *M,
+                                 int64_t ldm, double tol, int64_t *kept, int64_t *t_row,
+                                 double *t_coeff, int64_t *width_at, int64_t *width_out) {
+  if (!ctx || rows < 0 || cols < 0 || !width_out || ldm < std::max<int64_t>(rows, 1) || tol < 0) {
+    set_error("ftt_depar_general: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  *width_out = 0;
+  if (cols == 0) return FTT_OK;
+  double *bn = nullptr;
+  int64_t *wdev = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&bn, 8 * (size_t)cols));
+  FTT_CHECK(owned_alloc(ctx, (void **)&wdev, 64));
+  k_depar_general<<<1, 1024, 0, ctx->stream>>>(rows, cols, M, ldm, tol, kept, bn, t_row, t_coeff,
+                                               width_at, wdev);
+  FTT_LAUNCHED(ctx);
+  FTT_CHECK(copy_to_host(ctx, width_out, wdev, sizeof(int64_t)));
+  owned_free(ctx, bn);
+  owned_free(ctx, wdev);
+  return FTT_OK;
+}

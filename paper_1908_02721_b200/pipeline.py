@@ -63,6 +63,7 @@ __all__ = [
     "TruncationBudget",
     "DecompositionReport",
     "depar_quasi_perm",
+    "depar_general",
     "build_structured_tt",
     "parallel_vector_round",
     "efficient_tt_rounding",
@@ -275,10 +276,52 @@ class DeviceSweeps:
         self.r_next = r_next
 
 
-def index_sweeps_device(df) -> DeviceSweeps:
-    """_index_sweeps (fasttt.py:181-211) as one fused kernel chain per mode."""
+def _index_sweeps_batched(df):
+    """All sweep steps in one native call (ftt_index_sweeps_all, one host
+    round trip); None when a step's flag bound is too large for it."""
     dims, p, R = df.dims, df.pivot, df.R
     d = len(dims)
+    steps = list(range(p)) + list(range(d - 1, p, -1))
+    bounds, prod_l, prod_r = [], 1, 1
+    for k in steps:
+        if k < p:
+            bounds.append(min(R, prod_l) * dims[k])
+            prod_l *= dims[k]
+        else:
+            bounds.append(min(R, prod_r) * dims[k])
+            prod_r *= dims[k]
+    if any(not (b <= 2 ** 31 - 1 and (b <= 2 ** 24 or b <= 8 * R)) for b in bounds):
+        return None
+    kept = [_empty(max(min(R, b), 1), "i64") for b in bounds]
+    maps = [_empty(max(R, 1), "i64") for _ in steps]
+    kp = (nat.ctypes.c_void_p * len(steps))(*[t.data_ptr() for t in kept])
+    mp = (nat.ctypes.c_void_p * len(steps))(*[t.data_ptr() for t in maps])
+    counts = (nat.ctypes.c_int64 * len(steps))()
+    nat.check(nat.lib().ftt_index_sweeps_all(nat.context(), nat.ptr(df.fixed_lin), R, d,
+                                              nat.i64_array(dims), p, kp, mp, counts),
+              "ftt_index_sweeps_all")
+    left, right = [], []
+    t_map, r_prev, s_map, r_next = None, 1, None, 1
+    for i, k in enumerate(steps):
+        n = int(counts[i])
+        if k < p:
+            left.append((kept[i][:n], r_prev))
+            t_map, r_prev = maps[i][:R], n
+        else:
+            right.append((kept[i][:n], r_next))
+            s_map, r_next = maps[i][:R], n
+    return DeviceSweeps(left, t_map, r_prev, right, s_map, r_next)
+
+
+def index_sweeps_device(df) -> DeviceSweeps:
+    """_index_sweeps (fasttt.py:181-211): every step in one native call when
+    the flag bounds allow, else one fused kernel chain per mode."""
+    dims, p, R = df.dims, df.pivot, df.R
+    d = len(dims)
+    if R > 0 and d > 1:
+        sw = _index_sweeps_batched(df)
+        if sw is not None:
+            return sw
     lib, ctx = nat.lib(), nat.context()
     t_map, r_prev, left = None, 1, []
     for k in range(p):
@@ -345,6 +388,51 @@ def _lossless_bond_ranks(s: StructuredTT):
     if df.R == 0:
         return (0,) * (s.ndim - 1)
     return _lossless_ranks_from(index_sweeps_device(df), s.ndim)
+
+
+def depar_general(m, tol: float = 1e-12):
+    """Split ``m`` into ``n @ t`` keeping one representative per parallel
+    class of columns, in first-occurrence order (fasttt.py:96-145), on the
+    GPU (ftt_depar_general).  Column ``u`` is parallel to a kept ``v`` when
+    ``norm(u - (u . v_hat) v_hat) <= tol * norm(u)``; zero columns are
+    dropped.  Returns dense ``(n, t)`` and counts the same float work as the
+    reference into ``float_ops``."""
+    import scipy.sparse
+
+    if isinstance(m, QuasiPermMatrix):
+        m = m.to_dense()
+    elif scipy.sparse.issparse(m):
+        m = m.toarray()
+    m = np.asarray(m, dtype=np.float64)
+    if m.ndim != 2:
+        raise ValueError("deparallelisation expects a matrix")
+    rows, cols = m.shape
+    if cols == 0:
+        return np.zeros((rows, 0)), np.zeros((0, 0))
+    torch = _torch()
+    md = to_device(np.ascontiguousarray(m.T))  # column-major rows x cols
+    kept = torch.empty(cols, dtype=torch.int64, device="cuda")
+    t_row = torch.empty(cols, dtype=torch.int64, device="cuda")
+    t_coeff = torch.empty(cols, dtype=torch.float64, device="cuda")
+    width_at = torch.empty(cols, dtype=torch.int64, device="cuda")
+    width = nat.ctypes.c_int64(0)
+    nat.check(nat.lib().ftt_depar_general(nat.context(), rows, cols, nat.ptr(md), max(rows, 1),
+                                          float(tol), nat.ptr(kept), nat.ptr(t_row),
+                                          nat.ptr(t_coeff), nat.ptr(width_at),
+                                          nat.ctypes.byref(width)), "ftt_depar_general")
+    w = int(width.value)
+    kept_h = kept[:w].cpu().numpy()
+    t_row_h = t_row.cpu().numpy()
+    t_coeff_h = t_coeff.cpu().numpy()
+    wat = width_at.cpu().numpy()
+    # float work of the reference loop: 2 rows per column norm, 6 rows per
+    # tested basis column (fasttt.py:117-127)
+    nonzero = t_row_h >= 0
+    float_ops.add(float(2 * rows * cols + 6 * rows * int(np.sum(wat[nonzero]))))
+    n = np.ascontiguousarray(m[:, kept_h])
+    t = np.zeros((w, cols))
+    t[t_row_h[nonzero], np.flatnonzero(nonzero)] = t_coeff_h[nonzero]
+    return n, t
 
 
 def depar_quasi_perm(q: QuasiPermMatrix):

@@ -18,6 +18,7 @@ import numpy as np
 from . import _native as nat
 from .coo import (
     FiberSet,
+    FormatError,
     SparseTensor,
     check_shape,
     delinearize,
@@ -240,22 +241,51 @@ def _factor_dims(dims, total, what):
     return dims
 
 
-def tensorize_matrix(m, row_dims, col_dims) -> SparseTensor:
+def tensorize_matrix(m, row_dims, col_dims, device: bool = False) -> SparseTensor:
     """Matrix -> fused ``d``-way tensor, ``f_i = x_i * col_dims[i] + y_i``
-    (ttformat.py:414-433). Duplicates are coalesced first (scipy COO)."""
+    (ttformat.py:414-433). Duplicates are coalesced first (scipy COO).
+
+    ``device=True`` does the fusing, the canonical sort and the duplicate
+    coalescing on the GPU (``ftt_tensorize_matrix``): only the matrix
+    entries (24 B each) cross PCIe and the fused COO stays resident for the
+    decomposition."""
     import scipy.sparse
 
     if not scipy.sparse.issparse(m):
         m = scipy.sparse.coo_matrix(np.asarray(m, dtype=np.float64))
-    m = m.tocsr().tocoo()
     rdims = _factor_dims(row_dims, m.shape[0], "row factors")
     cdims = _factor_dims(col_dims, m.shape[1], "column factors")
     if len(rdims) != len(cdims):
         raise ValueError("row and column factorizations need equal length")
+    if device:
+        return _tensorize_device(m.tocoo(), rdims, cdims)
+    m = m.tocsr().tocoo()
     x = delinearize(rdims, m.row.astype(np.int64))
     y = delinearize(cdims, m.col.astype(np.int64))
     fused = x * np.asarray(cdims, dtype=np.int64) + y
     return SparseTensor(tuple(a * b for a, b in zip(rdims, cdims)), fused, m.data)
+
+
+def _tensorize_device(m, rdims, cdims) -> SparseTensor:
+    torch = nat.torch_mod()
+    vals = np.asarray(m.data, dtype=np.float64)
+    if not np.isfinite(vals).all():
+        raise FormatError("tensor values must be finite")
+    d = len(rdims)
+    dims = tuple(a * b for a, b in zip(rdims, cdims))
+    nnz = int(vals.shape[0])
+    rows = to_device(np.asarray(m.row, dtype=np.int64))
+    cols = to_device(np.asarray(m.col, dtype=np.int64))
+    vd = to_device(vals)
+    coords = torch.empty((max(nnz, 1), d), dtype=torch.int64, device="cuda")
+    vout = torch.empty(max(nnz, 1), dtype=torch.float64, device="cuda")
+    kept = nat.ctypes.c_int64(0)
+    nat.check(nat.lib().ftt_tensorize_matrix(nat.context(), nnz, nat.ptr(rows), nat.ptr(cols),
+                                             nat.ptr(vd), d, nat.i64_array(rdims),
+                                             nat.i64_array(cdims), nat.ptr(coords), nat.ptr(vout),
+                                             nat.ctypes.byref(kept)), "ftt_tensorize_matrix")
+    k = int(kept.value)
+    return SparseTensor._from_canonical_device(dims, coords[:k].contiguous(), vout[:k].contiguous())
 
 
 def tt_split_mpo(t: TTTensor, row_dims, col_dims) -> TTMatrix:

@@ -166,6 +166,41 @@ def config(cfg: int):
     save_config(f"c{cfg}", t, eps, cores, meta)
 
 
+def config5_index():
+    """Config 5 (8.5M nonzeros, 32^12): the reference cannot decompose it at
+    any pivot within this container's memory (the dense pivot core alone is
+    10.5 GB at p = 2, fasttt.py:253), so its golden is the reference's own
+    INDEX path -- per-pivot fiber counts, select_p, FiberSet / kept / map
+    digests, lossless ranks -- plus seeded zero positions.  The float check
+    on the GPU is size-independent: a sum of 16 generic rank-1 terms has
+    every unfolding rank 16, so the train must have ranks (16,)*11 and
+    reproduce the input at every nonzero and 0 at the zero positions
+    (tests/test_gpu_parity.py::test_config5_parity)."""
+    shape, coords, vals, eps = G.gen_config(5, seed=0)
+    t = sparsett.SparseTensor(shape, coords, vals)
+    meta = {"config": 5, "seed": 0, "generator": G.CONFIGS[5]["name"]}
+    t0 = time.time()
+    meta["fiber_counts"] = fiber_counts(t)
+    p = sparsett.select_p(t)
+    meta["select_p_s"] = time.time() - t0
+    meta["auto_pivot"] = int(p)
+    t0 = time.time()
+    meta["index"] = index_goldens(t, p)
+    meta["index_s"] = time.time() - t0
+    meta["input_coords"] = digest(t.coords)
+    meta["input_values"] = digest(t.values)
+    meta["nnz"] = int(t.nnz)
+    meta["shape"] = list(t.shape)
+    meta["eps"] = eps
+    meta["source"] = ("reference index-only functions (select_p, build_structured_tt, "
+                      "_index_sweeps); float check by construction (rank-16 sum)")
+    zc = G.zero_positions(t.shape, t.coords, ZERO_SAMPLES, seed=12345)
+    np.savez_compressed(os.path.join(HERE, "c5idx.npz"), zero_coords=zc)
+    with open(os.path.join(HERE, "c5idx.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("c5idx", meta["auto_pivot"], meta["index"]["ranks_lossless"], flush=True)
+
+
 def rand_sparse(rng, shape, density):
     size = math.prod(shape)
     nnz = int(density * size)
@@ -234,6 +269,9 @@ def small():
 
 if __name__ == "__main__":
     for arg in sys.argv[1:] or ["small", "c1", "c2", "c4"]:
+        if arg == "c5idx":
+            config5_index()
+            continue
         if arg == "small":
             small()
         else:

@@ -476,3 +476,160 @@ def test_sparse_pivot_core_lowrank_matches_dense(dims, R, s, pivot, monkeypatch)
     rng = np.random.default_rng(3)
     probe = np.concatenate([t.coords, np.stack([rng.integers(0, d, 20000) for d in dims], 1)])
     assert rel_err(ft.tt_entries(tt, probe), O.tt_entries(cores, probe)) <= RECON_TOL
+
+
+def _depar_general_numpy(m, tol=1e-12):
+    """The reference loop (fasttt.py:96-145) restated in numpy (checker)."""
+    rows, cols = m.shape
+    basis, bn, t_row, t_coeff = [], [], np.full(cols, -1), np.zeros(cols)
+    for j in range(cols):
+        u = m[:, j]
+        un = float(u @ u)
+        if un == 0.0:
+            continue
+        hit = None
+        for i, b in enumerate(basis):
+            c = float(b @ u) / bn[i]
+            r = u - b * c
+            if float(r @ r) <= tol * tol * un:
+                hit = (i, c)
+                break
+        if hit is None:
+            basis.append(u)
+            bn.append(un)
+            t_row[j], t_coeff[j] = len(basis) - 1, 1.0
+        else:
+            t_row[j], t_coeff[j] = hit
+    n = np.column_stack(basis) if basis else np.zeros((rows, 0))
+    t = np.zeros((len(basis), cols))
+    k = t_row >= 0
+    t[t_row[k], np.flatnonzero(k)] = t_coeff[k]
+    return n, t
+
+
+def test_depar_general_reference_cases():
+    """depar_general on the GPU: the reference's own cases
+    (test_fasttt.py:33-67) -- planted parallel classes in first-occurrence
+    order, zero matrix, no parallel columns, scaling within tolerance, float
+    work counted -- and agreement with the quasi-permutation route."""
+    rng = np.random.default_rng(20260816)
+    u, v, w = (rng.standard_normal(6) for _ in range(3))
+    m = np.column_stack([u, 2.0 * u, v, np.zeros(6), -3.0 * v, w])
+    n, t = ft.depar_general(m)
+    assert n.shape == (6, 3)
+    assert np.array_equal(n[:, 0], u) and np.array_equal(n[:, 1], v) and np.array_equal(n[:, 2], w)
+    assert np.allclose(n @ t, m, atol=1e-12)
+    assert np.array_equal(t[:, 3], np.zeros(3))
+    n, t = ft.depar_general(np.zeros((4, 3)))
+    assert n.shape == (4, 0) and t.shape == (0, 3)
+    m = rng.standard_normal((8, 5))
+    n, t = ft.depar_general(m)
+    assert n.shape == (8, 5) and np.allclose(n @ t, m, atol=1e-12)
+    u = rng.standard_normal(50)
+    n, _ = ft.depar_general(np.column_stack([u, u * (1.0 + 1e-14)]), tol=1e-12)
+    assert n.shape[1] == 1
+    P.float_ops.reset()
+    ft.depar_general(rng.standard_normal((10, 6)))
+    assert P.float_ops.count > 0
+    for _ in range(10):
+        rows = int(rng.integers(2, 25))
+        cols = int(rng.integers(1, 60))
+        q = T.QuasiPermMatrix(rows, cols, rng.integers(0, rows, cols))
+        nq, tq = ft.depar_quasi_perm(q)
+        ng, tg = ft.depar_general(q.to_dense())
+        assert nq.n_cols == ng.shape[1]
+        assert np.allclose(ng @ tg, q.to_dense(), atol=1e-13)
+
+
+@pytest.mark.parametrize("rows,cols,classes", [(30, 200, 17), (300, 64, 64), (7, 500, 3)])
+def test_depar_general_matches_loop(rows, cols, classes):
+    """Random planted classes (scaled copies + zeros): kept columns, t rows
+    and coefficients equal to the reference loop's."""
+    rng = np.random.default_rng(rows * cols)
+    base = rng.standard_normal((rows, classes))
+    pick = rng.integers(0, classes, cols)
+    scale = rng.uniform(-2, 2, cols)
+    m = base[:, pick] * scale
+    m[:, rng.integers(0, cols, cols // 10)] = 0.0
+    n, t = ft.depar_general(m)
+    n0, t0 = _depar_general_numpy(m)
+    assert n.shape == n0.shape and np.array_equal(n, n0)
+    assert np.array_equal(t != 0, t0 != 0)
+    assert np.allclose(t, t0, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("gen", ["laplacian", "random_dups"])
+def test_tensorize_matrix_device_matches_host(gen):
+    """On-device tensorize_matrix: identical canonical COO to the host
+    conversion (ttformat.py:414-433): fused coordinates, C-order, duplicates
+    summed, zeros dropped; the device copy is reused by fasttt."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(4)
+    if gen == "laplacian":
+        n = 64
+        T1 = sp.diags([-1.0, 2.0, -1.0], [-1, 0, 1], shape=(n, n))
+        L = (sp.kron(T1, sp.eye(n)) + sp.kron(sp.eye(n), T1)).tocoo()
+        D = sp.diags(rng.uniform(0.5, 1.5, n * n))
+        M = (D @ L @ D).tocoo()
+        rd = cd = (4, 4, 4, 4, 4, 4)
+    else:
+        r = rng.integers(0, 96, 5000)
+        c = rng.integers(0, 60, 5000)
+        v = rng.standard_normal(5000)
+        v[:40] = 0.0
+        M = sp.coo_matrix((v, (r, c)), shape=(96, 60))
+        rd, cd = (4, 3, 8), (5, 3, 4)
+    host = ft.tensorize_matrix(M, rd, cd)
+    dev = ft.tensorize_matrix(M, rd, cd, device=True)
+    assert dev.shape == host.shape
+    assert np.array_equal(dev.coords, host.coords)
+    # duplicates are summed in input order on the device (scipy's order may
+    # differ): equal up to the rounding of a few-term sum
+    assert np.abs(dev.values - host.values).max() <= 4e-16 * 4 * np.abs(M.data).max()
+    if gen == "laplacian":
+        assert np.array_equal(dev.values, host.values)
+        tt_h, rep_h = ft.fasttt(host, eps=1e-10)
+        tt_d, rep_d = ft.fasttt(dev, eps=1e-10)
+        assert rep_h.ranks == rep_d.ranks
+
+
+@pytest.mark.slow
+def test_config5_parity():
+    """Config 5 (8,503,056 nonzeros, 32^12): every integer output bit-exact
+    against the reference's own index functions (fiber counts per pivot,
+    select_p, FiberSet arrays, kept rows, group maps, lossless ranks); the
+    float result by construction -- a sum of 16 generic rank-1 terms has
+    every unfolding rank 16, so the train must have ranks (16,)*11 and
+    reproduce the input at every nonzero (1e-10 relative) and vanish at
+    20,000 seeded zero positions (1e-10 of the input norm)."""
+    g = load_golden("c5idx")
+    if g is None:
+        pytest.skip("golden c5idx not generated")
+    meta, z = g
+    shape, coords, vals, eps = G.gen_config(5)
+    t = ft.SparseTensor(shape, coords, vals)
+    assert digest(t.coords) == meta["input_coords"]
+    assert digest(t.values) == meta["input_values"]
+    assert P._fiber_counts_device(t) == meta["fiber_counts"]
+    p = ft.select_p(t)
+    assert p == meta["auto_pivot"]
+    idx = meta["index"]
+    fs = ft.extract_nonzero_fibers(t, p)
+    assert digest(fs.fixed_coords) == idx["fixed_coords"]
+    assert digest(fs.indptr) == idx["indptr"]
+    assert digest(fs.pivot_index) == idx["pivot_index"]
+    assert digest(fs.values) == idx["fiber_values"]
+    sw = P.index_sweeps_device(fs._dev)
+    assert [digest(k.cpu().numpy()) for k, _ in sw.left] == idx["left_kept"]
+    assert [digest(k.cpu().numpy()) for k, _ in sw.right] == idx["right_kept"]
+    assert digest(sw.t_map.cpu().numpy()) == idx["t_map"]
+    assert digest(sw.s_map.cpu().numpy()) == idx["s_map"]
+    tt, rep = ft.fasttt(t, eps=eps)
+    assert list(rep.ranks_lossless) == idx["ranks_lossless"]
+    assert tuple(rep.ranks) == (16,) * 11
+    cores_d = [T.to_device(c) for c in tt.cores]
+    got = T.dev_tt_entries(cores_d, T.to_device(t.coords)).cpu().numpy()
+    assert rel_err(got, t.values) <= RECON_TOL
+    zv = T.dev_tt_entries(cores_d, T.to_device(z["zero_coords"])).cpu().numpy()
+    assert np.linalg.norm(zv) <= RECON_TOL * np.linalg.norm(t.values)
