@@ -489,9 +489,15 @@ __global__ void k_copy_keys(int64_t n, const int64_t *in, uint64_t *out) {
 __global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
 
 constexpr int HS_MAXP = 32;
+constexpr int HS_PASS = 16;  // pivots per launch (first probes held in registers)
+// Key with the mode-q digit removed from the C-order linear index:
+// (lin / T_q) * S_q + lin % S_q with S_q = prod of the dims after q and
+// T_q = n_q S_q (exact magic-number divisions, lin < 2^63).
 struct HashSpec {
   int d, np, lg;
-  int64_t mult[HS_MAXP][32];  // key multipliers per pivot of the group (pivot -> 0)
+  int64_t stride[32];  // C-order strides of the full index
+  uint64_t S[HS_MAXP], mS[HS_MAXP], mT[HS_MAXP];
+  int shS[HS_MAXP], shT[HS_MAXP];
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -500,8 +506,16 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+__device__ __forceinline__ uint64_t hs_div(uint64_t x, uint64_t m, int sh) {
+  return sh < 0 ? x : (__umul64hi(x, m) >> sh);
+}
+
 // Insert the np fixed-tuple keys of every nonzero into np hash sets (empty
-// slot = ~0, keys < 2^63); count first insertions per set.
+// slot = ~0, keys < 2^63); count first insertions per set.  One nonzero per
+// thread: the linear index is accumulated straight from the coordinates,
+// each pivot's key derived from it, and the first probe of every pivot is
+// issued before any result is examined (independent atomics in flight);
+// collisions (rare at load factor <= 1/2) then probe linearly.
 __global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict__ coords, int64_t n,
                                                        HashSpec hs,
                                                        unsigned long long *__restrict__ tables,
@@ -511,27 +525,49 @@ __global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict
   const int lane = threadIdx.x & 31;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = base + threadIdx.x;
-    int64_t c[32];
-    if (i < n)
-      for (int k = 0; k < hs.d; ++k) c[k] = coords[i * hs.d + k];
-    for (int q = 0; q < hs.np; ++q) {
-      int fresh = 0;
-      if (i < n) {
-        uint64_t key = 0;
-        for (int k = 0; k < hs.d; ++k) key += (uint64_t)c[k] * (uint64_t)hs.mult[q][k];
-        unsigned long long *tab = tables + (int64_t)q * T;
-        uint64_t h = mix64(key) & mask;
-        while (true) {
-          unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)key);
-          if (old == ~0ull) {
-            fresh = 1;
-            break;
-          }
-          if (old == key) break;
-          h = (h + 1) & mask;
+    uint64_t lin = 0;
+    if (i < n) {
+      const int64_t *c = coords + i * hs.d;
+      for (int k = 0; k < hs.d; ++k) lin += (uint64_t)c[k] * (uint64_t)hs.stride[k];
+    }
+    unsigned fresh_mask = 0, pending = 0;
+    unsigned long long got[HS_PASS];
+    auto key_of = [&](int q) -> uint64_t {
+      const uint64_t hi = hs_div(lin, hs.mT[q], hs.shT[q]);
+      const uint64_t lo = lin - hs_div(lin, hs.mS[q], hs.shS[q]) * hs.S[q];
+      return hi * hs.S[q] + lo;
+    };
+#pragma unroll
+    for (int q = 0; q < HS_PASS; ++q) {
+      got[q] = 0;
+      if (q >= hs.np || i >= n) continue;
+      const uint64_t k = key_of(q);
+      got[q] = atomicCAS(tables + (int64_t)q * T + (mix64(k) & mask), ~0ull, (unsigned long long)k);
+    }
+#pragma unroll
+    for (int q = 0; q < HS_PASS; ++q) {
+      if (q >= hs.np || i >= n) continue;
+      if (got[q] == ~0ull) fresh_mask |= 1u << q;
+      else if (got[q] != key_of(q)) pending |= 1u << q;
+    }
+    while (pending) {  // linear probing for the colliding pivots
+      const int q = __ffs(pending) - 1;
+      pending &= pending - 1;
+      unsigned long long *tab = tables + (int64_t)q * T;
+      const uint64_t k = key_of(q);
+      uint64_t h = mix64(k) & mask;
+      while (true) {
+        h = (h + 1) & mask;
+        const unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)k);
+        if (old == ~0ull) {
+          fresh_mask |= 1u << q;
+          break;
         }
+        if (old == k) break;
       }
-      const unsigned b = __ballot_sync(0xffffffffu, fresh);
+    }
+    for (int q = 0; q < hs.np; ++q) {
+      const unsigned b = __ballot_sync(0xffffffffu, (fresh_mask >> q) & 1u);
       if (lane == 0 && b) atomicAdd(counts + q, (unsigned long long)__popc(b));
     }
   }
@@ -1271,6 +1307,7 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
   if (force_part || (!force_hash && 8 * T > ((int64_t)32 << 20)))
     return fiber_counts_partition(ctx, coords, nnz, d, dims_host, counts_host);
   int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));  // 4 GiB
+  group = std::min(group, HS_PASS);
   uint64_t *tables = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&tables, 8 * (size_t)T * group));
   FTT_CHECK(arena_reserve(ctx, 4096));
@@ -1282,15 +1319,22 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
     hs.d = d;
     hs.np = np;
     hs.lg = lg;
+    {
+      int64_t st = 1;
+      for (int k = d - 1; k >= 0; --k) {
+        hs.stride[k] = st;
+        st *= dims_host[k];
+      }
+    }
     for (int q = 0; q < np; ++q) {
-      KeySpec ks;
-      uint64_t bound;
-      make_spec(d, dims_host, p0 + q, false, &ks, &bound);
-      for (int k = 0; k < d; ++k) hs.mult[q][k] = ks.mult[k];
+      const uint64_t S = (uint64_t)hs.stride[p0 + q];
+      hs.S[q] = S;
+      magic_u63(S, &hs.mS[q], &hs.shS[q]);
+      magic_u63(S * (uint64_t)dims_host[p0 + q], &hs.mT[q], &hs.shT[q]);
     }
     FTT_CUDA(cudaMemsetAsync(tables, 0xff, 8 * (size_t)T * np, ctx->stream));
     const int pb = prof_begin(ctx);
-    k_distinct_hash<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(
+    k_distinct_hash<<<grid_for(nnz, 256, 1), 256, 0, ctx->stream>>>(
         coords, nnz, hs, reinterpret_cast<unsigned long long *>(tables), cnt + p0);
     FTT_LAUNCHED(ctx);
     // coordinates read once + one 8-byte CAS per pivot and nonzero
