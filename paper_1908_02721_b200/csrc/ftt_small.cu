@@ -501,6 +501,107 @@ Tree make_tree(int64_t M, int n, int64_t root_rows_max) {
   return t;
 }
 
+// Hestenes one-sided Jacobi directly on a short tall block (m x n, n <= 16,
+// m * n doubles in shared memory): X P = Y with orthogonal columns; the same
+// convergence rule and noise floor as cta_jacobi.  A warp per column pair,
+// column length m looped by the lanes.  For the small inner SVDs of the
+// low-rank path (B^T, e.g. 512 x 8) this replaces a TSQR tree + Jacobi on R^T
+// + Q expansion (5 launches) by one launch.
+__global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const double *__restrict__ A,
+                                                          int64_t lda, int trans,
+                                                          double *__restrict__ Yo,
+                                                          double *__restrict__ Po,
+                                                          double *__restrict__ norms,
+                                                          int max_sweeps, int *__restrict__ status) {
+  extern __shared__ double S[];  // X m x n (ld m) | P n x n
+  __shared__ double red[SVD_NT / 32];
+  __shared__ int s_any;
+  double *X = S;
+  double *P = S + (size_t)m * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double f = 0.0;
+  int bad = 0;
+  for (int e = tid; e < m * n; e += (int)blockDim.x) {
+    const int j = e / m, i = e - j * m;
+    const double v = trans ? A[j + (int64_t)i * lda] : A[i + (int64_t)j * lda];
+    bad |= !isfinite(v);
+    X[e] = v;
+    f += v * v;
+  }
+  for (int e = tid; e < n * n; e += (int)blockDim.x) P[e] = (e / n == e % n) ? 1.0 : 0.0;
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) atomicOr(status, 1);
+    return;
+  }
+  const double fro2 = cta_sum(f, red);
+  const double tol = kEps * sqrt((double)n);
+  const double floor = 0.01 * kEps * kEps * (double)m * fro2;
+  const int ne = n + (n & 1), npairs = ne / 2;
+  int sweeps = -1;
+  for (int sw = 0; sw < max_sweeps && n > 1; ++sw) {
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int round = 0; round < ne - 1; ++round) {
+      for (int pi = warp; pi < npairs; pi += nw) {
+        int p, q;
+        rr_pair(ne, round, pi, &p, &q);
+        if (p >= n || q >= n) continue;
+        double *xp = X + (size_t)p * m, *xq = X + (size_t)q * m;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          const double u = xp[i], v = xq[i];
+          a += u * u;
+          b += v * v;
+          g += u * v;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        if (a > floor && b > floor && fabs(g) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = copysign(1.0 / (fabs(zeta) + sqrt(1.0 + zeta * zeta)), zeta);
+          const double c = rsqrt(1.0 + t * t);
+          const double sn = c * t;
+          for (int i = lane; i < m; i += 32) {
+            const double u = xp[i], v = xq[i];
+            xp[i] = c * u - sn * v;
+            xq[i] = sn * u + c * v;
+          }
+          double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
+          if (lane < n) {
+            const double pu = pp[lane], pv = pq[lane];
+            pp[lane] = c * pu - sn * pv;
+            pq[lane] = sn * pu + c * pv;
+          }
+          if (lane == 0) s_any = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_any) {
+      sweeps = sw + 1;
+      break;
+    }
+    __syncthreads();
+  }
+  if (n <= 1) sweeps = 1;
+  if (tid == 0) {
+    status[1] = sweeps;
+    if (sweeps < 0) atomicOr(status, 2);
+  }
+  for (int j = warp; j < n; j += nw) {
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) s2 += X[i + (size_t)j * m] * X[i + (size_t)j * m];
+    s2 = warp_sum(s2);
+    if (lane == 0) norms[j] = sqrt(s2);
+  }
+  for (int e = tid; e < m * n; e += (int)blockDim.x) Yo[e] = X[e];
+  for (int e = tid; e < n * n; e += (int)blockDim.x) Po[e] = P[e];
+}
+
 }  // namespace
 
 bool tsqr_ok(int64_t m, int64_t n) { return n >= 1 && n <= 64 && m >= n; }
@@ -650,6 +751,53 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   if (W) owned_free(ctx, W);
   for (double *p : qs) owned_free(ctx, p);
   // one round trip: status, the caller's device scalar and the norms
+  if (extra_dev)
+    FTT_CUDA(cudaMemcpyAsync(dev + 1, extra_dev, sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  std::vector<double> h(n + 2);
+  FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));
+  if (extra_dev && extra_host) *extra_host = h[1];
+  owned_free(ctx, dev);
+  int st[2];
+  memcpy(st, h.data(), 8);
+  if (st[0] & 1) {
+    set_error("matrix entries must be finite");
+    return FTT_ERR_NONFINITE;
+  }
+  if (st[0] & 2) {
+    set_error("Jacobi SVD did not converge in %d sweeps", max_sweeps);
+    return FTT_ERR_NOCONV;
+  }
+  if (sweeps) *sweeps = st[1];
+  memcpy(norms_host, h.data() + 2, 8 * (size_t)n);
+  return FTT_OK;
+}
+
+bool direct_small_ok(int64_t m, int64_t n) {
+  static const bool off = getenv("FTT_NO_DIRECT_SMALL") != nullptr;
+  return !off && n >= 1 && n <= 16 && m >= n && m * n * 8 <= 160 * 1024;
+}
+
+// One-sided Jacobi directly on the short tall A_tall (m x n): Y = A_tall P
+// (m x n, ld m), P (n x n), norms_host[j] = ||Y_j|| (unsorted).
+int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, int trans,
+                     double *Y, double *P, double *norms_host, int *sweeps,
+                     const double *extra_dev, double *extra_host) {
+  static bool attr = false;
+  if (!attr) {
+    FTT_CUDA(cudaFuncSetAttribute(k_jacobi_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    attr = true;
+  }
+  double *dev = nullptr;  // status (2 ints) | pad | norms n
+  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n)));
+  int *status = reinterpret_cast<int *>(dev);
+  FTT_CUDA(cudaMemsetAsync(status, 0, 16, ctx->stream));
+  const int jt = 32 * std::max(1, std::min(SVD_NT / 32, (int)((n + 1) / 2)));
+  const int max_sweeps = 60;
+  k_jacobi_direct<<<1, jt, 8 * (size_t)(m * n + n * n), ctx->stream>>>(
+      (int)m, (int)n, A, lda, trans, Y, P, dev + 2, max_sweeps, status);
+  FTT_LAUNCHED(ctx);
   if (extra_dev)
     FTT_CUDA(cudaMemcpyAsync(dev + 1, extra_dev, sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));

@@ -551,9 +551,12 @@ namespace {
 // Phase 1 (QR + Jacobi) on a given state; see the file header.
 // extra_dev / extra_host: a device scalar of the caller brought back with
 // the narrow path's single round trip (ignored on the wide path).
+// allow_direct: the caller only uses singular triplets well above the noise
+// floor (the low-rank path's inner factor), so the direct one-sided Jacobi on
+// A_tall (U = Y / sigma) may be used for short narrow operands.
 int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A, int64_t lda,
                int32_t a_row_major, const double *extra_dev = nullptr,
-               double *extra_host = nullptr) {
+               double *extra_host = nullptr, bool allow_direct = false) {
   st->m = m;
   st->n = n;
   st->transposed = m < n;
@@ -562,6 +565,29 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
   const int64_t mA = st->mA, nA = st->nA;
   if (nA == 0) return FTT_OK;
   static const bool no_small = getenv("FTT_NO_SMALL") != nullptr;
+  if (!no_small && allow_direct && direct_small_ok(mA, nA)) {
+    // short narrow operand (e.g. the k x n_A factor B of the low-rank path):
+    // one-sided Jacobi directly on A_tall in one CTA (Y = A_tall P aliases
+    // Af; phase 2 takes the `direct` branch: U = Y / sigma, V = P)
+    st->direct = true;
+    const bool need_t = a_row_major ? !st->transposed : st->transposed;
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->P, 8 * (size_t)nA * nA));
+    st->Y = st->Af;
+    std::vector<double> raw(nA);
+    const int pb = prof_begin(ctx);
+    FTT_CHECK(direct_small_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, st->P, raw.data(),
+                               &st->sweeps, extra_dev, extra_host));
+    prof_end(ctx, pb, PT_JACOBI, 8.0 * ((double)mA * nA * 2 + (double)nA * nA),
+             6.0 * std::max(st->sweeps, 1) * (double)nA * nA / 2.0 * (double)mA);
+    st->perm.resize(nA);
+    std::iota(st->perm.begin(), st->perm.end(), 0);
+    std::stable_sort(st->perm.begin(), st->perm.end(),
+                     [&](int64_t a, int64_t b) { return raw[a] > raw[b]; });
+    st->sigma.resize(nA);
+    for (int64_t i = 0; i < nA; ++i) st->sigma[i] = raw[st->perm[i]];
+    return FTT_OK;
+  }
   if (!no_small && tsqr_ok(mA, nA)) {
     // narrow operand: CTA-local QR (+ TSQR tree) and CTA-local Jacobi, one
     // host round trip for the whole factorisation
@@ -943,7 +969,7 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
     else FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
                                     nullptr, rest2_dev));
     st->inner = new SvdState();
-    if (svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0, rest2_dev, &rest2) != FTT_OK) {
+    if (svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0, rest2_dev, &rest2, true) != FTT_OK) {
       // speculative factorisation failed: decide on the certificate alone
       // (an accepted certificate re-runs the factorisation below and reports)
       svd_state_release(ctx, st->inner);
@@ -982,7 +1008,7 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   if (!loose) return FTT_OK;  // (a speculative inner state is released with st)
   if (!st->inner) {
     st->inner = new SvdState();
-    FTT_CHECK(svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0));
+    FTT_CHECK(svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0, nullptr, nullptr, true));
   }
   st->sigma = st->inner->sigma;
   if (s_host) memcpy(s_host, st->sigma.data(), 8 * st->sigma.size());

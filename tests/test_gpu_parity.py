@@ -633,3 +633,21 @@ def test_config5_parity():
     assert rel_err(got, t.values) <= RECON_TOL
     zv = T.dev_tt_entries(cores_d, T.to_device(z["zero_coords"])).cpu().numpy()
     assert np.linalg.norm(zv) <= RECON_TOL * np.linalg.norm(t.values)
+
+
+@pytest.mark.parametrize("mode,eps", [("dynamic", 1e-6), ("static", 1e-3), ("fixed_rank", None)])
+def test_sparse_pivot_core_other_modes(mode, eps, monkeypatch):
+    """The lazily densified / sparse pivot core under every rounding mode
+    (dynamic budgets, a loose static eps that truncates real rank, fixed
+    ranks -- which always densify): ranks equal to the oracle's, entries
+    within 1e-10 of the oracle train."""
+    monkeypatch.setattr(P, "_SPARSE_PIVOT_DENSITY", 1.0)
+    t = _rank_r_sparse((24,) * 5, 5, 3, seed=99)
+    kw = {"fixed_ranks": 3} if mode == "fixed_rank" else {}
+    tt, rep = ft.fasttt(t, eps=eps, pivot=1, mode=mode, **kw)
+    cores, info = O.fasttt(t.shape, t.coords, t.values, eps=eps if eps else 1e-14, pivot=1,
+                           mode=mode, report=False, **kw)
+    assert tuple(rep.ranks) == info["ranks"]
+    rng = np.random.default_rng(5)
+    probe = np.concatenate([t.coords, np.stack([rng.integers(0, 24, 5000) for _ in range(5)], 1)])
+    assert rel_err(ft.tt_entries(tt, probe), O.tt_entries(cores, probe)) <= RECON_TOL
