@@ -26,7 +26,7 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys
-constexpr int RS_MIN_TILE = RS_THREADS * 8;     // smallest tile variant (status sizing)
+constexpr int RS_MIN_TILE = RS_TILE;            // status sizing
 constexpr int RADIX = 256;
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;
@@ -919,13 +919,9 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
   FTT_CHECK(copy_to_host(ctx, h.data(), ghist, sizeof(uint32_t) * num_passes * RADIX));
   k_hist_scan<<<num_passes, RADIX, 0, ctx->stream>>>(ghist);
   FTT_LAUNCHED(ctx);
-  // tile size: RS_ITEMS (16) or 24 keys per thread (A/B knob FTT_RS_ITEMS)
-  static const int items = [] {
-    const char *e = getenv("FTT_RS_ITEMS");
-    const int v = e ? atoi(e) : RS_ITEMS;
-    return (v == 8 || v == 12 || v == 24) ? v : RS_ITEMS;
-  }();
-  const int tile = RS_THREADS * items;
+  // tile: RS_ITEMS = 16 keys per thread (measured on config 5: 8 / 12 / 24
+  // items per thread were 13 % / 50 % / 140 % slower per pass)
+  const int tile = RS_TILE;
   int64_t ntiles = ceil_div(n, tile);
   int cur = 0;
   for (int p = 0; p < num_passes; ++p) {
@@ -938,34 +934,20 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
     static bool attr_set = false;
     if (!attr_set) {
       const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, RS_ITEMS>, a, 12 * RS_TILE));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, RS_ITEMS>, a, 12 * RS_TILE));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, 24>, a, 12 * RS_THREADS * 24));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, 24>, a, 12 * RS_THREADS * 24));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, 12>, a, 12 * RS_THREADS * 12));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, 12>, a, 12 * RS_THREADS * 12));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, 8>, a, 12 * RS_THREADS * 8));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, 8>, a, 12 * RS_THREADS * 8));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true>, a, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false>, a, 12 * RS_TILE));
       attr_set = true;
     }
     const int pb = prof_begin(ctx);
-#define FTT_ONESWEEP(V_, I_)                                                                  \
-  k_onesweep<V_, I_><<<(unsigned)ntiles, RS_THREADS, (V_ ? 12 : 8) * RS_THREADS * I_,         \
-                       ctx->stream>>>(keys[cur], V_ ? vals[cur] : nullptr, keys[cur ^ 1],      \
-                                      V_ ? vals[cur ^ 1] : nullptr, n, 8 * p,                 \
-                                      ghist + p * RADIX, status, counters + p)
     if (vals[0]) {
-      if (items == 24) FTT_ONESWEEP(true, 24);
-      else if (items == 12) FTT_ONESWEEP(true, 12);
-      else if (items == 8) FTT_ONESWEEP(true, 8);
-      else FTT_ONESWEEP(true, RS_ITEMS);
+      k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
+          keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, ghist + p * RADIX, status,
+          counters + p);
     } else {
-      if (items == 24) FTT_ONESWEEP(false, 24);
-      else if (items == 12) FTT_ONESWEEP(false, 12);
-      else if (items == 8) FTT_ONESWEEP(false, 8);
-      else FTT_ONESWEEP(false, RS_ITEMS);
+      k_onesweep<false><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
+          keys[cur], nullptr, keys[cur ^ 1], nullptr, n, 8 * p, ghist + p * RADIX, status,
+          counters + p);
     }
-#undef FTT_ONESWEEP
     FTT_LAUNCHED(ctx);
     // algorithmic bytes: read + write every key (and payload) once
     prof_end(ctx, pb, PT_SORT, (double)n * (vals[0] ? 24.0 : 16.0), 0.0);
