@@ -509,6 +509,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 __device__ __forceinline__ uint64_t hs_div(uint64_t x, uint64_t m, int sh) {
   return sh < 0 ? x : (__umul64hi(x, m) >> sh);
 }
+__device__ __forceinline__ uint64_t sm_div(uint64_t x, uint64_t m, int sh) { return hs_div(x, m, sh); }
 
 // Insert the np fixed-tuple keys of every nonzero into np hash sets (empty
 // slot = ~0, keys < 2^63); count first insertions per set.  One nonzero per
@@ -711,6 +712,109 @@ __global__ void __launch_bounds__(256) k_part_count(const uint64_t *__restrict__
   if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(&s_cnt, fresh);
   __syncthreads();
   if (threadIdx.x == 0 && s_cnt) atomicAdd(counts + q, s_cnt);
+}
+
+// ---- select_p counts from a sorted order (group-local shared hash) ------
+// With the linear keys K = sum_k c_k w_k sorted (C order: the canonical
+// input; or the reversed-mode order after one radix sort), the nonzeros of a
+// pivot-p fiber share hi = K / T_p (T_p = w_p n_p) and lo = K mod w_p, and
+// all nonzeros with the same hi are contiguous.  A CTA takes a group-aligned
+// chunk (whole hi-groups, <= GC_CAP entries) and counts distinct dropped
+// keys hi w_p + lo in a shared-memory hash set: one streaming read of the
+// sorted keys per pivot, no scatter.  A group longer than the cap flags the
+// pivot (the other order, then the partition path, count it instead).
+constexpr int GC_L = 1024;       // nominal entries per CTA
+constexpr int GC_CAP = 2048;     // max entries per chunk (hash load <= 1/2)
+constexpr int GC_SLOTS = 4096;
+
+// Both linear keys of every nonzero in one read of the COO: C order (lin)
+// and the reversed-mode order (rlin).
+__global__ void __launch_bounds__(256) k_linearize2(const int64_t *__restrict__ coords, int64_t n,
+                                                    LinSpec ls, LinSpec rs,
+                                                    uint64_t *__restrict__ lin,
+                                                    uint64_t *__restrict__ rlin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t *c = coords + i * ls.d;
+    uint64_t x = 0, y = 0;
+    for (int k = 0; k < ls.d; ++k) {
+      const uint64_t v = (uint64_t)c[k];
+      x += v * (uint64_t)ls.stride[k];
+      y += v * (uint64_t)rs.stride[k];
+    }
+    lin[i] = x;
+    rlin[i] = y;
+  }
+}
+
+__global__ void k_sorted_check(const uint64_t *__restrict__ k, int64_t n, int *__restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (k[i] <= k[i - 1]) atomicOr(bad, 1);
+}
+
+__global__ void __launch_bounds__(256) k_group_count(const uint64_t *__restrict__ K, int64_t n,
+                                                     uint64_t S, uint64_t mS, int shS, uint64_t mT,
+                                                     int shT, unsigned long long *__restrict__ count,
+                                                     int *__restrict__ flag) {
+  extern __shared__ unsigned long long tab[];  // GC_SLOTS
+  __shared__ int64_t s_start, s_end;
+  __shared__ unsigned long long s_cnt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * GC_L;
+  auto grp = [&](int64_t i) -> uint64_t { return sm_div(K[i], mT, shT); };
+  // first group start >= c0 and >= c0 + L: the CTA tests 256 consecutive
+  // positions per round (keys sorted, so grp is monotone) and stops at the
+  // first round holding a boundary; no boundary within CAP -> "none"
+  __shared__ unsigned s_j[2];
+  if (threadIdx.x < 2) s_j[threadIdx.x] = 0xffffffffu;
+  __syncthreads();
+  for (int w = 0; w < 2; ++w) {
+    const int64_t from = c0 + (w ? GC_L : 0);
+    if (from >= n) continue;  // uniform over the CTA
+    for (int r = 0; r < GC_CAP / 256; ++r) {
+      const int j = r * 256 + (int)threadIdx.x;
+      const int64_t i = from + j;
+      const bool st = i <= n && (i == n || i == 0 || grp(i) != grp(i - 1));
+      const unsigned mj = __reduce_min_sync(0xffffffffu, st ? (unsigned)j : 0xffffffffu);
+      if (lane == 0 && mj != 0xffffffffu) atomicMin(&s_j[w], mj);
+      if (__syncthreads_or(st)) break;
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_start = c0 >= n ? n : (s_j[0] == 0xffffffffu ? INT64_MAX : c0 + s_j[0]);
+    s_end = c0 + GC_L >= n ? n : (s_j[1] == 0xffffffffu ? INT64_MAX : c0 + GC_L + s_j[1]);
+  }
+  for (int e = threadIdx.x; e < GC_SLOTS; e += blockDim.x) tab[e] = ~0ull;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int64_t start = s_start, end = s_end;
+  if (start == INT64_MAX) return;  // a long group covers the window; its owner decides
+  if (end == INT64_MAX || end - start > GC_CAP) {
+    if (threadIdx.x == 0) atomicOr(flag, 1);
+    return;
+  }
+  unsigned long long fresh = 0;
+  for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
+    const uint64_t k = K[i];
+    const uint64_t hi = sm_div(k, mT, shT);
+    const uint64_t lo = k - sm_div(k, mS, shS) * S;
+    const uint64_t key = hi * S + lo;
+    uint64_t h = mix64(key) & (GC_SLOTS - 1);
+    while (true) {
+      const unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)key);
+      if (old == ~0ull) {
+        ++fresh;
+        break;
+      }
+      if (old == key) break;
+      h = (h + 1) & (GC_SLOTS - 1);
+    }
+  }
+  for (int o = 16; o; o >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, o);
+  if (lane == 0 && fresh) atomicAdd(&s_cnt, fresh);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(count, s_cnt);
 }
 
 __global__ void k_count_changes(const uint64_t *k, int64_t n, unsigned long long *out) {
@@ -1130,8 +1234,119 @@ void magic_u63(uint64_t D, uint64_t *m, int *sh) {
   *sh = l - 1;
 }
 
+// Grouped counts from sorted orders (k_group_count): pivots p >= d/2 use the
+// canonical C order (groups = the p leading modes), p < d/2 the reversed
+// order (groups = the d-1-p trailing modes; one radix sort), each retried in
+// the other order on overflow.  done[p] marks the pivots counted.
+int fiber_counts_grouped(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                         const int64_t *dims, int64_t *counts_host, bool *done) {
+  for (int p = 0; p < d; ++p) done[p] = false;
+  static const bool off = getenv("FTT_NO_GROUPED") != nullptr;
+  if (off || d < 2) return FTT_OK;
+  int64_t wc[32], wr[32];
+  {
+    int64_t st = 1;
+    for (int k = d - 1; k >= 0; --k) {
+      wc[k] = st;
+      st *= dims[k];
+    }
+    st = 1;
+    for (int k = 0; k < d; ++k) {
+      wr[k] = st;
+      st *= dims[k];
+    }
+  }
+  uint64_t *lin = nullptr, *rlin = nullptr, *rsorted = nullptr;
+  unsigned long long *cnt = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&lin, 8 * (size_t)nnz));
+  FTT_CHECK(owned_alloc(ctx, (void **)&cnt, 8 * 64 + 4 * 64 + 8));
+  int *flags = reinterpret_cast<int *>(cnt + 64);
+  int *unsorted = flags + 64;
+  FTT_CUDA(cudaMemsetAsync(cnt, 0, 8 * 64 + 4 * 64 + 8, ctx->stream));
+  LinSpec ls, rs;
+  ls.d = rs.d = d;
+  for (int k = 0; k < d; ++k) {
+    ls.stride[k] = wc[k];
+    rs.stride[k] = wr[k];
+  }
+  const bool need_rev = true;  // p = 0 always prefers the reversed order (d >= 2)
+  FTT_CHECK(owned_alloc(ctx, (void **)&rlin, 8 * (size_t)nnz));
+  FTT_CHECK(owned_alloc(ctx, (void **)&rsorted, 8 * (size_t)nnz));
+  int pb = prof_begin(ctx);
+  k_linearize2<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(coords, nnz, ls, rs, lin, rlin);
+  FTT_LAUNCHED(ctx);
+  // read the COO once, write both linear keys
+  prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 16.0), 0.0);
+  k_sorted_check<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(lin, nnz, unsorted);
+  FTT_LAUNCHED(ctx);
+  {
+    FTT_CHECK(arena_reserve(ctx, radix_sort_scratch_bytes(nnz, false) + 4096));
+    uint64_t prod = 1;
+    for (int k = 0; k < d; ++k) prod *= (uint64_t)dims[k];
+    FTT_CHECK(radix_sort(ctx, rlin, nullptr, rsorted, nullptr, nnz, bit_length(prod - 1)));
+    owned_free(ctx, rlin);
+  }
+  const unsigned nb = (unsigned)ceil_div(nnz, GC_L);
+  static bool attr = false;
+  if (!attr) {
+    FTT_CUDA(cudaFuncSetAttribute(k_group_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  8 * GC_SLOTS));
+    attr = true;
+  }
+  auto launch = [&](int p, bool rev, int slot) -> int {
+    const uint64_t S = (uint64_t)(rev ? wr[p] : wc[p]);
+    uint64_t mS, mT;
+    int shS, shT;
+    magic_u63(S, &mS, &shS);
+    magic_u63(S * (uint64_t)dims[p], &mT, &shT);
+    const int pb2 = prof_begin(ctx);
+    k_group_count<<<nb, 256, 8 * GC_SLOTS, ctx->stream>>>(rev ? rsorted : lin, nnz, S, mS, shS, mT, shT,
+                                               cnt + slot, flags + slot);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb2, PT_SEGMENT, 8.0 * (double)nnz, 0.0);
+    return FTT_OK;
+  };
+  // pass 1: preferred order (slots 0..d-1); pass 2: the other order (d..2d-1)
+  for (int p = 0; p < d; ++p) FTT_CHECK(launch(p, 2 * p < d, p));
+  unsigned long long h[64];
+  int hf[64], hu = 0;
+  FTT_CHECK(copy_to_host(ctx, h, cnt, 8 * 64));
+  FTT_CHECK(copy_to_host(ctx, hf, flags, 4 * 64));
+  FTT_CHECK(copy_to_host(ctx, &hu, unsorted, sizeof(int)));
+  bool retried[32] = {false};
+  bool retry = false;
+  for (int p = 0; p < d; ++p) {
+    const bool rev = 2 * p < d;
+    const bool valid = !hf[p] && (rev || !hu);  // the C order needs sorted input
+    if (valid) {
+      counts_host[p] = (int64_t)h[p];
+      done[p] = true;
+      continue;
+    }
+    // the other order: C needs sorted input, the reversed order its sort
+    const bool other_ok = rev ? !hu : need_rev;
+    if (other_ok) {
+      FTT_CHECK(launch(p, !rev, d + p));
+      retried[p] = retry = true;
+    }
+  }
+  if (retry) {
+    FTT_CHECK(copy_to_host(ctx, h, cnt, 8 * 64));
+    FTT_CHECK(copy_to_host(ctx, hf, flags, 4 * 64));
+    for (int p = 0; p < d; ++p)
+      if (retried[p] && !hf[d + p]) {
+        counts_host[p] = (int64_t)h[d + p];
+        done[p] = true;
+      }
+  }
+  owned_free(ctx, lin);
+  if (rsorted) owned_free(ctx, rsorted);
+  owned_free(ctx, cnt);
+  return FTT_OK;
+}
+
 int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
-                           const int64_t *dims, int64_t *counts_host) {
+                           const int64_t *dims, int64_t *counts_host, const bool *skip) {
   // One pivot per pass: the bucketed key array (~1.2 x 8 B x nnz) then stays
   // resident in L2 between the scatter and the count, so the scattered 8-byte
   // writes merge in L2 instead of reaching DRAM as partial sectors (measured
@@ -1181,6 +1396,7 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
   FTT_LAUNCHED(ctx);
   prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0), 0.0);
   for (int p0 = 0, grp = 0; p0 < d; p0 += G, ++grp) {
+    if (G == 1 && skip && skip[p0]) continue;  // counted by the grouped path
     PartSpec ps;
     ps.g = std::min(G, d - p0);
     ps.bits = bits;
@@ -1216,6 +1432,7 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
   owned_free(ctx, cnt);
   static const bool debug = getenv("FTT_DEBUG") != nullptr;
   for (int p = 0; p < d; ++p) {
+    if (G == 1 && skip && skip[p]) continue;
     if (debug && hf[p]) fprintf(stderr, "[ftt] select_p partition overflow at pivot %d\n", p);
     if (hf[p]) FTT_CHECK(ftt_fiber_count(ctx, coords, nnz, d, dims, p, &counts_host[p]));
     else counts_host[p] = (int64_t)h[p];
@@ -1281,13 +1498,28 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
   const bool force_part = path && !strcmp(path, "part");
   const bool force_sort = path && !strcmp(path, "sort");
   const bool force_hash = path && !strcmp(path, "hash");
+  const bool force_group = path && !strcmp(path, "group");
   if (force_sort) {
     for (int p = 0; p < d; ++p)
       FTT_CHECK(ftt_fiber_count(ctx, coords, nnz, d, dims_host, p, &counts_host[p]));
     return FTT_OK;
   }
-  if (force_part || (!force_hash && 8 * T > ((int64_t)32 << 20)))
-    return fiber_counts_partition(ctx, coords, nnz, d, dims_host, counts_host);
+  if (force_part)
+    return fiber_counts_partition(ctx, coords, nnz, d, dims_host, counts_host, nullptr);
+  if (force_group || (!force_hash && 8 * T > ((int64_t)32 << 20))) {
+    // large inputs: group-local counts from the sorted orders first, the
+    // bucket partition for any pivot whose groups are too long
+    bool done[32];
+    FTT_CHECK(fiber_counts_grouped(ctx, coords, nnz, d, dims_host, counts_host, done));
+    bool all = true;
+    for (int p = 0; p < d; ++p) all &= done[p];
+    static const bool debug = getenv("FTT_DEBUG") != nullptr;
+    if (debug)
+      for (int p = 0; p < d; ++p)
+        if (!done[p]) fprintf(stderr, "[ftt] select_p grouped count: pivot %d -> partition\n", p);
+    if (all) return FTT_OK;
+    return fiber_counts_partition(ctx, coords, nnz, d, dims_host, counts_host, done);
+  }
   int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));  // 4 GiB
   group = std::min(group, HS_PASS);
   uint64_t *tables = nullptr;
