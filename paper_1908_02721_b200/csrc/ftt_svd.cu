@@ -66,7 +66,12 @@ constexpr int JB = 16;
 constexpr int JP = 2 * JB;  // 32 columns per pair
 constexpr int JT = 256;
 constexpr int CH = 64;      // rows per staged chunk
-constexpr int MAX_INNER = 3;  // inner sweeps on the Gram before a fresh recompute
+// Inner two-sided sweeps on the pair's Gram before the next fresh
+// recompute.  They only pick rotations (convergence is decided on fresh
+// Grams), and each costs 31 rounds x 3 CTA barriers: measured on config 4's
+// 2064 x 766 operand, 1 inner sweep = 23 outer sweeps / 97 ms, 3 = 21 / 153 ms.
+constexpr int MAX_INNER = 3;
+__device__ int g_max_inner = 1;  // A/B knob FTT_JINNER (1..3)
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -244,7 +249,8 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
     track->last_mod[bb] = track->t;
   }
   // ---- cyclic two-sided Jacobi on G (parallel: 16 disjoint pairs per round)
-  for (int sw = 0; sw < MAX_INNER; ++sw) {
+  const int max_inner = g_max_inner;
+  for (int sw = 0; sw < max_inner; ++sw) {
     int sweep_any = 0;
     for (int round = 0; round < JP - 1; ++round) {
       int flag = 0;
@@ -702,6 +708,15 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     const double floor = 0.01 * 2.220446049250313e-16 * 2.220446049250313e-16 * (double)mX * fro2;
     const int max_sweeps = 60;
     FTT_CUDA(cudaMemsetAsync(rot, 0, sizeof(unsigned long long) * 64, ctx->stream));
+    static bool inner_set = false;
+    if (!inner_set) {
+      const char *e = getenv("FTT_JINNER");
+      if (e) {
+        const int v = std::max(1, std::min(MAX_INNER, atoi(e)));
+        FTT_CUDA(cudaMemcpyToSymbol(g_max_inner, &v, sizeof(int)));
+      }
+      inner_set = true;
+    }
     static int coresident = 0;
     if (!coresident) {
       int per_sm = 0;

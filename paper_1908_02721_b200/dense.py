@@ -72,6 +72,11 @@ def lowrank_k(min_dim: int, hint) -> int:
     # narrow operands (<= 64 columns) also take the sketch when it is narrower:
     # the full path's column-sequential TSQR + Jacobi cost grows with the
     # width, the sketch path's with the (certified) rank
+    # sketches wider than 64 columns (bonds of rank > 28) belong to operands
+    # with genuine tails (configs 3 and 4): measured always rejected there, so
+    # the attempt is skipped
+    if k > 64:
+        return 0
     if k < min_dim and (2 * k <= min_dim or min_dim <= 64):
         return k
     return 0
