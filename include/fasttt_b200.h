@@ -307,6 +307,45 @@ int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
                 const int64_t *ranks_host, const double *const *cores_host,
                 double *norm_out);
 
+/* ------------------------------------------------------ rounding driver */
+/* One core of the structured train handed to ftt_sweep_rounding:
+ *  kind 0: dense (r0, n, r1) C-order buffer `data` (caller-owned, read only);
+ *  kind 1 / 2: left / right 0/1 core as its kept rows (`kept`, K entries,
+ *    r_other = the bond on the far side), the SideCore of the Python mirror;
+ *  kind 3: the pivot core given by its entries (ftt_sparse_pivot). */
+typedef struct {
+  int32_t kind;
+  int64_t r0, n, r1;
+  double *data;
+  const int64_t *kept;
+  int64_t K, r_other;
+} ftt_core_desc;
+/* The pivot core's entries (fasttt.py:256-259): value[e] at
+ * (t_map[fiber_of[e]], pivot_index[e], s_map[fiber_of[e]]); NULL maps for
+ * unit edge bonds. */
+typedef struct {
+  int64_t nnz;
+  const int64_t *fiber_of, *pivot_index;
+  const double *values;
+  const int64_t *t_map, *s_map;
+} ftt_sparse_pivot;
+/* _sweep_rounding (fasttt.py:324-356) in one call: SVD sweep p..d-2, QR
+ * sweep d-1..p+1, SVD sweep p..1, with policy 0 = static (delta per step,
+ * fasttt.py:364-386), 1 = dynamic (left / right budgets re-absorbed,
+ * fasttt.py:389-428), 2 = fixed ranks (targets[d+1], fasttt.py:431-453);
+ * interval_ok lets a static step accept a low-rank certificate whose
+ * interval decides the same rank (dense.dev_svd_truncate).  Output cores:
+ * out_ptrs[k] fresh device buffers (release with ftt_free_device), shapes
+ * out_shapes[3k..3k+2]; *zero_out = 1 (and no outputs) when a truncation
+ * reaches rank 0 (the zero train, fasttt.py:337-338, 351-352). */
+int ftt_sweep_rounding(ftt_ctx *ctx, int32_t d, int32_t pivot,
+                       const ftt_core_desc *cores, const ftt_sparse_pivot *sp,
+                       int32_t policy, double delta, double left, double right,
+                       const int64_t *targets, int32_t interval_ok,
+                       double **out_ptrs, int64_t *out_shapes, int32_t *zero_out);
+/* Release a device buffer returned by ftt_sweep_rounding (stream-ordered). */
+int ftt_free_device(ftt_ctx *ctx, void *p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -642,10 +642,98 @@ class _Trunc:
         return r, tail_error(s, r)
 
 
+class _CoreDesc(nat.ctypes.Structure):
+    _fields_ = [("kind", nat.ctypes.c_int32), ("r0", nat.ctypes.c_int64),
+                ("n", nat.ctypes.c_int64), ("r1", nat.ctypes.c_int64),
+                ("data", nat.ctypes.c_void_p), ("kept", nat.ctypes.c_void_p),
+                ("K", nat.ctypes.c_int64), ("r_other", nat.ctypes.c_int64)]
+
+
+class _SparsePivot(nat.ctypes.Structure):
+    _fields_ = [("nnz", nat.ctypes.c_int64), ("fiber_of", nat.ctypes.c_void_p),
+                ("pivot_index", nat.ctypes.c_void_p), ("values", nat.ctypes.c_void_p),
+                ("t_map", nat.ctypes.c_void_p), ("s_map", nat.ctypes.c_void_p)]
+
+
+class _NativeCore:
+    """A core buffer allocated by ftt_sweep_rounding, exposed to torch through
+    __cuda_array_interface__ (zero copy) and released (ftt_free_device,
+    stream-ordered) when the last tensor viewing it is gone."""
+
+    __slots__ = ("ptr", "shape", "__weakref__")
+
+    def __init__(self, ptr, shape):
+        self.ptr, self.shape = int(ptr), tuple(int(x) for x in shape)
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": self.shape, "typestr": "<f8", "data": (self.ptr, False), "version": 3,
+                "strides": None}
+
+    def __del__(self):
+        try:
+            nat.lib().ftt_free_device(nat.context(), nat.ctypes.c_void_p(self.ptr))
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
+
+
 def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
-    """_sweep_rounding (fasttt.py:324-356) on device cores; 0/1 cores are
-    SideCore objects whose contractions are scatters. Returns dense device
-    cores, or None for the zero train."""
+    """_sweep_rounding (fasttt.py:324-356) in one native call
+    (ftt_sweep_rounding: the three sweeps and the truncation policy run in
+    C++ over the same kernels).  FTT_PY_SWEEP=1 selects the step-by-step
+    Python driver below (same kernels, same order)."""
+    import os
+
+    if os.environ.get("FTT_PY_SWEEP") == "1":
+        return _sweep_rounding_python(cores, pivot, policy)
+    torch = _torch()
+    d = len(cores)
+    descs = (_CoreDesc * d)()
+    sp = None
+    keep = []  # contiguous copies referenced by the descriptors
+    for k, c in enumerate(cores):
+        dsc = descs[k]
+        if isinstance(c, SideCore):
+            dsc.kind = 1 if c.kind == "L" else 2
+            dsc.kept, dsc.K, dsc.r_other = c.kept.data_ptr(), c.K, c.r_other
+            dsc.r0, dsc.n, dsc.r1 = c.shape
+        elif isinstance(c, SparsePivotCore):
+            dsc.kind = 3
+            dsc.r0, dsc.n, dsc.r1 = c.shape
+            df, sw = c.df, c.sw
+            sp = _SparsePivot(df.nnz, df.fiber_of.data_ptr(), df.pivot_index.data_ptr(),
+                              df.values.data_ptr(),
+                              sw.t_map.data_ptr() if sw.t_map is not None else None,
+                              sw.s_map.data_ptr() if sw.s_map is not None else None)
+        else:
+            c = c.contiguous()
+            keep.append(c)
+            dsc.kind = 0
+            dsc.r0, dsc.n, dsc.r1 = (int(x) for x in c.shape)
+            dsc.data = c.data_ptr()
+    kind = {"static": 0, "dynamic": 1, "fixed": 2}[policy.kind]
+    targets = nat.i64_array(policy.targets) if kind == 2 else None
+    outs = (nat.ctypes.c_void_p * d)()
+    shapes = (nat.ctypes.c_int64 * (3 * d))()
+    zero = nat.ctypes.c_int32(0)
+    vp = nat.ctypes.c_void_p
+    cast = nat.ctypes.cast
+    nat.check(nat.lib().ftt_sweep_rounding(
+        nat.context(), d, pivot, cast(descs, vp),
+        cast(nat.ctypes.pointer(sp), vp) if sp is not None else None, kind,
+        float(policy.delta), float(policy.left), float(policy.right),
+        cast(targets, vp) if targets is not None else None, 1 if kind == 0 else 0,
+        cast(outs, vp), cast(shapes, vp), nat.ctypes.byref(zero)), "ftt_sweep_rounding")
+    if zero.value:
+        return None
+    return [torch.as_tensor(_NativeCore(outs[k], shapes[3 * k:3 * k + 3]), device="cuda")
+            for k in range(d)]
+
+
+def _sweep_rounding_python(cores, pivot: int, policy: _Trunc):
+    """_sweep_rounding (fasttt.py:324-356) on device cores, one C-ABI call per
+    step; 0/1 cores are SideCore objects whose contractions are scatters.
+    Returns dense device cores, or None for the zero train."""
     torch = _torch()
     lib, ctx = nat.lib(), nat.context()
     cs = list(cores)

@@ -651,3 +651,27 @@ def test_sparse_pivot_core_other_modes(mode, eps, monkeypatch):
     rng = np.random.default_rng(5)
     probe = np.concatenate([t.coords, np.stack([rng.integers(0, 24, 5000) for _ in range(5)], 1)])
     assert rel_err(ft.tt_entries(tt, probe), O.tt_entries(cores, probe)) <= RECON_TOL
+
+
+def test_native_sweep_matches_python_driver(monkeypatch):
+    """The one-call native rounding driver (ftt_sweep_rounding) against the
+    step-by-step Python driver over the same kernels: identical ranks and
+    cores on the small reference suite in every mode."""
+    g = load_golden("small")
+    assert g is not None
+    cases, z = g
+    import os
+    for case in cases[:12]:
+        if "runs" not in case:
+            continue
+        i = case["id"]
+        t = ft.SparseTensor(case["shape"], z[f"t{i}_coords"], z[f"t{i}_values"])
+        for run in case["runs"]:
+            kw = dict(run["kw"])
+            monkeypatch.setenv("FTT_PY_SWEEP", "1")
+            tt_p, rep_p = ft.fasttt(t, eps=run["eps"], pivot=run["pivot"], mode=run["mode"], **kw)
+            monkeypatch.delenv("FTT_PY_SWEEP")
+            tt_n, rep_n = ft.fasttt(t, eps=run["eps"], pivot=run["pivot"], mode=run["mode"], **kw)
+            assert rep_n.ranks == rep_p.ranks, run["tag"]
+            for a, b in zip(tt_n.cores, tt_p.cores):
+                assert np.array_equal(a, b), run["tag"]
