@@ -112,6 +112,60 @@ __global__ void __launch_bounds__(256) k_entries_grp(TrainDesc t, const int64_t 
   }
 }
 
+// Ranks <= R (4 / 8): one thread per coordinate, the running row vector in
+// R registers; each core slice row is read as double2 pairs (rows of r_{k+1}
+// contiguous doubles).  ~20 warp instructions per coordinate for config 2
+// (ranks 8) against ~10x that for the lane-group kernel; consecutive
+// coordinates share their leading modes (C-sorted input), so the slice
+// loads of those modes are broadcast within a warp.
+template <int R>
+__global__ void __launch_bounds__(256) k_entries_thr(TrainDesc t, const int64_t *__restrict__ coords,
+                                                     int64_t n, double *__restrict__ out,
+                                                     int aligned16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] = a == 0 ? 1.0 : 0.0;
+    const int64_t *c = coords + i * t.d;
+    for (int k = 0; k < t.d; ++k) {
+      const int r0 = (int)t.ranks[k], r1 = (int)t.ranks[k + 1];
+      const int64_t rowst = t.dims[k] * r1;
+      const double *G = t.cores[k] + c[k] * r1;
+      double acc[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] = 0.0;
+      if ((r1 & 1) == 0 && aligned16) {
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          if (a < r0) {
+            const double2 *row = reinterpret_cast<const double2 *>(G + a * rowst);
+#pragma unroll
+            for (int b = 0; b < R; b += 2)
+              if (b < r1) {
+                const double2 g = __ldg(row + b / 2);
+                acc[b] += v[a] * g.x;
+                acc[b + 1] += v[a] * g.y;
+              }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+          if (a < r0) {
+            const double *row = G + a * rowst;
+#pragma unroll
+            for (int b = 0; b < R; ++b)
+              if (b < r1) acc[b] += v[a] * __ldg(row + b);
+          }
+      }
+#pragma unroll
+      for (int b = 0; b < R; ++b) v[b] = acc[b];
+    }
+    out[i] = v[0];
+  }
+}
+
 __global__ void k_first_rows(int64_t n, const int64_t *__restrict__ coords, int d, const double *core0,
                              int64_t r1, const int64_t *__restrict__ idx, double *__restrict__ V) {
   int64_t total = n * r1;
@@ -392,6 +446,19 @@ extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
   for (int k = 0; k < d; ++k) steps += (double)ranks_host[k];
   if (rmax <= 64 && d >= 4 && (double)n * steps > 4e8 && n < ((int64_t)1 << 31))
     return entries_mitm(ctx, t, coords, n, out);
+  if (rmax <= 8 && !getenv("FTT_ENTRIES_GRP")) {
+    double steps_sum = 0.0;
+    for (int k = 0; k < d; ++k) steps_sum += (double)ranks_host[k] * ranks_host[k + 1];
+    const int pb = prof_begin(ctx);
+    const int grid = grid_for(n, 256, 1, 148 * 16);
+    int al = 1;
+    for (int k = 0; k < d; ++k) al &= (((uintptr_t)cores_host[k]) & 15) == 0;
+    if (rmax <= 4) k_entries_thr<4><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out, al);
+    else k_entries_thr<8><<<grid, 256, 0, ctx->stream>>>(t, coords, n, out, al);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb, PT_ENTRIES, (double)n * (8.0 * d + 8.0), 2.0 * steps_sum * (double)n);
+    return FTT_OK;
+  }
   if (rmax <= 32) {
     const int L = rmax <= 4 ? 4 : rmax <= 8 ? 8 : rmax <= 16 ? 16 : 32;
     const int grid = grid_for(n, 8 * (32 / L), 1, 148 * 64);
