@@ -307,7 +307,7 @@ def run_ours(args):
     # ---------------- e2e through the public API (host buffers)
     e2e = None
     if not args.no_e2e:
-        h2d = a.coords.nbytes + a.values.nbytes
+        h2d = a.h2d_bytes  # canonical linear index + values (coords rebuilt on the device)
         for _ in range(2):
             a.drop_device_copy()
             ft.fasttt(a, eps=eps)

@@ -110,6 +110,12 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz,
  *   fiber_of[nnz]  fiber id of every sorted entry (may be NULL)
  *   pivot_index[nnz], values_out[nnz]  entries in fiber order
  * num_fibers_out (host) receives R. */
+/* delinearize (tensor.py:75-100): coords_out (nnz x d int64 row-major) =
+ * the C-order digits of lin[i] over dims.  The drop-in moves a canonical
+ * COO to the device as its linear index (8 B per nonzero) and rebuilds the
+ * coordinate rows here. */
+int ftt_delinearize(ftt_ctx *ctx, const int64_t *lin, int64_t nnz, int32_t d,
+                    const int64_t *dims_host, int64_t *coords_out);
 int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords,
                        const double *values, int64_t nnz, int32_t d,
                        const int64_t *dims_host, int32_t pivot,

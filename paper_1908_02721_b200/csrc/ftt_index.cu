@@ -747,6 +747,28 @@ __global__ void __launch_bounds__(256) k_linearize2(const int64_t *__restrict__ 
   }
 }
 
+// coords[i][k] = digit k of the C-order linear index lin[i] (the inverse of
+// linearize, tensor.py:75-100), magic-number divisions by the strides.
+struct DelinSpec {
+  int d;
+  int64_t stride[32];
+  uint64_t m[32];
+  int sh[32];
+};
+__global__ void k_delinearize(const int64_t *__restrict__ lin, int64_t n, DelinSpec ds,
+                              int64_t *__restrict__ coords) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = (uint64_t)lin[i];
+    int64_t *c = coords + i * ds.d;
+    for (int k = 0; k < ds.d; ++k) {
+      const uint64_t q = udiv_magic(x, ds.m[k], ds.sh[k]);
+      c[k] = (int64_t)q;
+      x -= q * (uint64_t)ds.stride[k];
+    }
+  }
+}
+
 __global__ void k_sorted_check(const uint64_t *__restrict__ k, int64_t n, int *__restrict__ bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1924,6 +1946,30 @@ int ftt_tensorize_matrix(ftt_ctx *ctx, int64_t nnz, const int64_t *rows, const i
     return FTT_ERR_INVALID;
   }
   *nnz_out = h[0];
+  return FTT_OK;
+}
+
+
+int ftt_delinearize(ftt_ctx *ctx, const int64_t *lin, int64_t nnz, int32_t d,
+                    const int64_t *dims_host, int64_t *coords_out) {
+  if (!ctx || d < 1 || d > 32 || nnz < 0) {
+    set_error("ftt_delinearize: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  FTT_CHECK(check_dims(d, dims_host, 0, false));
+  if (nnz == 0) return FTT_OK;
+  DelinSpec ds;
+  ds.d = d;
+  int64_t st = 1;
+  for (int k = d - 1; k >= 0; --k) {
+    ds.stride[k] = st;
+    st *= dims_host[k];
+  }
+  for (int k = 0; k < d; ++k) magic_u63((uint64_t)ds.stride[k], &ds.m[k], &ds.sh[k]);
+  const int pb = prof_begin(ctx);
+  k_delinearize<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(lin, nnz, ds, coords_out);
+  FTT_LAUNCHED(ctx);
+  prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 + 8.0 * d), 0.0);
   return FTT_OK;
 }
 
