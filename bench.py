@@ -254,14 +254,15 @@ def run_ours(args):
     def device_step():
         return ft.fasttt_device(a, cd, vd, eps, None, "static", None, False, 1.0, report=True)
 
+    # DMMA peak (fp64 tensor pipe) on this GPU, for the tensor-bound roofline;
+    # measured before the warm-up so its power/clock transient is absorbed
+    # by the untimed steps
+    dmma = nat.ctypes.c_double(0.0)
+    nat.check(lib.ftt_bench_dmma(ctx, 20000, nat.ctypes.byref(dmma)), "ftt_bench_dmma")
     for _ in range(max(args.warmup, 1)):
         res = device_step()
     torch.cuda.synchronize()
     ranks = res.ranks
-
-    # DMMA peak (fp64 tensor pipe) on this GPU, for the tensor-bound roofline
-    dmma = nat.ctypes.c_double(0.0)
-    nat.check(lib.ftt_bench_dmma(ctx, 20000, nat.ctypes.byref(dmma)), "ftt_bench_dmma")
 
     # ---------------- timed: device resident
     if world > 1:
