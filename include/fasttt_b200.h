@@ -312,6 +312,13 @@ int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
 int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
                 const int64_t *ranks_host, const double *const *cores_host,
                 double *norm_out);
+/* sparse_inner_error's data terms (fasttt.py:587-602) in one round trip:
+ * out_host[0] = <values, entries> over n points, out_host[1] = ||t||^2 of the
+ * train (dims / ranks / cores as ftt_tt_entries). */
+int ftt_inner_terms(ftt_ctx *ctx, int64_t n, const double *values,
+                    const double *entries, int32_t d, const int64_t *dims_host,
+                    const int64_t *ranks_host, const double *const *cores_host,
+                    double *out_host);
 
 /* ------------------------------------------------------ rounding driver */
 /* One core of the structured train handed to ftt_sweep_rounding:

@@ -89,6 +89,8 @@ SIGNATURES = {
     "ftt_delinearize": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_p],
     "ftt_sync_stats": [_c_p, ctypes.POINTER(ctypes.c_int64), _P_d],
     "ftt_tt_norm": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _P_d],
+    "ftt_inner_terms": [_c_p, _c_i64, _c_p, _c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p),
+                        _P_d],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],
 }
 _RESTYPES = {

@@ -162,6 +162,9 @@ int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in,
 constexpr int kSumSqBlocks = 148 * 8;
 int sum_squares(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_host);
 int sum_squares_dev(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_dev);
+// x . y into a device scalar (same deterministic reduction; partial as above)
+int dot_dev(ftt_ctx *ctx, int64_t n, const double *x, const double *y, double *partial,
+            double *out_dev);
 
 // Exclusive scan of int64 block counts (small arrays, single block).
 int scan_block_counts(ftt_ctx *ctx, int64_t *counts, int64_t nblocks, int64_t *total_dev);

@@ -542,13 +542,9 @@ extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
 // 198-203): W_0 = [1]; per core G (a x n x b): T = W G (a x n b), W' = G^T T
 // over the (a n) rows (b x b); ||t||^2 = W_d.  Two DMMA GEMMs per core, one
 // host round trip.
-extern "C" int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
-                           const int64_t *ranks_host, const double *const *cores_host,
-                           double *norm_out) {
-  if (!ctx || !norm_out || d < 1 || d > 32) {
-    set_error("ftt_tt_norm: invalid train");
-    return FTT_ERR_INVALID;
-  }
+// ||t||^2 into the device scalar out_dev (no host round trip).
+static int tt_norm2_dev(ftt_ctx *ctx, int32_t d, const int64_t *dims_host, const int64_t *ranks_host,
+                        const double *const *cores_host, double *out_dev) {
   int64_t wmax = 1, tmax = 1;
   size_t ske = 1;
   for (int k = 0; k < d; ++k) {
@@ -574,13 +570,47 @@ extern "C" int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
     FTT_CHECK(gemm(ctx, 0, 1, b, b, a * n, 1.0, T, b, cores_host[k], b, 0.0, W[cur ^ 1], b, sk, ske));
     cur ^= 1;
   }
-  double v = 0.0;
-  FTT_CHECK(copy_to_host(ctx, &v, W[cur], sizeof(double)));
+  FTT_CUDA(cudaMemcpyAsync(out_dev, W[cur], sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   owned_free(ctx, W[0]);
   owned_free(ctx, W[1]);
   owned_free(ctx, T);
   owned_free(ctx, sk);
+  return FTT_OK;
+}
+
+extern "C" int ftt_tt_norm(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
+                           const int64_t *ranks_host, const double *const *cores_host,
+                           double *norm_out) {
+  if (!ctx || !norm_out || d < 1 || d > 32) {
+    set_error("ftt_tt_norm: invalid train");
+    return FTT_ERR_INVALID;
+  }
+  double *dev = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 64));
+  FTT_CHECK(tt_norm2_dev(ctx, d, dims_host, ranks_host, cores_host, dev));
+  double v = 0.0;
+  FTT_CHECK(copy_to_host(ctx, &v, dev, sizeof(double)));
+  owned_free(ctx, dev);
   *norm_out = std::sqrt(std::max(v, 0.0));
+  return FTT_OK;
+}
+
+// The three terms of sparse_inner_error (fasttt.py:587-602) with one host
+// round trip: out_host[0] = <values, entries>, out_host[1] = ||t||^2.
+extern "C" int ftt_inner_terms(ftt_ctx *ctx, int64_t n, const double *values,
+                               const double *entries, int32_t d, const int64_t *dims_host,
+                               const int64_t *ranks_host, const double *const *cores_host,
+                               double *out_host) {
+  if (!ctx || !out_host || d < 1 || d > 32 || n < 0) {
+    set_error("ftt_inner_terms: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  double *dev = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(kSumSqBlocks + 4)));
+  FTT_CHECK(dot_dev(ctx, n, values, entries, dev + 2, dev));
+  FTT_CHECK(tt_norm2_dev(ctx, d, dims_host, ranks_host, cores_host, dev + 1));
+  FTT_CHECK(copy_to_host(ctx, out_host, dev, 2 * sizeof(double)));
+  owned_free(ctx, dev);
   return FTT_OK;
 }
 

@@ -1178,6 +1178,20 @@ int sum_squares(ftt_ctx *ctx, int64_t n, const double *x, double *partial, doubl
 }
 
 // The same, leaving the total in device memory (*out_dev; 0 for n <= 0).
+int dot_dev(ftt_ctx *ctx, int64_t n, const double *x, const double *y, double *partial,
+            double *out_dev) {
+  if (n <= 0) {
+    FTT_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), ctx->stream));
+    return FTT_OK;
+  }
+  int nb = grid_for(n, 256, 4, kSumSqBlocks);
+  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, y, partial);
+  FTT_LAUNCHED(ctx);
+  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, out_dev);
+  FTT_LAUNCHED(ctx);
+  return FTT_OK;
+}
+
 int sum_squares_dev(ftt_ctx *ctx, int64_t n, const double *x, double *partial, double *out_dev) {
   if (n <= 0) {
     FTT_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), ctx->stream));

@@ -529,7 +529,7 @@ def _as_dense(c):
     return c.dense() if isinstance(c, (SideCore, SparsePivotCore)) else c
 
 
-def _structured_train(df, sw: DeviceSweeps, lazy_pivot: bool = False):
+def _structured_train(df, sw: DeviceSweeps, lazy_pivot: bool = False, na2=None):
     d = len(df.dims)
     cores = [None] * d
     for k, (kept, rp) in enumerate(sw.left):
@@ -540,9 +540,10 @@ def _structured_train(df, sw: DeviceSweeps, lazy_pivot: bool = False):
     if lazy_pivot:
         spc = SparsePivotCore(df, sw)
         if spc.density < _SPARSE_PIVOT_DENSITY and df.pivot < d - 1:
-            # ||pivot core||_F = ||values||_2 (fasttt.py:359-361)
+            # ||pivot core||_F = ||values||_2 (fasttt.py:359-361); the caller's
+            # sum of squares of the input values when it has one
             cores[df.pivot] = spc
-            return cores, math.sqrt(device_dot(df.values, None))
+            return cores, math.sqrt(na2 if na2 is not None else device_dot(df.values, None))
     pc, norm = _pivot_core(df, sw)
     cores[df.pivot] = pc
     return cores, norm
@@ -975,9 +976,18 @@ def _inner_error_device(coords_d, values_d, nnz, approx_d, na2=None):
     if na2 == 0.0:
         return 0.0 if dev_tt_norm(approx_d) == 0.0 else math.inf
     ent = dev_tt_entries(approx_d, coords_d)
-    dot = device_dot(values_d, ent)
-    nb = dev_tt_norm(approx_d)
-    return math.sqrt(max(na2 - 2.0 * dot + nb * nb, 0.0) / na2)
+    # <a, b> and |b|^2 with one host round trip (ftt_inner_terms)
+    d = len(approx_d)
+    cs = [c.contiguous() for c in approx_d]
+    dims = [int(c.shape[1]) for c in cs]
+    ranks = [int(cs[0].shape[0])] + [int(c.shape[2]) for c in cs]
+    ptrs = (nat.ctypes.c_void_p * d)(*[c.data_ptr() for c in cs])
+    terms = (nat.ctypes.c_double * 2)()
+    nat.check(nat.lib().ftt_inner_terms(nat.context(), int(values_d.numel()), nat.ptr(values_d),
+                                        nat.ptr(ent), d, nat.i64_array(dims), nat.i64_array(ranks),
+                                        ptrs, terms), "ftt_inner_terms")
+    dot, nb2 = float(terms[0]), max(float(terms[1]), 0.0)
+    return math.sqrt(max(na2 - 2.0 * dot + nb2, 0.0) / na2)
 
 
 def sparse_inner_error(a: SparseTensor, approx: TTTensor) -> float:
@@ -1079,7 +1089,8 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
         raise ValueError("inconsistent fiber index pointers")
     sw = index_sweeps_device(df)
     ranks_lossless = _lossless_ranks_from(sw, d)
-    cores, pnorm = _structured_train(df, sw, lazy_pivot=mode != "fixed_rank")
+    na2 = device_dot(values_d, None) if report else None
+    cores, pnorm = _structured_train(df, sw, lazy_pivot=mode != "fixed_rank", na2=na2)
     budget = TruncationBudget(eps=eps, pivot=pivot, mode=mode, fixed_ranks=fixed_ranks)
     if mode == "fixed_rank":
         policy = _Trunc("fixed", d, targets=_fixed_targets(budget, dims))
@@ -1094,7 +1105,8 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
     res = DeviceResult(cores=out, pivot=pivot, mode=mode, eps=eps, num_fibers=df.R,
                        ranks_lossless=ranks_lossless, ranks=ranks, notes=notes, zero=zero)
     if report:
-        na2 = device_dot(values_d, None)
+        if na2 is None:
+            na2 = device_dot(values_d, None)
         norm_a = math.sqrt(na2)
         inner = _inner_error_device(coords_d, values_d, nnz, out, na2)
         exact_shapes = [tuple(c.shape) for c in cores]
