@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(256) k_group_count(const uint64_t *__restrict_
   extern __shared__ unsigned long long tab[];  // GC_SLOTS
   __shared__ int64_t s_start, s_end;
   __shared__ unsigned long long s_cnt;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t c0 = (int64_t)blockIdx.x * GC_L;
   auto grp = [&](int64_t i) -> uint64_t { return sm_div(K[i], mT, shT); };
   // first group start >= c0 and >= c0 + L: the CTA tests 256 consecutive

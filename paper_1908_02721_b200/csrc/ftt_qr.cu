@@ -45,12 +45,6 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&acc)[32], int l
   return acc[0];
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-  return v;
-}
-
 // Factor the mp x jb panel (jb <= 32) at A (lda).  partials: gridDim.x * PSLOTS.
 __global__ void __launch_bounds__(PT) k_panel(int64_t mp, int jb, double *__restrict__ A,
                                               int64_t lda, double *__restrict__ tau,
@@ -143,25 +137,6 @@ __global__ void k_extract_v(int64_t mp, int jb, const double *__restrict__ A, in
   }
 }
 
-// dlarft('F','C'): T upper triangular from VtV = V^T V and tau (one block).
-__global__ void k_larft(int nb, const double *__restrict__ VtV, int64_t ldg,
-                        const double *__restrict__ tau, double *__restrict__ T, int64_t ldt) {
-  const int r = threadIdx.x;
-  for (int64_t e = r; e < (int64_t)nb * nb; e += blockDim.x) T[(e % nb) + (e / nb) * ldt] = 0.0;
-  __syncthreads();
-  for (int i = 0; i < nb; ++i) {
-    double ti = tau[i];
-    double v = 0.0;
-    if (r < i && ti != 0.0) {
-      for (int l = r; l < i; ++l) v += T[r + (int64_t)l * ldt] * VtV[l + (int64_t)i * ldg];
-      v = -ti * v;
-    }
-    __syncthreads();
-    if (r < i) T[r + (int64_t)i * ldt] = v;
-    if (r == i) T[i + (int64_t)i * ldt] = ti;
-    __syncthreads();
-  }
-}
 
 // Blocked dlarft for nb <= 128 in one CTA of 1024 threads, T staged in
 // shared memory: 32x32 diagonal blocks by the scalar recurrence (one warp

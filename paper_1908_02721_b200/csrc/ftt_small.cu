@@ -430,7 +430,6 @@ __global__ void __launch_bounds__(256) k_tsqr_expand(int64_t M, int n, int r, in
 }
 
 constexpr size_t kSmemCapBytes = 200 * 1024;
-constexpr int kCapElems = (int)(kSmemCapBytes / 8);
 
 int nmax_for(int n) { return n <= 8 ? 8 : n <= 16 ? 16 : n <= 24 ? 24 : n <= 32 ? 32 : n <= 48 ? 48 : 64; }
 

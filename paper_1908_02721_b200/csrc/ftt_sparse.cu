@@ -173,10 +173,15 @@ __global__ void __launch_bounds__(256) k_spmm_seg(int64_t nA, int kr, int ldq, i
     for (int j = 0; j < KR; ++j) acc[j] = 0.0;
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const double w = v[e];
-      const double *q = Qr + (int64_t)ridx[e] * ldq;
+      // Q row as 16-byte pairs (ldq even; entries kr..ldq-1 of a row are zero)
+      const double2 *q = reinterpret_cast<const double2 *>(Qr + (int64_t)ridx[e] * ldq);
 #pragma unroll
-      for (int j = 0; j < KR; ++j)
-        if (j < kr) acc[j] += w * q[j];
+      for (int j = 0; j < KR; j += 2)
+        if (j < kr) {
+          const double2 t = __ldg(q + j / 2);
+          acc[j] += w * t.x;
+          acc[j + 1] += w * t.y;
+        }
     }
 #pragma unroll
     for (int j = 0; j < KR; ++j) {
@@ -306,12 +311,16 @@ __global__ void __launch_bounds__(256) k_sp_resid_on(int64_t nnz, int kr, int ld
   const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(nnz, e0 + per);
   double acc = 0.0;
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const double *q = Qr + (int64_t)ridx[e] * ldq;
+    const double2 *q = reinterpret_cast<const double2 *>(Qr + (int64_t)ridx[e] * ldq);
     const double *bc = B + (int64_t)cidx[e] * kr;
     double qb = 0.0;
 #pragma unroll
-    for (int j = 0; j < KR; ++j)
-      if (j < kr) qb += q[j] * bc[j];
+    for (int j = 0; j < KR; j += 2)
+      if (j < kr) {
+        const double2 t = __ldg(q + j / 2);
+        qb += t.x * bc[j];
+        if (j + 1 < kr) qb += t.y * bc[j + 1];
+      }
     const double d = v[e] - qb;
     acc += d * d;
   }

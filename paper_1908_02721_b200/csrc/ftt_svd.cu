@@ -164,7 +164,6 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
   auto &rqq = sm.rqq;
   auto &rpq = sm.rpq;
   auto &col = sm.col;
-  auto &s_round_any = sm.s_round_any;
   const int tid = threadIdx.x;
   __syncthreads();  // the previous pair of this CTA is done with sm
   int ba, bb;
