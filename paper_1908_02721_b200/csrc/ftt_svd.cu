@@ -79,30 +79,60 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-constexpr int LPT = 64 * 32 / 256;  // chunk elements per thread (CH * JP / JT)
+// Column streams of a pair go through a NSTAGE-deep cp.async pipeline: a
+// stage is one 64-row chunk of the pair's 32 columns stored column-major
+// with a 68-double column stride (16-byte aligned; the DMMA fragment reads
+// of both the Gram and the rotation hit every bank pair at most twice, the
+// minimum for 32 doubles).  Deep pipelining is what the pair loop needs:
+// one CTA per SM streams ~1.3 MB per column pass, and a single chunk in
+// flight left it latency bound at ~1.3 TB/s over the GPU.
+constexpr int NSTAGE = 4;
+constexpr int CHS = CH + 4;
+constexpr int STAGE_ELEMS = JP * CHS;
+constexpr size_t JAC_DYN_BYTES = sizeof(double) * NSTAGE * STAGE_ELEMS;
+static_assert(NSTAGE * STAGE_ELEMS >= (JT / 32) * 10 * 64, "Gram partials fit the stages");
 
-// One 64-row chunk of the pair's 32 columns: all LPT loads issued back to
-// back into registers (memory-level parallelism), stored to smem later so
-// the next chunk's loads overlap the current chunk's MMAs.
-__device__ __forceinline__ void chunk_load(double (&pre)[LPT], const double *__restrict__ M,
-                                           int64_t r0, int64_t n, int64_t ld, const int *col,
-                                           int tid) {
-#pragma unroll
-  for (int q = 0; q < LPT; ++q) {
-    const int e = q * 256 + tid;
-    const int c = e >> 6, r = e & 63;
-    const int64_t row = r0 + r;
-    const int cc = col[c];
-    pre[q] = (cc >= 0 && row < n) ? __ldcg(M + row + (int64_t)cc * ld) : 0.0;
-  }
+__device__ __forceinline__ void cp_async16(double *smem, const double *gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int STRIDE>
-__device__ __forceinline__ void chunk_store(const double (&pre)[LPT], double (*S)[STRIDE], int tid) {
+// Issue the copies of rows [r0, r0 + CH) of the pair's columns into one
+// stage (zero-filled past `rows` and for padding columns).
+__device__ __forceinline__ void chunk_issue(double *stage, const double *__restrict__ M, int64_t r0,
+                                            int64_t rows, int64_t ld, const int *col, int tid,
+                                            bool vec16) {
+  if (vec16) {
 #pragma unroll
-  for (int q = 0; q < LPT; ++q) {
-    const int e = q * 256 + tid;
-    S[e & 63][e >> 6] = pre[q];
+    for (int q = 0; q < CH * JP / 2 / JT; ++q) {
+      const int e = q * JT + tid;
+      const int c = e >> 5, seg = e & 31;
+      const int64_t row = r0 + 2 * seg;
+      const int cc = col[c];
+      const int bytes = (cc < 0 || row >= rows) ? 0 : (row + 1 < rows ? 16 : 8);
+      cp_async16(stage + c * CHS + 2 * seg, bytes ? M + row + (int64_t)cc * ld : M, bytes);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < CH * JP / JT; ++q) {
+      const int e = q * JT + tid;
+      const int c = e >> 6, r = e & 63;
+      const int64_t row = r0 + r;
+      const int cc = col[c];
+      const int bytes = (cc < 0 || row >= rows) ? 0 : 8;
+      cp_async8(stage + c * CHS + r, bytes ? M + row + (int64_t)cc * ld : M, bytes);
+    }
   }
 }
 
@@ -130,7 +160,6 @@ __device__ __forceinline__ void pair_of(int nblk, int step, int c, int *a, int *
 struct JacSmem {
   double G[JP][JP + 1];
   double Z[JP][JP + 1];
-  double S[CH][JP + 4];  // row stride 36 doubles == 8 banks: conflict-free DMMA fragments
   double rc[16], rs[16], rt[16], rpp[16], rqq[16], rpq[16];
   int col[JP];
   int s_round_any;
@@ -153,10 +182,9 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
                             double *__restrict__ P, int64_t ldp,
                             int nblk, int step, int pc, double tol, double floor,
                             unsigned long long *__restrict__ rotated, JacSmem &sm,
-                            const JacTrack *track = nullptr) {
+                            double *__restrict__ stages, const JacTrack *track = nullptr) {
   auto &G = sm.G;
   auto &Z = sm.Z;
-  auto &S = sm.S;
   auto &rc = sm.rc;
   auto &rs = sm.rs;
   auto &rt = sm.rt;
@@ -189,45 +217,69 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
     col[tid] = cidx < n ? cidx : -1;
   }
   __syncthreads();
-  // ---- Gram of the pair's current columns on the DMMA pipe: 16 8x8 tiles,
-  // two per warp, K = the n rows streamed through shared memory in chunks
+  // ---- Gram of the pair's current columns on the DMMA pipe.  Only the 10
+  // upper 8x8 tiles are formed; warp w takes k-steps w and w + 8 of every
+  // 64-row chunk for all 10 tiles (4 fragment loads feed 10 MMAs), and the
+  // eight partial Grams are summed in fixed warp order afterwards.
   const int lane = tid & 31, warp = tid >> 5;
   const int gi = tid >> 3;          // convergence test: row of G
   const int gj = (tid & 7) * 4;     //   and 4 consecutive columns
+  const bool vx16 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && !(ldx & 1);
+  const int64_t nchX = (mX + CH - 1) / CH;
   {
-    double gacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    double pre[LPT];
-    chunk_load(pre, X, 0, mX, ldx, col, tid);
-    for (int64_t r0 = 0; r0 < mX; r0 += CH) {
-      chunk_store(pre, S, tid);
-      __syncthreads();
-      if (r0 + CH < mX) chunk_load(pre, X, r0 + CH, mX, ldx, col, tid);  // in flight during the MMAs
-#pragma unroll 4
-      for (int k0 = 0; k0 < CH; k0 += 4) {
+    double gacc[10][2];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int ti = (2 * warp + t) >> 2, tj = (2 * warp + t) & 3;
-          double a = S[k0 + (lane & 3)][ti * 8 + (lane >> 2)];
-          double b = S[k0 + (lane & 3)][tj * 8 + (lane >> 2)];
-          dmma(gacc[t][0], gacc[t][1], a, b);
-        }
-      }
-      __syncthreads();
+    for (int t = 0; t < 10; ++t) gacc[t][0] = gacc[t][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NSTAGE - 1; ++c) {
+      if (c < nchX) chunk_issue(stages + c * STAGE_ELEMS, X, c * CH, mX, ldx, col, tid, vx16);
+      cp_async_commit();
     }
+    for (int64_t c = 0; c < nchX; ++c) {
+      cp_async_wait<NSTAGE - 2>();
+      __syncthreads();
+      if (c + NSTAGE - 1 < nchX)
+        chunk_issue(stages + ((c + NSTAGE - 1) % NSTAGE) * STAGE_ELEMS, X, (c + NSTAGE - 1) * CH,
+                    mX, ldx, col, tid, vx16);
+      cp_async_commit();
+      const double *Sb = stages + (c % NSTAGE) * STAGE_ELEMS;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int ti = (2 * warp + t) >> 2, tj = (2 * warp + t) & 3;
-      G[ti * 8 + (lane >> 2)][tj * 8 + 2 * (lane & 3)] = gacc[t][0];
-      G[ti * 8 + (lane >> 2)][tj * 8 + 2 * (lane & 3) + 1] = gacc[t][1];
+      for (int kk = 0; kk < 2; ++kk) {
+        const int k = (warp + 8 * kk) * 4 + (lane & 3);
+        double f[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) f[t] = Sb[(t * 8 + (lane >> 2)) * CHS + k];
+        int idx = 0;
+#pragma unroll
+        for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+          for (int tj = ti; tj < 4; ++tj, ++idx) dmma(gacc[idx][0], gacc[idx][1], f[ti], f[tj]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    double *part = stages;  // [warp][tile][64]
+#pragma unroll
+    for (int t = 0; t < 10; ++t) {
+      part[(warp * 10 + t) * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = gacc[t][0];
+      part[(warp * 10 + t) * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = gacc[t][1];
+    }
+    __syncthreads();
+    for (int e = tid; e < 640; e += JT) {
+      const int t = e >> 6, w = e & 63;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < JT / 32; ++q) v += part[(q * 10 + t) * 64 + w];
+      const int ti = t < 4 ? 0 : t < 7 ? 1 : t < 9 ? 2 : 3;
+      const int tj = ti + t - (ti == 0 ? 0 : ti == 1 ? 4 : ti == 2 ? 7 : 9);
+      const int i = ti * 8 + (w >> 3), j = tj * 8 + (w & 7);
+      if (i <= j) {
+        G[i][j] = v;
+        G[j][i] = v;
+      }
     }
   }
   for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = (e / JP == e % JP) ? 1.0 : 0.0;
-  __syncthreads();
-  // the two triangles come from different DMMA tiles; use the upper one for both
-  for (int e = tid; e < JP * JP; e += JT) {
-    int i = e / JP, j = e % JP;
-    if (j < i) G[i][j] = G[j][i];
-  }
   __syncthreads();
   // ---- fresh convergence test
   int need = 0;
@@ -328,10 +380,10 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
     double v = 0.0;
 #pragma unroll 8
     for (int r = 0; r < JP; ++r) v += Z[i][r] * G[r][j];
-    S[i][j] = 1.5 * Z[i][j] - 0.5 * v;
+    stages[e] = 1.5 * Z[i][j] - 0.5 * v;
   }
   __syncthreads();
-  for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = S[e / JP][e % JP];
+  for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = stages[e];
   __syncthreads();
   if (tid == 0) atomicAdd(rotated, 1ull);
   // ---- apply Z to the pair's columns of X and P on the DMMA pipe: warp w
@@ -346,44 +398,51 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
     double *M = mat == 0 ? X : P;
     const int64_t rows = mat == 0 ? mX : n;
     const int64_t ld = mat == 0 ? ldx : ldp;
-    double pre[LPT];
-    chunk_load(pre, M, 0, rows, ld, col, tid);
-    for (int64_t r0 = 0; r0 < rows; r0 += CH) {
-      chunk_store(pre, S, tid);
+    const bool v16 = ((reinterpret_cast<uintptr_t>(M) & 15) == 0) && !(ld & 1);
+    const int64_t nch = (rows + CH - 1) / CH;
+    __syncthreads();  // stages free (Newton-Schulz scratch / previous matrix)
+#pragma unroll
+    for (int c = 0; c < NSTAGE - 1; ++c) {
+      if (c < nch) chunk_issue(stages + c * STAGE_ELEMS, M, c * CH, rows, ld, col, tid, v16);
+      cp_async_commit();
+    }
+    for (int64_t c = 0; c < nch; ++c) {
+      cp_async_wait<NSTAGE - 2>();
       __syncthreads();
-      if (r0 + CH < rows) chunk_load(pre, M, r0 + CH, rows, ld, col, tid);
+      if (c + NSTAGE - 1 < nch)
+        chunk_issue(stages + ((c + NSTAGE - 1) % NSTAGE) * STAGE_ELEMS, M, (c + NSTAGE - 1) * CH,
+                    rows, ld, col, tid, v16);
+      cp_async_commit();
+      const double *Sb = stages + (c % NSTAGE) * STAGE_ELEMS;
       double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        double a = S[warp * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+        const double a = Sb[(ks * 4 + (lane & 3)) * CHS + warp * 8 + (lane >> 2)];
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[j][0], acc[j][1], a, bz[j][ks]);
       }
-      __syncwarp();
+      // rows of this chunk are read only from the stage: write straight back
+      const int64_t row = c * CH + warp * 8 + (lane >> 2);
+      if (row < rows) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        S[warp * 8 + (lane >> 2)][j * 8 + 2 * (lane & 3)] = acc[j][0];
-        S[warp * 8 + (lane >> 2)][j * 8 + 2 * (lane & 3) + 1] = acc[j][1];
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = col[j * 8 + 2 * (lane & 3) + h];
+            if (cc >= 0) M[row + (int64_t)cc * ld] = acc[j][h];
+          }
       }
-      __syncthreads();
-      for (int e = tid; e < CH * JP; e += JT) {
-        int c = e / CH, r = e % CH;
-        int64_t row = r0 + r;
-        int cc = col[c];
-        if (cc >= 0 && row < rows) M[row + (int64_t)cc * ld] = S[r][c];
-      }
-      __syncthreads();
     }
+    cp_async_wait<0>();
   }
 }
-
 
 // Whole Jacobi iteration in one cooperative launch: sweeps x steps x pairs
 // with a grid barrier between steps; the sweep's rotation count decides
 // convergence on the device (no host round trip per sweep).  counters
 // [max_sweeps] must be zero; status[0] receives the sweeps used (or -1).
 // X is mX x n (ld ldx), P is n x n (ld ldp).
-__global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, int64_t mX,
+__global__ void __launch_bounds__(JT, 2) k_jacobi_persistent(int64_t n, int64_t mX,
                                                           double *__restrict__ X, int64_t ldx,
                                                           double *__restrict__ P, int64_t ldp,
                                                           int nblk, double tol, double floor,
@@ -393,13 +452,14 @@ __global__ void __launch_bounds__(JT) k_jacobi_persistent(int64_t n, int64_t mX,
                                                           int *__restrict__ last_mod,
                                                           int *__restrict__ last_ok) {
   __shared__ JacSmem sm;
+  extern __shared__ __align__(16) double jac_stages[];
   cg::grid_group grid = cg::this_grid();
   const int npairs = nblk / 2;
   for (int sw = 0; sw < max_sweeps; ++sw) {
     for (int step = 0; step < nblk - 1; ++step) {
       const JacTrack track{last_mod, last_ok, sw * (nblk - 1) + step};
       for (int pc = blockIdx.x; pc < npairs; pc += gridDim.x)
-        jacobi_pair(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, &track);
+        jacobi_pair(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, jac_stages, &track);
       grid.sync();
     }
     const unsigned long long rot = *((volatile unsigned long long *)(counters + sw));
@@ -719,7 +779,9 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     static int coresident = 0;
     if (!coresident) {
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_persistent, JT, 0);
+      FTT_CUDA(cudaFuncSetAttribute(k_jacobi_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)JAC_DYN_BYTES));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_persistent, JT, JAC_DYN_BYTES);
       coresident = std::max(1, per_sm) * ctx->num_sms;
     }
     int G = std::min(nblk / 2, coresident);
@@ -738,7 +800,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
                     &status, &last_mod, &last_ok};
     const int pb = prof_begin(ctx);
     FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_persistent, dim3(G), dim3(JT), args,
-                                         0, ctx->stream));
+                                         JAC_DYN_BYTES, ctx->stream));
     FTT_LAUNCHED(ctx);
     int sw_used = 0;
     FTT_CHECK(copy_to_host(ctx, &sw_used, status, sizeof(int)));
