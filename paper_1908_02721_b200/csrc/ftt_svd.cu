@@ -72,6 +72,7 @@ constexpr int CH = 64;      // rows per staged chunk
 // 2064 x 766 operand, 1 inner sweep = 23 outer sweeps / 97 ms, 3 = 21 / 153 ms.
 constexpr int MAX_INNER = 3;
 __device__ int g_max_inner = 1;  // A/B knob FTT_JINNER (1..3)
+int g_last_csize = 1;             // debug print only
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -90,7 +91,8 @@ constexpr int NSTAGE = 4;
 constexpr int CHS = CH + 4;
 constexpr int STAGE_ELEMS = JP * CHS;
 constexpr size_t JAC_DYN_BYTES = sizeof(double) * NSTAGE * STAGE_ELEMS;
-static_assert(NSTAGE * STAGE_ELEMS >= (JT / 32) * 10 * 64, "Gram partials fit the stages");
+constexpr int JAC_GP_OFF = (JT / 32) * 10 * 64;  // Gram of this CTA, after the warp partials
+static_assert(NSTAGE * STAGE_ELEMS >= JAC_GP_OFF + JP * JP, "Gram partials fit the stages");
 
 __device__ __forceinline__ void cp_async16(double *smem, const double *gmem, int bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -182,7 +184,8 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
                             double *__restrict__ P, int64_t ldp,
                             int nblk, int step, int pc, double tol, double floor,
                             unsigned long long *__restrict__ rotated, JacSmem &sm,
-                            double *__restrict__ stages, const JacTrack *track = nullptr) {
+                            double *__restrict__ stages, int crank, int csize,
+                            const JacTrack *track = nullptr) {
   auto &G = sm.G;
   auto &Z = sm.Z;
   auto &rc = sm.rc;
@@ -225,22 +228,32 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
   const int gi = tid >> 3;          // convergence test: row of G
   const int gj = (tid & 7) * 4;     //   and 4 consecutive columns
   const bool vx16 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && !(ldx & 1);
-  const int64_t nchX = (mX + CH - 1) / CH;
+  // row slice of this CTA within its cluster (whole 64-row chunks)
+  auto slice = [&](int64_t rows, int64_t *c_lo, int64_t *c_hi) {
+    const int64_t nch = (rows + CH - 1) / CH, per = (nch + csize - 1) / csize;
+    *c_lo = min(nch, per * crank);
+    *c_hi = min(nch, per * (crank + 1));
+  };
+  int64_t gx0, gx1;
+  slice(mX, &gx0, &gx1);
+  const int64_t nchX = gx1 - gx0;
+  const double *Xs = X + gx0 * CH;  // rows of the slice start here
+  const int64_t mXs = min(mX - gx0 * CH, nchX * CH);
   {
     double gacc[10][2];
 #pragma unroll
     for (int t = 0; t < 10; ++t) gacc[t][0] = gacc[t][1] = 0.0;
 #pragma unroll
     for (int c = 0; c < NSTAGE - 1; ++c) {
-      if (c < nchX) chunk_issue(stages + c * STAGE_ELEMS, X, c * CH, mX, ldx, col, tid, vx16);
+      if (c < nchX) chunk_issue(stages + c * STAGE_ELEMS, Xs, c * CH, mXs, ldx, col, tid, vx16);
       cp_async_commit();
     }
     for (int64_t c = 0; c < nchX; ++c) {
       cp_async_wait<NSTAGE - 2>();
       __syncthreads();
       if (c + NSTAGE - 1 < nchX)
-        chunk_issue(stages + ((c + NSTAGE - 1) % NSTAGE) * STAGE_ELEMS, X, (c + NSTAGE - 1) * CH,
-                    mX, ldx, col, tid, vx16);
+        chunk_issue(stages + ((c + NSTAGE - 1) % NSTAGE) * STAGE_ELEMS, Xs, (c + NSTAGE - 1) * CH,
+                    mXs, ldx, col, tid, vx16);
       cp_async_commit();
       const double *Sb = stages + (c % NSTAGE) * STAGE_ELEMS;
 #pragma unroll
@@ -265,6 +278,10 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
       part[(warp * 10 + t) * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = gacc[t][1];
     }
     __syncthreads();
+    // this CTA's Gram (both triangles) -> Gp (in the stages, past the
+    // partials); with a cluster the members' Gp are summed in rank order, so
+    // every member holds the bitwise same G
+    double *Gp = stages + JAC_GP_OFF;
     for (int e = tid; e < 640; e += JT) {
       const int t = e >> 6, w = e & 63;
       double v = 0.0;
@@ -274,9 +291,22 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
       const int tj = ti + t - (ti == 0 ? 0 : ti == 1 ? 4 : ti == 2 ? 7 : 9);
       const int i = ti * 8 + (w >> 3), j = tj * 8 + (w & 7);
       if (i <= j) {
-        G[i][j] = v;
-        G[j][i] = v;
+        Gp[i * JP + j] = v;
+        Gp[j * JP + i] = v;
       }
+    }
+    if (csize > 1) {
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();
+      for (int e = tid; e < JP * JP; e += JT) {
+        double v = 0.0;
+        for (int r = 0; r < csize; ++r) v += cl.map_shared_rank(Gp, r)[e];
+        G[e / JP][e % JP] = v;
+      }
+      cl.sync();  // members' Gp no longer read
+    } else {
+      __syncthreads();
+      for (int e = tid; e < JP * JP; e += JT) G[e / JP][e % JP] = Gp[e];
     }
   }
   for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = (e / JP == e % JP) ? 1.0 : 0.0;
@@ -292,10 +322,10 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
     }
   }
   if (!__syncthreads_or(need)) {
-    if (track && tid == 0) track->last_ok[pidx] = track->t;
+    if (track && tid == 0 && crank == 0) track->last_ok[pidx] = track->t;
     return;
   }
-  if (track && tid == 0) {
+  if (track && tid == 0 && crank == 0) {
     track->last_mod[ba] = track->t;
     track->last_mod[bb] = track->t;
   }
@@ -385,7 +415,7 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
   __syncthreads();
   for (int e = tid; e < JP * JP; e += JT) Z[e / JP][e % JP] = stages[e];
   __syncthreads();
-  if (tid == 0) atomicAdd(rotated, 1ull);
+  if (tid == 0 && crank == 0) atomicAdd(rotated, 1ull);
   // ---- apply Z to the pair's columns of X and P on the DMMA pipe: warp w
   // owns rows 8w..8w+7 of every 64-row chunk (4 output tiles), the Z
   // fragments stay in registers for the whole pair
@@ -396,10 +426,13 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
     for (int ks = 0; ks < 8; ++ks) bz[j][ks] = Z[ks * 4 + (lane & 3)][j * 8 + (lane >> 2)];
   for (int mat = 0; mat < 2; ++mat) {
     double *M = mat == 0 ? X : P;
-    const int64_t rows = mat == 0 ? mX : n;
     const int64_t ld = mat == 0 ? ldx : ldp;
     const bool v16 = ((reinterpret_cast<uintptr_t>(M) & 15) == 0) && !(ld & 1);
-    const int64_t nch = (rows + CH - 1) / CH;
+    int64_t c0, c1;
+    slice(mat == 0 ? mX : n, &c0, &c1);
+    M += c0 * CH;
+    const int64_t rows = min((mat == 0 ? mX : n) - c0 * CH, (c1 - c0) * CH);
+    const int64_t nch = c1 - c0;
     __syncthreads();  // stages free (Newton-Schulz scratch / previous matrix)
 #pragma unroll
     for (int c = 0; c < NSTAGE - 1; ++c) {
@@ -446,7 +479,7 @@ __global__ void __launch_bounds__(JT, 2) k_jacobi_persistent(int64_t n, int64_t 
                                                           double *__restrict__ X, int64_t ldx,
                                                           double *__restrict__ P, int64_t ldp,
                                                           int nblk, double tol, double floor,
-                                                          int max_sweeps,
+                                                          int max_sweeps, int csize,
                                                           unsigned long long *__restrict__ counters,
                                                           int *__restrict__ status,
                                                           int *__restrict__ last_mod,
@@ -455,11 +488,14 @@ __global__ void __launch_bounds__(JT, 2) k_jacobi_persistent(int64_t n, int64_t 
   extern __shared__ __align__(16) double jac_stages[];
   cg::grid_group grid = cg::this_grid();
   const int npairs = nblk / 2;
+  // csize CTAs (one cluster, or csize == 1) share a pair, each on a row slice
+  const int cid = blockIdx.x / csize, crank = blockIdx.x % csize, ncl = gridDim.x / csize;
   for (int sw = 0; sw < max_sweeps; ++sw) {
     for (int step = 0; step < nblk - 1; ++step) {
       const JacTrack track{last_mod, last_ok, sw * (nblk - 1) + step};
-      for (int pc = blockIdx.x; pc < npairs; pc += gridDim.x)
-        jacobi_pair(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, jac_stages, &track);
+      for (int pc = cid; pc < npairs; pc += ncl)
+        jacobi_pair(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, jac_stages,
+                    crank, csize, &track);
       grid.sync();
     }
     const unsigned long long rot = *((volatile unsigned long long *)(counters + sw));
@@ -784,7 +820,43 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_persistent, JT, JAC_DYN_BYTES);
       coresident = std::max(1, per_sm) * ctx->num_sms;
     }
-    int G = std::min(nblk / 2, coresident);
+    // Pairs are split over a cluster of csize CTAs (row slices, DSMEM Gram
+    // sum) when there are fewer pairs than co-resident CTAs: each slice
+    // keeps >= 3 chunks of 64 rows (config 4: 4-CTA clusters 165 -> 131 ms).  FTT_JCLUSTER=c forces c (1 = off).
+    const int npairs = nblk / 2;
+    static const int cs_env = getenv("FTT_JCLUSTER") ? atoi(getenv("FTT_JCLUSTER")) : 0;
+    int csize = cs_env > 0 ? std::min(8, cs_env)
+                           : (int)std::max<int64_t>(1, std::min<int64_t>({8, coresident / std::max(1, npairs),
+                                                                          ceil_div(mX, CH) / 3}));
+    int G = std::min(npairs, coresident);
+    cudaLaunchAttribute lattr[2];
+    lattr[0].id = cudaLaunchAttributeCooperative;
+    lattr[0].val.cooperative = 1;
+    lattr[1].id = cudaLaunchAttributeClusterDimension;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(JT);
+    cfg.dynamicSmemBytes = JAC_DYN_BYTES;
+    cfg.stream = ctx->stream;
+    cfg.attrs = lattr;
+    cfg.numAttrs = 1;
+    if (csize > 1) {
+      lattr[1].val.clusterDim.x = csize;
+      lattr[1].val.clusterDim.y = 1;
+      lattr[1].val.clusterDim.z = 1;
+      cfg.numAttrs = 2;
+      cfg.gridDim = dim3(npairs * csize);
+      int maxc = 0;
+      if (cudaOccupancyMaxActiveClusters(&maxc, (const void *)k_jacobi_persistent, &cfg) != cudaSuccess ||
+          maxc < 1) {
+        cudaGetLastError();
+        csize = 1;
+        cfg.numAttrs = 1;
+      } else {
+        G = std::min(npairs, maxc) * csize;
+      }
+    }
+    cfg.gridDim = dim3(G);
+    g_last_csize = csize;
     int64_t nA_ = nA, mX_ = mX;
     double *Y = st->Y, *Pm = st->P;
     int nblk_ = nblk;
@@ -796,11 +868,10 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     int *last_mod = track_buf;
     int *last_ok = track_buf + nblk;
     FTT_CUDA(cudaMemsetAsync(track_buf, 0xff, sizeof(int) * (size_t)nblk * (nblk + 1), ctx->stream));
-    void *args[] = {&nA_, &mX_, &Y, &mX_, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &cnt,
+    void *args[] = {&nA_, &mX_, &Y, &mX_, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &csize, &cnt,
                     &status, &last_mod, &last_ok};
     const int pb = prof_begin(ctx);
-    FTT_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_persistent, dim3(G), dim3(JT), args,
-                                         JAC_DYN_BYTES, ctx->stream));
+    FTT_CUDA(cudaLaunchKernelExC(&cfg, (const void *)k_jacobi_persistent, args));
     FTT_LAUNCHED(ctx);
     int sw_used = 0;
     FTT_CHECK(copy_to_host(ctx, &sw_used, status, sizeof(int)));
@@ -824,6 +895,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     fprintf(stderr, "[ftt] svd m=%lld n=%lld (mA=%lld nA=%lld%s) qr %.3f ms jacobi %.3f ms sweeps %d",
             (long long)m, (long long)n, (long long)mA, (long long)nA, st->direct ? " direct" : "",
             qr_ms, jac_ms, st->sweeps);
+    fprintf(stderr, " cluster %d", g_last_csize);
     if (st->sweeps > 0) {
       std::vector<unsigned long long> cnt(st->sweeps);
       cudaMemcpy(cnt.data(), rot, 8 * st->sweeps, cudaMemcpyDeviceToHost);
