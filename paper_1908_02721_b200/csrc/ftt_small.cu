@@ -506,14 +506,18 @@ Tree make_tree(int64_t M, int n, int64_t root_rows_max) {
 // column length m looped by the lanes.  For the small inner SVDs of the
 // low-rank path (B^T, e.g. 512 x 8) this replaces a TSQR tree + Jacobi on R^T
 // + Q expansion (5 launches) by one launch.
+// wpp warps per column pair: each forms partial dots over its rows, the
+// pair's partials are summed in warp order (every warp of the pair gets the
+// bitwise same rotation), then each warp rotates its own rows.
 __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const double *__restrict__ A,
-                                                          int64_t lda, int trans,
+                                                          int64_t lda, int trans, int wpp,
                                                           double *__restrict__ Yo,
                                                           double *__restrict__ Po,
                                                           double *__restrict__ norms,
                                                           int max_sweeps, int *__restrict__ status) {
   extern __shared__ double S[];  // X m x n (ld m) | P n x n
   __shared__ double red[SVD_NT / 32];
+  __shared__ double s_dot[SVD_NT / 32][3];
   __shared__ int s_any;
   double *X = S;
   double *P = S + (size_t)m * n;
@@ -536,18 +540,19 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const do
   const double tol = kEps * sqrt((double)n);
   const double floor = 0.01 * kEps * kEps * (double)m * fro2;
   const int ne = n + (n & 1), npairs = ne / 2;
+  const int pi = warp / wpp, sub = warp - pi * wpp;  // nw == npairs * wpp
   int sweeps = -1;
   for (int sw = 0; sw < max_sweeps && n > 1; ++sw) {
     if (tid == 0) s_any = 0;
     __syncthreads();
     for (int round = 0; round < ne - 1; ++round) {
-      for (int pi = warp; pi < npairs; pi += nw) {
-        int p, q;
-        rr_pair(ne, round, pi, &p, &q);
-        if (p >= n || q >= n) continue;
-        double *xp = X + (size_t)p * m, *xq = X + (size_t)q * m;
+      int p, q;
+      rr_pair(ne, round, pi, &p, &q);
+      const bool live = pi < npairs && p < n && q < n;
+      double *xp = X + (size_t)(live ? p : 0) * m, *xq = X + (size_t)(live ? q : 0) * m;
+      if (live) {
         double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = lane; i < m; i += 32) {
+        for (int i = sub * 32 + lane; i < m; i += 32 * wpp) {
           const double u = xp[i], v = xq[i];
           a += u * u;
           b += v * v;
@@ -559,23 +564,39 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const do
           b += __shfl_xor_sync(0xffffffffu, b, o);
           g += __shfl_xor_sync(0xffffffffu, g, o);
         }
+        if (lane == 0) {
+          s_dot[warp][0] = a;
+          s_dot[warp][1] = b;
+          s_dot[warp][2] = g;
+        }
+      }
+      __syncthreads();
+      if (live) {
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int w = pi * wpp; w < pi * wpp + wpp; ++w) {
+          a += s_dot[w][0];
+          b += s_dot[w][1];
+          g += s_dot[w][2];
+        }
         if (a > floor && b > floor && fabs(g) > tol * sqrt(a * b)) {
           const double zeta = (b - a) / (2.0 * g);
           const double t = copysign(1.0 / (fabs(zeta) + sqrt(1.0 + zeta * zeta)), zeta);
           const double c = rsqrt(1.0 + t * t);
           const double sn = c * t;
-          for (int i = lane; i < m; i += 32) {
+          for (int i = sub * 32 + lane; i < m; i += 32 * wpp) {
             const double u = xp[i], v = xq[i];
             xp[i] = c * u - sn * v;
             xq[i] = sn * u + c * v;
           }
-          double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
-          if (lane < n) {
-            const double pu = pp[lane], pv = pq[lane];
-            pp[lane] = c * pu - sn * pv;
-            pq[lane] = sn * pu + c * pv;
+          if (sub == 0) {
+            double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
+            if (lane < n) {
+              const double pu = pp[lane], pv = pq[lane];
+              pp[lane] = c * pu - sn * pv;
+              pq[lane] = sn * pu + c * pv;
+            }
+            if (lane == 0) s_any = 1;
           }
-          if (lane == 0) s_any = 1;
         }
       }
       __syncthreads();
@@ -792,10 +813,15 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
   FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n)));
   int *status = reinterpret_cast<int *>(dev);
   FTT_CUDA(cudaMemsetAsync(status, 0, 16, ctx->stream));
-  const int jt = 32 * std::max(1, std::min(SVD_NT / 32, (int)((n + 1) / 2)));
+  // warps per pair: enough that each lane holds <= ~8 rows, <= SVD_NT total
+  static const int wpp_env = getenv("FTT_DIRECT_WPP") ? atoi(getenv("FTT_DIRECT_WPP")) : 0;
+  const int npairs = (int)((n + 1) / 2);
+  int wpp = wpp_env > 0 ? wpp_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(m, 256)));
+  wpp = std::max(1, std::min(wpp, SVD_NT / 32 / std::max(1, npairs)));
+  const int jt = 32 * std::max(1, npairs) * wpp;
   const int max_sweeps = 60;
   k_jacobi_direct<<<1, jt, 8 * (size_t)(m * n + n * n), ctx->stream>>>(
-      (int)m, (int)n, A, lda, trans, Y, P, dev + 2, max_sweeps, status);
+      (int)m, (int)n, A, lda, trans, wpp, Y, P, dev + 2, max_sweeps, status);
   FTT_LAUNCHED(ctx);
   if (extra_dev)
     FTT_CUDA(cudaMemcpyAsync(dev + 1, extra_dev, sizeof(double), cudaMemcpyDeviceToDevice,
