@@ -14,6 +14,7 @@
 namespace ftt {
 
 constexpr int kNumSMs = 148;  // B200
+constexpr int kTileCnt = 65536;  // split-K tile counters per context (+64 reduction counters)
 
 void set_error(const char *fmt, ...);
 
@@ -73,6 +74,8 @@ struct ftt_ctx {
   int64_t syncs = 0;
   double sync_wait_ms = 0.0;
   int *sticky = nullptr;
+  // split-K tile arrival counters (zero between products; ftt_gemm.cu)
+  unsigned *tile_cnt = nullptr;
   // live per-class kernel timing (off by default)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;

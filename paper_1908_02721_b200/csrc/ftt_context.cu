@@ -198,7 +198,10 @@ int ftt_create(int device, void *stream, ftt_ctx **ctx_out) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ring_ev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMalloc((void **)&ctx->sticky, 64);
   if (e == cudaSuccess) e = cudaMemset(ctx->sticky, 0, 64);
+  if (e == cudaSuccess) e = cudaMalloc((void **)&ctx->tile_cnt, sizeof(unsigned) * (kTileCnt + 64));
+  if (e == cudaSuccess) e = cudaMemset(ctx->tile_cnt, 0, sizeof(unsigned) * (kTileCnt + 64));
   if (e != cudaSuccess) {
+    if (ctx->tile_cnt) cudaFree(ctx->tile_cnt);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->ring) cudaFreeHost(ctx->ring);
     if (ctx->ring_ev) cudaEventDestroy(ctx->ring_ev);
@@ -224,6 +227,7 @@ int ftt_destroy(ftt_ctx *ctx) {
   if (ctx->ring) cudaFreeHost(ctx->ring);
   if (ctx->ring_ev) cudaEventDestroy(ctx->ring_ev);
   if (ctx->sticky) cudaFree(ctx->sticky);
+  if (ctx->tile_cnt) cudaFree(ctx->tile_cnt);
   delete ctx;
   return FTT_OK;
 }

@@ -35,13 +35,43 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 // Tile TBM x TBN (64x64, 128x32 for narrow outputs, 32x128 for short ones),
 // 4 warps of 32x32 each (4x4 DMMA 8x8 tiles), BK = 16, register prefetch of
 // the next k-tile into the second shared buffer.
+// Called by every thread after thread 0 wrote this CTA's npart entry: the
+// last CTA of the grid to arrive (counter, reset by it) sums the nt
+// partials in index order into *out (replaces a separate k_sum_partials).
+__device__ __forceinline__ void last_cta_sum(const double *npart, int64_t nt, double *out,
+                                             unsigned *counter) {
+  __shared__ int s_last;
+  __shared__ double s_w[32];
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned tk = atomicAdd(counter, 1u);
+    s_last = tk == (unsigned)(nt - 1);
+    if (s_last) *counter = 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < nt; i += blockDim.x) a += __ldcg(npart + i);
+  for (int o = 16; o; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+    *out = t;
+  }
+}
+
 template <bool TA, bool TB, int EPI = 0, int TBM = 64, int TBN = 64>
 __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, double alpha,
                                               const double *__restrict__ A, int64_t lda,
                                               const double *__restrict__ B, int64_t ldb, double beta,
                                               double *__restrict__ C, int64_t ldc, int64_t kps,
                                               double *__restrict__ partial, int c_trans = 0,
-                                              double *__restrict__ npart = nullptr) {
+                                              double *__restrict__ npart = nullptr,
+                                              unsigned *__restrict__ tile_cnt = nullptr,
+                                              double *__restrict__ sum_out = nullptr) {
   constexpr int WM = TBM / 32;           // warps along M
   constexpr int RA = TBM * BK / GT;      // A-tile elements per thread
   constexpr int RB = TBN * BK / GT;      // B-tile elements per thread
@@ -174,6 +204,45 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
       }
     }
   }
+  // fused split-K reduction (tile_cnt != nullptr): the last of the tile's
+  // gridDim.z CTAs to finish sums the partials in split order (fixed
+  // association, so bit-reproducible) and resets the tile's counter
+  if (EPI == 0 && partial && tile_cnt) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned tix = blockIdx.x + blockIdx.y * gridDim.x;
+      const unsigned t = atomicAdd(tile_cnt + tix, 1u);
+      s_last = t == gridDim.z - 1;
+      if (s_last) tile_cnt[tix] = 0u;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const int rows = (int)min((int64_t)TBM, m - tm), cols = (int)min((int64_t)TBN, n - tn);
+      const int Z = (int)gridDim.z;
+      for (int e = tid; e < rows * cols; e += GT) {
+        const int c = e / rows, r = e - c * rows;
+        const int64_t row = tm + r, col = tn + c;
+        const double *pp = partial + col * m + row;
+        const int64_t zs = n * m;
+        double sacc = 0.0;
+        int z = 0;
+        for (; z + 8 <= Z; z += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp + (int64_t)(z + u) * zs);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sacc += v[u];
+        }
+        for (; z < Z; ++z) sacc += __ldcg(pp + (int64_t)z * zs);
+        double v = alpha * sacc;
+        if (beta != 0.0) v += beta * C[row + col * ldc];
+        C[row + col * ldc] = v;
+      }
+    }
+  }
   if (EPI == 1) {
     __shared__ double s_ss[GT / 32];
 #pragma unroll
@@ -185,6 +254,7 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
       for (int w = 0; w < GT / 32; ++w) t += s_ss[w];
       npart[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = t;
     }
+    if (sum_out) last_cta_sum(npart, (int64_t)gridDim.x * gridDim.y, sum_out, tile_cnt);
   }
 }
 
@@ -201,7 +271,9 @@ __global__ void __launch_bounds__(128) k_resid_rows(int64_t m, int64_t n, int k,
                                                     const double *__restrict__ B, int64_t ldb,
                                                     const double *__restrict__ R0, int64_t ldr,
                                                     int64_t tiles_per_cta,
-                                                    double *__restrict__ npart) {
+                                                    double *__restrict__ npart,
+                                                    double *__restrict__ sum_out,
+                                                    unsigned *__restrict__ counter) {
   extern __shared__ double rs_smem[];
   double(*Qs)[128 + PAD] = reinterpret_cast<double(*)[128 + PAD]>(rs_smem);       // [kp][128]
   double(*Bs)[64 + PAD] = reinterpret_cast<double(*)[64 + PAD]>(rs_smem + (size_t)kp * (128 + PAD));
@@ -262,6 +334,7 @@ __global__ void __launch_bounds__(128) k_resid_rows(int64_t m, int64_t n, int k,
   if (lane == 0) s_ss[warp] = ss;
   __syncthreads();
   if (tid == 0) npart[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = (s_ss[0] + s_ss[1]) + (s_ss[2] + s_ss[3]);
+  last_cta_sum(npart, (int64_t)gridDim.x * gridDim.y, sum_out, counter);
 }
 
 // Column-block variant for a column-major R0 (rows contiguous): a CTA owns
@@ -274,7 +347,9 @@ __global__ void __launch_bounds__(128) k_resid_cols(int64_t m, int64_t n, int k,
                                                     const double *__restrict__ B, int64_t ldb,
                                                     const double *__restrict__ R0, int64_t ldr,
                                                     int64_t rows_per_cta,
-                                                    double *__restrict__ npart) {
+                                                    double *__restrict__ npart,
+                                                    double *__restrict__ sum_out,
+                                                    unsigned *__restrict__ counter) {
   extern __shared__ double rs_smem[];
   double(*Qs)[128 + PAD] = reinterpret_cast<double(*)[128 + PAD]>(rs_smem);       // [kp][128]
   double(*Bs)[64 + PAD] = reinterpret_cast<double(*)[64 + PAD]>(rs_smem + (size_t)kp * (128 + PAD));
@@ -333,6 +408,7 @@ __global__ void __launch_bounds__(128) k_resid_cols(int64_t m, int64_t n, int k,
   if (lane == 0) s_ss[warp] = ss;
   __syncthreads();
   if (tid == 0) npart[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = (s_ss[0] + s_ss[1]) + (s_ss[2] + s_ss[3]);
+  last_cta_sum(npart, (int64_t)gridDim.x * gridDim.y, sum_out, counter);
 }
 
 // Tile shape for an m x n output: narrow outputs (n <= 32) use 128x32,
@@ -346,19 +422,6 @@ inline TileShape pick_tile(int64_t m, int64_t n) {
 }
 inline int tile_m(TileShape t) { return t == T128x32 ? 128 : (t == T32x128 ? 32 : 64); }
 inline int tile_n(TileShape t) { return t == T128x32 ? 32 : (t == T32x128 ? 128 : 64); }
-
-__global__ void k_sum_partials(const double *__restrict__ p, int64_t n, double *__restrict__ out) {
-  __shared__ double s[1024];
-  double a = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += p[i];
-  s[threadIdx.x] = a;
-  __syncthreads();
-  for (int off = blockDim.x / 2; off; off >>= 1) {
-    if ((int)threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = s[0];
-}
 
 // Deterministic split-K reduction.  Block = 64 outputs x 4 split groups:
 // thread (o, g) sums the contiguous group g of the partials of output o in
@@ -491,10 +554,19 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
   }
   dim3 grid((unsigned)tiles_m, (unsigned)tiles_n, (unsigned)splits);
   double *part = splits > 1 ? splitk_ws : nullptr;
+  // small outputs: the last CTA per tile reduces (no second launch); the
+  // serial depth stays <= ~256 loads per thread of that CTA
+  const int64_t tile_elems = std::min<int64_t>(m, tile_m(ts)) * std::min<int64_t>(n, tile_n(ts));
+  static const bool no_fuse = getenv("FTT_NO_SPLITK_FUSE") != nullptr;
+  unsigned *tcnt = (splits > 1 && !no_fuse && ctx->tile_cnt && tiles <= kTileCnt &&
+                    tile_elems * splits <= 256 * GT)
+                       ? ctx->tile_cnt
+                       : nullptr;
   const int pb = prof_begin(ctx);
 #define FTT_GEMM_LAUNCH(TA_, TB_, M_, N_)                                                     \
   k_dgemm<TA_, TB_, 0, M_, N_><<<grid, GT, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, \
-                                                            beta, C, ldc, kps, part)
+                                                            beta, C, ldc, kps, part, 0,      \
+                                                            nullptr, tcnt)
 #define FTT_GEMM_TILES(TA_, TB_)                                  \
   do {                                                            \
     if (ts == T128x32) FTT_GEMM_LAUNCH(TA_, TB_, 128, 32);        \
@@ -508,7 +580,7 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
 #undef FTT_GEMM_TILES
 #undef FTT_GEMM_LAUNCH
   FTT_LAUNCHED(ctx);
-  if (splits > 1) {
+  if (splits > 1 && !tcnt) {
     const int64_t rb = std::min<int64_t>(ceil_div(m * n, SR_OUT), 4 * (int64_t)ctx->num_sms);
     k_splitk_reduce<<<(unsigned)rb, SR_OUT * SR_GRP, 0, ctx->stream>>>(m, n, splits, part, alpha,
                                                                       beta, C, ldc);
@@ -601,17 +673,17 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
     double *npart = nullptr;
     FTT_CHECK(owned_alloc(ctx, (void **)&npart, 8 * (size_t)(nt + 1)));
     const int pb = prof_begin(ctx);
+    double *sum = out_dev ? out_dev : npart + nt;
+    unsigned *cnt = ctx->tile_cnt + kTileCnt + 1;
     if (r_trans)
       k_resid_rows<true><<<grid, 128, smem, ctx->stream>>>(m, n, (int)k, kp, A, lda, B, ldb, R0, ldr,
-                                                           per, npart);
+                                                           per, npart, sum, cnt);
     else
       k_resid_cols<<<grid, 128, smem, ctx->stream>>>(m, n, (int)k, kp, A, lda, B, ldb, R0, ldr, per,
-                                                     npart);
+                                                     npart, sum, cnt);
     FTT_LAUNCHED(ctx);
     prof_end(ctx, pb, PT_GEMM, 8.0 * ((double)m * n + (double)m * k + (double)k * n),
              2.0 * (double)m * n * k);
-    k_sum_partials<<<1, 1024, 0, ctx->stream>>>(npart, nt, out_dev ? out_dev : npart + nt);
-    FTT_LAUNCHED(ctx);
     if (out_host) FTT_CHECK(copy_to_host(ctx, out_host, npart + nt, sizeof(double)));
     owned_free(ctx, npart);
     return FTT_OK;
@@ -627,16 +699,16 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
   dim3 grid((unsigned)tiles_m, (unsigned)tiles_n, 1);
   const int64_t kps = ceil_div(std::max<int64_t>(k, 1), BK) * BK;
   double *C = const_cast<double *>(R0);
+  double *sum = out_dev ? out_dev : npart + nt;
+  unsigned *cnt = ctx->tile_cnt + kTileCnt + 1;
 #define FTT_RESID_LAUNCH(TA_, TB_)                                                              \
   k_dgemm<TA_, TB_, 1><<<grid, GT, 0, ctx->stream>>>(m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldr, \
-                                                     kps, nullptr, r_trans, npart)
+                                                     kps, nullptr, r_trans, npart, cnt, sum)
   if (!ta && !tb) FTT_RESID_LAUNCH(false, false);
   else if (!ta && tb) FTT_RESID_LAUNCH(false, true);
   else if (ta && !tb) FTT_RESID_LAUNCH(true, false);
   else FTT_RESID_LAUNCH(true, true);
 #undef FTT_RESID_LAUNCH
-  FTT_LAUNCHED(ctx);
-  k_sum_partials<<<1, 1024, 0, ctx->stream>>>(npart, nt, out_dev ? out_dev : npart + nt);
   FTT_LAUNCHED(ctx);
   if (out_host) FTT_CHECK(copy_to_host(ctx, out_host, npart + nt, sizeof(double)));
   owned_free(ctx, npart);

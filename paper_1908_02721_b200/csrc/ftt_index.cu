@@ -904,21 +904,48 @@ __global__ void k_reduce_partials(const double *partial, int nb, double *out) {
   if (threadIdx.x == 0) *out = s[0];
 }
 
-__global__ void k_dot_partial(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
-                              double *partial) {
+// Block partials of x.y (x.x when y == nullptr).  With `out` set, the last
+// block to finish (arrival counter, reset by it) also sums the partials in
+// index order into *out -- one launch instead of two, same result for the
+// same grid.
+__global__ void __launch_bounds__(256) k_dot_partial(int64_t n, const double *__restrict__ x,
+                                                     const double *__restrict__ y, double *partial,
+                                                     double *out = nullptr,
+                                                     unsigned *counter = nullptr) {
   double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     acc += x[i] * (y ? y[i] : x[i]);
   for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
   __shared__ double s[32];
+  __shared__ int s_last;
   if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
     partial[blockIdx.x] = t;
+    if (out) {
+      __threadfence();
+      const unsigned tk = atomicAdd(counter, 1u);
+      s_last = tk == gridDim.x - 1;
+      if (s_last) *counter = 0u;
+    }
   }
+  if (!out) return;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ double r[256];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) a += __ldcg(partial + i);
+  r[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off; off >>= 1) {
+    if ((int)threadIdx.x < off) r[threadIdx.x] += r[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = r[0];
 }
 
 __global__ void k_side_core(int32_t side, const int64_t *kept, int64_t K, int64_t n, int64_t ro,
@@ -1185,9 +1212,7 @@ int dot_dev(ftt_ctx *ctx, int64_t n, const double *x, const double *y, double *p
     return FTT_OK;
   }
   int nb = grid_for(n, 256, 4, kSumSqBlocks);
-  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, y, partial);
-  FTT_LAUNCHED(ctx);
-  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, out_dev);
+  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, y, partial, out_dev, ctx->tile_cnt + kTileCnt);
   FTT_LAUNCHED(ctx);
   return FTT_OK;
 }
@@ -1198,9 +1223,8 @@ int sum_squares_dev(ftt_ctx *ctx, int64_t n, const double *x, double *partial, d
     return FTT_OK;
   }
   int nb = grid_for(n, 256, 4, kSumSqBlocks);
-  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, nullptr, partial);
-  FTT_LAUNCHED(ctx);
-  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, out_dev);
+  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, nullptr, partial, out_dev,
+                                             ctx->tile_cnt + kTileCnt);
   FTT_LAUNCHED(ctx);
   return FTT_OK;
 }
@@ -1904,9 +1928,8 @@ int ftt_dot(ftt_ctx *ctx, int64_t n, const double *x, const double *y, double *o
   int nb = grid_for(n, 256, 4, 148 * 8);
   FTT_CHECK(arena_reserve(ctx, align_up(8 * (nb + 1)) + 256));
   double *partial = take<double>(ctx, nb + 1);
-  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, y, partial);
-  FTT_LAUNCHED(ctx);
-  k_reduce_partials<<<1, 1024, 0, ctx->stream>>>(partial, nb, partial + nb);
+  k_dot_partial<<<nb, 256, 0, ctx->stream>>>(n, x, y, partial, partial + nb,
+                                             ctx->tile_cnt + kTileCnt);
   FTT_LAUNCHED(ctx);
   return copy_to_host(ctx, out_host, partial + nb, sizeof(double));
 }

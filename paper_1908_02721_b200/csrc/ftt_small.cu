@@ -514,7 +514,11 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const do
                                                           double *__restrict__ Yo,
                                                           double *__restrict__ Po,
                                                           double *__restrict__ norms,
-                                                          int max_sweeps, int *__restrict__ status) {
+                                                          int max_sweeps, int *__restrict__ status,
+                                                          const double *__restrict__ extra_src,
+                                                          double *__restrict__ extra_dst) {
+  // status needs no memset: thread 0 writes both words; extra_dst receives
+  // *extra_src (a caller's device scalar riding on the same round trip)
   extern __shared__ double S[];  // X m x n (ld m) | P n x n
   __shared__ double red[SVD_NT / 32];
   __shared__ double s_dot[SVD_NT / 32][3];
@@ -532,8 +536,12 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const do
     f += v * v;
   }
   for (int e = tid; e < n * n; e += (int)blockDim.x) P[e] = (e / n == e % n) ? 1.0 : 0.0;
+  if (tid == 0 && extra_src) *extra_dst = *extra_src;
   if (__syncthreads_or(bad)) {
-    if (tid == 0) atomicOr(status, 1);
+    if (tid == 0) {
+      status[0] = 1;
+      status[1] = 0;
+    }
     return;
   }
   const double fro2 = cta_sum(f, red);
@@ -609,8 +617,8 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const do
   }
   if (n <= 1) sweeps = 1;
   if (tid == 0) {
+    status[0] = sweeps < 0 ? 2 : 0;
     status[1] = sweeps;
-    if (sweeps < 0) atomicOr(status, 2);
   }
   for (int j = warp; j < n; j += nw) {
     double s2 = 0.0;
@@ -812,7 +820,6 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
   double *dev = nullptr;  // status (2 ints) | pad | norms n
   FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n)));
   int *status = reinterpret_cast<int *>(dev);
-  FTT_CUDA(cudaMemsetAsync(status, 0, 16, ctx->stream));
   // warps per pair: enough that each lane holds <= ~8 rows, <= SVD_NT total
   static const int wpp_env = getenv("FTT_DIRECT_WPP") ? atoi(getenv("FTT_DIRECT_WPP")) : 0;
   const int npairs = (int)((n + 1) / 2);
@@ -821,11 +828,8 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
   const int jt = 32 * std::max(1, npairs) * wpp;
   const int max_sweeps = 60;
   k_jacobi_direct<<<1, jt, 8 * (size_t)(m * n + n * n), ctx->stream>>>(
-      (int)m, (int)n, A, lda, trans, wpp, Y, P, dev + 2, max_sweeps, status);
+      (int)m, (int)n, A, lda, trans, wpp, Y, P, dev + 2, max_sweeps, status, extra_dev, dev + 1);
   FTT_LAUNCHED(ctx);
-  if (extra_dev)
-    FTT_CUDA(cudaMemcpyAsync(dev + 1, extra_dev, sizeof(double), cudaMemcpyDeviceToDevice,
-                             ctx->stream));
   std::vector<double> h(n + 2);
   FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));
   if (extra_dev && extra_host) *extra_host = h[1];
