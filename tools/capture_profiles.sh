@@ -19,6 +19,9 @@ python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-c5-index > 
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-c5-index > $OUT/ncu_bench.log 2>&1
 
 # 3. per-launch DRAM traffic of one warm decomposition per config
+#    (ncu cannot replay the cooperative launch of clustered Jacobi pairs, so
+#    these captures run the Jacobi with one CTA per pair: FTT_JCLUSTER=1)
+export FTT_JCLUSTER=1
 for c in 2 5 1 4; do
   python tools/profile_step.py $c > $OUT/step_c$c.log 2>&1 &&
     $NCU --profile-from-start off \
