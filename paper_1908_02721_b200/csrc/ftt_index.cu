@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(256) k_part_count(const uint64_t *__restrict__
 constexpr int GC_L = 1024;       // nominal entries per CTA
 constexpr int GC_CAP = 2048;     // max entries per chunk (hash load <= 1/2)
 constexpr int GC_SLOTS = 4096;
+static_assert(8 * GC_CAP + 4 * GC_SLOTS <= 8 * GC_SLOTS, "keys + positions fit the dynamic smem");
 
 // Both linear keys of every nonzero in one read of the COO: C order (lin)
 // and the reversed-mode order (rlin).
@@ -791,24 +792,33 @@ __global__ void __launch_bounds__(256) k_group_count(const uint64_t *__restrict_
   __shared__ unsigned s_j[2];
   if (threadIdx.x < 2) s_j[threadIdx.x] = 0xffffffffu;
   __syncthreads();
-  for (int w = 0; w < 2; ++w) {
-    const int64_t from = c0 + (w ? GC_L : 0);
-    if (from >= n) continue;  // uniform over the CTA
-    for (int r = 0; r < GC_CAP / 256; ++r) {
-      const int j = r * 256 + (int)threadIdx.x;
-      const int64_t i = from + j;
-      const bool st = i <= n && (i == n || i == 0 || grp(i) != grp(i - 1));
-      const unsigned mj = __reduce_min_sync(0xffffffffu, st ? (unsigned)j : 0xffffffffu);
-      if (lane == 0 && mj != 0xffffffffu) atomicMin(&s_j[w], mj);
-      if (__syncthreads_or(st)) break;
+  // both windows advance together (one dependent load round for the
+  // common case of a boundary within the first 256 positions of each)
+  bool open0 = c0 < n, open1 = c0 + GC_L < n;
+  for (int r = 0; r < GC_CAP / 256 && (open0 || open1); ++r) {
+    const int j = r * 256 + (int)threadIdx.x;
+    bool st0 = false, st1 = false;
+    if (open0) {
+      const int64_t i = c0 + j;
+      st0 = i <= n && (i == n || i == 0 || grp(i) != grp(i - 1));
     }
+    if (open1) {
+      const int64_t i = c0 + GC_L + j;
+      st1 = i <= n && (i == n || grp(i) != grp(i - 1));
+    }
+    const unsigned m0 = __reduce_min_sync(0xffffffffu, st0 ? (unsigned)j : 0xffffffffu);
+    const unsigned m1 = __reduce_min_sync(0xffffffffu, st1 ? (unsigned)j : 0xffffffffu);
+    if (lane == 0 && m0 != 0xffffffffu) atomicMin(&s_j[0], m0);
+    if (lane == 0 && m1 != 0xffffffffu) atomicMin(&s_j[1], m1);
+    const int any0 = __syncthreads_or(st0);
+    const int any1 = __syncthreads_or(st1);
+    open0 = open0 && !any0;
+    open1 = open1 && !any1;
   }
   if (threadIdx.x == 0) {
     s_start = c0 >= n ? n : (s_j[0] == 0xffffffffu ? INT64_MAX : c0 + s_j[0]);
     s_end = c0 + GC_L >= n ? n : (s_j[1] == 0xffffffffu ? INT64_MAX : c0 + GC_L + s_j[1]);
   }
-  for (int e = threadIdx.x; e < GC_SLOTS; e += blockDim.x) tab[e] = ~0ull;
-  if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   const int64_t start = s_start, end = s_end;
   if (start == INT64_MAX) return;  // a long group covers the window; its owner decides
@@ -816,20 +826,41 @@ __global__ void __launch_bounds__(256) k_group_count(const uint64_t *__restrict_
     if (threadIdx.x == 0) atomicOr(flag, 1);
     return;
   }
+  // the chunk's reduced keys go to shared memory and the hash table holds
+  // 32-bit chunk positions (native 32-bit shared CAS; the 64-bit CAS is a
+  // spin loop on this part); a probe compares the stored keys
+  constexpr int PER = GC_CAP / 256;
+  uint64_t *skey = reinterpret_cast<uint64_t *>(tab);        // GC_CAP keys
+  unsigned *tab32 = reinterpret_cast<unsigned *>(skey + GC_CAP);  // GC_SLOTS positions
+  const int cnt = (int)(end - start);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = q * 256 + threadIdx.x;
+    if (j < cnt) {
+      const uint64_t k = __ldg(K + start + j);
+      const uint64_t hi = sm_div(k, mT, shT);
+      const uint64_t lo = k - sm_div(k, mS, shS) * S;
+      skey[j] = hi * S + lo;
+    }
+  }
+  for (int e = threadIdx.x; e < GC_SLOTS / 4; e += blockDim.x)
+    reinterpret_cast<uint4 *>(tab32)[e] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
   unsigned long long fresh = 0;
-  for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
-    const uint64_t k = K[i];
-    const uint64_t hi = sm_div(k, mT, shT);
-    const uint64_t lo = k - sm_div(k, mS, shS) * S;
-    const uint64_t key = hi * S + lo;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = q * 256 + threadIdx.x;
+    if (j >= cnt) break;
+    const uint64_t key = skey[j];
     uint64_t h = mix64(key) & (GC_SLOTS - 1);
     while (true) {
-      const unsigned long long old = atomicCAS(tab + h, ~0ull, (unsigned long long)key);
-      if (old == ~0ull) {
+      const unsigned old = atomicCAS(tab32 + h, ~0u, (unsigned)j);
+      if (old == ~0u) {
         ++fresh;
         break;
       }
-      if (old == key) break;
+      if (skey[old] == key) break;
       h = (h + 1) & (GC_SLOTS - 1);
     }
   }
