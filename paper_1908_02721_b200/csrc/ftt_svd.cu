@@ -355,39 +355,48 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
       }
       if (!__syncthreads_or(flag)) continue;  // barrier 1 (uniform)
       sweep_any = 1;
-      // columns: G J and Z J  (16 pairs x 32 rows, 2 matrices)
-      for (int e = tid; e < 16 * JP; e += JT) {
-        const int pr = e / JP, r = e % JP;
-        const double c = rc[pr], s = rs[pr];
-        if (s == 0.0) continue;
-        const int p = sm.tp[round][pr], q = sm.tq[round][pr];
-        double gp = G[r][p], gq = G[r][q];
-        G[r][p] = c * gp - s * gq;
-        G[r][q] = s * gp + c * gq;
-        double zp = Z[r][p], zq = Z[r][q];
-        Z[r][p] = c * zp - s * zq;
-        Z[r][q] = s * zp + c * zq;
-      }
-      __syncthreads();  // barrier 2
-      // rows: J^T G; the pair's own 2x2 block exactly (Rutishauser)
-      for (int e = tid; e < 16 * JP; e += JT) {
-        const int pr = e / JP, r = e % JP;
-        const double c = rc[pr], s = rs[pr];
-        if (s == 0.0) continue;
-        const int p = sm.tp[round][pr], q = sm.tq[round][pr];
-        if (r == p) {
-          G[p][p] = rpp[pr] - rt[pr] * rpq[pr];
-          G[q][p] = 0.0;
-        } else if (r == q) {
-          G[p][q] = 0.0;
-          G[q][q] = rqq[pr] + rt[pr] * rpq[pr];
+      // G <- J^T G J in one phase: thread (bi, bj) owns the 2x2 block of
+      // pairs bi x bj (disjoint, so no read/write overlap); the pair's own
+      // diagonal block exactly (Rutishauser).  Z <- Z J: 2 entries each.
+      {
+        static_assert(JT == 256, "one thread per 2x2 block of the 16 x 16 pairs");
+        const int bi = tid >> 4, bj = tid & 15;
+        const int p1 = sm.tp[round][bi], q1 = sm.tq[round][bi];
+        const double c1 = rc[bi], s1 = rs[bi];
+        if (bi == bj) {
+          if (s1 != 0.0) {
+            G[p1][p1] = rpp[bi] - rt[bi] * rpq[bi];
+            G[q1][q1] = rqq[bi] + rt[bi] * rpq[bi];
+            G[p1][q1] = 0.0;
+            G[q1][p1] = 0.0;
+          }
         } else {
-          double gp = G[p][r], gq = G[q][r];
-          G[p][r] = c * gp - s * gq;
-          G[q][r] = s * gp + c * gq;
+          const int p2 = sm.tp[round][bj], q2 = sm.tq[round][bj];
+          const double c2 = rc[bj], s2 = rs[bj];
+          if (s1 != 0.0 || s2 != 0.0) {
+            const double g11 = G[p1][p2], g12 = G[p1][q2], g21 = G[q1][p2], g22 = G[q1][q2];
+            const double a11 = c2 * g11 - s2 * g12, a12 = s2 * g11 + c2 * g12;
+            const double a21 = c2 * g21 - s2 * g22, a22 = s2 * g21 + c2 * g22;
+            G[p1][p2] = c1 * a11 - s1 * a21;
+            G[q1][p2] = s1 * a11 + c1 * a21;
+            G[p1][q2] = c1 * a12 - s1 * a22;
+            G[q1][q2] = s1 * a12 + c1 * a22;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = tid + h * JT;
+          const int pr = e >> 5, r = e & 31;
+          const double c = rc[pr], sn = rs[pr];
+          if (sn != 0.0) {
+            const int p = sm.tp[round][pr], q = sm.tq[round][pr];
+            const double zp = Z[r][p], zq = Z[r][q];
+            Z[r][p] = c * zp - sn * zq;
+            Z[r][q] = sn * zp + c * zq;
+          }
         }
       }
-      __syncthreads();  // barrier 3
+      __syncthreads();  // barrier 2
     }
     if (!sweep_any) break;
   }
