@@ -80,19 +80,19 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Column streams of a pair go through a NSTAGE-deep cp.async pipeline: a
+// Column streams of a pair go through an NSTAGE-deep cp.async pipeline
+// (4 stages at 2 CTAs per SM by default, 3 stages at 3 CTAs per SM): a
 // stage is one 64-row chunk of the pair's 32 columns stored column-major
 // with a 68-double column stride (16-byte aligned; the DMMA fragment reads
 // of both the Gram and the rotation hit every bank pair at most twice, the
 // minimum for 32 doubles).  Deep pipelining is what the pair loop needs:
 // one CTA per SM streams ~1.3 MB per column pass, and a single chunk in
 // flight left it latency bound at ~1.3 TB/s over the GPU.
-constexpr int NSTAGE = 4;
 constexpr int CHS = CH + 4;
 constexpr int STAGE_ELEMS = JP * CHS;
-constexpr size_t JAC_DYN_BYTES = sizeof(double) * NSTAGE * STAGE_ELEMS;
+constexpr size_t jac_dyn_bytes(int ns) { return sizeof(double) * ns * STAGE_ELEMS; }
 constexpr int JAC_GP_OFF = (JT / 32) * 10 * 64;  // Gram of this CTA, after the warp partials
-static_assert(NSTAGE * STAGE_ELEMS >= JAC_GP_OFF + JP * JP, "Gram partials fit the stages");
+static_assert(3 * STAGE_ELEMS >= JAC_GP_OFF + JP * JP, "Gram partials fit the stages");
 
 __device__ __forceinline__ void cp_async16(double *smem, const double *gmem, int bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -179,7 +179,9 @@ struct JacTrack {
   int t;  // global step index (sweep * (nblk - 1) + step)
 };
 
-// n columns; X is mX x n (ld ldx), P is n x n (ld ldp).
+// n columns; X is mX x n (ld ldx), P is n x n (ld ldp).  NSTAGE-deep
+// column pipeline.
+template <int NSTAGE>
 __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64_t ldx,
                             double *__restrict__ P, int64_t ldp,
                             int nblk, int step, int pc, double tol, double floor,
@@ -484,7 +486,8 @@ __device__ void jacobi_pair(int64_t n, int64_t mX, double *__restrict__ X, int64
 // convergence on the device (no host round trip per sweep).  counters
 // [max_sweeps] must be zero; status[0] receives the sweeps used (or -1).
 // X is mX x n (ld ldx), P is n x n (ld ldp).
-__global__ void __launch_bounds__(JT, 2) k_jacobi_persistent(int64_t n, int64_t mX,
+template <int NS>
+__global__ void __launch_bounds__(JT, NS == 4 ? 2 : 3) k_jacobi_persistent(int64_t n, int64_t mX,
                                                           double *__restrict__ X, int64_t ldx,
                                                           double *__restrict__ P, int64_t ldp,
                                                           int nblk, double tol, double floor,
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(JT, 2) k_jacobi_persistent(int64_t n, int64_t 
     for (int step = 0; step < nblk - 1; ++step) {
       const JacTrack track{last_mod, last_ok, sw * (nblk - 1) + step};
       for (int pc = cid; pc < npairs; pc += ncl)
-        jacobi_pair(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, jac_stages,
+        jacobi_pair<NS>(n, mX, X, ldx, P, ldp, nblk, step, pc, tol, floor, counters + sw, sm, jac_stages,
                     crank, csize, &track);
       grid.sync();
     }
@@ -821,30 +824,45 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
       }
       inner_set = true;
     }
-    static int coresident = 0;
+    static int coresident = 0, coresident3 = 0;
     if (!coresident) {
-      int per_sm = 0;
-      FTT_CUDA(cudaFuncSetAttribute(k_jacobi_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)JAC_DYN_BYTES));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_persistent, JT, JAC_DYN_BYTES);
+      int per_sm = 0, per_sm3 = 0;
+      FTT_CUDA(cudaFuncSetAttribute(k_jacobi_persistent<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)jac_dyn_bytes(4)));
+      FTT_CUDA(cudaFuncSetAttribute(k_jacobi_persistent<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)jac_dyn_bytes(3)));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_persistent<4>, JT, jac_dyn_bytes(4));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k_jacobi_persistent<3>, JT, jac_dyn_bytes(3));
       coresident = std::max(1, per_sm) * ctx->num_sms;
+      coresident3 = std::max(1, per_sm3) * ctx->num_sms;
     }
     // Pairs are split over a cluster of csize CTAs (row slices, DSMEM Gram
     // sum) when there are fewer pairs than co-resident CTAs: each slice
-    // keeps >= 3 chunks of 64 rows (config 4: 4-CTA clusters 165 -> 131 ms).  FTT_JCLUSTER=c forces c (1 = off).
+    // keeps >= 3 chunks of 64 rows (config 4: 4-CTA clusters 165 -> 131 ms).
+    // Between coresident/2 and coresident3/2 pairs (e.g. config 3's 154) the
+    // 3-stage / 3-CTAs-per-SM variant runs 2-CTA clusters instead of leaving
+    // a few SMs with two whole pairs (~10 % per sweep).  FTT_JCLUSTER=c
+    // forces c (1 = off).
     const int npairs = nblk / 2;
     static const int cs_env = getenv("FTT_JCLUSTER") ? atoi(getenv("FTT_JCLUSTER")) : 0;
     int csize = cs_env > 0 ? std::min(8, cs_env)
                            : (int)std::max<int64_t>(1, std::min<int64_t>({8, coresident / std::max(1, npairs),
                                                                           ceil_div(mX, CH) / 3}));
-    int G = std::min(npairs, coresident);
+    int ns = 4;
+    if (cs_env <= 0 && csize == 1 && 2 * npairs > coresident && 2 * npairs <= coresident3 &&
+        ceil_div(mX, CH) >= 6) {
+      ns = 3;
+      csize = 2;
+    }
+    const void *kfn = ns == 4 ? (const void *)k_jacobi_persistent<4> : (const void *)k_jacobi_persistent<3>;
+    int G = std::min(npairs, ns == 4 ? coresident : coresident3);
     cudaLaunchAttribute lattr[2];
     lattr[0].id = cudaLaunchAttributeCooperative;
     lattr[0].val.cooperative = 1;
     lattr[1].id = cudaLaunchAttributeClusterDimension;
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(JT);
-    cfg.dynamicSmemBytes = JAC_DYN_BYTES;
+    cfg.dynamicSmemBytes = jac_dyn_bytes(ns);
     cfg.stream = ctx->stream;
     cfg.attrs = lattr;
     cfg.numAttrs = 1;
@@ -855,7 +873,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
       cfg.numAttrs = 2;
       cfg.gridDim = dim3(npairs * csize);
       int maxc = 0;
-      if (cudaOccupancyMaxActiveClusters(&maxc, (const void *)k_jacobi_persistent, &cfg) != cudaSuccess ||
+      if (cudaOccupancyMaxActiveClusters(&maxc, kfn, &cfg) != cudaSuccess ||
           maxc < 1) {
         cudaGetLastError();
         csize = 1;
@@ -880,7 +898,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     void *args[] = {&nA_, &mX_, &Y, &mX_, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &csize, &cnt,
                     &status, &last_mod, &last_ok};
     const int pb = prof_begin(ctx);
-    FTT_CUDA(cudaLaunchKernelExC(&cfg, (const void *)k_jacobi_persistent, args));
+    FTT_CUDA(cudaLaunchKernelExC(&cfg, kfn, args));
     FTT_LAUNCHED(ctx);
     int sw_used = 0;
     FTT_CHECK(copy_to_host(ctx, &sw_used, status, sizeof(int)));
