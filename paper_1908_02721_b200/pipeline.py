@@ -1124,6 +1124,18 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
     return res
 
 
+def _cores_to_host(cores):
+    """D2H of the final cores into pinned host buffers (torch's caching host
+    allocator), one stream sync for all of them.  ``.cpu()`` lands in fresh
+    pageable memory: 0.9 s instead of 34 ms for config 3's 1.9 GB of cores."""
+    torch = _torch()
+    host = [torch.empty(tuple(c.shape), dtype=c.dtype, pin_memory=True) for c in cores]
+    for h, c in zip(host, cores):
+        h.copy_(c, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in host]
+
+
 def fasttt(a: SparseTensor, eps: float | None = 1e-14, pivot: int | None = None,
            mode: str = "static", fixed_ranks=None, precise_pivot: bool = False,
            c_svd: float = 1.0):
@@ -1147,7 +1159,7 @@ def fasttt(a: SparseTensor, eps: float | None = 1e-14, pivot: int | None = None,
             eps_actual_method="exact", eps_actual_inner=0.0, flops_fasttt_model=0.0,
             flops_ttsvd_model=0.0, wall_time_s=time.perf_counter() - wall0,
             cpu_time_s=time.process_time() - cpu0, warnings=tuple(res.notes))
-    tt = TTTensor([c.cpu().numpy() for c in res.cores], copy=False)
+    tt = TTTensor(_cores_to_host(res.cores), copy=False)
     report = DecompositionReport(
         shape=a.shape, nnz=a.nnz, pivot=res.pivot, mode=mode, eps=eps, num_fibers=res.num_fibers,
         ranks_lossless=res.ranks_lossless, ranks=tt.ranks[1:-1], eps_actual=res.eps_actual,
