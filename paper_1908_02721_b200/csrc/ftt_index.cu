@@ -1094,9 +1094,13 @@ int bit_length(uint64_t x) {
 // Shared driver for the per-pass onesweep kernels once keys + histograms
 // exist.  keys[0]/vals[0] hold the input; the result pointer is returned in
 // *kres / *vres (one of the two ping-pong buffers).
+// kin/vin (optional): the first executed pass reads these instead of
+// keys[0]/vals[0]; kout/vout (optional): the last executed pass writes there
+// (no staging copies in or out of the ping-pong buffers).
 int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t n, int num_passes,
                     uint32_t *ghist, uint32_t *status, uint32_t *counters, uint64_t **kres,
-                    uint32_t **vres) {
+                    uint32_t **vres, const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
+                    uint32_t *vout) {
   // decide which passes are needed (constant digit -> skip)
   static thread_local std::vector<uint32_t> h;
   h.assign((size_t)num_passes * RADIX, 0);
@@ -1107,38 +1111,61 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
   // items per thread were 13 % / 50 % / 140 % slower per pass)
   const int tile = RS_TILE;
   int64_t ntiles = ceil_div(n, tile);
-  int cur = 0;
+  std::vector<int> active;
   for (int p = 0; p < num_passes; ++p) {
     bool trivial = false;
     for (int b = 0; b < RADIX; ++b)
       if ((int64_t)h[(size_t)p * RADIX + b] == n) trivial = true;
-    if (trivial) continue;
+    if (!trivial) active.push_back(p);
+  }
+  const bool has_vals = vals[0] != nullptr;
+  if (active.empty()) {  // already ordered: the input is the result
+    if (kin && kout) {
+      FTT_CUDA(cudaMemcpyAsync(kout, kin, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      if (has_vals && vin && vout)
+        FTT_CUDA(cudaMemcpyAsync(vout, vin, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      *kres = kout;
+      *vres = has_vals ? (vout ? vout : const_cast<uint32_t *>(vin)) : nullptr;
+    } else {
+      *kres = kin ? const_cast<uint64_t *>(kin) : keys[0];
+      *vres = has_vals ? (vin ? const_cast<uint32_t *>(vin) : vals[0]) : nullptr;
+    }
+    return FTT_OK;
+  }
+  int cur = 0;
+  const uint64_t *ksrc = kin ? kin : keys[0];
+  const uint32_t *vsrc = vin ? vin : vals[0];
+  for (size_t a = 0; a < active.size(); ++a) {
+    const int p = active[a];
+    const bool last = a + 1 == active.size();
+    uint64_t *kdst = (last && kout) ? kout : keys[cur ^ 1];
+    uint32_t *vdst = has_vals ? ((last && vout) ? vout : vals[cur ^ 1]) : nullptr;
     FTT_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * ntiles * RADIX, ctx->stream));
     FTT_CUDA(cudaMemsetAsync(counters + p, 0, sizeof(uint32_t), ctx->stream));
     static bool attr_set = false;
     if (!attr_set) {
-      const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true>, a, 12 * RS_TILE));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false>, a, 12 * RS_TILE));
+      const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true>, at, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false>, at, 12 * RS_TILE));
       attr_set = true;
     }
     const int pb = prof_begin(ctx);
-    if (vals[0]) {
+    if (has_vals) {
       k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
-          keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, ghist + p * RADIX, status,
-          counters + p);
+          ksrc, vsrc, kdst, vdst, n, 8 * p, ghist + p * RADIX, status, counters + p);
     } else {
       k_onesweep<false><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
-          keys[cur], nullptr, keys[cur ^ 1], nullptr, n, 8 * p, ghist + p * RADIX, status,
-          counters + p);
+          ksrc, nullptr, kdst, nullptr, n, 8 * p, ghist + p * RADIX, status, counters + p);
     }
     FTT_LAUNCHED(ctx);
     // algorithmic bytes: read + write every key (and payload) once
-    prof_end(ctx, pb, PT_SORT, (double)n * (vals[0] ? 24.0 : 16.0), 0.0);
+    prof_end(ctx, pb, PT_SORT, (double)n * (has_vals ? 24.0 : 16.0), 0.0);
+    ksrc = kdst;
+    vsrc = vdst;
     cur ^= 1;
   }
-  *kres = keys[cur];
-  *vres = vals[cur];
+  *kres = const_cast<uint64_t *>(ksrc);
+  *vres = has_vals ? const_cast<uint32_t *>(vsrc) : nullptr;
   return FTT_OK;
 }
 
@@ -1215,17 +1242,21 @@ int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in, u
     set_error("radix_sort: arena reservation too small");
     return FTT_ERR_INVALID;
   }
-  FTT_CUDA(cudaMemcpyAsync(kb[0], keys_in, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-  if (vals_in)
-    FTT_CUDA(cudaMemcpyAsync(vb[0], vals_in, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   FTT_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
-  k_hist<<<grid_for(n, 256, 8), 256, 0, ctx->stream>>>(kb[0], n, num_passes, ghist, nullptr);
+  k_hist<<<grid_for(n, 256, 8), 256, 0, ctx->stream>>>(keys_in, n, num_passes, ghist, nullptr);
   FTT_LAUNCHED(ctx);
+  // first pass reads the caller's arrays, last pass writes the caller's
   uint64_t *kr;
   uint32_t *vr;
-  FTT_CHECK(onesweep_passes(ctx, kb, vb, n, num_passes, ghist, status, counters, &kr, &vr));
-  FTT_CUDA(cudaMemcpyAsync(keys_out, kr, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
-  if (vals_out && vr)
+  // (an in-place call keeps the staging: a pass must not scatter into the
+  // array it reads)
+  uint64_t *ko = keys_out == keys_in ? nullptr : keys_out;
+  uint32_t *vo = (vals_out && vals_out == vals_in) ? nullptr : vals_out;
+  FTT_CHECK(onesweep_passes(ctx, kb, vb, n, num_passes, ghist, status, counters, &kr, &vr, keys_in,
+                            vals_in, ko, vo));
+  if (kr != keys_out)
+    FTT_CUDA(cudaMemcpyAsync(keys_out, kr, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (vals_out && vr && vr != vals_out)
     FTT_CUDA(cudaMemcpyAsync(vals_out, vr, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
   return FTT_OK;
 }
@@ -1297,7 +1328,8 @@ static int sort_coords(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t
   FTT_LAUNCHED(ctx);
   // read the COO coordinates, write one key (+ identity payload) per nonzero
   prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0 + (include_pivot ? 4.0 : 0.0)), 0.0);
-  return onesweep_passes(ctx, kb, vb, nnz, num_passes, ghist, status, counters, kres, vres);
+  return onesweep_passes(ctx, kb, vb, nnz, num_passes, ghist, status, counters, kres, vres, nullptr,
+                         nullptr, nullptr, nullptr);
 }
 
 static size_t sort_coords_bytes(int64_t nnz, bool with_perm) {
