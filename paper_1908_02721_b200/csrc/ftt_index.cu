@@ -1132,6 +1132,9 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
     }
     return FTT_OK;
   }
+  // one look-back status region per executed pass (<= 8), cleared at once
+  FTT_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * active.size() * ntiles * RADIX, ctx->stream));
+  FTT_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * 8, ctx->stream));
   int cur = 0;
   const uint64_t *ksrc = kin ? kin : keys[0];
   const uint32_t *vsrc = vin ? vin : vals[0];
@@ -1140,8 +1143,7 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
     const bool last = a + 1 == active.size();
     uint64_t *kdst = (last && kout) ? kout : keys[cur ^ 1];
     uint32_t *vdst = has_vals ? ((last && vout) ? vout : vals[cur ^ 1]) : nullptr;
-    FTT_CUDA(cudaMemsetAsync(status, 0, sizeof(uint32_t) * ntiles * RADIX, ctx->stream));
-    FTT_CUDA(cudaMemsetAsync(counters + p, 0, sizeof(uint32_t), ctx->stream));
+    uint32_t *st = status + a * ntiles * RADIX;
     static bool attr_set = false;
     if (!attr_set) {
       const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -1152,10 +1154,10 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
     const int pb = prof_begin(ctx);
     if (has_vals) {
       k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
-          ksrc, vsrc, kdst, vdst, n, 8 * p, ghist + p * RADIX, status, counters + p);
+          ksrc, vsrc, kdst, vdst, n, 8 * p, ghist + p * RADIX, st, counters + p);
     } else {
       k_onesweep<false><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
-          ksrc, nullptr, kdst, nullptr, n, 8 * p, ghist + p * RADIX, status, counters + p);
+          ksrc, nullptr, kdst, nullptr, n, 8 * p, ghist + p * RADIX, st, counters + p);
     }
     FTT_LAUNCHED(ctx);
     // algorithmic bytes: read + write every key (and payload) once
@@ -1171,7 +1173,7 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
 
 size_t onesweep_scratch(int64_t n) {
   int64_t ntiles = ceil_div(n, RS_MIN_TILE);
-  return align_up(sizeof(uint32_t) * 8 * RADIX) + align_up(sizeof(uint32_t) * ntiles * RADIX) +
+  return align_up(sizeof(uint32_t) * 8 * RADIX) + align_up(sizeof(uint32_t) * 8 * ntiles * RADIX) +
          align_up(sizeof(uint32_t) * 8);
 }
 
@@ -1230,7 +1232,7 @@ int radix_sort(ftt_ctx *ctx, const uint64_t *keys_in, const uint32_t *vals_in, u
   int num_passes = (end_bit + 7) / 8;
   if (num_passes < 1) num_passes = 1;
   uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
-  uint32_t *status = take<uint32_t>(ctx, ceil_div(n, RS_MIN_TILE) * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, 8 * ceil_div(n, RS_MIN_TILE) * RADIX);
   uint32_t *counters = take<uint32_t>(ctx, 8);
   uint64_t *kb[2] = {take<uint64_t>(ctx, n), take<uint64_t>(ctx, n)};
   uint32_t *vb[2] = {nullptr, nullptr};
@@ -1309,7 +1311,7 @@ static int sort_coords(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t
   int num_passes = (end_bit + 7) / 8;
   if (num_passes < 1) num_passes = 1;
   uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
-  uint32_t *status = take<uint32_t>(ctx, ceil_div(nnz, RS_MIN_TILE) * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, 8 * ceil_div(nnz, RS_MIN_TILE) * RADIX);
   uint32_t *counters = take<uint32_t>(ctx, 8);
   uint64_t *kb[2] = {take<uint64_t>(ctx, nnz), take<uint64_t>(ctx, nnz)};
   uint32_t *vb[2] = {nullptr, nullptr};
