@@ -568,7 +568,8 @@ __global__ void k_gather_cols(int64_t rows, int64_t src_rows, int64_t r, const d
 // _fix_signs (linalg.py:56-63): first argmax |U[:, j]|; flip U[:, j] and
 // V[:, j] if that entry is negative; then optionally V[:, j] *= s[j].
 // k_sign_pick: one CTA per column decides the sign (fixed-order tree);
-// k_sign_apply: grid (rank, chunks) rescales the rows.
+// k_sign_apply: grid (rank, chunks) rescales the rows (wide factors);
+// k_sign_write: sign + layout in one pass (rank <= 32).
 __global__ void k_sign_pick(int64_t mu, const double *__restrict__ U, int64_t ldu,
                             double *__restrict__ fac) {
   const int64_t j = blockIdx.x;
@@ -598,6 +599,33 @@ __global__ void k_sign_pick(int64_t mu, const double *__restrict__ U, int64_t ld
     __syncthreads();
   }
   if (threadIdx.x == 0) fac[j] = U[si[0] + j * ldu] < 0.0 ? -1.0 : 1.0;
+}
+
+// Sign rule + output layout in one pass: U_out = U fac, V_out = V fac
+// (times sigma with scale_v), each written column- or row-major into the
+// caller's buffer (replaces k_sign_apply + a transpose/copy per factor).
+__global__ void k_sign_write(int64_t mu, int64_t mv, int64_t rank, const double *__restrict__ U,
+                             const double *__restrict__ V, const double *__restrict__ fac,
+                             const double *__restrict__ sig, int scale_v, double *__restrict__ Uo,
+                             int64_t ldu, int u_row_major, double *__restrict__ Vo, int64_t ldv,
+                             int v_row_major) {
+  const int64_t nu = Uo ? mu * rank : 0, nv = Vo ? mv * rank : 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nu + nv;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < nu) {
+      // row-major destination: consecutive threads write consecutive columns
+      const int64_t i = u_row_major ? e / rank : e % mu, j = u_row_major ? e % rank : e / mu;
+      const double v = fac[j] * U[i + j * mu];
+      if (u_row_major) Uo[j + i * ldu] = v;
+      else Uo[i + j * ldu] = v;
+    } else {
+      const int64_t f = e - nu;
+      const int64_t i = v_row_major ? f / rank : f % mv, j = v_row_major ? f % rank : f / mv;
+      const double v = fac[j] * (scale_v ? sig[j] : 1.0) * V[i + j * mv];
+      if (v_row_major) Vo[j + i * ldv] = v;
+      else Vo[i + j * ldv] = v;
+    }
+  }
 }
 
 __global__ void k_sign_apply(int64_t mu, int64_t mv, double *__restrict__ U, int64_t ldu,
@@ -1237,24 +1265,21 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
     return FTT_ERR_INVALID;
   }
   if (rank == 0) return FTT_OK;
-  double *UA = nullptr, *VA = nullptr;
+  double *UA = nullptr, *VA = nullptr, *UAi = nullptr, *VAi = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&UA, 8 * (size_t)mA * rank));
-  FTT_CHECK(owned_alloc(ctx, (void **)&VA, 8 * (size_t)nA * rank));
   if (st->lowrank) {
-    // A_tall ~= Qk B with B = U_B S V_B^T  =>  U_A = Qk U_B, V_A = V_B
+    // A_tall ~= Qk B with B = U_B S V_B^T  =>  U_A = Qk U_B, V_A = V_B (used
+    // in place in the inner state's output, no copy)
     SvdState *in = st->inner;
-    double *UAi = nullptr, *VAi = nullptr;
     FTT_CHECK(owned_alloc(ctx, (void **)&UAi, 8 * (size_t)in->mA * rank));
     FTT_CHECK(owned_alloc(ctx, (void **)&VAi, 8 * (size_t)in->nA * rank));
     FTT_CHECK(svd_raw_vectors(ctx, in, rank, UAi, VAi));
     const int64_t k = in->m;  // B is k x nA
     double *UB = in->transposed ? VAi : UAi;  // k x rank
-    double *VB = in->transposed ? UAi : VAi;  // nA x rank
+    VA = in->transposed ? UAi : VAi;          // nA x rank
     FTT_CHECK(gemm(ctx, 0, 0, mA, rank, k, 1.0, st->Qk, mA, UB, k, 0.0, UA, mA, nullptr, 0));
-    FTT_CHECK(copy_matrix(ctx, nA, rank, VB, nA, VA, nA));
-    owned_free(ctx, UAi);
-    owned_free(ctx, VAi);
   } else {
+    FTT_CHECK(owned_alloc(ctx, (void **)&VA, 8 * (size_t)nA * rank));
     FTT_CHECK(svd_raw_vectors(ctx, st, rank, UA, VA));
   }
   double *UM = st->transposed ? VA : UA;
@@ -1268,20 +1293,38 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
     FTT_CHECK(stage_to_device(ctx, sig2, st->sigma.data(), 8 * rank));
     k_sign_pick<<<(unsigned)rank, 256, 0, ctx->stream>>>(mu, UM, mu, fac);
     FTT_LAUNCHED(ctx);
-    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(std::max(mu, mv), 4096)));
-    k_sign_apply<<<dim3((unsigned)rank, (unsigned)nch), 256, 0, ctx->stream>>>(mu, mv, UM, mu, VM, mv,
-                                                                              fac, sig2, scale_v);
-  }
-  FTT_LAUNCHED(ctx);
-  if (U) {
-    if (u_row_major) FTT_CHECK(transpose(ctx, mu, rank, UM, mu, U, ldu));
-    else FTT_CHECK(copy_matrix(ctx, mu, rank, UM, mu, U, ldu));
-  }
-  if (V) {
-    if (v_row_major) FTT_CHECK(transpose(ctx, mv, rank, VM, mv, V, ldv));
-    else FTT_CHECK(copy_matrix(ctx, mv, rank, VM, mv, V, ldv));
+    if (rank <= 32) {
+      // narrow factors: one fused pass (row-major reads stay within a few
+      // sectors per warp)
+      if (U || V) {
+        const int64_t tot = (U ? mu * rank : 0) + (V ? mv * rank : 0);
+        k_sign_write<<<grid_for(tot, 256, 4), 256, 0, ctx->stream>>>(
+            mu, mv, rank, UM, VM, fac, sig2, scale_v, U, ldu, u_row_major, V, ldv, v_row_major);
+        FTT_LAUNCHED(ctx);
+      }
+    } else {
+      // wide factors: in-place sign pass, then tiled transposes / copies
+      const int64_t nch =
+          std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(std::max(mu, mv), 4096)));
+      k_sign_apply<<<dim3((unsigned)rank, (unsigned)nch), 256, 0, ctx->stream>>>(
+          mu, mv, UM, mu, VM, mv, fac, sig2, scale_v);
+      FTT_LAUNCHED(ctx);
+      if (U) {
+        if (u_row_major) FTT_CHECK(transpose(ctx, mu, rank, UM, mu, U, ldu));
+        else FTT_CHECK(copy_matrix(ctx, mu, rank, UM, mu, U, ldu));
+      }
+      if (V) {
+        if (v_row_major) FTT_CHECK(transpose(ctx, mv, rank, VM, mv, V, ldv));
+        else FTT_CHECK(copy_matrix(ctx, mv, rank, VM, mv, V, ldv));
+      }
+    }
   }
   owned_free(ctx, UA);
-  owned_free(ctx, VA);
+  if (st->lowrank) {
+    owned_free(ctx, UAi);
+    owned_free(ctx, VAi);
+  } else {
+    owned_free(ctx, VA);
+  }
   return FTT_OK;
 }
