@@ -976,17 +976,28 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
 // The leading `rank` triplets of a full (non-low-rank) state in its tall
 // orientation: UA (mA x rank), VA (nA x rank), column-major, unscaled and
 // without the sign rule.
-int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double *VA) {
+// sig_host (optional): rank values staged with the selection in the same
+// host->device copy; *sig_dev receives their device address, followed by
+// rank doubles of device scratch.
+int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double *VA,
+                    const double *sig_host = nullptr, double **sig_dev = nullptr) {
   const int64_t mA = st->mA, nA = st->nA;
   size_t wse = qr_apply_workspace_elems(mA, nA, rank);
-  FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + 2 * align_up(8 * rank) + 4096));
+  FTT_CHECK(arena_reserve(ctx, align_up(8 * wse) + align_up(8 * 4 * rank) + 4096));
   double *ws = take<double>(ctx, wse);
-  int64_t *sel = take<int64_t>(ctx, rank);
-  double *inv = take<double>(ctx, rank);
-  std::vector<double> hinv(rank);
-  for (int64_t j = 0; j < rank; ++j) hinv[j] = st->sigma[j] != 0.0 ? 1.0 / st->sigma[j] : 0.0;
-  FTT_CHECK(stage_to_device(ctx, sel, st->perm.data(), 8 * rank));
-  FTT_CHECK(stage_to_device(ctx, inv, hinv.data(), 8 * rank));
+  // one staged copy: [sel (int64) | 1/sigma | sig_host], then scratch
+  double *packed = take<double>(ctx, 4 * rank);
+  int64_t *sel = reinterpret_cast<int64_t *>(packed);
+  double *inv = packed + rank;
+  std::vector<double> h(3 * rank);
+  memcpy(h.data(), st->perm.data(), 8 * rank);
+  for (int64_t j = 0; j < rank; ++j) h[rank + j] = st->sigma[j] != 0.0 ? 1.0 / st->sigma[j] : 0.0;
+  const int64_t nst = sig_host ? 3 * rank : 2 * rank;
+  if (sig_host) {
+    memcpy(h.data() + 2 * rank, sig_host, 8 * rank);
+    *sig_dev = packed + 2 * rank;
+  }
+  FTT_CHECK(stage_to_device(ctx, packed, h.data(), 8 * nst));
   if (st->small) {
     // U_A = (Q P)[:, sel],  V_A = Y[:, sel] / sigma
     k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, mA, rank, st->Af, mA,
@@ -1265,7 +1276,8 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
     return FTT_ERR_INVALID;
   }
   if (rank == 0) return FTT_OK;
-  double *UA = nullptr, *VA = nullptr, *UAi = nullptr, *VAi = nullptr;
+  double *UA = nullptr, *VA = nullptr, *UAi = nullptr, *VAi = nullptr, *sig2 = nullptr,
+         *fac = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&UA, 8 * (size_t)mA * rank));
   if (st->lowrank) {
     // A_tall ~= Qk B with B = U_B S V_B^T  =>  U_A = Qk U_B, V_A = V_B (used
@@ -1273,24 +1285,23 @@ extern "C" int ftt_svd_vectors(ftt_ctx *ctx, int64_t rank, double *U, int64_t ld
     SvdState *in = st->inner;
     FTT_CHECK(owned_alloc(ctx, (void **)&UAi, 8 * (size_t)in->mA * rank));
     FTT_CHECK(owned_alloc(ctx, (void **)&VAi, 8 * (size_t)in->nA * rank));
-    FTT_CHECK(svd_raw_vectors(ctx, in, rank, UAi, VAi));
+    FTT_CHECK(svd_raw_vectors(ctx, in, rank, UAi, VAi, st->sigma.data(), &sig2));
     const int64_t k = in->m;  // B is k x nA
     double *UB = in->transposed ? VAi : UAi;  // k x rank
     VA = in->transposed ? UAi : VAi;          // nA x rank
     FTT_CHECK(gemm(ctx, 0, 0, mA, rank, k, 1.0, st->Qk, mA, UB, k, 0.0, UA, mA, nullptr, 0));
   } else {
     FTT_CHECK(owned_alloc(ctx, (void **)&VA, 8 * (size_t)nA * rank));
-    FTT_CHECK(svd_raw_vectors(ctx, st, rank, UA, VA));
+    FTT_CHECK(svd_raw_vectors(ctx, st, rank, UA, VA, st->sigma.data(), &sig2));
   }
   double *UM = st->transposed ? VA : UA;
   double *VM = st->transposed ? UA : VA;
   const int64_t mu = st->transposed ? nA : mA;  // == caller m
   const int64_t mv = st->transposed ? mA : nA;  // == caller n
   {
-    FTT_CHECK(arena_reserve(ctx, 2 * align_up(8 * rank) + 256));
-    double *sig2 = take<double>(ctx, rank);
-    double *fac = take<double>(ctx, rank);
-    FTT_CHECK(stage_to_device(ctx, sig2, st->sigma.data(), 8 * rank));
+    // (sig2 was staged with the selection; the arena block stays valid: no
+    // reservation happened since)
+    fac = sig2 + rank;
     k_sign_pick<<<(unsigned)rank, 256, 0, ctx->stream>>>(mu, UM, mu, fac);
     FTT_LAUNCHED(ctx);
     if (rank <= 32) {
