@@ -37,7 +37,9 @@ constexpr int CQ_MAX = 64;
 constexpr int CQ_NT = 512;
 __global__ void __launch_bounds__(CQ_NT) k_chol_inv(int k, const double *__restrict__ G, int64_t ldg,
                                                     double tau, int *__restrict__ out,
-                                                    int64_t *__restrict__ piv_out) {
+                                                    int64_t *__restrict__ piv_out,
+                                                    const double *__restrict__ aux_src,
+                                                    double *__restrict__ aux_dst) {
   extern __shared__ double cq_smem[];
   double(*A)[CQ_MAX + 1] = reinterpret_cast<double(*)[CQ_MAX + 1]>(cq_smem);  // Schur complement
   __shared__ double lcol[CQ_MAX];
@@ -52,6 +54,7 @@ __global__ void __launch_bounds__(CQ_NT) k_chol_inv(int k, const double *__restr
     A[i][j] = 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]);
   }
   if (tid < k) done[tid] = 0;
+  if (tid == 0 && aux_src) *aux_dst = *aux_src;  // caller's scalar rides on the rank read
   __syncthreads();
   if (tid < 32) {
     double m = 0.0;
@@ -139,25 +142,21 @@ int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau
     attr = true;
   }
   const size_t ske = std::max(gemm_splitk_elems(k, k, mA), (size_t)1);
-  double *G = nullptr, *sk = nullptr;
-  int *dev_r = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&G, 8 * (size_t)k * k));
-  FTT_CHECK(owned_alloc(ctx, (void **)&sk, 8 * ske));
-  FTT_CHECK(owned_alloc(ctx, (void **)&dev_r, 64));
+  // one allocation: rank word + aux scalar (16 B) | G (k x k) | split-K space
+  double *blk = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&blk, 8 * (2 + (size_t)k * k + ske)));
+  int *dev_r = reinterpret_cast<int *>(blk);
+  double *G = blk + 2, *sk = G + (size_t)k * k;
   FTT_CHECK(gemm(ctx, 1, 0, k, k, mA, 1.0, Y, mA, Y, mA, 0.0, G, k, sk, ske));
-  k_chol_inv<<<1, CQ_NT, CQ_SMEM, ctx->stream>>>((int)k, G, k, tau, dev_r, sel_dev);
+  // one round trip for the rank and the caller's device scalar (copied by
+  // the kernel)
+  k_chol_inv<<<1, CQ_NT, CQ_SMEM, ctx->stream>>>((int)k, G, k, tau, dev_r, sel_dev, aux_dev, blk + 1);
   FTT_LAUNCHED(ctx);
-  // one round trip for the rank and the caller's device scalar
-  if (aux_dev)
-    FTT_CUDA(cudaMemcpyAsync(dev_r + 2, aux_dev, sizeof(double), cudaMemcpyDeviceToDevice,
-                             ctx->stream));
   int hb[4] = {0, 0, 0, 0};
   FTT_CHECK(copy_to_host(ctx, hb, dev_r, aux_dev ? 16 : 4));
   const int r = hb[0];
   if (aux_dev && aux_host) memcpy(aux_host, hb + 2, sizeof(double));
-  owned_free(ctx, G);
-  owned_free(ctx, sk);
-  owned_free(ctx, dev_r);
+  owned_free(ctx, blk);
   *rank = r;
   return FTT_OK;
 }
