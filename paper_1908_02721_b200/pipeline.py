@@ -154,8 +154,13 @@ def flops_fasttt(shape, pivot: int, ranks_lossless, ranks_final, c_svd: float = 
     _check_pivot(pivot, d)
     if d == 1:
         return 0.0
-    rt = full_ranks(dims, ranks_lossless)
-    r = full_ranks(dims, ranks_final)
+    return _flops_core(dims, pivot, full_ranks(dims, ranks_lossless), full_ranks(dims, ranks_final),
+                       c_svd)
+
+
+def _flops_core(dims, pivot, rt, r, c_svd):
+    """flops_fasttt on validated full rank vectors (select_p's inner loop)."""
+    d = len(dims)
     p1 = pivot + 1
 
     def cost(m, n):
@@ -224,7 +229,7 @@ def select_p(a: SparseTensor, target_ranks=None, precise: bool = False, c_svd: f
             if targets is not None:
                 feas = min(feas, targets[k - 1])
             r_est.append(feas)
-        cost = flops_fasttt(dims, pivot, rt, tuple(r_est), c_svd)
+        cost = _flops_core(dims, pivot, (1,) + tuple(rt) + (1,), (1,) + tuple(r_est) + (1,), c_svd)
         if cost < best_cost:
             best_cost, best_pivot = cost, pivot
     return best_pivot
