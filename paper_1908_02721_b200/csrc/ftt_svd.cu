@@ -882,7 +882,8 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
       ns = 3;
       csize = 2;
     }
-    const void *kfn = ns == 4 ? (const void *)k_jacobi_persistent<4> : (const void *)k_jacobi_persistent<3>;
+    const void *kfn =
+        ns == 4 ? (const void *)k_jacobi_persistent<4> : (const void *)k_jacobi_persistent<3>;
     int G = std::min(npairs, ns == 4 ? coresident : coresident3);
     cudaLaunchAttribute lattr[2];
     lattr[0].id = cudaLaunchAttributeCooperative;
@@ -926,7 +927,20 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     void *args[] = {&nA_, &mX_, &Y, &mX_, &Pm, &nA_, &nblk_, &tol_, &floor_, &maxsw, &csize, &cnt,
                     &status, &last_mod, &last_ok};
     const int pb = prof_begin(ctx);
-    FTT_CUDA(cudaLaunchKernelExC(&cfg, kfn, args));
+    cudaError_t le = cudaLaunchKernelExC(&cfg, kfn, args);
+    if (le != cudaSuccess && csize > 1) {
+      // a cooperative launch of clusters refused (e.g. under a replaying
+      // profiler): the same iteration with one CTA per pair
+      cudaGetLastError();
+      csize = 1;
+      g_last_csize = 1;
+      kfn = (const void *)k_jacobi_persistent<4>;
+      cfg.numAttrs = 1;
+      cfg.dynamicSmemBytes = jac_dyn_bytes(4);
+      cfg.gridDim = dim3(std::min(npairs, coresident));
+      le = cudaLaunchKernelExC(&cfg, kfn, args);
+    }
+    FTT_CUDA(le);
     FTT_LAUNCHED(ctx);
     int sw_used = 0;
     FTT_CHECK(copy_to_host(ctx, &sw_used, status, sizeof(int)));
