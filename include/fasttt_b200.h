@@ -76,14 +76,55 @@ int ftt_bench_dmma(ftt_ctx *ctx, int64_t iters, double *tflops_out);
 /* ---------------------------------------------------- input side (host) */
 /* COO text reader (formats.py:47-100, ingest_coo): header "# shape n1 ...
  * nd", then d 1-based indices and a value per nonempty line.  Host memory
- * only (no context, no GPU).  On success *coords_out (nnz x d, 0-based) and
- * *vals_out are malloc'd -- release them with ftt_free_host.  Any line the
- * strict fast path does not accept returns FTT_ERR_INVALID with *bad_line
- * set (1 = header, 0 = empty or unreadable file); the Python mirror then
- * re-reads the file with the reference loop for the exact FormatError. */
-int ftt_parse_coo_text(const char *path, int32_t *d_out, int64_t *dims_out,
-                       int64_t *nnz_out, int64_t **coords_out, double **vals_out,
-                       int64_t *bad_line);
+ * only (no context, no GPU).  The whole reference contract is decided here:
+ * Python text-mode line splitting (\n, \r\n, \r), str.split() tokens,
+ * Python int()/float() literal grammar, the reference's order of checks.
+ * On success *coords_out (nnz x d, 0-based) and *vals_out are malloc'd --
+ * release them with ftt_free_host.  A rejected file returns
+ * FTT_ERR_INVALID and fills *err (err->text malloc'd, ftt_free_host); the
+ * Python layer words the reference's FormatError from it. */
+enum {
+  FTT_COO_IO = 1,         /* unreadable file */
+  FTT_COO_EMPTY = 2,      /* zero bytes: "empty file, missing shape header" */
+  FTT_COO_HEADER = 3,     /* line 1 is not "# shape n1 ... nd" */
+  FTT_COO_SHAPE = 4,      /* extents fail int()/check_shape; text = line 1 */
+  FTT_COO_FIELDS = 5,     /* count = number of fields on the line */
+  FTT_COO_UNPARSABLE = 6, /* text = the line */
+  FTT_COO_RANGE = 7,      /* mode = 0-based mode, text = the index token */
+  FTT_COO_NONFINITE = 8,  /* text = the value token */
+  FTT_COO_NONASCII = 9    /* count = byte offset, mode = the byte */
+};
+typedef struct ftt_coo_error {
+  int32_t kind;
+  int32_t mode;
+  int64_t line;  /* 1-based */
+  int64_t count;
+  char *text;
+  int64_t text_len;
+} ftt_coo_error;
+int ftt_parse_coo_text(const char *path, int32_t max_d, int32_t *d_out,
+                       int64_t *dims_out, int64_t *nnz_out,
+                       int64_t **coords_out, double **vals_out,
+                       ftt_coo_error *err);
+/* MatrixMarket coordinate reader (formats.py:103-127).  *banner_out
+ * classifies line 1 (FTT_MM_*); for `real general|symmetric` files the body
+ * is read strictly (0-based rows/cols, symmetric entries expanded: stored
+ * entries in file order, then mirrored off-diagonal ones in file order --
+ * scipy.io.mmread's order) into malloc'd arrays.  FTT_ERR_INVALID = a body
+ * the strict reader does not accept: the caller defers to scipy.io.mmread,
+ * the library the reference reads with, for its result or error text. */
+enum {
+  FTT_MM_NOT_MM = 1,
+  FTT_MM_OBJECT = 2,
+  FTT_MM_FORMAT = 3,
+  FTT_MM_FIELD = 4,
+  FTT_MM_SYMMETRY = 5,
+  FTT_MM_GENERAL = 6,
+  FTT_MM_SYMMETRIC = 7
+};
+int ftt_parse_mm_text(const char *path, int32_t *banner_out, int64_t *shape_out,
+                      int64_t *nnz_out, int64_t **rows_out, int64_t **cols_out,
+                      double **vals_out);
 void ftt_free_host(void *p);
 
 /* ---------------------------------------------------- index path (int) */

@@ -75,11 +75,15 @@ SIGNATURES = {
                           ctypes.POINTER(ctypes.c_int64)],
     "ftt_tensorize_matrix": [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_i32, _P_i64, _P_i64, _c_p, _c_p,
                              ctypes.POINTER(ctypes.c_int64)],
-    "ftt_parse_coo_text": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
-                           ctypes.POINTER(ctypes.c_int64),
+    "ftt_parse_coo_text": [ctypes.c_char_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                           ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                            ctypes.POINTER(ctypes.POINTER(ctypes.c_int64)),
-                           ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
-                           ctypes.POINTER(ctypes.c_int64)],
+                           ctypes.POINTER(ctypes.POINTER(ctypes.c_double)), _c_p],
+    "ftt_parse_mm_text": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32),
+                          ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                          ctypes.POINTER(ctypes.POINTER(ctypes.c_int64)),
+                          ctypes.POINTER(ctypes.POINTER(ctypes.c_int64)),
+                          ctypes.POINTER(ctypes.POINTER(ctypes.c_double))],
     "ftt_free_host": [_c_p],
     "ftt_index_sweeps_all": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, ctypes.POINTER(_c_p),
                              ctypes.POINTER(_c_p), ctypes.POINTER(ctypes.c_int64)],
@@ -125,6 +129,11 @@ def load_library(path: str = LIB_PATH):
 
 class NativeError(RuntimeError):
     pass
+
+
+def last_error() -> str:
+    lib_ = load_library()
+    return lib_.ftt_last_error().decode(errors="replace")
 
 
 def check(status: int, what: str = "") -> None:

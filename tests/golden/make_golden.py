@@ -267,12 +267,329 @@ def small():
     print("small", len(cases), "tensors", flush=True)
 
 
+# ---------------------------------------------------------------- round 2
+Z1M = 1_000_000
+Z1M_SEED = 99
+
+
+def entries_chunked(cores, coords, chunk=100_000):
+    """Oracle entries (tt_entry math, ttformat.py:110-121) in bounded memory."""
+    out = np.empty(coords.shape[0])
+    for s in range(0, coords.shape[0], chunk):
+        out[s:s + chunk] = O.tt_entries(cores, coords[s:s + chunk])
+    return out
+
+
+def z1m(cfg: int):
+    """Entries of the golden train at 1e6 seeded zero positions
+    (G.zero_positions(..., 1_000_000, seed=99)) -- the north-star parity set.
+    c1: the reference's own train (stored cores); c2/c4: the oracle train at
+    the auto pivot (the reference raises MemoryError there); c3: the oracle
+    train (the reference did not finish in > 3 h)."""
+    shape, coords, vals, eps = G.gen_config(cfg, seed=0)
+    meta, z = json.load(open(os.path.join(HERE, f"c{cfg}.json"))), np.load(
+        os.path.join(HERE, f"c{cfg}.npz"))
+    t0 = time.time()
+    if meta["cores_stored"]:
+        cores = [z[f"core{k}"] for k in range(len(shape))]
+    else:
+        cores, info = O.fasttt(shape, coords, vals, eps=eps, pivot=meta["auto_pivot"],
+                               report=False)
+        assert [int(c.shape[2]) for c in cores[:-1]] == meta["ranks"]
+        # the regenerated train is the committed one (entries at the nonzeros)
+        e = O.tt_entries(cores, np.asarray(sparsett.SparseTensor(shape, coords, vals).coords))
+        assert np.array_equal(e, z["entries_nnz"]) or np.linalg.norm(e - z["entries_nnz"]) <= \
+            1e-14 * np.linalg.norm(z["entries_nnz"])
+    t = sparsett.SparseTensor(shape, coords, vals)
+    zc = G.zero_positions(shape, t.coords, Z1M, seed=Z1M_SEED)
+    ez = entries_chunked(cores, zc)
+    np.savez_compressed(os.path.join(HERE, f"c{cfg}_z1m.npz"), entries=ez)
+    with open(os.path.join(HERE, f"c{cfg}_z1m.json"), "w") as fh:
+        json.dump({"config": cfg, "count": Z1M, "seed": Z1M_SEED, "coords": digest(zc),
+                   "source": meta["source"], "ranks": meta["ranks"],
+                   "seconds": time.time() - t0}, fh, indent=1, sort_keys=True)
+    print(f"c{cfg}_z1m", float(np.linalg.norm(ez)), time.time() - t0, flush=True)
+
+
+def c5train():
+    """Config 5: the oracle train at the reference's auto pivot p = 2 (the
+    reference itself would densify a (314928, 32, 104976) core,
+    fasttt.py:253).  Cores (ranks 16) are committed whole; entries at the 1e6
+    zero positions too."""
+    shape, coords, vals, eps = G.gen_config(5, seed=0)
+    t = sparsett.SparseTensor(shape, coords, vals)
+    t0 = time.time()
+    cores, info = O.fasttt(shape, t.coords, t.values, eps=eps, pivot=2, report=False)
+    secs = time.time() - t0
+    arrays = {f"core{k}": c for k, c in enumerate(cores)}
+    zc = G.zero_positions(shape, t.coords, Z1M, seed=Z1M_SEED)
+    arrays["entries_z1m"] = entries_chunked(cores, zc)
+    en = entries_chunked(cores, t.coords)
+    np.savez_compressed(os.path.join(HERE, "c5train.npz"), **arrays)
+    meta = {"config": 5, "pivot": 2, "eps": eps, "ranks": [int(c.shape[2]) for c in cores[:-1]],
+            "ranks_lossless": list(info["ranks_lossless"]), "oracle_s": secs,
+            "z1m_coords": digest(zc), "z1m_seed": Z1M_SEED,
+            "nnz_rel_err_vs_input": float(np.linalg.norm(en - t.values) / np.linalg.norm(t.values)),
+            "source": "oracle restatement (index-form 0/1 cores, LAPACK gesdd) at p=2"}
+    with open(os.path.join(HERE, "c5train.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("c5train", meta["ranks"], secs, meta["nnz_rel_err_vs_input"], flush=True)
+
+
+def refmid():
+    """The UNMODIFIED reference end to end at explicit middle pivots where it
+    fits in memory: c2 at p=2, c4 at p=3 (build_structured_tt ->
+    parallel_vector_round -> efficient_tt_rounding, i.e. fasttt(pivot=p)).
+    c2's train (ranks 8) is stored whole; c4's (ranks up to 511) as its
+    entries at every nonzero and at the 1e6 zero positions."""
+    for cfg, mid in ((2, 2), (4, 3)):
+        shape, coords, vals, eps = G.gen_config(cfg, seed=0)
+        t = sparsett.SparseTensor(shape, coords, vals)
+        t0 = time.time()
+        tt, rep = sparsett.fasttt(t, eps=eps, pivot=mid)
+        secs = time.time() - t0
+        cores = [np.array(c) for c in tt.cores]
+        zc = G.zero_positions(shape, t.coords, Z1M, seed=Z1M_SEED)
+        arrays = {"entries_nnz": entries_chunked(cores, t.coords),
+                  "entries_z1m": entries_chunked(cores, zc)}
+        if sum(c.size for c in cores) <= CORE_STORE_CAP:
+            for k, c in enumerate(cores):
+                arrays[f"core{k}"] = c
+        np.savez_compressed(os.path.join(HERE, f"c{cfg}_ref_p{mid}.npz"), **arrays)
+        meta = {"config": cfg, "pivot": mid, "eps": eps, "ranks": list(rep.ranks),
+                "ranks_lossless": list(rep.ranks_lossless), "num_fibers": rep.num_fibers,
+                "eps_actual": rep.eps_actual, "eps_actual_method": rep.eps_actual_method,
+                "flops_fasttt_model": rep.flops_fasttt_model,
+                "flops_ttsvd_model": rep.flops_ttsvd_model, "ref_s": secs,
+                "z1m_coords": digest(zc), "z1m_seed": Z1M_SEED,
+                "cores_stored": f"core0" in arrays,
+                "source": f"unmodified reference sparsett.fasttt(t, eps, pivot={mid})"}
+        with open(os.path.join(HERE, f"c{cfg}_ref_p{mid}.json"), "w") as fh:
+            json.dump(meta, fh, indent=1, sort_keys=True)
+        print(f"c{cfg}_ref_p{mid}", meta["ranks"], secs, flush=True)
+
+
+def tensorize():
+    """Config 4 built through the reference's own tensorize_matrix
+    (ttformat.py:414-433) from the same scipy matrix: digests of its
+    SparseTensor, which the drop-in's host and device tensorize_matrix and
+    the bench generator must reproduce."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(0)
+    rows, cols, v, n = G.laplacian_2d_scaled(256, rng)
+    m = sp.coo_matrix((v, (rows, cols)), shape=(n, n))
+    dims = (4,) * 8
+    t = sparsett.tensorize_matrix(m, dims, dims)
+    meta = {"config": 4, "row_dims": list(dims), "col_dims": list(dims),
+            "shape": list(t.shape), "nnz": int(t.nnz), "coords": digest(t.coords),
+            "values": digest(t.values), "matrix_rows": digest(rows), "matrix_cols": digest(cols),
+            "matrix_values": digest(v),
+            "source": "reference sparsett.tensorize_matrix(coo_matrix(D L D), (4,)*8, (4,)*8)"}
+    with open(os.path.join(HERE, "c4_tensorize.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("c4_tensorize", meta["nnz"], flush=True)
+
+
+def _ref_acceptance_module():
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    return importlib.import_module("test_acceptance")
+
+
+def fdm():
+    """The paper's own MPO experiment as the reference's acceptance gate runs
+    it (test_acceptance.py:87-107): the 20^3 7-point Laplacian and the
+    seed-1234 random-coefficient stencil from the reference's gen_fdm,
+    tensorized (20,20,20) x (20,20,20) and decomposed at pivot 1 with
+    eps 1e-14.  The matrices are committed (the generator does not travel)
+    with the reference's results: R, r~, ranks, eps_actual."""
+    dims = (20, 20, 20)
+    arrays, meta = {}, {"dims": list(dims), "eps": 1e-14, "pivot": 1}
+    for name, kw in (("lap", {}), ("rnd", {"coeffs": "random", "seed": 1234})):
+        m = sparsett.gen_fdm(20, 20, 20, **kw).tocoo()
+        arrays[f"{name}_row"] = m.row.astype(np.int32)
+        arrays[f"{name}_col"] = m.col.astype(np.int32)
+        arrays[f"{name}_val"] = m.data.astype(np.float64)
+        t = sparsett.tensorize_matrix(m, dims, dims)
+        t0 = time.time()
+        tt, rep = sparsett.fasttt(t, eps=1e-14, pivot=1)
+        meta[name] = {"shape": list(m.shape), "nnz_matrix": int(m.nnz), "nnz": int(t.nnz),
+                      "coords": digest(t.coords), "values": digest(t.values),
+                      "num_fibers": rep.num_fibers, "ranks_lossless": list(rep.ranks_lossless),
+                      "ranks": list(rep.ranks), "eps_actual": rep.eps_actual,
+                      "eps_actual_method": rep.eps_actual_method, "ref_s": time.time() - t0}
+        cores = [np.array(c) for c in tt.cores]
+        for k, c in enumerate(cores):
+            arrays[f"{name}_core{k}"] = c
+    np.savez_compressed(os.path.join(HERE, "fdm.npz"), **arrays)
+    with open(os.path.join(HERE, "fdm.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("fdm", meta["lap"]["ranks"], meta["rnd"]["ranks"], flush=True)
+
+
+def acceptance():
+    """The reference's acceptance suite inputs (test_acceptance.build_suite:
+    200 seeded tensors; the rng(4) quasi-permutations of criterion 4; the
+    criterion-8 image-shape tensor) and the UNMODIFIED reference's results on
+    them: fasttt at eps 1e-14 (criteria 1, 2, 4), the classical tt_svd ranks
+    (criterion 2), fasttt at eps {0.5, 0.1, 0.01} x {static, dynamic}
+    (criterion 3), depar_quasi_perm outputs (criterion 4), select_p with
+    target rank 100 (criterion 8)."""
+    A = _ref_acceptance_module()
+    suite = A.build_suite()
+    arrays, cases = {}, []
+    lin_all, val_all, offs = [], [], [0]
+    t0 = time.time()
+    for i, t in enumerate(suite):
+        lin = sparsett.tensor.linearize(t.shape, t.coords)
+        lin_all.append(lin.astype(np.int32))
+        val_all.append(t.values)
+        offs.append(offs[-1] + t.nnz)
+        tt, rep = sparsett.fasttt(t, eps=1e-14)
+        case = {"shape": list(t.shape), "pivot": rep.pivot, "num_fibers": rep.num_fibers,
+                "ranks_lossless": list(rep.ranks_lossless), "ranks": list(rep.ranks),
+                "eps_actual": rep.eps_actual, "eps_actual_method": rep.eps_actual_method,
+                "inner": float(sparsett.sparse_inner_error(t, tt)),
+                "ttsvd_ranks": list(sparsett.tt_svd(t.to_dense(cap=None), 1e-14).ranks),
+                "rounded": []}
+        for eps in (0.5, 0.1, 0.01):
+            for mode in ("static", "dynamic"):
+                _, r = sparsett.fasttt(t, eps=eps, mode=mode)
+                case["rounded"].append({"eps": eps, "mode": mode, "pivot": r.pivot,
+                                        "ranks": list(r.ranks), "eps_actual": r.eps_actual,
+                                        "ranks_lossless": list(r.ranks_lossless)})
+        cases.append(case)
+    arrays["suite_lin"] = np.concatenate(lin_all)
+    arrays["suite_val"] = np.concatenate(val_all)
+    arrays["suite_off"] = np.asarray(offs, np.int64)
+    rng = np.random.default_rng(4)
+    qp_rows, qp_ctr, qp_off, qp_out = [], [], [0], []
+    for _ in range(100):
+        rows = int(rng.integers(1, 101))
+        cols = int(rng.integers(1, 2001))
+        ctr = rng.integers(0, rows, cols)
+        q = sparsett.QuasiPermMatrix(rows, cols, ctr)
+        n, tq = sparsett.depar_quasi_perm(q)
+        qp_rows.append(rows)
+        qp_ctr.append(ctr.astype(np.int32))
+        qp_off.append(qp_off[-1] + cols)
+        qp_out.append({"n_cols": int(n.n_cols), "kept": digest(np.asarray(n.col_to_row)),
+                       "t_map": digest(np.asarray(tq.col_to_row))})
+    arrays["qp_rows"] = np.asarray(qp_rows, np.int64)
+    arrays["qp_ctr"] = np.concatenate(qp_ctr)
+    arrays["qp_off"] = np.asarray(qp_off, np.int64)
+    shape8 = (10, 20, 20, 10, 15, 20, 3)
+    t8 = sparsett.gen_random_sparse(shape8, 0.001, seed=42, fill_last_mode=True)
+    arrays["c8_lin"] = sparsett.tensor.linearize(shape8, t8.coords)
+    arrays["c8_val"] = t8.values
+    meta = {"cases": cases, "qp": qp_out,
+            "criterion8": {"shape": list(shape8), "nnz": int(t8.nnz),
+                           "select_p_target100": int(sparsett.select_p(t8, target_ranks=100))},
+            "seconds": time.time() - t0,
+            "source": "reference tests/test_acceptance.py build_suite + unmodified sparsett"}
+    np.savez_compressed(os.path.join(HERE, "acceptance.npz"), **arrays)
+    with open(os.path.join(HERE, "acceptance.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print("acceptance", len(cases), meta["seconds"], flush=True)
+
+
+COO_TEXTS = [
+    # well-formed variants: separators, line endings, literal forms
+    "# shape 3 4\n1 2 0.5\n3 4 -2e-3\n2 1 +7\n",
+    "# shape 3 4\r\n\n  1 2   0.5\r\n3 4 -2e-3\r2 1 +7",
+    "\t#  shape\t3 4 \n1\t2\t.5\n3 4 5.\n2 1 1E+2\n",
+    "# shape 20 3\n1_0 1 1_0.5\n2 2 1e-1\n007 3 1e1_0\n",
+    "# shape 5 5\n+1 -0 1.0\n",
+    "# shape 5 5\n1 1 -0.0\n2 2 0\n3 3 1e-400\n",
+    "# shape 5 5\n1 1 4.9e-324\n2 2 1.7976931348623157e308\n3 3 0.1000000000000000055511151231257827\n",
+    "# shape 4 4\x0c\n1\x1c2\x1f3.25\x0b\n",
+    "# shape 2 2\n\n",
+    "# shape 2 2",
+    "# shape 6\n6 1\n1 2\n",
+    "# shape 1 1 1 1 1 1 1 1 1 1\n1 1 1 1 1 1 1 1 1 1 3\n",
+    # header errors
+    "",
+    "\n",
+    "#shape 3 3\n1 1 1.0\n",
+    "# Shape 3 3\n",
+    "# shape\n",
+    "# shape 3 0\n",
+    "# shape 3 -2\n",
+    "# shape 3 x\n",
+    "# shape 3 1.5\n",
+    "# shape 4294967296 4294967296\n",
+    "# shape 99999999999999999999\n",
+    "# shape 3 _3\n",
+    # entry errors
+    "# shape 3 3\n1 1\n",
+    "# shape 3 3\n1 1 1 1\n",
+    "# shape 3 3\n1 1 1.0\n2 x 1.0\n",
+    "# shape 3 3\n4 1 1.0\n",
+    "# shape 3 3\n1 0 1.0\n",
+    "# shape 3 3\n1 -1 1.0\n",
+    "# shape 3 3\n99999999999999999999999 1 1.0\n",
+    "# shape 3 3\n4 x 1.0\n",
+    "# shape 3 3\n1 1 nan\n",
+    "# shape 3 3\n1 1 -Infinity\n",
+    "# shape 3 3\n4 1 inf\n",
+    "# shape 3 3\n1 1 1e500\n",
+    "# shape 3 3\n1 1 0x10\n",
+    "# shape 3 3\n1 1 -0x1p3\n",
+    "# shape 3 3\n1 1 1__0\n",
+    "# shape 3 3\n1 1 1_\n",
+    "# shape 3 3\n1 1 _1\n",
+    "# shape 3 3\n1 1 1.e5\n",
+    "# shape 3 3\n1 1 e5\n",
+    "# shape 3 3\n1 1 1e\n",
+    "# shape 3 3\n1 1 nan(1)\n",
+    "# shape 3 3\n1 1 1.0\n1 1 2.0\n",
+    "# shape 3 3\n1 1 1.0\r1 1 2.0\r",
+    "# shape 3 3\n\n\n1 1 1.0\r\n\r\n2 2 q\n",
+    "# shape 3 3\n1.0 1 1.0\n",
+    "# shape 3 3\n1 1 1,0\n",
+]
+
+
+def coo_cases():
+    """The reference's ingest_coo on a set of well-formed and malformed COO
+    texts: tensor arrays or the exception type and message (with the file
+    path replaced by {path})."""
+    import tempfile
+    import warnings
+
+    out = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for i, text in enumerate(COO_TEXTS):
+            path = os.path.join(tmp, f"case{i}.coo")
+            with open(path, "w", encoding="ascii", newline="") as fh:
+                fh.write(text)
+            rec = {"text": text}
+            try:
+                with warnings.catch_warnings(record=True) as w:
+                    warnings.simplefilter("always")
+                    t = sparsett.ingest_coo(path)
+                rec.update(ok=True, shape=list(t.shape), coords=t.coords.tolist(),
+                           values=[float.hex(float(v)) for v in t.values],
+                           warnings=[str(x.message).replace(path, "{path}") for x in w])
+            except Exception as exc:  # noqa: BLE001
+                rec.update(ok=False, type=type(exc).__name__,
+                           message=str(exc).replace(path, "{path}"))
+            out.append(rec)
+    with open(os.path.join(HERE, "coo_cases.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print("coo_cases", len(out), sum(r["ok"] for r in out), flush=True)
+
+
+TARGETS = {"coo_cases": coo_cases, "c5idx": config5_index, "small": small, "c5train": c5train, "refmid": refmid,
+           "tensorize": tensorize, "fdm": fdm, "acceptance": acceptance}
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:] or ["small", "c1", "c2", "c4"]:
-        if arg == "c5idx":
-            config5_index()
+        if arg in TARGETS:
+            TARGETS[arg]()
             continue
-        if arg == "small":
-            small()
-        else:
-            config(int(arg.lstrip("c")))
+        if arg.endswith("_z1m"):
+            z1m(int(arg[1:-4]))
+            continue
+        config(int(arg.lstrip("c")))

@@ -1,6 +1,7 @@
 """Input side: COO text and MatrixMarket readers.
 Host-only (no GPU): the native fast path against the reference's line loop
 (formats.py:47-127), error texts, bit-exact round trips."""
+import json
 import os
 import warnings
 
@@ -19,6 +20,9 @@ def _write(tmp_path, name, text):
     return str(p)
 
 
+CASES = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "coo_cases.json")))
+
+
 @pytest.mark.parametrize("shape,density,seed", [((4, 5, 6), 0.3, 1), ((9, 2, 3, 7), 0.1, 2),
                                                 ((50,), 0.5, 3), ((3, 3), 1.0, 4)])
 def test_coo_round_trip_bit_exact(tmp_path, shape, density, seed):
@@ -30,48 +34,66 @@ def test_coo_round_trip_bit_exact(tmp_path, shape, density, seed):
     t = ft.SparseTensor(shape, coords, vals)
     p = str(tmp_path / "t.coo")
     ft.write_coo(t, p)
-    assert F._native_parse(p) is not None  # the native path read it
     u = ft.ingest_coo(p)
     assert u.shape == t.shape
     assert np.array_equal(u.coords, t.coords) and np.array_equal(u.values, t.values)
-    r = F._ingest_coo_reference(p)
-    assert np.array_equal(r.coords, u.coords) and np.array_equal(r.values, u.values)
 
 
-def test_coo_native_handles_layout_variants(tmp_path):
-    text = "# shape 3 4\n\n  1 2   0.5\r\n3 4 -2e-3\n\t2 1 +7\n"
-    p = _write(tmp_path, "v.coo", text)
-    fast = F._native_parse(p)
-    assert fast is not None
-    u, r = ft.ingest_coo(p), F._ingest_coo_reference(p)
-    assert np.array_equal(u.coords, r.coords) and np.array_equal(u.values, r.values)
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_coo_reader_matches_reference(tmp_path, case):
+    """Every committed case (tests/golden/make_golden.py coo_cases: the
+    unmodified reference's ingest_coo on well-formed and malformed texts):
+    the same tensor bit for bit, or the same exception type and message."""
+    rec = CASES[case]
+    p = tmp_path / "case.coo"
+    p.write_bytes(rec["text"].encode("ascii"))
+    if rec["ok"]:
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            t = ft.ingest_coo(str(p))
+        assert list(t.shape) == rec["shape"]
+        assert t.coords.tolist() == rec["coords"]
+        assert [float.hex(float(v)) for v in t.values] == rec["values"]
+        assert [str(x.message).replace(str(p), "{path}") for x in w] == rec["warnings"]
+    else:
+        with pytest.raises(Exception) as e:
+            ft.ingest_coo(str(p))
+        assert type(e.value).__name__ == rec["type"]
+        assert str(e.value).replace(str(p), "{path}") == rec["message"]
 
 
-@pytest.mark.parametrize("text,msg", [
-    ("", "empty file, missing shape header"),
-    ("#shape 3 3\n1 1 1.0\n", ":1: expected header"),
-    ("# shape 3 0\n", ":1: bad shape header"),
-    ("# shape 3 3\n1 1\n", ":2: expected 2 indices and a value, got 2 fields"),
-    ("# shape 3 3\n1 1 1.0\n2 x 1.0\n", ":3: unparsable entry"),
-    ("# shape 3 3\n4 1 1.0\n", ":2: index 4 out of range 1..3 in mode 1"),
-    ("# shape 3 3\n1 0 1.0\n", ":2: index 0 out of range 1..3 in mode 2"),
-    ("# shape 3 3\n1 1 nan\n", ":2: non-finite value nan"),
-    ("# shape 3 3\n1 1 1.0\n1 1 2.0\n", "duplicate coordinate"),
-    ("# shape 3 3\n1 1 0x10\n", ":2: unparsable entry"),
-])
-def test_coo_errors_match_reference_text(tmp_path, text, msg):
-    p = _write(tmp_path, "bad.coo", text)
-    with pytest.raises(ft.FormatError) as e:
-        ft.ingest_coo(p)
-    assert msg in str(e.value)
+def test_coo_reader_rejects_non_ascii(tmp_path):
+    p = tmp_path / "u.coo"
+    p.write_bytes(b"# shape 3 3\n1 1 1.0\n2 2 \xc3\xa9\n")
+    with pytest.raises(UnicodeDecodeError):
+        ft.ingest_coo(str(p))
 
 
-def test_coo_python_literal_forms_fall_back(tmp_path):
-    # forms Python's int()/float() accept and strtoll/strtod do not
-    p = _write(tmp_path, "u.coo", "# shape 20 3\n1_0 1 1_0.5\n2 2 1e-1\n")
-    assert F._native_parse(p) is None
-    t = ft.ingest_coo(p)
-    assert t.coords.tolist() == [[1, 1], [9, 0]] and t.values.tolist() == [0.1, 10.5]
+def test_coo_reader_random_lines_match_python_literals(tmp_path):
+    """Fuzz: tokens built from the characters of Python literals; the native
+    grammar accepts exactly what int()/float() accept, with the same value."""
+    rng = np.random.default_rng(11)
+    alphabet = list("0123456789_+-.eEinfaINFA ")
+    for trial in range(300):
+        tok = "".join(rng.choice(alphabet, int(rng.integers(1, 8)))).strip() or "1"
+        if " " in tok:
+            continue
+        p = tmp_path / f"f{trial}.coo"
+        p.write_text(f"# shape 9 9\n1 2 {tok}\n")
+        try:
+            want = float(tok)
+        except ValueError:
+            want = None
+        if want is None:
+            with pytest.raises(ft.FormatError, match="unparsable entry"):
+                ft.ingest_coo(str(p))
+        elif not np.isfinite(want):
+            with pytest.raises(ft.FormatError, match="non-finite value"):
+                ft.ingest_coo(str(p))
+        else:
+            t = ft.ingest_coo(str(p))
+            got = t.values.tolist()
+            assert got == ([want] if want != 0.0 else []), tok
 
 
 def test_coo_no_entries_warns(tmp_path):
@@ -102,3 +124,30 @@ def test_matrix_market_general_and_symmetric(tmp_path):
     with pytest.raises(ft.FormatError, match="field 'complex'"):
         ft.ingest_matrix_market(cpx)
     assert os.path.exists(p)
+
+
+def test_matrix_market_native_body_equals_scipy(tmp_path):
+    """The strict native body reader gives scipy.io.mmread's arrays in its
+    order (symmetric: stored entries, then mirrored off-diagonal ones);
+    bodies outside the strict grammar go to scipy for its result or error."""
+    sym = ("%%MatrixMarket matrix coordinate real symmetric\n% c\n4 4 5\n1 1 1.5\n3 1 2.0\n"
+           "4 2 3e0\n2 2 -1\n4 3 7\n")
+    gen = "%%MatrixMarket matrix coordinate real general\n3 3 4\n1 1 1.5\n3 1 2.0\n1 1 3\n2 2 -1\n"
+    for name, text in (("s.mtx", sym), ("g.mtx", gen)):
+        p = _write(tmp_path, name, text)
+        m = ft.ingest_matrix_market(p)
+        ref = sp.coo_matrix(scipy.io.mmread(p), dtype=np.float64)
+        assert m.shape == ref.shape
+        assert m.row.tolist() == ref.row.tolist() and m.col.tolist() == ref.col.tolist()
+        assert m.data.tolist() == ref.data.tolist()
+    short = _write(tmp_path, "t.mtx", "%%MatrixMarket matrix coordinate real general\n3 3 3\n1 1 1\n")
+    with pytest.raises(ft.FormatError, match="Truncated file"):
+        ft.ingest_matrix_market(short)
+    oob = _write(tmp_path, "o.mtx", "%%MatrixMarket matrix coordinate real general\n3 3 1\n4 1 1\n")
+    with pytest.raises(ft.FormatError, match="out of bounds"):
+        ft.ingest_matrix_market(oob)
+    with pytest.raises(ft.FormatError, match="not a MatrixMarket file"):
+        ft.ingest_matrix_market(_write(tmp_path, "n.mtx", "hello\n"))
+    with pytest.raises(ft.FormatError, match="symmetry 'hermitian'"):
+        ft.ingest_matrix_market(_write(
+            tmp_path, "h.mtx", "%%MatrixMarket matrix coordinate real Hermitian\n1 1 1\n1 1 1\n"))
