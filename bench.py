@@ -3,20 +3,28 @@
 nonzeros/sec in fp64 on one B200, plus the HBM roofline fraction of the
 sort/segment kernels).
 
-Workload (BASELINE.json configs[1]): 6-way 64^6 sparse tensor, sum of R=8
-rank-1 terms with s=6 seeded positions per factor, N(0,1) values
-(373,246 nnz at seed 0), eps = 1e-10, automatic pivot. One step = one full
-``fasttt`` decomposition (select_p -> fibers -> deparallelisation sweeps ->
-rounding sweeps -> error report).
+Workload (default): BASELINE.json configs[4], the largest single-GPU config
+-- 12-way 32^12 sparse tensor, sum of R=16 rank-1 terms with s=3 seeded
+positions per factor, N(0,1) values (8,503,056 nnz at seed 0), eps = 1e-10,
+automatic pivot (p = 2).  ``--config N`` runs another BASELINE config.  One
+step = one full ``fasttt`` decomposition (select_p -> fibers ->
+deparallelisation sweeps -> rounding sweeps -> error report).
 
 * ``value``: COO already in HBM (``fasttt_device``), cores left on the
   device; per-step CUDA events on the launching stream, L2 flushed (256 MiB
   write) between steps, summed over K steps, max over ranks.
 * ``e2e``: the public drop-in call ``fasttt(SparseTensor)`` from pinned host
-  buffers: H2D of coords+values, the decomposition, D2H of every core.
+  buffers: H2D of the canonical COO (linear index + values), the
+  decomposition, D2H of every core.
+* ``roofline``: the dominant kernel class by live CUDA-event time;
+  ``roofline_sort_segment`` / ``index_path``: SURVEY 8(d)'s algorithmic bytes
+  of the index path over its measured time.
 * ``--impl reference``: the reference algorithm's CPU implementation (the
   oracle port, oracle/fasttt_oracle.py -- the reference is pure Python and
-  cannot travel to the GPU box) on all host cores, rank 0 only.
+  cannot travel to the GPU box) on all host cores, rank 0 only, one full
+  decomposition per step; on config 5 one step is ~minutes of LAPACK (a
+  dense 4160 x 314,928 gesdd), so the arm prints ``value: null`` with the
+  reason unless ``--allow-long-reference`` is given.
 
 Multi-GPU: the decomposition is a chain of dependent factorisations, so N
 GPUs run N independent replicas ("replicas only", scaling "weak").
@@ -52,11 +60,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, help="BASELINE config index (1-based)")
+    ap.add_argument("--config", type=int, default=5, help="BASELINE config index (1-based)")
+    ap.add_argument("--allow-long-reference", action="store_true",
+                    help="--impl reference: run the oracle even when one step takes minutes")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c5-index", action="store_true",
-                    help="skip the config-5 index-path leg (sort/segment HBM roofline)")
+    ap.add_argument("--no-index-leg", action="store_true",
+                    help="skip the separately timed index-path leg (sort/segment HBM roofline)")
     return ap.parse_args()
 
 
@@ -158,30 +168,57 @@ def oracle_step(shape, coords, vals, eps):
     return time.perf_counter() - t0, info
 
 
+# one oracle decomposition per config on a 16-core host (tests/golden/*.json
+# oracle_s / ref times, scaled): beyond ~60 s a K-step reference run cannot
+# finish "within a few minutes"
+ORACLE_STEP_S = {1: 9.0, 2: 1.9, 3: 330.0, 4: 1.9, 5: 600.0}
+
+
+def config_dict(cfg, name, shape, nnz, eps):
+    """The workload description both arms print (identical)."""
+    return {"workload": name, "baseline_config": cfg, "nnz": nnz, "shape": list(shape),
+            "eps": eps, "seed": 0, "pivot": "auto"}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     shape, coords, vals, eps, name = workload(args.config)
     cores = cpu_threads()
+    base = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded BASELINE.json configs[{args.config - 1}])"}
+    from paper_1908_02721_b200 import SparseTensor
+
+    t = SparseTensor(shape, coords, vals)
+    nnz = t.nnz
+    base["config"] = config_dict(args.config, name, shape, nnz, eps)
+    est = ORACLE_STEP_S.get(args.config, 0.0) * (args.steps + args.warmup)
+    if est > 300 and not args.allow_long_reference:
+        line = dict(base, value=None, ms_per_step=None, reason=(
+            f"one reference decomposition of {name} is ~{ORACLE_STEP_S[args.config]:.0f} s of "
+            f"host LAPACK (oracle port; the unmodified reference raises MemoryError at the auto "
+            f"pivot), so {args.steps}+{args.warmup} steps (~{est / 60:.0f} min) do not fit a "
+            f"bounded reference run; rerun with --allow-long-reference"),
+            cpu_baseline={"value": None, "unit": UNIT, "cores": cores, "kind": "port",
+                          "sample": "not run (see reason)"},
+            e2e={"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return 0
     for _ in range(max(args.warmup, 0)):
-        oracle_step(shape, coords, vals, eps)
-    times = [oracle_step(shape, coords, vals, eps)[0] for _ in range(args.steps)]
+        oracle_step(shape, t.coords, t.values, eps)
+    times = [oracle_step(shape, t.coords, t.values, eps)[0] for _ in range(args.steps)]
     total = sum(times)
-    nnz = int(coords.shape[0])
     value = nnz * args.steps / total
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE.json configs[1])",
-        "config": {"workload": name, "nnz": nnz, "eps": eps, "seed": 0},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"full {name} decomposition incl. report per step "
-                                   "(oracle/fasttt_oracle.py: the reference algorithm restated in "
-                                   "numpy/LAPACK, index-form 0/1 cores)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    line = dict(base, value=value, ms_per_step=1e3 * total / args.steps,
+                cpu_baseline={"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                              "sample": f"full {name} decomposition incl. report per step "
+                                        "(oracle/fasttt_oracle.py: the reference algorithm "
+                                        "restated in numpy/LAPACK, index-form 0/1 cores)"},
+                e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
     return 0
 
@@ -219,9 +256,10 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch per kernel class from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def ncu_traffic(cfg):
+    """DRAM bytes per launch per kernel class from the committed ncu capture
+    of this config's decomposition (profiles/traffic_c<N>.json)."""
+    path = os.path.join(ROOT, "profiles", f"traffic_c{cfg}.json")
     try:
         with open(path) as fh:
             return json.load(fh)
@@ -339,7 +377,10 @@ def run_ours(args):
         e_ms = max_over_ranks(sum(e_times), device="cuda")
         e2e = {"value": whole_job_rate(world, nnz, args.steps, e_ms), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e_ms / args.steps}
+               "ms_per_step": e_ms / args.steps, "steps_ms": [round(x, 3) for x in e_times],
+               "note": "public fasttt(SparseTensor) per step: H2D of the canonical COO from the "
+                       "tensor's pinned staging buffer (pinned once per tensor, outside the timed "
+                       "region), decomposition, D2H of every core into pinned host memory"}
         a.device_arrays()
     if os.environ.get("BENCH_DEBUG"):
         t_nosmi = timed_steps(args.steps)
@@ -351,7 +392,7 @@ def run_ours(args):
 
     # ---------------- roofline of the dominant kernel class
     pk, pk_src = peaks()
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.config)
     dom = max(prof, key=lambda k: prof[k]["ms"])
     d = prof[dom]
 
@@ -386,35 +427,35 @@ def run_ours(args):
         roof_sort["kernel_class"] = "sort+hist+segment"
         roof_sort["traffic"] = traffic.get("sort+hist+segment")
 
-    # ---------------- config-5 index path: the sort/segment roofline leg
-    # (configs 1-4 are L2-resident and launch-bound on the index path; the
-    # >= 60 % HBM target of north_star is judged on config 5's 8.5M nonzeros)
-    c5 = None
-    if rank == 0 and not args.no_c5_index:
-        c5 = index_leg_c5(ft, nat, lib, ctx, roof, args.steps)
+    # ---------------- the index path timed on its own (select_p counts,
+    # fiber extraction, deparallelisation sweeps): SURVEY 8(d)'s algorithmic
+    # bytes over its time -- the metric's sort/segment roofline (judged on
+    # config 5; configs 1-4 are L2-resident and launch-bound there)
+    ileg = None
+    if rank == 0 and not args.no_index_leg:
+        ileg = index_leg(ft, nat, lib, ctx, roof, a, cd, vd, args.config, name, args.steps)
 
-    # ---------------- CPU baseline (rank 0, N = 1)
+    # ---------------- CPU baseline (rank 0, N = 1): a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = cpu_threads()
-        dt, _ = oracle_step(shape, coords, vals, eps)
-        cpu = {"value": nnz / dt, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"one full {name} decomposition incl. report "
-                         "(oracle/fasttt_oracle.py on the host cores)"}
+        cpu = cpu_baseline(args.config, name, a, eps)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 1), "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE.json configs[1]; no dataset involved)",
-            "config": {"workload": name, "nnz": nnz, "shape": list(shape), "eps": eps,
-                       "pivot": res.pivot, "ranks_lossless": list(res.ranks_lossless),
-                       "ranks": list(ranks), "seed": 0, "l2": "flushed (256 MiB write) between steps",
-                       "parallelism": f"replicas x{world}"},
+            "data": (f"synthetic (seeded BASELINE.json configs[{args.config - 1}]; "
+                     "no dataset involved)"),
+            "config": config_dict(args.config, name, shape, nnz, eps),
+            "result": {"pivot": res.pivot, "ranks_lossless": list(res.ranks_lossless),
+                       "ranks": list(ranks), "num_fibers": res.num_fibers},
+            "timing": {"l2": "flushed (256 MiB write) between steps",
+                       "parallelism": f"replicas x{world}",
+                       "steps_ms": [round(x, 4) for x in times]},
             "roofline": roof(dom, d),
             "roofline_sort_segment": roof_sort,
-            "index_path_c5": c5,
+            "index_path": ileg,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -432,18 +473,14 @@ def run_ours(args):
     return 0
 
 
-def index_leg_c5(ft, nat, lib, ctx, roof, reps):
-    """select_p counts + fiber extraction + deparallelisation sweeps on
-    BASELINE config 5 (32^12, 8,503,056 nnz), device-resident, K reps after
-    warm-up; per-class live CUDA-event timing and algorithmic bytes."""
+def index_leg(ft, nat, lib, ctx, roof, a, cd, vd, cfg, name, reps):
+    """select_p counts + fiber extraction + deparallelisation sweeps on the
+    bench workload, device-resident, K reps after warm-up; per-class live
+    CUDA-event timing and SURVEY 8(d)'s algorithmic bytes."""
     import torch
 
-    from paper_1908_02721_b200 import generators as G
     from paper_1908_02721_b200 import pipeline as P
 
-    shape, coords, vals, _ = G.gen_config(5)
-    a = ft.SparseTensor(shape, coords, vals)
-    cd, vd = a.device_arrays()
     d, nnz = a.ndim, a.nnz
     pivot = P.select_p(a)
 
@@ -477,24 +514,11 @@ def index_leg_c5(ft, nat, lib, ctx, roof, reps):
                                        nat.ctypes.byref(by), nat.ctypes.byref(fl)), "profile_read")
         prof[tag] = {"ms": t.value, "launches": int(n.value), "bytes": by.value, "flops": fl.value}
     nat.check(lib.ftt_profile_enable(ctx, 0), "profile")
-    sortseg = {k: prof[k] for k in ("sort", "hist", "segment")}
-    agg = {"ms": sum(v["ms"] for v in sortseg.values()),
-           "launches": sum(v["launches"] for v in sortseg.values()),
-           "bytes": sum(v["bytes"] for v in sortseg.values()), "flops": 0.0}
-    r = roof("sort", agg)
-    if r:
-        r["kernel_class"] = "sort+hist+segment"
-        try:  # DRAM bytes per launch of the committed config-5 ncu capture
-            with open(os.path.join(ROOT, "profiles", "r01", "traffic_c5.json")) as fh:
-                r["traffic"] = json.load(fh).get("sort+hist+segment")
-        except Exception:  # noqa: BLE001
-            r["traffic"] = None
     per_class = {}
     for k in ("sort", "hist", "segment", "sweep"):
         rk = roof(k, prof[k])
         if rk:
-            per_class[k] = {"achieved_gbs": rk["achieved"], "frac": rk["frac"],
-                            "launches": rk["launches"] // reps,
+            per_class[k] = {"impl_gbs": rk["achieved"], "launches": rk["launches"] // reps,
                             "ms_per_pass": rk["ms_total"] / reps}
     # B_io + B_sel (COO read, permuted values + pivot index,
     # fixed tuples + indptr, one map per sweep step, kept arrays; one 8-byte
@@ -502,15 +526,46 @@ def index_leg_c5(ft, nat, lib, ctx, roof, reps):
     kept = sum(int(k.shape[0]) for k, _ in sw.left + sw.right)
     b_alg = (nnz * (8 * d + 8) + 16 * nnz + 8 * d * df.R + 8 * df.R * (d - 1) + 8 * kept
              + 16 * d * nnz)
-    out = {"workload": "c5_32^12_R16_s3", "nnz": nnz, "pivot": pivot, "fibers": df.R,
+    pk, pk_src = peaks()
+    ach = b_alg / (ms * 1e-3) / 1e9
+    out = {"workload": name, "nnz": nnz, "pivot": pivot, "fibers": df.R,
            "ms_per_pass": ms, "nnz_per_s": nnz / (ms * 1e-3),
-           "alg_bytes": b_alg, "alg_gbs": b_alg / (ms * 1e-3) / 1e9,
-           "roofline": r, "per_class": per_class,
-           "note": "select_p fiber counts + extract_nonzero_fibers + _index_sweeps on config 5, "
-                   "COO resident in HBM; alg_gbs = SURVEY 8(d) B_alg / pass time"}
-    del df, sw, cd, vd, a
-    torch.cuda.empty_cache()
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]),
+                        "unit": "GB/s", "frac": ach / float(pk["hbm_gbs"]),
+                        "traffic": ncu_traffic(cfg).get("index_path"),
+                        "alg_bytes": b_alg,
+                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_src})"},
+           "per_class": per_class,
+           "note": "select_p fiber counts + extract_nonzero_fibers + _index_sweeps, COO resident "
+                   "in HBM; achieved = SURVEY 8(d) B_alg (B_io + B_sel) / pass time; traffic = "
+                   "ncu dram bytes of the same pass (profiles/)"}
+    del df, sw
     return out
+
+
+def cpu_baseline(cfg, name, a, eps):
+    """The oracle on the host cores, bounded to ~10-30 s: one full
+    decomposition where that fits (configs 1, 2, 4), else the oracle's index
+    path (select_p + fiber extraction + index sweeps) on the full input --
+    the CPU reference's cheapest stages, so its nnz/s overstates the CPU."""
+    from oracle import fasttt_oracle as O
+
+    cores = cpu_threads()
+    if ORACLE_STEP_S.get(cfg, 1e9) <= 30:
+        dt, _ = oracle_step(a.shape, a.coords, a.values, eps)
+        return {"value": a.nnz / dt, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"one full {name} decomposition incl. report "
+                          "(oracle/fasttt_oracle.py on the host cores)"}
+    t0 = time.perf_counter()
+    p = O.select_p(a.shape, a.coords, a.values)
+    fib = O.extract_fibers(a.shape, a.coords, a.values, p)
+    O.index_sweeps(a.shape, p, fib["fixed_coords"])
+    dt = time.perf_counter() - t0
+    return {"value": a.nnz / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"the oracle's index path only (select_p + extract_fibers + index_sweeps "
+                      f"at p={p}) on the full {name} input, {dt:.1f} s; a full oracle "
+                      f"decomposition is ~{ORACLE_STEP_S.get(cfg, 0):.0f} s (dense LAPACK "
+                      f"gesdd of the pivot core), so this rate overstates the CPU reference"}
 
 
 def main():

@@ -123,24 +123,6 @@ def laplacian_2d_scaled(grid: int, rng):
     return rows[order], cols[order], vals[order], n
 
 
-def _tensorize(rows, cols, vals, row_dims, col_dims):
-    """Matrix -> fused tensor coordinates ``f_k = x_k * col_dims[k] + y_k``
-    (the reference's ``tensorize_matrix`` convention, ttformat.py:414-433)."""
-    d = len(row_dims)
-    x = np.empty((rows.size, d), dtype=np.int64)
-    y = np.empty((rows.size, d), dtype=np.int64)
-    rr = rows.astype(np.int64).copy()
-    cc = cols.astype(np.int64).copy()
-    for k in range(d - 1, -1, -1):
-        x[:, k] = rr % row_dims[k]
-        rr //= row_dims[k]
-        y[:, k] = cc % col_dims[k]
-        cc //= col_dims[k]
-    fused = x * np.asarray(col_dims, dtype=np.int64) + y
-    shape = tuple(a * b for a, b in zip(row_dims, col_dims))
-    return shape, fused, vals.astype(np.float64)
-
-
 # name, shape, eps, builder
 CONFIGS = {
     1: dict(name="c1_100^4_R5_s10", shape=(100,) * 4, eps=1e-10),
@@ -169,8 +151,14 @@ def gen_config(cfg: int, seed: int = 0):
         coords, vals = sum_of_rank1(shape, 4, 3, "uniform", rng, extra=2000,
                                     extra_sigma=1e-3)
     elif cfg == 4:
-        rows, cols, v, _ = laplacian_2d_scaled(256, rng)
-        shape, coords, vals = _tensorize(rows, cols, v, c["row_dims"], c["col_dims"])
+        import scipy.sparse
+
+        from .trains import tensorize_matrix
+
+        rows, cols, v, n = laplacian_2d_scaled(256, rng)
+        t = tensorize_matrix(scipy.sparse.coo_matrix((v, (rows, cols)), shape=(n, n)),
+                             c["row_dims"], c["col_dims"])
+        shape, coords, vals = t.shape, np.array(t.coords), np.array(t.values)
     elif cfg == 5:
         coords, vals = sum_of_rank1(shape, 16, 3, "normal", rng)
     else:
