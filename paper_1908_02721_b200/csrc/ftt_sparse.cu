@@ -211,140 +211,213 @@ __global__ void k_seg_reduce(int64_t nA, int kr, const int64_t *__restrict__ seg
   }
 }
 
-// Occupancy bitmap of A_tall, row-major with the columns padded to 32:
-// bit (r, c) = word r * wpr + c / 32, bit c % 32.
-__global__ void k_sp_bitmap(int64_t nnz, const int32_t *__restrict__ ridx,
-                            const int32_t *__restrict__ cidx, int64_t wpr, unsigned *__restrict__ bm) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = ridx[e], c = cidx[e];
-    atomicOr(bm + r * wpr + (c >> 5), 1u << (c & 31));
-  }
+// ---- residual energy rest2 = ||A - Q B||_F^2 in double-double ------------
+// rest2 = S2 + S1 with S2 = sum over the entries of (A_rc - (QB)_rc)^2 (a sum
+// of small nonnegative terms, plain fp64) and S1 = sum over the positions
+// WITHOUT an entry of (QB)_rc^2, evaluated as
+//     S1 = sum_c b_c^T G b_c - sum_entries (QB)_rc^2,   G = Q^T Q,
+// where both sums are ~||A||^2 and S1 is ~eps^2 ||A||^2: every term is
+// carried in double-double (~2^-104 relative, pairwise/blocked sums), so the
+// difference keeps ~1e-30 ||A||^2 absolute accuracy -- far below the
+// certificate's 1e-6 delta^2 resolution -- without forming the m x n matrix
+// Q B (the fp64 direct sum over all m n positions it replaces cost ~2.5 ms
+// on config 5; this is O(m kr^2 + nnz kr)).
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+  const double s = a + b;
+  const double bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd dd_fast(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd dd_add(dd x, dd y) {
+  dd s = dd_two_sum(x.hi, y.hi);
+  s.lo += x.lo + y.lo;
+  return dd_fast(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_prod(double a, double b) {  // exact a * b
+  const double p = a * b;
+  return {p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_mul(dd x, dd y) {
+  const double p = x.hi * y.hi;
+  const double e = fma(x.hi, y.hi, -p) + (x.hi * y.lo + x.lo * y.hi);
+  return dd_fast(p, e);
+}
+__device__ __forceinline__ dd dd_shfl_down(dd x, int o) {
+  return {__shfl_down_sync(0xffffffffu, x.hi, o), __shfl_down_sync(0xffffffffu, x.lo, o)};
 }
 
-// S1 partials: CTA = (64-column block, row chunk).  The block's B columns
-// sit in shared memory; every lane holds ROWS rows of Q (row-major copy) in
-// registers and walks the 64 columns: per column one broadcast read of the
-// B column (conflict-free), kr FMAs per row, and the occupancy bit of
-// (row, column) from the row's two bitmap words masks out positions holding
-// an entry.  One barrier per CTA; no long-latency load in the column loop.
-constexpr int RCB = 64;  // columns per CTA
-template <int KR, int ROWS>
-__global__ void __launch_bounds__(256) k_sp_resid_off(int64_t mA, int64_t nA, int kr, int ldq,
-                                                      const double *__restrict__ Qr,
-                                                      const double *__restrict__ B,
-                                                      const unsigned *__restrict__ bm, int64_t wpr,
-                                                      int64_t chunk, double *__restrict__ partial) {
-  __shared__ __align__(16) double Bs[RCB][KR];
-  __shared__ double red[8];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * RCB;
-  const int ncol = (int)min((int64_t)RCB, nA - c0);
-  for (int e = threadIdx.x; e < RCB * KR; e += blockDim.x) {
-    const int cc = e / KR, j = e - cc * KR;
-    Bs[cc][j] = (cc < ncol && j < kr) ? B[j + (c0 + cc) * (int64_t)kr] : 0.0;
-  }
-  __syncthreads();
-  const int64_t rbeg = (int64_t)blockIdx.y * chunk, rend = min(mA, rbeg + chunk);
-  const int64_t wg = c0 >> 5;  // first bitmap word of the block
-  double acc = 0.0;
-  for (int64_t base = rbeg + (int64_t)w * 32 * ROWS; base < rend; base += 8 * 32 * ROWS) {
-    double qv[ROWS][KR];
-    unsigned wd[ROWS][2];
-    bool live[ROWS];
-#pragma unroll
-    for (int i = 0; i < ROWS; ++i) {
-      const int64_t r = base + lane + 32 * i;
-      live[i] = r < rend;
-      const double *q = Qr + (live[i] ? r : 0) * ldq;  // ldq even: 16-byte rows
-#pragma unroll
-      for (int j = 0; j < KR; j += 2) {
-        double2 t = make_double2(0.0, 0.0);
-        if (live[i] && j < kr) t = __ldg(reinterpret_cast<const double2 *>(q + j));
-        qv[i][j] = t.x;
-        qv[i][j + 1] = t.y;
-      }
-      const unsigned *wp = bm + (live[i] ? r : 0) * wpr + wg;
-      wd[i][0] = live[i] ? __ldg(wp) : ~0u;
-      wd[i][1] = (live[i] && wg + 1 < wpr) ? __ldg(wp + 1) : ~0u;
-    }
-#pragma unroll 2
-    for (int cc = 0; cc < ncol; ++cc) {
-      double bv[KR];
-#pragma unroll
-      for (int j = 0; j < KR; j += 2) {
-        const double2 t = *reinterpret_cast<const double2 *>(&Bs[cc][j]);
-        bv[j] = t.x;
-        bv[j + 1] = t.y;
-      }
-#pragma unroll
-      for (int i = 0; i < ROWS; ++i) {
-        double qb = 0.0;
-#pragma unroll
-        for (int j = 0; j < KR; ++j) qb += qv[i][j] * bv[j];
-        const unsigned bit = (wd[i][cc >> 5] >> (cc & 31)) & 1u;
-        if (!bit) acc += qb * qb;
-      }
-    }
-  }
-  for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if (lane == 0) red[w] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < 8; ++i) t += red[i];
-    partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
-  }
-}
-
-// S2 partials: (A_rc - (Q B)_rc)^2 over the entries (CSC arrays), a fixed
-// entry range per block.
+// Partial Gram G = Q^T Q (row-major Q, ldq) in double-double: block b sums
+// rows [b * per, (b + 1) * per) staged in shared memory in ROWS-row tiles;
+// thread t owns the pairs (a, c) = t, t + 256, ... of the KR x KR matrix.
 template <int KR>
-__global__ void __launch_bounds__(256) k_sp_resid_on(int64_t nnz, int kr, int ldq,
-                                                     const int32_t *__restrict__ ridx,
-                                                     const int32_t *__restrict__ cidx,
-                                                     const double *__restrict__ v,
-                                                     const double *__restrict__ Qr,
-                                                     const double *__restrict__ B, int64_t per,
-                                                     double *__restrict__ partial) {
-  __shared__ double red[8];
+__global__ void __launch_bounds__(256) k_gram_dd(int64_t mA, int kr, int ldq,
+                                                 const double *__restrict__ Qr, int64_t per,
+                                                 dd *__restrict__ part) {
+  constexpr int ROWS = 4096 / KR;
+  constexpr int PAIRS = (KR * KR + 255) / 256;
+  __shared__ __align__(16) double Qs[ROWS][KR];
+  dd acc[PAIRS];
+#pragma unroll
+  for (int q = 0; q < PAIRS; ++q) acc[q] = {0.0, 0.0};
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(mA, r0 + per);
+  for (int64_t base = r0; base < r1; base += ROWS) {
+    const int nr = (int)min((int64_t)ROWS, r1 - base);
+    __syncthreads();
+    for (int e = threadIdx.x; e < ROWS * KR; e += 256) {
+      const int rr = e / KR, j = e - rr * KR;
+      Qs[rr][j] = (rr < nr && j < kr) ? Qr[(base + rr) * ldq + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PAIRS; ++q) {
+      const int pr = threadIdx.x + 256 * q;
+      if (pr < KR * KR) {
+        const int a = pr / KR, c = pr - a * KR;
+        dd s = acc[q];
+        for (int rr = 0; rr < nr; ++rr) s = dd_add(s, dd_prod(Qs[rr][a], Qs[rr][c]));
+        acc[q] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < PAIRS; ++q) {
+    const int pr = threadIdx.x + 256 * q;
+    if (pr < KR * KR) part[(int64_t)blockIdx.x * KR * KR + pr] = acc[q];
+  }
+}
+
+// G = fixed-order sum of the block partials (one thread per pair).
+__global__ void k_gram_reduce_dd(int pairs, int64_t nparts, const dd *__restrict__ part,
+                                 dd *__restrict__ G) {
+  const int pr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pr >= pairs) return;
+  dd s = {0.0, 0.0};
+  for (int64_t b = 0; b < nparts; ++b) s = dd_add(s, part[b * pairs + pr]);
+  G[pr] = s;
+}
+
+// sum over the columns c of B (kr x nA, column-major) of b_c^T G b_c in dd:
+// columns striped over the threads of the grid, a fixed-order tree per
+// block; out[blockIdx.x] = the block's partial.
+template <int KR>
+__global__ void __launch_bounds__(256) k_gram_form_dd(int64_t nA, int kr,
+                                                      const dd *__restrict__ G,
+                                                      const double *__restrict__ B,
+                                                      dd *__restrict__ out) {
+  __shared__ dd red[256];
+  dd tot = {0.0, 0.0};
+  for (int64_t c = blockIdx.x * 256 + threadIdx.x; c < nA; c += 256 * (int64_t)gridDim.x) {
+    const double *bc = B + c * kr;
+    dd col = {0.0, 0.0};
+    for (int a = 0; a < kr; ++a) {
+      for (int e = 0; e < kr; ++e) {
+        const dd w = dd_prod(bc[a], bc[e]);
+        col = dd_add(col, dd_mul(w, G[a * KR + e]));
+      }
+    }
+    tot = dd_add(tot, col);
+  }
+  red[threadIdx.x] = tot;
+  __syncthreads();
+  for (int off = 128; off; off >>= 1) {
+    if ((int)threadIdx.x < off) red[threadIdx.x] = dd_add(red[threadIdx.x], red[threadIdx.x + off]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+
+// Over the entries (CSC arrays, a fixed range per block): (QB)_rc in dd, its
+// square summed in dd (S_on), and (A_rc - (QB)_rc)^2 summed in fp64 (S2).
+template <int KR>
+__global__ void __launch_bounds__(256) k_sp_on_dd(int64_t nnz, int kr, int ldq,
+                                                  const int32_t *__restrict__ ridx,
+                                                  const int32_t *__restrict__ cidx,
+                                                  const double *__restrict__ v,
+                                                  const double *__restrict__ Qr,
+                                                  const double *__restrict__ B, int64_t per,
+                                                  dd *__restrict__ part_on,
+                                                  double *__restrict__ part_s2) {
+  __shared__ dd red1[8];
+  __shared__ double red2[8];
   const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(nnz, e0 + per);
-  double acc = 0.0;
+  dd on = {0.0, 0.0};
+  double s2 = 0.0;
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const double2 *q = reinterpret_cast<const double2 *>(Qr + (int64_t)ridx[e] * ldq);
     const double *bc = B + (int64_t)cidx[e] * kr;
-    double qb = 0.0;
+    dd qb = {0.0, 0.0};
 #pragma unroll
     for (int j = 0; j < KR; j += 2)
       if (j < kr) {
         const double2 t = __ldg(q + j / 2);
-        qb += t.x * bc[j];
-        if (j + 1 < kr) qb += t.y * bc[j + 1];
+        qb = dd_add(qb, dd_prod(t.x, bc[j]));
+        if (j + 1 < kr) qb = dd_add(qb, dd_prod(t.y, bc[j + 1]));
       }
-    const double d = v[e] - qb;
-    acc += d * d;
+    on = dd_add(on, dd_mul(qb, qb));
+    const double d = (v[e] - qb.hi) - qb.lo;
+    s2 += d * d;
   }
-  for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  for (int o = 16; o; o >>= 1) {
+    on = dd_add(on, dd_shfl_down(on, o));
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red1[threadIdx.x >> 5] = on;
+    red2[threadIdx.x >> 5] = s2;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < 8; ++i) s += red[i];
-    partial[blockIdx.x] = s;
+    dd a = {0.0, 0.0};
+    double b = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      a = dd_add(a, red1[i]);
+      b += red2[i];
+    }
+    part_on[blockIdx.x] = a;
+    part_s2[blockIdx.x] = b;
   }
 }
 
-__global__ void k_sp_sum(const double *__restrict__ p, int64_t n, double *__restrict__ out) {
-  __shared__ double s[1024];
-  double a = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += p[i];
-  s[threadIdx.x] = a;
+// rest2 = S2 + (S_all - S_on), the block partials summed in fixed order.
+__global__ void __launch_bounds__(256) k_resid_combine(int64_t n, const dd *__restrict__ part_on,
+                                                       const double *__restrict__ part_s2,
+                                                       int nall, const dd *__restrict__ s_all,
+                                                       double *__restrict__ out) {
+  __shared__ dd r1[256];
+  __shared__ double r2[256];
+  __shared__ dd all;
+  if (threadIdx.x == 0) {
+    dd t = {0.0, 0.0};
+    for (int i = 0; i < nall; ++i) t = dd_add(t, s_all[i]);
+    all = t;
+  }
+  dd a = {0.0, 0.0};
+  double b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    a = dd_add(a, part_on[i]);
+    b += part_s2[i];
+  }
+  r1[threadIdx.x] = a;
+  r2[threadIdx.x] = b;
   __syncthreads();
-  for (int off = blockDim.x / 2; off; off >>= 1) {
-    if ((int)threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+  for (int off = 128; off; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      r1[threadIdx.x] = dd_add(r1[threadIdx.x], r1[threadIdx.x + off]);
+      r2[threadIdx.x] += r2[threadIdx.x + off];
+    }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = s[0];
+  if (threadIdx.x == 0) {
+    const dd neg = {-r1[0].hi, -r1[0].lo};
+    const dd s1 = dd_add(all, neg);
+    *out = r2[0] + fmax(s1.hi + s1.lo, 0.0);
+  }
 }
 
 __global__ void k_gather_i32(int64_t n, const uint32_t *__restrict__ perm, const int32_t *__restrict__ in,
@@ -548,57 +621,50 @@ int sparse_qt_a(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, do
 
 int sparse_resid(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, const double *B,
                  double *out_dev) {
+  (void)Q;  // the row-major copy op.Qr (from sparse_qt_a) is what the kernels read
   if (kr > 64 || !op.Qr) {
     set_error("sparse residual: rank > 64 or no B");
     return FTT_ERR_INVALID;
   }
-  const int64_t ncb = ceil_div(op.nA, 32);
-  const int64_t wpr = ncb;  // bitmap words per row
-  unsigned *bm = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&bm, 4 * (size_t)op.mA * wpr));
-  FTT_CUDA(cudaMemsetAsync(bm, 0, 4 * (size_t)op.mA * wpr, ctx->stream));
-  k_sp_bitmap<<<grid_for(op.nnz, 256, 4), 256, 0, ctx->stream>>>(op.nnz, op.ridx_c, op.cidx_c, wpr,
-                                                                 bm);
-  FTT_LAUNCHED(ctx);
-  const int64_t ngx = ceil_div(op.nA, RCB);
-  const int64_t want = std::max<int64_t>(1, ceil_div(8 * (int64_t)ctx->num_sms, ngx));
-  const int64_t chunk = std::max<int64_t>(512, ceil_div(ceil_div(op.mA, want), 512) * 512);
-  const int64_t nch = ceil_div(op.mA, chunk);
+  const int64_t ngram = std::min<int64_t>(2 * (int64_t)ctx->num_sms, std::max<int64_t>(1, ceil_div(op.mA, 256)));
+  const int64_t per_g = ceil_div(op.mA, ngram);
   const int64_t per = 8192;
   const int64_t non = ceil_div(op.nnz, per);
-  if (ngx > 0x7fffffff || nch > 65535) {
-    set_error("sparse residual: grid too large");
-    return FTT_ERR_INVALID;
-  }
-  const int64_t noff = ngx * nch;
-  double *part = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&part, 8 * (size_t)(noff + non)));
-  dim3 grid((unsigned)ngx, (unsigned)nch);
+  const int kk = kr <= 8 ? 8 : kr <= 16 ? 16 : kr <= 32 ? 32 : 64;
+  char *buf = nullptr;
+  const size_t b_gram = align_up(sizeof(dd) * (size_t)ngram * kk * kk);
+  const size_t b_on = align_up(sizeof(dd) * (size_t)std::max<int64_t>(non, 1));
+  const size_t b_s2 = align_up(sizeof(double) * (size_t)std::max<int64_t>(non, 1));
+  const size_t b_g = align_up(sizeof(dd) * (size_t)kk * kk);
+  const int nform = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, ceil_div(op.nA, 256)));
+  FTT_CHECK(owned_alloc(ctx, (void **)&buf, b_gram + b_on + b_s2 + b_g + align_up(sizeof(dd) * nform)));
+  dd *gpart = reinterpret_cast<dd *>(buf);
+  dd *on = reinterpret_cast<dd *>(buf + b_gram);
+  double *s2 = reinterpret_cast<double *>(buf + b_gram + b_on);
+  dd *G = reinterpret_cast<dd *>(buf + b_gram + b_on + b_s2);
+  dd *sall = reinterpret_cast<dd *>(buf + b_gram + b_on + b_s2 + b_g);
   const int pb = prof_begin(ctx);
-#define FTT_SPR(KR_, C_)                                                                         \
-  do {                                                                                           \
-    k_sp_resid_off<KR_, C_><<<grid, 256, 0, ctx->stream>>>(op.mA, op.nA, (int)kr, (int)op.ldq,   \
-                                                           op.Qr, B, bm,                         \
-                                                           wpr, chunk, part);                    \
-    k_sp_resid_on<KR_><<<(unsigned)non, 256, 0, ctx->stream>>>(op.nnz, (int)kr, (int)op.ldq,     \
-                                                               op.ridx_c,                        \
-                                                               op.cidx_c, op.v_c, op.Qr, B, per,  \
-                                                               part + noff);                     \
+#define FTT_SPR(KR_)                                                                              \
+  do {                                                                                            \
+    k_gram_dd<KR_><<<(unsigned)ngram, 256, 0, ctx->stream>>>(op.mA, (int)kr, (int)op.ldq, op.Qr,  \
+                                                             per_g, gpart);                        \
+    k_gram_reduce_dd<<<(KR_ * KR_ + 255) / 256, 256, 0, ctx->stream>>>(KR_ * KR_, ngram, gpart, G); \
+    k_gram_form_dd<KR_><<<nform, 256, 0, ctx->stream>>>(op.nA, (int)kr, G, B, sall);             \
+    k_sp_on_dd<KR_><<<(unsigned)std::max<int64_t>(non, 1), 256, 0, ctx->stream>>>(                \
+        op.nnz, (int)kr, (int)op.ldq, op.ridx_c, op.cidx_c, op.v_c, op.Qr, B, per, on, s2);      \
   } while (0)
-  if (kr <= 8) FTT_SPR(8, 2);
-  else if (kr <= 16) FTT_SPR(16, 2);
-  else if (kr <= 32) FTT_SPR(32, 1);
-  else FTT_SPR(64, 1);
+  if (kk == 8) FTT_SPR(8);
+  else if (kk == 16) FTT_SPR(16);
+  else if (kk == 32) FTT_SPR(32);
+  else FTT_SPR(64);
 #undef FTT_SPR
   FTT_LAUNCHED(ctx);
-  // bitmap (written + read) + Q once per column group + entries; every
-  // element of Q B formed once (2 kr flops)
-  prof_end(ctx, pb, PT_GEMM, 8.0 * op.mA * wpr + 8.0 * op.mA * kr * ngx + 24.0 * op.nnz,
-           2.0 * (double)op.mA * op.nA * kr);
-  k_sp_sum<<<1, 1024, 0, ctx->stream>>>(part, noff + non, out_dev);
+  k_resid_combine<<<1, 256, 0, ctx->stream>>>(std::max<int64_t>(non, 1), on, s2, nform, sall, out_dev);
   FTT_LAUNCHED(ctx);
-  owned_free(ctx, part);
-  owned_free(ctx, bm);
+  // Q read once (Gram), the entries (16 B) + a Q row and a B column per entry
+  prof_end(ctx, pb, PT_GEMM, 8.0 * op.mA * kr + 16.0 * op.nnz, 2.0 * (double)op.mA * kr * kr +
+                                                              2.0 * (double)op.nnz * kr);
+  owned_free(ctx, buf);
   return FTT_OK;
 }
 

@@ -112,7 +112,11 @@ def test_reference_train_at_middle_pivot(cfg, pivot):
     assert rep.flops_fasttt_model == m["flops_fasttt_model"]
     assert rep.flops_ttsvd_model == m["flops_ttsvd_model"]
     assert rep.eps_actual_method == m["eps_actual_method"]
-    assert abs(rep.eps_actual - m["eps_actual"]) <= 1e-9
+    # the inner-product identity resolves ~1e-8 (the reference clamps its
+    # negative rounding noise to 0, fasttt.py:561-602): equal within 1e-6,
+    # the reference acceptance gate's floor; the TT difference within 1e-9
+    tol = 1e-6 if m["eps_actual_method"] == "inner_identity" else 1e-9
+    assert abs(rep.eps_actual - m["eps_actual"]) <= tol
     zc = _z1m(t, m["z1m_coords"])
     got = np.concatenate([ft.tt_entries(tt, t.coords), ft.tt_entries(tt, zc)])
     want = np.concatenate([z["entries_nnz"], z["entries_z1m"]])
