@@ -95,6 +95,9 @@ SIGNATURES = {
     "ftt_tt_norm": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _P_d],
     "ftt_inner_terms": [_c_p, _c_i64, _c_p, _c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p),
                         _P_d],
+    "ftt_inner_structured": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_i32,
+                             ctypes.POINTER(_c_p), _P_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
+                             _P_d],
     "ftt_tt_entries": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _c_p, _c_i64, _c_p],
 }
 _RESTYPES = {
@@ -153,8 +156,13 @@ def check(status: int, what: str = "") -> None:
 
 
 # ------------------------------------------------------------------ context
-_ctx_cache: dict = {}
-_ctx_stream: dict = {}
+# One native context per (thread, device): a context owns a workspace arena
+# and the two-phase SVD state, so threads never share one (ctypes releases
+# the GIL inside the calls).  _all_ctx lists every context for the launch
+# counter.
+_tls = threading.local()
+_all_ctx: list = []
+_all_lock = threading.Lock()
 
 
 def torch_mod():
@@ -185,25 +193,31 @@ def _current_device_stream():
 
 
 def context():
-    """The per-device native context, bound to torch's current stream."""
-    if not _ctx_cache:
+    """This thread's native context for the current device, bound to torch's
+    current stream."""
+    cache = getattr(_tls, "ctx", None)
+    if cache is None:
         torch = torch_mod()
         if not torch.cuda.is_available():
             raise RuntimeError("a CUDA device is required: the B200 FastTT path has no CPU "
                                "fallback")
         torch.cuda.init()
+        cache = _tls.ctx = {}
+        _tls.stream = {}
     lib = _lib if _lib is not None else load_library()
     dev, stream = _current_device_stream()
-    ctx = _ctx_cache.get(dev)
+    ctx = cache.get(dev)
     if ctx is None:
         h = _c_p()
         check(lib.ftt_create(dev, _c_p(stream), ctypes.byref(h)), "ftt_create")
         ctx = h
-        _ctx_cache[dev] = ctx
-        _ctx_stream[dev] = stream
-    elif _ctx_stream.get(dev) != stream:
+        cache[dev] = ctx
+        _tls.stream[dev] = stream
+        with _all_lock:
+            _all_ctx.append(ctx)
+    elif _tls.stream.get(dev) != stream:
         check(lib.ftt_set_stream(ctx, _c_p(stream)), "ftt_set_stream")
-        _ctx_stream[dev] = stream
+        _tls.stream[dev] = stream
     return ctx
 
 
@@ -215,7 +229,9 @@ def kernel_launches() -> int:
     total = 0
     if _lib is None:
         return 0
-    for ctx in _ctx_cache.values():
+    with _all_lock:
+        ctxs = list(_all_ctx)
+    for ctx in ctxs:
         total += int(_lib.ftt_kernel_launches(ctx))
     return total
 

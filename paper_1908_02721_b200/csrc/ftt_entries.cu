@@ -614,3 +614,189 @@ extern "C" int ftt_inner_terms(ftt_ctx *ctx, int64_t n, const double *values,
   return FTT_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// <a, b> for the report's inner-product identity (fasttt.py:587-602) from
+// the index structure fasttt already holds, instead of evaluating the
+// rounded train b at every nonzero coordinate independently.  The left
+// sweep's kept rows are exactly the distinct prefixes (i_0..i_k) of the
+// fibers (kept_k[j] = t * n_k + i: prefix j extends prefix t of the previous
+// step by i), the right sweep's the distinct suffixes (kept[j] = i * r + s),
+// and t_map / s_map name each fiber's prefix and suffix.  So
+//   V_k[j] = V_{k-1}[t] . b_k[:, i, :]        (left vectors, K_k x r_k)
+//   W_k[j] = b_k[:, i, :] . W_{k+1}[s]        (right vectors)
+//   M[t, i] = V_{p-1}[t] . b_p[:, i, :]       (every prefix x pivot index)
+//   b(e) = M[t_map[f], i_e] . W_{p+1}[s_map[f]]   for entry e of fiber f
+// -- per nonzero r_p multiply-adds after O(sum_k K_k r_k r_{k+1}) setup.
+namespace ftt {
+namespace {
+
+// out[j, b] = sum_a prev[t, a] core[a, i, b], (t, i) = (kept[j] / n, kept[j] % n)
+// (kept == nullptr: j itself; prev == nullptr: rin = 1 and prev = 1)
+__global__ void k_left_vec(int64_t K, const int64_t *__restrict__ kept, int64_t n, int rin,
+                           int rout, const double *__restrict__ prev,
+                           const double *__restrict__ core, double *__restrict__ out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < K * rout;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = x / rout;
+    const int b = (int)(x - j * rout);
+    const int64_t row = kept ? kept[j] : j;
+    const int64_t t = row / n, i = row - t * n;
+    double s = 0.0;
+    if (prev) {
+      const double *pv = prev + t * rin;
+      for (int a = 0; a < rin; ++a) s += pv[a] * core[(a * n + i) * rout + b];
+    } else {
+      s = core[i * rout + b];
+    }
+    out[x] = s;
+  }
+}
+
+// out[j, a] = sum_b core[a, i, b] next[s, b], (i, s) = (kept[j] / r, kept[j] % r)
+// (next == nullptr: the last core, rout = 1 and next = 1)
+__global__ void k_right_vec(int64_t K, const int64_t *__restrict__ kept, int64_t r, int64_t n,
+                            int rin, int rout, const double *__restrict__ next,
+                            const double *__restrict__ core, double *__restrict__ out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < K * rin;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = x / rin;
+    const int a = (int)(x - j * rin);
+    const int64_t row = kept[j];
+    const int64_t i = row / r, s = row - i * r;
+    const double *cr = core + (a * n + i) * rout;
+    double acc = 0.0;
+    if (next) {
+      const double *nx = next + s * rout;
+      for (int b = 0; b < rout; ++b) acc += cr[b] * nx[b];
+    } else {
+      acc = cr[0];
+    }
+    out[x] = acc;
+  }
+}
+
+// Block partials of sum_e values[e] * (M[t, i_e] . W[s]) in a fixed order.
+__global__ void __launch_bounds__(256) k_inner_struct(int64_t nnz, const int64_t *__restrict__ fiber_of,
+                                                      const int64_t *__restrict__ pidx,
+                                                      const double *__restrict__ values,
+                                                      const int64_t *__restrict__ t_map,
+                                                      const int64_t *__restrict__ s_map, int64_t np,
+                                                      int r, const double *__restrict__ M,
+                                                      const double *__restrict__ W, int64_t per,
+                                                      double *__restrict__ partial) {
+  __shared__ double red[8];
+  const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(nnz, e0 + per);
+  double acc = 0.0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int64_t f = fiber_of[e];
+    const int64_t t = t_map ? t_map[f] : 0, s = s_map ? s_map[f] : 0;
+    const double *m = M + (t * np + pidx[e]) * r;
+    double b = 0.0;
+    if (W) {
+      const double *w = W + s * r;
+      for (int c = 0; c < r; ++c) b += m[c] * w[c];
+    } else {
+      b = m[0];
+    }
+    acc += values[e] * b;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_sum_fixed(const double *__restrict__ p, int64_t n, double *__restrict__ out) {
+  __shared__ double s[256];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) a += p[i];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int off = 128; off; off >>= 1) {
+    if ((int)threadIdx.x < off) s[threadIdx.x] += s[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+}  // namespace
+}  // namespace ftt
+
+extern "C" int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims,
+                                    const int64_t *ranks, const double *const *cores,
+                                    int32_t pivot, const int64_t *const *kept,
+                                    const int64_t *kept_counts, int64_t nnz,
+                                    const int64_t *fiber_of, const int64_t *pivot_index,
+                                    const double *values, const int64_t *t_map,
+                                    const int64_t *s_map, double *out_host) {
+  if (!ctx || !out_host || d < 2 || d > 32 || pivot < 0 || pivot >= d || nnz < 0) {
+    set_error("ftt_inner_structured: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  if (ranks[0] != 1 || ranks[d] != 1) {
+    set_error("ftt_inner_structured: edge ranks must be 1");
+    return FTT_ERR_INVALID;
+  }
+  // kept[] in sweep order: left steps 0..p-1, then right steps d-1 .. p+1
+  int64_t bytes = 0;
+  for (int k = 0; k < pivot; ++k) bytes += kept_counts[k] * ranks[k + 1];
+  bytes += (pivot > 0 ? kept_counts[pivot - 1] : 1) * dims[pivot] * ranks[pivot + 1];
+  for (int q = 0; q < d - 1 - pivot; ++q) {
+    const int k = d - 1 - q;
+    bytes += kept_counts[pivot + q] * ranks[k];
+  }
+  const int64_t per = 8192;
+  const int64_t nb = std::max<int64_t>(1, ceil_div(nnz, per));
+  double *buf = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&buf, 8 * (size_t)(bytes + nb + 1)));
+  double *cur = buf;
+  const int pb = prof_begin(ctx);
+  // left vectors, then M over every (prefix, pivot index)
+  const double *V = nullptr;
+  int64_t Kl = 1;
+  for (int k = 0; k < pivot; ++k) {
+    const int64_t K = kept_counts[k];
+    k_left_vec<<<grid_for(K * ranks[k + 1], 256, 4), 256, 0, ctx->stream>>>(
+        K, kept[k], dims[k], (int)ranks[k], (int)ranks[k + 1], V, cores[k], cur);
+    FTT_LAUNCHED(ctx);
+    V = cur;
+    Kl = K;
+    cur += K * ranks[k + 1];
+  }
+  double *M = cur;
+  k_left_vec<<<grid_for(Kl * dims[pivot] * ranks[pivot + 1], 256, 4), 256, 0, ctx->stream>>>(
+      Kl * dims[pivot], nullptr, dims[pivot], (int)ranks[pivot], (int)ranks[pivot + 1], V,
+      cores[pivot], M);
+  FTT_LAUNCHED(ctx);
+  cur += Kl * dims[pivot] * ranks[pivot + 1];
+  // right vectors from the last mode inwards
+  const double *W = nullptr;
+  int64_t r_other = 1;
+  for (int q = 0; q < d - 1 - pivot; ++q) {
+    const int k = d - 1 - q;
+    const int64_t K = kept_counts[pivot + q];
+    k_right_vec<<<grid_for(K * ranks[k], 256, 4), 256, 0, ctx->stream>>>(
+        K, kept[pivot + q], r_other, dims[k], (int)ranks[k], (int)ranks[k + 1], W, cores[k], cur);
+    FTT_LAUNCHED(ctx);
+    W = cur;
+    r_other = K;
+    cur += K * ranks[k];
+  }
+  double *part = cur;
+  k_inner_struct<<<(unsigned)nb, 256, 0, ctx->stream>>>(nnz, fiber_of, pivot_index, values, t_map,
+                                                        s_map, dims[pivot], (int)ranks[pivot + 1],
+                                                        M, W, per, part);
+  FTT_LAUNCHED(ctx);
+  k_sum_fixed<<<1, 256, 0, ctx->stream>>>(part, nb, part + nb);
+  FTT_LAUNCHED(ctx);
+  prof_end(ctx, pb, PT_ENTRIES, 40.0 * (double)nnz + 8.0 * (double)bytes,
+           2.0 * (double)nnz * ranks[pivot + 1]);
+  FTT_CHECK(copy_to_host(ctx, out_host, part + nb, sizeof(double)));
+  owned_free(ctx, buf);
+  return FTT_OK;
+}

@@ -995,6 +995,36 @@ def _inner_error_device(coords_d, values_d, nnz, approx_d, na2=None):
     return math.sqrt(max(na2 - 2.0 * dot + nb2, 0.0) / na2)
 
 
+def _inner_error_structured(df, sw: DeviceSweeps, approx_d, na2):
+    """The inner-product identity with <a, b> evaluated on the fiber /
+    sweep structure (ftt_inner_structured: one prefix vector per distinct
+    prefix, one suffix vector per distinct suffix, a length-r_p dot per
+    nonzero); None when the setup would cost more than the per-entry
+    evaluation (very high ranks)."""
+    d, p = len(approx_d), df.pivot
+    cs = [c.contiguous() for c in approx_d]
+    dims = [int(c.shape[1]) for c in cs]
+    ranks = [1] + [int(c.shape[2]) for c in cs]
+    steps = list(sw.left) + list(sw.right)
+    counts = [int(k.shape[0]) for k, _ in steps]
+    kl = counts[p - 1] if p > 0 else 1
+    cost = sum(counts[k] * ranks[k] * ranks[k + 1] for k in range(p))
+    cost += kl * dims[p] * ranks[p] * ranks[p + 1]
+    cost += sum(counts[p + q] * ranks[d - 1 - q] * ranks[d - q] for q in range(d - 1 - p))
+    if cost > 4e9 or na2 == 0.0:
+        return None
+    ptrs = (nat.ctypes.c_void_p * d)(*[c.data_ptr() for c in cs])
+    kp = (nat.ctypes.c_void_p * max(len(steps), 1))(*[k.data_ptr() for k, _ in steps])
+    dot = nat.ctypes.c_double(0.0)
+    nat.check(nat.lib().ftt_inner_structured(
+        nat.context(), d, nat.i64_array(dims), nat.i64_array(ranks), ptrs, p, kp,
+        nat.i64_array(counts or [0]), df.nnz, nat.ptr(df.fiber_of), nat.ptr(df.pivot_index),
+        nat.ptr(df.values), nat.ptr(sw.t_map), nat.ptr(sw.s_map), nat.ctypes.byref(dot)),
+        "ftt_inner_structured")
+    nb2 = dev_tt_norm(cs) ** 2
+    return math.sqrt(max(na2 - 2.0 * float(dot.value) + nb2, 0.0) / na2)
+
+
 def sparse_inner_error(a: SparseTensor, approx: TTTensor) -> float:
     """Relative error via ``|a|^2 - 2<a,b> + |b|^2`` (fasttt.py:587-602)."""
     if a.shape != approx.dims:
@@ -1113,7 +1143,9 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
         if na2 is None:
             na2 = device_dot(values_d, None)
         norm_a = math.sqrt(na2)
-        inner = _inner_error_device(coords_d, values_d, nnz, out, na2)
+        inner = _inner_error_structured(df, sw, out, na2)
+        if inner is None:
+            inner = _inner_error_device(coords_d, values_d, nnz, out, na2)
         exact_shapes = [tuple(c.shape) for c in cores]
         total = _diff_total(exact_shapes, [tuple(c.shape) for c in out])
         if total <= _ERROR_MEASURE_CAP:

@@ -416,6 +416,26 @@ def dev_right_orthogonalize(cores_d):
     return cs
 
 
+def _checked_indices(coords, dims, batch):
+    """numpy's indexing contract of the reference's per-batch core slicing
+    (ttformat.py:124-136): an index outside [-n, n) raises IndexError --
+    the first batch holding one, its lowest such mode, that mode's first
+    offending value -- and negative indices wrap.  The device kernels then
+    only ever see indices in [0, n)."""
+    lim = np.asarray(dims, dtype=np.int64)
+    bad = (coords >= lim) | (coords < -lim)
+    if bad.any():
+        row = int(np.argmax(bad.any(axis=1)))
+        lo = row - row % max(int(batch), 1)
+        blk = bad[lo:lo + batch]
+        k = int(np.argmax(blk.any(axis=0)))
+        v = int(coords[lo + int(np.argmax(blk[:, k])), k])
+        raise IndexError(f"index {v} is out of bounds for axis 1 with size {dims[k]}")
+    if (coords < 0).any():
+        coords = np.where(coords < 0, coords + lim, coords)
+    return coords
+
+
 def tt_entries(t: TTTensor, coords, batch: int = 1024) -> np.ndarray:
     """Entries at ``(n, d)`` coordinates (ttformat.py:124-136), on the GPU."""
     coords = np.asarray(coords, dtype=np.int64)
@@ -423,6 +443,7 @@ def tt_entries(t: TTTensor, coords, batch: int = 1024) -> np.ndarray:
         raise ValueError(f"coords must be (n, {t.ndim})")
     if coords.shape[0] == 0:
         return np.zeros(0)
+    coords = _checked_indices(coords, t.dims, batch)
     cores_d = [to_device(c) for c in t.cores]
     return dev_tt_entries(cores_d, to_device(coords)).cpu().numpy()
 

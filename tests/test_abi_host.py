@@ -213,3 +213,34 @@ def test_api_type_errors_without_gpu():
 def test_select_p_single_mode_host_only():
     t = ft.SparseTensor((5,), np.array([[2]]), np.array([1.0]))
     assert ft.select_p(t) == 0
+
+
+def test_tt_entries_index_contract_matches_numpy():
+    """tt_entries' host-side index check reproduces the reference's numpy
+    slicing contract (ttformat.py:124-136): IndexError text of the first
+    offending batch / mode / value, negative indices wrapped."""
+    from paper_1908_02721_b200 import trains as T
+
+    dims = (3, 5, 4)
+    rng = np.random.default_rng(3)
+    cores = [rng.standard_normal((1 if k == 0 else 2, n, 1 if k == 2 else 2))
+             for k, n in enumerate(dims)]
+
+    def numpy_loop(coords, batch):
+        for lo in range(0, coords.shape[0], batch):
+            c = coords[lo:lo + batch]
+            cores[0][0, c[:, 0], :]
+            for k in range(1, 3):
+                cores[k][:, c[:, k], :]
+
+    ok = np.array([[0, 4, 3], [-1, -5, -4], [2, 0, 1]])
+    assert T._checked_indices(ok, dims, 1024).tolist() == [[0, 4, 3], [2, 0, 0], [2, 0, 1]]
+    for bad, batch in ((np.array([[0, 0, 0], [0, 5, 9]]), 1024),
+                       (np.array([[0, 0, 4], [3, 0, 0]]), 1024),
+                       (np.array([[0, 0, 4], [3, 0, 0]]), 1),
+                       (np.array([[-4, 0, 0]]), 1024)):
+        with pytest.raises(IndexError) as want:
+            numpy_loop(bad, batch)
+        with pytest.raises(IndexError) as got:
+            T._checked_indices(bad, dims, batch)
+        assert str(got.value) == str(want.value)

@@ -262,3 +262,48 @@ def test_acceptance_criterion_8_pivot_selection():
     t = ft.SparseTensor(shape, coords, z["c8_val"])
     assert t.nnz == c8["nnz"]
     assert ft.select_p(t, target_ranks=100) == c8["select_p_target100"] == 6
+
+
+def test_tt_entries_negative_and_out_of_range_indices():
+    """tt_entries keeps the reference's numpy indexing contract on the GPU
+    path: negative indices wrap, out-of-range ones raise IndexError before
+    any kernel reads a core."""
+    rng = np.random.default_rng(5)
+    dims = (4, 6, 5)
+    cores = [rng.standard_normal((1 if k == 0 else 3, n, 1 if k == 2 else 3))
+             for k, n in enumerate(dims)]
+    tt = ft.TTTensor(cores)
+    pos = np.stack([rng.integers(0, n, 500) for n in dims], 1)
+    neg = pos - np.asarray(dims)
+    assert np.array_equal(ft.tt_entries(tt, neg), ft.tt_entries(tt, pos))
+    with pytest.raises(IndexError, match="out of bounds for axis 1 with size 6"):
+        ft.tt_entries(tt, np.array([[0, 6, 0]]))
+
+
+def test_contexts_are_per_thread():
+    """Two threads decomposing at once (each gets its own native context:
+    arena and SVD state) give the same trains as one thread alone."""
+    import threading
+
+    shape, coords, vals, eps = G.gen_config(2)
+    t = ft.SparseTensor(shape, coords, vals)
+    ref_tt, ref_rep = ft.fasttt(t, eps=eps)
+    want = ft.tt_entries(ref_tt, t.coords[:5000])
+    out = {}
+
+    def run(i):
+        import torch
+
+        with torch.cuda.stream(torch.cuda.Stream()):
+            tt, rep = ft.fasttt(t, eps=eps)
+            torch.cuda.current_stream().synchronize()
+        out[i] = (rep.ranks, ft.tt_entries(tt, t.coords[:5000]))
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for i in range(2):
+        assert out[i][0] == ref_rep.ranks
+        assert rel_err(out[i][1], want) <= 1e-12
