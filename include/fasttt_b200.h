@@ -365,14 +365,15 @@ int ftt_inner_terms(ftt_ctx *ctx, int64_t n, const double *values,
  * then right steps d-1..p+1, in that order, kept_counts alike) name the
  * distinct prefixes / suffixes, t_map / s_map each fiber's; b's prefix and
  * suffix vectors are built once per distinct prefix / suffix and each
- * nonzero costs one length-r_p dot.  fiber_of / pivot_index / values: the
- * nonzeros in fiber order (ftt_extract_fibers); cores: the rounded train
- * b (ranks[0] = ranks[d] = 1).  *out_host = sum_e values[e] b(e). */
+ * nonzero costs one length-r_p dot.  indptr (R + 1) / pivot_index /
+ * values: the fibers and their nonzeros in fiber order
+ * (ftt_extract_fibers); cores: the rounded train b (ranks[0] = ranks[d] =
+ * 1).  *out_host = sum_e values[e] b(e). */
 int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims,
                          const int64_t *ranks, const double *const *cores,
                          int32_t pivot, const int64_t *const *kept,
-                         const int64_t *kept_counts, int64_t nnz,
-                         const int64_t *fiber_of, const int64_t *pivot_index,
+                         const int64_t *kept_counts, int64_t R,
+                         const int64_t *indptr, const int64_t *pivot_index,
                          const double *values, const int64_t *t_map,
                          const int64_t *s_map, double *out_host);
 

@@ -653,53 +653,105 @@ __global__ void k_left_vec(int64_t K, const int64_t *__restrict__ kept, int64_t 
   }
 }
 
-// out[j, a] = sum_b core[a, i, b] next[s, b], (i, s) = (kept[j] / r, kept[j] % r)
-// (next == nullptr: the last core, rout = 1 and next = 1)
+// out[j, :] = core[:, i, :] . next[s, :], (i, s) = (kept[j] / r, kept[j] % r):
+// RO lanes per kept row j (RO = 8 / 16 / 32 = rout): lane b holds next[s, b]
+// and reads core[a, i, b] for every a (coalesced rows), the products are
+// reduced over the RO lanes (butterfly) and lane a % RO keeps out[j, a].
+// RO = 0: generic thread-per-row loop (other ranks, the last core).
+template <int RO>
 __global__ void k_right_vec(int64_t K, const int64_t *__restrict__ kept, int64_t r, int64_t n,
                             int rin, int rout, const double *__restrict__ next,
                             const double *__restrict__ core, double *__restrict__ out) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < K * rin;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = x / rin;
-    const int a = (int)(x - j * rin);
+  if constexpr (RO > 0) {
+    constexpr int RPW = 32 / RO;  // kept rows per warp
+    const int lane = threadIdx.x & 31, b = lane % RO;
+    const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
+    const unsigned mask = 0xffffffffu;
+    for (int64_t base = wg * RPW; base < K; base += stride) {  // warp-uniform
+      const int64_t j0 = base + lane / RO;
+      const bool live = j0 < K;
+      const int64_t j = live ? j0 : 0;
+      const int64_t row = kept[j];
+      const int64_t i = row / r, s = row - i * r;
+      const double w = next[s * RO + b];
+      for (int a0 = 0; a0 < rin; a0 += RO) {
+        double keep = 0.0;
+        for (int a = a0; a < a0 + RO; ++a) {
+          double x = a < rin ? core[(a * n + i) * RO + b] * w : 0.0;
+#pragma unroll
+          for (int o = RO / 2; o; o >>= 1) x += __shfl_xor_sync(mask, x, o);
+          if (a - a0 == b) keep = x;
+        }
+        if (live && a0 + b < rin) out[j * rin + a0 + b] = keep;
+      }
+    }
+  } else {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < K;
+       j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = kept[j];
     const int64_t i = row / r, s = row - i * r;
-    const double *cr = core + (a * n + i) * rout;
-    double acc = 0.0;
-    if (next) {
-      const double *nx = next + s * rout;
-      for (int b = 0; b < rout; ++b) acc += cr[b] * nx[b];
-    } else {
-      acc = cr[0];
+    for (int a = 0; a < rin; ++a) {
+      const double *cr = core + (a * n + i) * rout;
+      double acc = 0.0;
+      if (next) {
+        const double *nx = next + s * rout;
+        for (int c = 0; c < rout; ++c) acc += cr[c] * nx[c];
+      } else {
+        acc = cr[0];
+      }
+      out[j * rin + a] = acc;
     }
-    out[x] = acc;
+  }
   }
 }
 
-// Block partials of sum_e values[e] * (M[t, i_e] . W[s]) in a fixed order.
-__global__ void __launch_bounds__(256) k_inner_struct(int64_t nnz, const int64_t *__restrict__ fiber_of,
+// Block partials of sum_e values[e] * (M[t, i_e] . W[s]) = sum_c W[s, c]
+// (sum_e values[e] M[t, i_e, c]): RR lanes per fiber f (lane c holds W[s, c]
+// and reads M rows coalesced), the fiber's nonzeros indptr[f]..indptr[f+1]
+// in order, each lane accumulating its own c; fixed-order block sums.
+// RR = 0: one thread per fiber (other ranks, no right part).
+template <int RR>
+__global__ void __launch_bounds__(256) k_inner_struct(int64_t R, const int64_t *__restrict__ indptr,
                                                       const int64_t *__restrict__ pidx,
                                                       const double *__restrict__ values,
                                                       const int64_t *__restrict__ t_map,
                                                       const int64_t *__restrict__ s_map, int64_t np,
                                                       int r, const double *__restrict__ M,
-                                                      const double *__restrict__ W, int64_t per,
+                                                      const double *__restrict__ W,
                                                       double *__restrict__ partial) {
   __shared__ double red[8];
-  const int64_t e0 = (int64_t)blockIdx.x * per, e1 = min(nnz, e0 + per);
   double acc = 0.0;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const int64_t f = fiber_of[e];
-    const int64_t t = t_map ? t_map[f] : 0, s = s_map ? s_map[f] : 0;
-    const double *m = M + (t * np + pidx[e]) * r;
-    double b = 0.0;
-    if (W) {
-      const double *w = W + s * r;
-      for (int c = 0; c < r; ++c) b += m[c] * w[c];
-    } else {
-      b = m[0];
+  if constexpr (RR > 0) {
+    const int c = threadIdx.x % RR;
+    const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / RR;
+    const int64_t gs = ((int64_t)gridDim.x * blockDim.x) / RR;
+    for (int64_t f = g0; f < R; f += gs) {
+      const int64_t t = t_map ? t_map[f] : 0, s = s_map[f];
+      const double w = W[s * RR + c];
+      const double *mrow = M + t * np * RR + c;
+      const int64_t e1 = indptr[f + 1];
+      double sv = 0.0;
+      for (int64_t e = indptr[f]; e < e1; ++e) sv += values[e] * mrow[pidx[e] * RR];
+      acc += w * sv;
     }
-    acc += values[e] * b;
+  } else {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
+         f += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t t = t_map ? t_map[f] : 0, s = s_map ? s_map[f] : 0;
+      const double *mrow = M + t * np * r;
+      for (int64_t e = indptr[f]; e < indptr[f + 1]; ++e) {
+        const double *m = mrow + pidx[e] * r;
+        double b = 0.0;
+        if (W) {
+          const double *w = W + s * r;
+          for (int c = 0; c < r; ++c) b += m[c] * w[c];
+        } else {
+          b = m[0];
+        }
+        acc += values[e] * b;
+      }
+    }
   }
   for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -730,11 +782,11 @@ __global__ void k_sum_fixed(const double *__restrict__ p, int64_t n, double *__r
 extern "C" int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims,
                                     const int64_t *ranks, const double *const *cores,
                                     int32_t pivot, const int64_t *const *kept,
-                                    const int64_t *kept_counts, int64_t nnz,
-                                    const int64_t *fiber_of, const int64_t *pivot_index,
+                                    const int64_t *kept_counts, int64_t R,
+                                    const int64_t *indptr, const int64_t *pivot_index,
                                     const double *values, const int64_t *t_map,
                                     const int64_t *s_map, double *out_host) {
-  if (!ctx || !out_host || d < 2 || d > 32 || pivot < 0 || pivot >= d || nnz < 0) {
+  if (!ctx || !out_host || d < 2 || d > 32 || pivot < 0 || pivot >= d || R < 0) {
     set_error("ftt_inner_structured: invalid arguments");
     return FTT_ERR_INVALID;
   }
@@ -750,8 +802,7 @@ extern "C" int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims
     const int k = d - 1 - q;
     bytes += kept_counts[pivot + q] * ranks[k];
   }
-  const int64_t per = 8192;
-  const int64_t nb = std::max<int64_t>(1, ceil_div(nnz, per));
+  const int64_t nb = std::min<int64_t>(16 * (int64_t)ctx->num_sms, std::max<int64_t>(1, ceil_div(R, 16)));
   double *buf = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&buf, 8 * (size_t)(bytes + nb + 1)));
   double *cur = buf;
@@ -780,22 +831,36 @@ extern "C" int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims
   for (int q = 0; q < d - 1 - pivot; ++q) {
     const int k = d - 1 - q;
     const int64_t K = kept_counts[pivot + q];
-    k_right_vec<<<grid_for(K * ranks[k], 256, 4), 256, 0, ctx->stream>>>(
-        K, kept[pivot + q], r_other, dims[k], (int)ranks[k], (int)ranks[k + 1], W, cores[k], cur);
+    const int ro = (int)ranks[k + 1];
+#define FTT_RV(RO_)                                                                           \
+  k_right_vec<RO_><<<grid_for(K * (RO_ > 0 ? RO_ : 1), 256, 1), 256, 0, ctx->stream>>>(       \
+      K, kept[pivot + q], r_other, dims[k], (int)ranks[k], ro, W, cores[k], cur)
+    if (ro == 1) FTT_RV(1);
+    else if (ro == 8) FTT_RV(8);
+    else if (ro == 16) FTT_RV(16);
+    else if (ro == 32) FTT_RV(32);
+    else FTT_RV(0);
+#undef FTT_RV
     FTT_LAUNCHED(ctx);
     W = cur;
     r_other = K;
     cur += K * ranks[k];
   }
   double *part = cur;
-  k_inner_struct<<<(unsigned)nb, 256, 0, ctx->stream>>>(nnz, fiber_of, pivot_index, values, t_map,
-                                                        s_map, dims[pivot], (int)ranks[pivot + 1],
-                                                        M, W, per, part);
+  const int rr = (int)ranks[pivot + 1];
+#define FTT_IS(RR_)                                                                           \
+  k_inner_struct<RR_><<<(unsigned)nb, 256, 0, ctx->stream>>>(R, indptr, pivot_index, values,  \
+                                                             t_map, s_map, dims[pivot], rr, M, \
+                                                             W, part)
+  if (rr == 8 && W) FTT_IS(8);
+  else if (rr == 16 && W) FTT_IS(16);
+  else if (rr == 32 && W) FTT_IS(32);
+  else FTT_IS(0);
+#undef FTT_IS
   FTT_LAUNCHED(ctx);
   k_sum_fixed<<<1, 256, 0, ctx->stream>>>(part, nb, part + nb);
   FTT_LAUNCHED(ctx);
-  prof_end(ctx, pb, PT_ENTRIES, 40.0 * (double)nnz + 8.0 * (double)bytes,
-           2.0 * (double)nnz * ranks[pivot + 1]);
+  prof_end(ctx, pb, PT_ENTRIES, 40.0 * (double)R + 8.0 * (double)bytes, 0.0);
   FTT_CHECK(copy_to_host(ctx, out_host, part + nb, sizeof(double)));
   owned_free(ctx, buf);
   return FTT_OK;

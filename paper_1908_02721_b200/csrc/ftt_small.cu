@@ -630,6 +630,202 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const do
   for (int e = tid; e < n * n; e += (int)blockDim.x) Po[e] = P[e];
 }
 
+// The same factorisation for a short tall block (m x n, n <= 16) with the
+// rotations chosen on R instead of on X: X = Q R (Householder in shared
+// memory, a warp per column for the dots, 2 barriers per column), one-sided
+// Jacobi R P = Y_R by ONE warp without CTA barriers (4 lanes per column
+// pair, 8 pairs per round; the dots are over n rows instead of m), then
+// Y = Q [Y_R; 0] (the reflectors in reverse).  Same outputs, convergence rule
+// and noise floor (m of X) as k_jacobi_direct; X P = Q R P = Y.
+constexpr int QJ_NT = 512;
+__global__ void __launch_bounds__(QJ_NT) k_jacobi_qr(int m, int n, const double *__restrict__ A,
+                                                     int64_t lda, int trans,
+                                                     double *__restrict__ Yo,
+                                                     double *__restrict__ Po,
+                                                     double *__restrict__ norms, int max_sweeps,
+                                                     int *__restrict__ status,
+                                                     const double *__restrict__ extra_src,
+                                                     double *__restrict__ extra_dst) {
+  extern __shared__ double S[];  // X m x n | Y m x n | R n x n | P n x n (all col-major)
+  __shared__ double red[QJ_NT / 32];
+  __shared__ double s_dot[16];
+  __shared__ double s_tau[16];
+  __shared__ int s_sweeps;
+  double *X = S, *Y = S + (size_t)m * n, *R = Y + (size_t)m * n, *P = R + n * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double f = 0.0;
+  int bad = 0;
+  for (int e = tid; e < m * n; e += QJ_NT) {
+    const int j = e / m, i = e - j * m;
+    const double v = trans ? A[j + (int64_t)i * lda] : A[i + (int64_t)j * lda];
+    bad |= !isfinite(v);
+    X[e] = v;
+    f += v * v;
+  }
+  if (tid == 0 && extra_src) *extra_dst = *extra_src;
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) {
+      status[0] = 1;
+      status[1] = 0;
+    }
+    return;
+  }
+  const double fro2 = cta_sum(f, red);
+  // ---- Householder QR: column j's reflector v = [1; x_j(j+1:) / v0]
+  __shared__ double s_w[16];
+  for (int j = 0; j < n; ++j) {
+    // warp w: column c = j + w; every warp also forms |x_j(j+1:)|^2 itself
+    // (same order in every warp: bitwise the same tau), then w_c =
+    // tau (x_jc + (x_j . x_c) / v0) before anything is updated
+    const int c = j + warp;
+    double tau = 0.0, beta = 0.0, v0 = 1.0;
+    if (c < n) {
+      const double *xj = X + (size_t)j * m, *xc = X + (size_t)c * m;
+      double d = 0.0, sub = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) {
+        const double u = xj[i];
+        d += u * xc[i];
+        sub += u * u;
+      }
+      d = warp_sum(d);
+      sub = warp_sum(sub);
+      const double alpha = xj[j];
+      beta = alpha;
+      if (sub > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sub), alpha);
+        v0 = alpha - beta;
+        tau = (beta - alpha) / beta;
+      }
+      if (lane == 0) {
+        s_w[warp] = tau * (xc[j] + d / v0);
+        if (warp == 0) {
+          s_tau[j] = tau;
+          s_dot[0] = beta;
+          s_dot[1] = v0;
+        }
+      }
+    }
+    __syncthreads();
+    tau = s_tau[j];
+    v0 = s_dot[1];
+    if (tau != 0.0) {
+      const double inv = 1.0 / v0;
+      const int nc = n - j - 1, mr = m - j;
+      for (int e = tid; e < nc * mr; e += QJ_NT) {
+        const int k = e / mr, i = j + (e - k * mr), cc = j + 1 + k;
+        X[i + (size_t)cc * m] -= s_w[k + 1] * (i == j ? 1.0 : X[i + (size_t)j * m] * inv);
+      }
+    }
+    __syncthreads();
+    if (tau != 0.0) {
+      const double inv = 1.0 / v0;
+      for (int i = j + 1 + tid; i < m; i += QJ_NT) X[i + (size_t)j * m] *= inv;
+    }
+    if (tid == 0) X[j + (size_t)j * m] = s_dot[0];
+    // the next step's dots read columns > j only, and its barrier orders
+    // these writes before column j is read again
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += QJ_NT) {
+    const int b = e / n, a = e - b * n;
+    R[e] = a <= b ? X[a + (size_t)b * m] : 0.0;
+    P[e] = a == b ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // ---- one-sided Jacobi on R by warp 0: pair g = lane / 4, rows lane % 4 + 4 k
+  if (warp == 0) {
+    const double tol = kEps * sqrt((double)n);
+    const double floor = 0.01 * kEps * kEps * (double)m * fro2;
+    const int ne = n + (n & 1), g = lane >> 2, sl = lane & 3;
+    int sweeps = -1;
+    for (int sw = 0; sw < max_sweeps && n > 1; ++sw) {
+      int any = 0;
+      for (int round = 0; round < ne - 1; ++round) {
+        int p = 0, q = 0;
+        const bool live = g < ne / 2;
+        if (live) rr_pair(ne, round, g, &p, &q);
+        const bool ok = live && p < n && q < n;
+        double *rp = R + (size_t)(ok ? p : 0) * n, *rq = R + (size_t)(ok ? q : 0) * n;
+        double a = 0.0, b = 0.0, gg = 0.0;
+        if (ok)
+          for (int i = sl; i < n; i += 4) {
+            const double u = rp[i], v = rq[i];
+            a += u * u;
+            b += v * v;
+            gg += u * v;
+          }
+        // sum over the pair's 4 lanes (xor 1, 2: bitwise the same in all 4)
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          gg += __shfl_xor_sync(0xffffffffu, gg, o);
+        }
+        if (ok && a > floor && b > floor && fabs(gg) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * gg);
+          const double t = copysign(1.0 / (fabs(zeta) + sqrt(1.0 + zeta * zeta)), zeta);
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
+          double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
+          for (int i = sl; i < n; i += 4) {
+            const double u = rp[i], v = rq[i];
+            rp[i] = cs * u - sn * v;
+            rq[i] = sn * u + cs * v;
+            const double pu = pp[i], pv = pq[i];
+            pp[i] = cs * pu - sn * pv;
+            pq[i] = sn * pu + cs * pv;
+          }
+          any = 1;
+        }
+        __syncwarp();
+      }
+      if (!__any_sync(0xffffffffu, any)) {
+        sweeps = sw + 1;
+        break;
+      }
+    }
+    if (n <= 1) sweeps = 1;
+    if (lane == 0) s_sweeps = sweeps;
+  }
+  __syncthreads();
+  // ---- Y = Q [Y_R; 0]: H_{n-1} first, H_0 last
+  for (int e = tid; e < m * n; e += QJ_NT) {
+    const int c = e / m, i = e - c * m;
+    Y[e] = i < n ? R[i + c * n] : 0.0;
+  }
+  __syncthreads();
+  for (int j = n - 1; j >= 0; --j) {
+    const double tau = s_tau[j];
+    if (tau == 0.0) continue;  // uniform: s_tau is shared
+    const int c = warp;
+    if (c < n) {
+      const double *v = X + (size_t)j * m, *yc = Y + (size_t)c * m;
+      double d = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) d += v[i] * yc[i];
+      d = warp_sum(d);
+      if (lane == 0) s_dot[c] = tau * (yc[j] + d);
+    }
+    __syncthreads();
+    for (int e = tid; e < n * (m - j); e += QJ_NT) {
+      const int cc = e / (m - j), i = j + e % (m - j);
+      Y[i + (size_t)cc * m] -= s_dot[cc] * (i == j ? 1.0 : X[i + (size_t)j * m]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    status[0] = s_sweeps < 0 ? 2 : 0;
+    status[1] = s_sweeps;
+  }
+  for (int j = warp; j < n; j += QJ_NT / 32) {
+    double s2 = 0.0;
+    for (int i = lane; i < n; i += 32) s2 += R[i + (size_t)j * n] * R[i + (size_t)j * n];
+    s2 = warp_sum(s2);
+    if (lane == 0) norms[j] = sqrt(s2);
+  }
+  for (int e = tid; e < m * n; e += QJ_NT) Yo[e] = Y[e];
+  for (int e = tid; e < n * n; e += QJ_NT) Po[e] = P[e];
+}
+
 }  // namespace
 
 bool tsqr_ok(int64_t m, int64_t n) { return n >= 1 && n <= 64 && m >= n; }
@@ -827,8 +1023,21 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
   wpp = std::max(1, std::min(wpp, SVD_NT / 32 / std::max(1, npairs)));
   const int jt = 32 * std::max(1, npairs) * wpp;
   const int max_sweeps = 60;
-  k_jacobi_direct<<<1, jt, 8 * (size_t)(m * n + n * n), ctx->stream>>>(
-      (int)m, (int)n, A, lda, trans, wpp, Y, P, dev + 2, max_sweeps, status, extra_dev, dev + 1);
+  static const bool qr_off = getenv("FTT_NO_QR_JACOBI") != nullptr;
+  const size_t qj_smem = 8 * (size_t)(2 * m * n + 2 * n * n);
+  if (!qr_off && n <= 16 && qj_smem <= 200 * 1024) {
+    static bool qattr = false;
+    if (!qattr) {
+      FTT_CUDA(cudaFuncSetAttribute(k_jacobi_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024));
+      qattr = true;
+    }
+    k_jacobi_qr<<<1, QJ_NT, qj_smem, ctx->stream>>>((int)m, (int)n, A, lda, trans, Y, P, dev + 2,
+                                                    max_sweeps, status, extra_dev, dev + 1);
+  } else {
+    k_jacobi_direct<<<1, jt, 8 * (size_t)(m * n + n * n), ctx->stream>>>(
+        (int)m, (int)n, A, lda, trans, wpp, Y, P, dev + 2, max_sweeps, status, extra_dev, dev + 1);
+  }
   FTT_LAUNCHED(ctx);
   std::vector<double> h(n + 2);
   FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));

@@ -1018,7 +1018,7 @@ def _inner_error_structured(df, sw: DeviceSweeps, approx_d, na2):
     dot = nat.ctypes.c_double(0.0)
     nat.check(nat.lib().ftt_inner_structured(
         nat.context(), d, nat.i64_array(dims), nat.i64_array(ranks), ptrs, p, kp,
-        nat.i64_array(counts or [0]), df.nnz, nat.ptr(df.fiber_of), nat.ptr(df.pivot_index),
+        nat.i64_array(counts or [0]), df.R, nat.ptr(df.indptr), nat.ptr(df.pivot_index),
         nat.ptr(df.values), nat.ptr(sw.t_map), nat.ptr(sw.s_map), nat.ctypes.byref(dot)),
         "ftt_inner_structured")
     nb2 = dev_tt_norm(cs) ** 2
