@@ -129,6 +129,28 @@ void ftt_free_host(void *p);
 
 /* ---------------------------------------------------- index path (int) */
 
+/* The device COO as its canonical C-order linear index (SparseTensor's
+ * sort key, tensor.py:75-100 linearize): one int64 per nonzero,
+ * strictly increasing.  The entry points below read it instead of the
+ * nnz x d coordinates (8 B per nonzero instead of 8d). */
+int ftt_linearize(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                  const int64_t *dims_host, int64_t *lin_out);
+/* select_p's fiber counts for every pivot (fasttt.py:536-541) from lin:
+ * pivots p >= ceil(d/2) on lin itself (chunks aligned to the prefix over
+ * modes < ceil(d/2)), the others on lin bucketed by a hash of the suffix
+ * over modes >= ceil(d/2) (two radix passes), shared-memory hash sets per
+ * chunk.  coords (optional) serve pivots whose groups exceed a chunk. */
+int ftt_fiber_counts_lin(ftt_ctx *ctx, const int64_t *lin, const int64_t *coords,
+                         int64_t nnz, int32_t d, const int64_t *dims_host,
+                         int64_t *counts_host);
+/* ftt_extract_fibers (tensor.py:374-403) with the fiber keys built from
+ * lin. */
+int ftt_extract_fibers_lin(ftt_ctx *ctx, const int64_t *lin, const double *values,
+                           int64_t nnz, int32_t d, const int64_t *dims_host,
+                           int32_t pivot, int64_t *fixed_lin, int64_t *indptr,
+                           int64_t *fiber_of, int64_t *pivot_index,
+                           double *values_out, int64_t *num_fibers_out);
+
 /* Distinct fixed tuples for one pivot mode: the fiber count R_p computed
  * by select_p, `np.unique(linearize(rest_dims, coords[:, rest])).size`
  * (fasttt.py:537-541).  coords: nnz x d int64 row-major. */

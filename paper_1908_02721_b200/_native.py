@@ -46,6 +46,10 @@ SIGNATURES = {
     "ftt_bench_dmma": [_c_p, _c_i64, _P_d],
     "ftt_fiber_count": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, _P_i64],
     "ftt_fiber_counts_all": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _P_i64],
+    "ftt_linearize": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_p],
+    "ftt_fiber_counts_lin": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _P_i64],
+    "ftt_extract_fibers_lin": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32,
+                               _c_p, _c_p, _c_p, _c_p, _c_p, _P_i64],
     "ftt_extract_fibers": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32,
                            _c_p, _c_p, _c_p, _c_p, _c_p, _P_i64],
     "ftt_depar_quasi_perm": [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _P_i64],

@@ -165,7 +165,7 @@ class SparseTensor:
         object.__setattr__(t, "coords", c)
         object.__setattr__(t, "values", v)
         object.__setattr__(t, "_lin", None)
-        object.__setattr__(t, "_dev", (coords_d, values_d))
+        object.__setattr__(t, "_dev", (coords_d, values_d, None))
         object.__setattr__(t, "_pin", None)
         return t
 
@@ -218,14 +218,29 @@ class SparseTensor:
                 object.__setattr__(self, "_pin", pin)
             c = pin[0].to("cuda", non_blocking=True)
             v = pin[1].to("cuda", non_blocking=True)
+            lin = None
             if compact:
                 coords = torch.empty(self.coords.shape, dtype=torch.int64, device="cuda")
                 nat.check(nat.lib().ftt_delinearize(nat.context(), nat.ptr(c), self.nnz, self.ndim,
                                                     nat.i64_array(self.shape), nat.ptr(coords)),
                           "ftt_delinearize")
-                c = coords
-            object.__setattr__(self, "_dev", (c, v))
-        return self._dev
+                lin, c = c, coords
+            object.__setattr__(self, "_dev", (c, v, lin))
+        return self._dev[0], self._dev[1]
+
+    def device_lin(self):
+        """The canonical C-order linear index on the device (cached): the
+        compact form the index kernels read (8 B per nonzero)."""
+        c, v = self.device_arrays()
+        lin = self._dev[2]
+        if lin is None:
+            torch = nat.torch_mod()
+            lin = torch.empty(max(self.nnz, 1), dtype=torch.int64, device="cuda")
+            nat.check(nat.lib().ftt_linearize(nat.context(), nat.ptr(c), self.nnz, self.ndim,
+                                              nat.i64_array(self.shape), nat.ptr(lin)),
+                      "ftt_linearize")
+            object.__setattr__(self, "_dev", (c, v, lin))
+        return lin
 
     @property
     def h2d_bytes(self) -> int:
@@ -359,8 +374,9 @@ class DeviceFibers:
         return np.ascontiguousarray(out.cpu().numpy().T)
 
 
-def fibers_device(dims, pivot, coords_d, values_d, nnz) -> DeviceFibers:
-    """ftt_extract_fibers on device arrays."""
+def fibers_device(dims, pivot, coords_d, values_d, nnz, lin_d=None) -> DeviceFibers:
+    """ftt_extract_fibers on device arrays (ftt_extract_fibers_lin when the
+    canonical linear index is given)."""
     torch = nat.torch_mod()
     d = len(dims)
     cap = max(nnz, 1)
@@ -370,10 +386,16 @@ def fibers_device(dims, pivot, coords_d, values_d, nnz) -> DeviceFibers:
     pidx = torch.empty(cap, dtype=torch.int64, device="cuda")
     vals = torch.empty(cap, dtype=torch.float64, device="cuda")
     R = nat.ctypes.c_int64(0)
-    nat.check(nat.lib().ftt_extract_fibers(
-        nat.context(), nat.ptr(coords_d), nat.ptr(values_d), int(nnz), d, nat.i64_array(dims),
-        int(pivot), nat.ptr(fixed_lin), nat.ptr(indptr), nat.ptr(fiber_of), nat.ptr(pidx),
-        nat.ptr(vals), nat.ctypes.byref(R)), "ftt_extract_fibers")
+    if lin_d is not None:
+        nat.check(nat.lib().ftt_extract_fibers_lin(
+            nat.context(), nat.ptr(lin_d), nat.ptr(values_d), int(nnz), d, nat.i64_array(dims),
+            int(pivot), nat.ptr(fixed_lin), nat.ptr(indptr), nat.ptr(fiber_of), nat.ptr(pidx),
+            nat.ptr(vals), nat.ctypes.byref(R)), "ftt_extract_fibers_lin")
+    else:
+        nat.check(nat.lib().ftt_extract_fibers(
+            nat.context(), nat.ptr(coords_d), nat.ptr(values_d), int(nnz), d, nat.i64_array(dims),
+            int(pivot), nat.ptr(fixed_lin), nat.ptr(indptr), nat.ptr(fiber_of), nat.ptr(pidx),
+            nat.ptr(vals), nat.ctypes.byref(R)), "ftt_extract_fibers")
     R = int(R.value)
     return DeviceFibers(tuple(dims), int(pivot), R, int(nnz), fixed_lin[:R], indptr[:R + 1],
                         fiber_of[:nnz], pidx[:nnz], vals[:nnz])
@@ -389,7 +411,7 @@ def extract_nonzero_fibers(t: SparseTensor, pivot: int) -> FiberSet:
         return FiberSet(t.shape, pivot, np.zeros((0, max(d - 1, 0)), np.int64),
                         np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
     c, v = t.device_arrays()
-    df = fibers_device(t.shape, pivot, c, v, t.nnz)
+    df = fibers_device(t.shape, pivot, c, v, t.nnz, lin_d=t.device_lin())
     fixed = df.fixed_coords_host() if d > 1 else np.zeros((df.R, 0), np.int64)
     return FiberSet(t.shape, pivot, fixed, df.indptr.cpu().numpy(), df.pivot_index.cpu().numpy(),
                     df.values.cpu().numpy(), _dev=df)

@@ -3,6 +3,8 @@
 
 #include <chrono>
 
+#include <stdlib.h>
+
 #include "ftt_common.cuh"
 
 namespace ftt {
@@ -191,6 +193,24 @@ int ftt_create(int device, void *stream, ftt_ctx **ctx_out) {
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      // Pre-grow the pool once: a decomposition's per-step buffers vary in
+      // size, and a request that does not fit the pool's free space maps new
+      // physical memory inside the call (measured ~2 ms per growth on
+      // config 5, recurring as the pool fragments).  The block is freed at
+      // once and stays reserved (threshold above) for sub-allocation.
+      uint64_t reserved = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      const char *env = getenv("FTT_POOL_RESERVE_MB");
+      const size_t want = (size_t)(env ? atoll(env) : 4096) << 20;
+      if (want > reserved) {
+        void *blk = nullptr;
+        if (cudaMallocAsync(&blk, want - reserved, ctx->stream) == cudaSuccess) {
+          cudaFreeAsync(blk, ctx->stream);
+          cudaStreamSynchronize(ctx->stream);
+        } else {
+          cudaGetLastError();
+        }
+      }
     }
   }
   cudaError_t e = cudaMallocHost(&ctx->pinned, 65536);

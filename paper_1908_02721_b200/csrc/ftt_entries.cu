@@ -835,7 +835,8 @@ extern "C" int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims
 #define FTT_RV(RO_)                                                                           \
   k_right_vec<RO_><<<grid_for(K * (RO_ > 0 ? RO_ : 1), 256, 1), 256, 0, ctx->stream>>>(       \
       K, kept[pivot + q], r_other, dims[k], (int)ranks[k], ro, W, cores[k], cur)
-    if (ro == 1) FTT_RV(1);
+    if (!W) FTT_RV(0);  // the last core: no next vector
+    else if (ro == 1) FTT_RV(1);
     else if (ro == 8) FTT_RV(8);
     else if (ro == 16) FTT_RV(16);
     else if (ro == 32) FTT_RV(32);

@@ -55,6 +55,15 @@ struct KeySpec {
   int64_t mult[32];
 };
 
+// Radix digit of a key for pass `shift` (bits [shift, shift + 8) of the key
+// itself: the ordinary LSD sort).
+struct DigitShift {
+  int shift;
+  __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
+    return (uint32_t)((k >> shift) & 255);
+  }
+};
+
 // Fused: build one key per nonzero from coords + per-block digit
 // histograms of every pass.  Writes keys and the identity payload.
 __global__ void __launch_bounds__(256) k_keys_hist(const int64_t *__restrict__ coords, int64_t n,
@@ -118,10 +127,10 @@ __global__ void k_hist_scan(uint32_t *ghist) {
   h[t] = s[t] - h[t];  // exclusive
 }
 
-template <bool HAS_VALS, int ITEMS = RS_ITEMS>
+template <bool HAS_VALS, int ITEMS = RS_ITEMS, class DG = DigitShift>
 __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
-    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ digit_start,
+    uint32_t *__restrict__ vout, int64_t n, DG dgf, const uint32_t *__restrict__ digit_start,
     uint32_t *__restrict__ status, uint32_t *__restrict__ tile_counter) {
   __shared__ uint32_t s_warp[RS_WARPS][RADIX];
   __shared__ uint32_t s_excl[RADIX];
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     int64_t idx = wbase + i * 32 + lane;
-    uint32_t dg = idx < n ? (uint32_t)((k[i] >> shift) & 255) : 256u;
+    uint32_t dg = idx < n ? dgf(k[i]) : 256u;
     uint32_t peers = __match_any_sync(0xffffffffu, dg);
     int leader = __ffs(peers) - 1;
     uint32_t b = 0;
@@ -219,7 +228,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
   for (int i = 0; i < ITEMS; ++i) {
     int64_t idx = wbase + i * 32 + lane;
     if (idx < n) {
-      uint32_t dg = (uint32_t)((k[i] >> shift) & 255);
+      uint32_t dg = dgf(k[i]);
       uint32_t pos = s_excl[dg] + s_warp[warp][dg] + rank[i];
       s_keys[pos] = k[i];
       if (HAS_VALS) s_vals[pos] = v[i];
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
   const int tile_n = (int)min((int64_t)(RS_THREADS * ITEMS), n - base);
   for (int j = tid; j < tile_n; j += RS_THREADS) {
     uint64_t key = s_keys[j];
-    uint32_t dg = (uint32_t)((key >> shift) & 255);
+    uint32_t dg = dgf(key);
     uint32_t out = s_gbase[dg] + (j - s_excl[dg]);
     kout[out] = key;
     if (HAS_VALS) vout[out] = s_vals[j];
@@ -517,7 +526,8 @@ __device__ __forceinline__ uint64_t sm_div(uint64_t x, uint64_t m, int sh) { ret
 // each pivot's key derived from it, and the first probe of every pivot is
 // issued before any result is examined (independent atomics in flight);
 // collisions (rare at load factor <= 1/2) then probe linearly.
-__global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict__ coords, int64_t n,
+__global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict__ coords,
+                                                       const uint64_t *__restrict__ lin_in, int64_t n,
                                                        HashSpec hs,
                                                        unsigned long long *__restrict__ tables,
                                                        unsigned long long *__restrict__ counts) {
@@ -528,8 +538,12 @@ __global__ void __launch_bounds__(256) k_distinct_hash(const int64_t *__restrict
     const int64_t i = base + threadIdx.x;
     uint64_t lin = 0;
     if (i < n) {
-      const int64_t *c = coords + i * hs.d;
-      for (int k = 0; k < hs.d; ++k) lin += (uint64_t)c[k] * (uint64_t)hs.stride[k];
+      if (lin_in) {
+        lin = lin_in[i];
+      } else {
+        const int64_t *c = coords + i * hs.d;
+        for (int k = 0; k < hs.d; ++k) lin += (uint64_t)c[k] * (uint64_t)hs.stride[k];
+      }
     }
     unsigned fresh_mask = 0, pending = 0;
     unsigned long long got[HS_PASS];
@@ -1097,10 +1111,11 @@ int bit_length(uint64_t x) {
 // kin/vin (optional): the first executed pass reads these instead of
 // keys[0]/vals[0]; kout/vout (optional): the last executed pass writes there
 // (no staging copies in or out of the ping-pong buffers).
-int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t n, int num_passes,
-                    uint32_t *ghist, uint32_t *status, uint32_t *counters, uint64_t **kres,
-                    uint32_t **vres, const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
-                    uint32_t *vout) {
+template <class MkDigit>
+int onesweep_passes_t(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t n, int num_passes,
+                      uint32_t *ghist, uint32_t *status, uint32_t *counters, uint64_t **kres,
+                      uint32_t **vres, const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
+                      uint32_t *vout, MkDigit mk) {
   // decide which passes are needed (constant digit -> skip)
   static thread_local std::vector<uint32_t> h;
   h.assign((size_t)num_passes * RADIX, 0);
@@ -1144,20 +1159,21 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
     uint64_t *kdst = (last && kout) ? kout : keys[cur ^ 1];
     uint32_t *vdst = has_vals ? ((last && vout) ? vout : vals[cur ^ 1]) : nullptr;
     uint32_t *st = status + a * ntiles * RADIX;
+    using DG = decltype(mk(0));
     static bool attr_set = false;
     if (!attr_set) {
       const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true>, at, 12 * RS_TILE));
-      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false>, at, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, RS_ITEMS, DG>, at, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, RS_ITEMS, DG>, at, 12 * RS_TILE));
       attr_set = true;
     }
     const int pb = prof_begin(ctx);
     if (has_vals) {
-      k_onesweep<true><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
-          ksrc, vsrc, kdst, vdst, n, 8 * p, ghist + p * RADIX, st, counters + p);
+      k_onesweep<true, RS_ITEMS, DG><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
+          ksrc, vsrc, kdst, vdst, n, mk(p), ghist + p * RADIX, st, counters + p);
     } else {
-      k_onesweep<false><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
-          ksrc, nullptr, kdst, nullptr, n, 8 * p, ghist + p * RADIX, st, counters + p);
+      k_onesweep<false, RS_ITEMS, DG><<<(unsigned)ntiles, RS_THREADS, 8 * RS_TILE, ctx->stream>>>(
+          ksrc, nullptr, kdst, nullptr, n, mk(p), ghist + p * RADIX, st, counters + p);
     }
     FTT_LAUNCHED(ctx);
     // algorithmic bytes: read + write every key (and payload) once
@@ -1169,6 +1185,14 @@ int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t 
   *kres = const_cast<uint64_t *>(ksrc);
   *vres = has_vals ? const_cast<uint32_t *>(vsrc) : nullptr;
   return FTT_OK;
+}
+
+int onesweep_passes(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t n, int num_passes,
+                    uint32_t *ghist, uint32_t *status, uint32_t *counters, uint64_t **kres,
+                    uint32_t **vres, const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
+                    uint32_t *vout) {
+  return onesweep_passes_t(ctx, keys, vals, n, num_passes, ghist, status, counters, kres, vres, kin,
+                           vin, kout, vout, [](int p) { return DigitShift{8 * p}; });
 }
 
 size_t onesweep_scratch(int64_t n) {
@@ -1567,6 +1591,393 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
 
 }  // namespace
 
+namespace ftt {
+namespace {
+
+// ---- select_p counts and fiber keys from the canonical linear index -----
+// The device COO is kept as its C-order linear index `lin` (8 B per nonzero,
+// strictly increasing: SparseTensor's canonical form) plus the values; every
+// digit a kernel needs is an exact magic-number division of lin.
+//
+// select_p counts (fasttt.py:536-541) per pivot p = distinct fixed tuples
+// (lin with digit p removed).  With pf = ceil(d / 2) and M = prod dims[pf:]:
+//  * pivots p >= pf: nonzeros sharing a fixed tuple share the prefix over
+//    modes < p, hence lin / M; chunks of lin aligned to lin / M groups hold
+//    whole fibers of all those pivots at once (one read, no sort);
+//  * pivots p < pf: they share lin mod M (the suffix over modes >= pf);
+//    lin is bucketed by h = mix64(lin mod M) >> 48 (two stable radix passes
+//    on digits of h, keys only) and chunks are aligned to h runs.
+// In a chunk, each pivot's fixed-tuple keys go into a shared-memory hash set
+// -- 32-bit keys relative to the chunk minimum when the chunk's key span fits
+// (a single CAS per insert), else 64-bit -- and first insertions are
+// counted: exact and independent of the insertion order.  A group longer
+// than the chunk capacity flags its pivots (the caller counts those another
+// way); unsorted input flags the lin-order pivots.
+constexpr int SC_L = 1024;       // nominal nonzeros per CTA (groups up to SC_CAP - SC_L)
+constexpr int SC_CAP = 4096;     // max nonzeros per chunk
+constexpr int SC_SLOTS = 8192;   // 32-bit hash slots (load <= 1/2)
+constexpr int SC_MAXP = 32;
+constexpr int SC_NT = 512;      // threads per chunk CTA
+
+struct SelSpec {
+  int np;
+  int align_hash;  // 0: group = lin / M; 1: group = mix64(lin mod M) >> 48
+  uint64_t M, mM;
+  int shM;
+  int lgM;  // log2 M when every extent is a power of two (shift / mask keys)
+  int lgS[SC_MAXP], lgT[SC_MAXP];
+  uint64_t S[SC_MAXP], mS[SC_MAXP], mT[SC_MAXP];
+  int shS[SC_MAXP], shT[SC_MAXP], slot[SC_MAXP];
+};
+
+template <bool POW2>
+__device__ __forceinline__ uint64_t sel_group(uint64_t x, const SelSpec &sp) {
+  if (POW2) {
+    if (!sp.align_hash) return x >> sp.lgM;
+    return mix64(x & ((1ull << sp.lgM) - 1)) >> 48;
+  }
+  const uint64_t q = udiv_magic(x, sp.mM, sp.shM);
+  if (!sp.align_hash) return q;
+  return mix64(x - q * sp.M) >> 48;
+}
+
+struct DigitHashMod {  // bits [shift, shift + 8) of mix64(lin mod M) >> 48
+  uint64_t M, mM;
+  int shM, shift;
+  __device__ __forceinline__ uint32_t operator()(uint64_t k) const {
+    const uint64_t lo = k - udiv_magic(k, mM, shM) * M;
+    return (uint32_t)(((mix64(lo) >> 48) >> shift) & 255);
+  }
+};
+
+__global__ void __launch_bounds__(256) k_hist_hashmod(const uint64_t *__restrict__ keys, int64_t n,
+                                                      DigitHashMod dg, uint32_t *__restrict__ ghist) {
+  __shared__ uint32_t sh[2][RADIX];
+  for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    const uint64_t lo = k - udiv_magic(k, dg.mM, dg.shM) * dg.M;
+    const uint32_t h = (uint32_t)(mix64(lo) >> 48);
+    atomicAdd(&sh[0][h & 255], 1u);
+    atomicAdd(&sh[1][h >> 8], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(&ghist[i], v);
+  }
+}
+
+template <bool POW2>
+__global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict__ K, int64_t n,
+                                                   SelSpec sp,
+                                                   unsigned long long *__restrict__ count,
+                                                   int *__restrict__ flag,
+                                                   int *__restrict__ unsorted) {
+  extern __shared__ unsigned long long smem[];
+  uint64_t *skey = reinterpret_cast<uint64_t *>(smem);             // SC_CAP keys
+  unsigned *tab32 = reinterpret_cast<unsigned *>(smem + SC_CAP);   // SC_SLOTS positions
+  __shared__ int64_t s_start, s_end;
+  __shared__ unsigned s_j[2];
+  __shared__ unsigned long long s_cnt;
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = (int64_t)blockIdx.x * SC_L;
+  auto grp = [&](int64_t i) -> uint64_t { return sel_group<POW2>(K[i], sp); };
+  if (threadIdx.x < 2) s_j[threadIdx.x] = 0xffffffffu;
+  __syncthreads();
+  // chunk = whole groups starting in [c0, c0 + L): first group start at or
+  // after c0 and at or after c0 + L (both windows searched together)
+  bool open0 = c0 < n, open1 = c0 + SC_L < n;
+  for (int r = 0; r < SC_CAP / SC_NT && (open0 || open1); ++r) {
+    const int j = r * SC_NT + (int)threadIdx.x;
+    bool st0 = false, st1 = false;
+    if (open0) {
+      const int64_t i = c0 + j;
+      st0 = i <= n && (i == n || i == 0 || grp(i) != grp(i - 1));
+    }
+    if (open1) {
+      const int64_t i = c0 + SC_L + j;
+      st1 = i <= n && (i == n || grp(i) != grp(i - 1));
+    }
+    const unsigned m0 = __reduce_min_sync(0xffffffffu, st0 ? (unsigned)j : 0xffffffffu);
+    const unsigned m1 = __reduce_min_sync(0xffffffffu, st1 ? (unsigned)j : 0xffffffffu);
+    if (lane == 0 && m0 != 0xffffffffu) atomicMin(&s_j[0], m0);
+    if (lane == 0 && m1 != 0xffffffffu) atomicMin(&s_j[1], m1);
+    const int any0 = __syncthreads_or(st0);
+    const int any1 = __syncthreads_or(st1);
+    open0 = open0 && !any0;
+    open1 = open1 && !any1;
+  }
+  if (threadIdx.x == 0) {
+    s_start = c0 >= n ? n : (s_j[0] == 0xffffffffu ? INT64_MAX : c0 + s_j[0]);
+    s_end = c0 + SC_L >= n ? n : (s_j[1] == 0xffffffffu ? INT64_MAX : c0 + SC_L + s_j[1]);
+  }
+  __syncthreads();
+  const int64_t start = s_start, end = s_end;
+  if (start == INT64_MAX) return;  // inside a long group: its owner flags it
+  if (end == INT64_MAX || end - start > SC_CAP) {
+    if (threadIdx.x == 0)
+      for (int q = 0; q < sp.np; ++q) atomicOr(flag + sp.slot[q], 1);
+    return;
+  }
+  constexpr int PER = SC_CAP / SC_NT;
+  const int cnt = (int)(end - start);
+  int bad = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = q * SC_NT + threadIdx.x;
+    if (j < cnt) {
+      const uint64_t k = __ldg(K + start + j);
+      skey[j] = k;
+      if (!sp.align_hash && start + j + 1 < n) bad |= __ldg(K + start + j + 1) <= k;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(unsorted, 1);
+  // per pivot: the table holds chunk positions (native 32-bit shared CAS);
+  // a probe that meets an occupied slot compares the fixed-tuple key of the
+  // stored position, recomputed from its lin
+  for (int q = 0; q < sp.np; ++q) {
+    const uint64_t S = sp.S[q];
+    const uint64_t mT = sp.mT[q], mS = sp.mS[q];
+    const int shT = sp.shT[q], shS = sp.shS[q], lgS = sp.lgS[q], lgT = sp.lgT[q];
+    auto reduce = [&](uint64_t x) -> uint64_t {
+      if (POW2) return ((x >> lgT) << lgS) | (x & ((1ull << lgS) - 1));
+      return udiv_magic(x, mT, shT) * S + (x - udiv_magic(x, mS, shS) * S);
+    };
+    // multiplicative hash (Fibonacci), 13 bits
+    auto slot = [](uint64_t k) -> unsigned {
+      return (unsigned)((k * 0x9E3779B97F4A7C15ull) >> (64 - 13));
+    };
+    for (int e = threadIdx.x; e < SC_SLOTS / 4; e += SC_NT)
+      reinterpret_cast<uint4 *>(tab32)[e] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    unsigned long long fresh = 0;
+    for (int j = threadIdx.x; j < cnt; j += SC_NT) {  // only the chunk's live rounds
+      const uint64_t r = reduce(skey[j]);
+      unsigned h = slot(r);
+      while (true) {
+        const unsigned old = atomicCAS(tab32 + h, ~0u, (unsigned)j);
+        if (old == ~0u) {
+          ++fresh;
+          break;
+        }
+        if (reduce(skey[old]) == r) break;
+        h = (h + 1) & (SC_SLOTS - 1);  // linear probing
+      }
+    }
+    for (int o = 16; o; o >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, o);
+    if (lane == 0 && fresh) atomicAdd(&s_cnt, fresh);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(count + sp.slot[q], s_cnt);
+  }
+}
+
+// Fiber keys straight from lin: key = fixed_lin * n_p + i_p with
+// fixed_lin = (lin / T) * S + lin mod S, i_p = (lin / S) mod n_p (S = prod of
+// the dims after the pivot, T = n_p S), identity payload, digit histograms
+// of every pass.  Reads 8 B per nonzero instead of the d coordinates.
+struct LinKeySpec {
+  uint64_t S, mS, T, mT, np, mN;
+  int shS, shT, shN;
+};
+
+__device__ __forceinline__ uint64_t lin_fiber_key(uint64_t x, const LinKeySpec &ks, uint64_t *ip) {
+  const uint64_t a = udiv_magic(x, ks.mS, ks.shS);  // lin / S
+  const uint64_t lo = x - a * ks.S;
+  const uint64_t hi = udiv_magic(x, ks.mT, ks.shT);  // lin / T
+  const uint64_t i = a - hi * ks.np;
+  if (ip) *ip = i;
+  return (hi * ks.S + lo) * ks.np + i;
+}
+
+__global__ void __launch_bounds__(256) k_keys_hist_lin(const uint64_t *__restrict__ lin, int64_t n,
+                                                       LinKeySpec ks, int num_passes,
+                                                       uint64_t *__restrict__ keys,
+                                                       uint32_t *__restrict__ idx,
+                                                       uint32_t *__restrict__ ghist) {
+  __shared__ uint32_t sh[8][RADIX];
+  for (int i = threadIdx.x; i < 8 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = lin_fiber_key(lin[i], ks, nullptr);
+    keys[i] = key;
+    idx[i] = (uint32_t)i;
+    for (int p = 0; p < num_passes; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < num_passes * RADIX; i += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(&ghist[i], v);
+  }
+}
+
+__global__ void k_linearize_c(const int64_t *__restrict__ coords, int64_t n, LinSpec ls,
+                              int64_t *__restrict__ lin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t *c = coords + i * ls.d;
+    uint64_t x = 0;
+    for (int k = 0; k < ls.d; ++k) x += (uint64_t)c[k] * (uint64_t)ls.stride[k];
+    lin[i] = (int64_t)x;
+  }
+}
+
+void c_strides(int32_t d, const int64_t *dims, int64_t *w) {
+  int64_t st = 1;
+  for (int k = d - 1; k >= 0; --k) {
+    w[k] = st;
+    st *= dims[k];
+  }
+}
+
+// Counts for every pivot from lin; done[p] false where the caller must
+// count pivot p another way (a group over capacity, or unsorted input).
+int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, const int64_t *dims,
+                     int64_t *counts_host, bool *done) {
+  for (int p = 0; p < d; ++p) done[p] = false;
+  if (d < 2) return FTT_OK;
+  int64_t w[32];
+  c_strides(d, dims, w);
+  const int pf = (d + 1) / 2;
+  const uint64_t M = (uint64_t)w[pf - 1];  // prod dims[pf:]
+  SelSpec fwd, rev;
+  fwd.align_hash = 0;
+  rev.align_hash = 1;
+  fwd.M = rev.M = M;
+  magic_u63(M, &fwd.mM, &fwd.shM);
+  rev.mM = fwd.mM;
+  rev.shM = fwd.shM;
+  fwd.np = rev.np = 0;
+  bool pow2 = true;
+  for (int p = 0; p < d; ++p) pow2 &= (dims[p] & (dims[p] - 1)) == 0;
+  auto lg2 = [](uint64_t x) {
+    int l = 0;
+    while ((1ull << l) < x) ++l;
+    return l;
+  };
+  fwd.lgM = rev.lgM = pow2 ? lg2(M) : 0;
+  for (int p = 0; p < d; ++p) {
+    SelSpec &sp = p >= pf ? fwd : rev;
+    const int q = sp.np++;
+    sp.S[q] = (uint64_t)w[p];
+    magic_u63((uint64_t)w[p], &sp.mS[q], &sp.shS[q]);
+    magic_u63((uint64_t)w[p] * (uint64_t)dims[p], &sp.mT[q], &sp.shT[q]);
+    sp.lgS[q] = pow2 ? lg2((uint64_t)w[p]) : 0;
+    sp.lgT[q] = pow2 ? lg2((uint64_t)w[p] * (uint64_t)dims[p]) : 0;
+    sp.slot[q] = p;
+  }
+  unsigned long long *cnt = nullptr;
+  uint64_t *bucketed = nullptr;
+  FTT_CHECK(owned_alloc(ctx, (void **)&cnt, 8 * 32 + 4 * 32 + 16));
+  int *flags = reinterpret_cast<int *>(cnt + 32);
+  int *unsorted = flags + 32;
+  FTT_CUDA(cudaMemsetAsync(cnt, 0, 8 * 32 + 4 * 32 + 16, ctx->stream));
+  static bool attr = false;
+  const size_t smem = 8 * (size_t)SC_CAP + 4 * (size_t)SC_SLOTS;
+  if (!attr) {
+    FTT_CUDA(cudaFuncSetAttribute(k_sel_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    FTT_CUDA(cudaFuncSetAttribute(k_sel_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr = true;
+  }
+  const unsigned nb = (unsigned)ceil_div(nnz, SC_L);
+  auto count = [&](const uint64_t *keys, const SelSpec &sp, int *uns) {
+    if (pow2) k_sel_count<true><<<nb, SC_NT, smem, ctx->stream>>>(keys, nnz, sp, cnt, flags, uns);
+    else k_sel_count<false><<<nb, SC_NT, smem, ctx->stream>>>(keys, nnz, sp, cnt, flags, uns);
+  };
+  int pb = prof_begin(ctx);
+  count(lin, fwd, unsorted);
+  FTT_LAUNCHED(ctx);
+  prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz, 0.0);
+  if (rev.np > 0) {
+    // bucket lin by h = mix64(lin mod M) >> 48: two stable passes, keys only
+    FTT_CHECK(owned_alloc(ctx, (void **)&bucketed, 8 * (size_t)nnz));
+    FTT_CHECK(arena_reserve(ctx, onesweep_scratch(nnz) + 2 * align_up(8 * (size_t)nnz) + 4096));
+    uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
+    uint32_t *status = take<uint32_t>(ctx, 8 * ceil_div(nnz, RS_MIN_TILE) * RADIX);
+    uint32_t *counters = take<uint32_t>(ctx, 8);
+    uint64_t *kb[2] = {take<uint64_t>(ctx, nnz), take<uint64_t>(ctx, nnz)};
+    uint32_t *vb[2] = {nullptr, nullptr};
+    FTT_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
+    DigitHashMod dg{M, fwd.mM, fwd.shM, 0};
+    pb = prof_begin(ctx);
+    k_hist_hashmod<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(lin, nnz, dg, ghist);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb, PT_HIST, 8.0 * (double)nnz, 0.0);
+    uint64_t *kr = nullptr;
+    uint32_t *vr = nullptr;
+    FTT_CHECK(onesweep_passes_t(ctx, kb, vb, nnz, 2, ghist, status, counters, &kr, &vr, lin, nullptr,
+                                bucketed, nullptr, [&](int p) {
+                                  DigitHashMod g = dg;
+                                  g.shift = 8 * p;
+                                  return g;
+                                }));
+    pb = prof_begin(ctx);
+    count(kr, rev, unsorted + 1);
+    FTT_LAUNCHED(ctx);
+    prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz, 0.0);
+  }
+  unsigned long long h[32];
+  int hf[34];
+  FTT_CHECK(copy_to_host(ctx, h, cnt, 8 * 32));
+  FTT_CHECK(copy_to_host(ctx, hf, flags, 4 * 34));
+  if (bucketed) owned_free(ctx, bucketed);
+  owned_free(ctx, cnt);
+  const bool sorted = hf[32] == 0;
+  for (int p = 0; p < d; ++p) {
+    if (hf[p] || (p >= pf && !sorted)) continue;
+    counts_host[p] = (int64_t)h[p];
+    done[p] = true;
+  }
+  return FTT_OK;
+}
+
+int fiber_keys_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, const int64_t *dims,
+                   int32_t pivot, uint64_t **kres, uint32_t **vres) {
+  int64_t w[32];
+  c_strides(d, dims, w);
+  LinKeySpec ks;
+  ks.S = (uint64_t)w[pivot];
+  ks.np = (uint64_t)dims[pivot];
+  ks.T = ks.S * ks.np;
+  magic_u63(ks.S, &ks.mS, &ks.shS);
+  magic_u63(ks.T, &ks.mT, &ks.shT);
+  magic_u63(ks.np, &ks.mN, &ks.shN);
+  uint64_t bound = 1;
+  for (int k = 0; k < d; ++k) bound *= (uint64_t)dims[k];
+  int num_passes = (bit_length(bound - 1) + 7) / 8;
+  if (num_passes < 1) num_passes = 1;
+  uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
+  uint32_t *status = take<uint32_t>(ctx, 8 * ceil_div(nnz, RS_MIN_TILE) * RADIX);
+  uint32_t *counters = take<uint32_t>(ctx, 8);
+  uint64_t *kb[2] = {take<uint64_t>(ctx, nnz), take<uint64_t>(ctx, nnz)};
+  uint32_t *vb[2] = {take<uint32_t>(ctx, nnz), take<uint32_t>(ctx, nnz)};
+  if (!ghist || !status || !counters || !kb[1] || !vb[1]) {
+    set_error("fiber_keys_lin: arena reservation too small");
+    return FTT_ERR_INVALID;
+  }
+  FTT_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * RADIX, ctx->stream));
+  const int pb = prof_begin(ctx);
+  k_keys_hist_lin<<<grid_for(nnz, 256, 8), 256, 0, ctx->stream>>>(lin, nnz, ks, num_passes, kb[0],
+                                                                  vb[0], ghist);
+  FTT_LAUNCHED(ctx);
+  prof_end(ctx, pb, PT_HIST, (double)nnz * 20.0, 0.0);
+  return onesweep_passes(ctx, kb, vb, nnz, num_passes, ghist, status, counters, kres, vres, nullptr,
+                         nullptr, nullptr, nullptr);
+}
+
+
+}  // namespace
+}  // namespace ftt
+
+namespace {
+}  // namespace
+
 extern "C" {
 
 int ftt_fiber_count(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
@@ -1674,7 +2085,7 @@ int ftt_fiber_counts_all(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32
     FTT_CUDA(cudaMemsetAsync(tables, 0xff, 8 * (size_t)T * np, ctx->stream));
     const int pb = prof_begin(ctx);
     k_distinct_hash<<<grid_for(nnz, 256, 1), 256, 0, ctx->stream>>>(
-        coords, nnz, hs, reinterpret_cast<unsigned long long *>(tables), cnt + p0);
+        coords, nullptr, nnz, hs, reinterpret_cast<unsigned long long *>(tables), cnt + p0);
     FTT_LAUNCHED(ctx);
     // coordinates read once + one 8-byte CAS per pivot and nonzero
     prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 * d + 8.0 * np), 0.0);
@@ -1720,6 +2131,133 @@ int ftt_extract_fibers(ftt_ctx *ctx, const int64_t *coords, const double *values
   k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr + R, nnz);
   FTT_LAUNCHED(ctx);
   *num_fibers_out = R;
+  return FTT_OK;
+}
+
+// select_p counts from the canonical linear index (see fiber_counts_lin);
+// coords (optional) serve the pivots the lin path hands back.
+int ftt_fiber_counts_lin(ftt_ctx *ctx, const int64_t *lin, const int64_t *coords, int64_t nnz,
+                         int32_t d, const int64_t *dims_host, int64_t *counts_host) {
+  if (!ctx || !counts_host || !lin) return FTT_ERR_INVALID;
+  FTT_CHECK(check_dims(d, dims_host, 0, false));
+  if (nnz >= ((int64_t)1 << 30)) {
+    set_error("nnz exceeds the 2^30 sort limit");
+    return FTT_ERR_INVALID;
+  }
+  if (nnz == 0) {
+    for (int p = 0; p < d; ++p) counts_host[p] = 0;
+    return FTT_OK;
+  }
+  int lg = 1;
+  while (((int64_t)1 << lg) < 2 * nnz) ++lg;
+  const int64_t T = (int64_t)1 << lg;
+  const char *path = getenv("FTT_COUNT_PATH");
+  const bool force_lin = path && !strcmp(path, "lin");
+  const bool force_other = path && !force_lin;
+  if (force_other && coords)
+    return ftt_fiber_counts_all(ctx, coords, nnz, d, dims_host, counts_host);
+  if (!force_lin && 8 * T <= ((int64_t)32 << 20)) {
+    // small inputs: one pass, d L2-resident global hash sets (as
+    // ftt_fiber_counts_all), keys derived from lin
+    int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));
+    group = std::min(group, HS_PASS);
+    uint64_t *tables = nullptr;
+    FTT_CHECK(owned_alloc(ctx, (void **)&tables, 8 * (size_t)T * group + 8 * 32));
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(tables + (size_t)T * group);
+    FTT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 32, ctx->stream));
+    for (int p0 = 0; p0 < d; p0 += group) {
+      const int np = std::min(group, d - p0);
+      HashSpec hs;
+      hs.d = d;
+      hs.np = np;
+      hs.lg = lg;
+      c_strides(d, dims_host, hs.stride);
+      for (int q = 0; q < np; ++q) {
+        const uint64_t S = (uint64_t)hs.stride[p0 + q];
+        hs.S[q] = S;
+        magic_u63(S, &hs.mS[q], &hs.shS[q]);
+        magic_u63(S * (uint64_t)dims_host[p0 + q], &hs.mT[q], &hs.shT[q]);
+      }
+      FTT_CUDA(cudaMemsetAsync(tables, 0xff, 8 * (size_t)T * np, ctx->stream));
+      const int pb = prof_begin(ctx);
+      k_distinct_hash<<<grid_for(nnz, 256, 1), 256, 0, ctx->stream>>>(
+          nullptr, reinterpret_cast<const uint64_t *>(lin), nnz, hs,
+          reinterpret_cast<unsigned long long *>(tables), cnt + p0);
+      FTT_LAUNCHED(ctx);
+      prof_end(ctx, pb, PT_HIST, (double)nnz * (8.0 + 8.0 * np), 0.0);
+    }
+    unsigned long long h[32];
+    FTT_CHECK(copy_to_host(ctx, h, cnt, sizeof(unsigned long long) * d));
+    owned_free(ctx, tables);
+    for (int p = 0; p < d; ++p) counts_host[p] = (int64_t)h[p];
+    return FTT_OK;
+  }
+  bool done[32];
+  FTT_CHECK(fiber_counts_lin(ctx, reinterpret_cast<const uint64_t *>(lin), nnz, d, dims_host,
+                             counts_host, done));
+  bool all = true;
+  for (int p = 0; p < d; ++p) all &= done[p];
+  if (all) return FTT_OK;
+  static const bool debug = getenv("FTT_DEBUG") != nullptr;
+  if (debug)
+    for (int p = 0; p < d; ++p)
+      if (!done[p]) fprintf(stderr, "[ftt] select_p lin count: pivot %d -> partition\n", p);
+  int64_t *cbuf = nullptr;
+  if (!coords) {  // the leftovers need coordinates: rebuild them from lin
+    FTT_CHECK(owned_alloc(ctx, (void **)&cbuf, 8 * (size_t)nnz * d));
+    FTT_CHECK(ftt_delinearize(ctx, lin, nnz, d, dims_host, cbuf));
+    coords = cbuf;
+  }
+  const int rc = fiber_counts_partition(ctx, coords, nnz, d, dims_host, counts_host, done);
+  if (cbuf) owned_free(ctx, cbuf);
+  return rc;
+}
+
+int ftt_extract_fibers_lin(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz,
+                           int32_t d, const int64_t *dims_host, int32_t pivot, int64_t *fixed_lin,
+                           int64_t *indptr, int64_t *fiber_of, int64_t *pivot_index,
+                           double *values_out, int64_t *num_fibers_out) {
+  if (!ctx || !num_fibers_out || !lin) return FTT_ERR_INVALID;
+  FTT_CHECK(check_dims(d, dims_host, pivot, true));
+  if (nnz >= ((int64_t)1 << 30)) {
+    set_error("nnz exceeds the 2^30 sort limit");
+    return FTT_ERR_INVALID;
+  }
+  if (nnz == 0) {
+    *num_fibers_out = 0;
+    k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr, 0);
+    FTT_LAUNCHED(ctx);
+    return FTT_OK;
+  }
+  FTT_CHECK(arena_reserve(ctx, sort_coords_bytes(nnz, true) + compact_scratch_bytes(nnz) + 1024));
+  uint64_t *kr;
+  uint32_t *vr;
+  FTT_CHECK(fiber_keys_lin(ctx, reinterpret_cast<const uint64_t *>(lin), nnz, d, dims_host, pivot,
+                           &kr, &vr));
+  int64_t *bc = take<int64_t>(ctx, ceil_div(nnz, CP_TILE) + 1);
+  int64_t *total = take<int64_t>(ctx, 1);
+  AdjDiffPred pred{kr, make_div63((uint64_t)dims_host[pivot])};
+  FiberEmit emit{kr, vr, values, make_div63((uint64_t)dims_host[pivot]), fixed_lin, indptr, fiber_of,
+                 pivot_index, values_out};
+  FTT_CHECK(compact(ctx, nnz, pred, emit, bc, total, PT_SEGMENT, 44.0 * (double)nnz));
+  int64_t R = 0;
+  FTT_CHECK(copy_to_host(ctx, &R, total, sizeof(R)));
+  k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr + R, nnz);
+  FTT_LAUNCHED(ctx);
+  *num_fibers_out = R;
+  return FTT_OK;
+}
+
+int ftt_linearize(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int32_t d,
+                  const int64_t *dims_host, int64_t *lin_out) {
+  if (!ctx || (nnz > 0 && (!coords || !lin_out))) return FTT_ERR_INVALID;
+  FTT_CHECK(check_dims(d, dims_host, 0, false));
+  if (nnz == 0) return FTT_OK;
+  LinSpec ls;
+  ls.d = d;
+  c_strides(d, dims_host, ls.stride);
+  k_linearize_c<<<grid_for(nnz, 256, 4), 256, 0, ctx->stream>>>(coords, nnz, ls, lin_out);
+  FTT_LAUNCHED(ctx);
   return FTT_OK;
 }
 

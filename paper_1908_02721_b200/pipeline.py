@@ -190,8 +190,9 @@ def _fiber_counts_device(a: SparseTensor):
         return [0] * a.ndim
     c, _ = a.device_arrays()
     counts = (nat.ctypes.c_int64 * a.ndim)()
-    nat.check(nat.lib().ftt_fiber_counts_all(nat.context(), nat.ptr(c), a.nnz, a.ndim,
-                                             nat.i64_array(a.shape), counts), "ftt_fiber_counts_all")
+    nat.check(nat.lib().ftt_fiber_counts_lin(nat.context(), nat.ptr(a.device_lin()), nat.ptr(c),
+                                             a.nnz, a.ndim, nat.i64_array(a.shape), counts),
+              "ftt_fiber_counts_lin")
     return [int(x) for x in counts]
 
 
@@ -1118,7 +1119,7 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
     d = a.ndim
     dims = a.shape
     nnz = a.nnz
-    df = fibers_device(dims, pivot, coords_d, values_d, nnz)
+    df = fibers_device(dims, pivot, coords_d, values_d, nnz, lin_d=a.device_lin())
     if d == 1:
         # the reference's FiberSet rejects its own d = 1 output (tensor.py:326-329)
         raise ValueError("inconsistent fiber index pointers")

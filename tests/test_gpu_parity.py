@@ -392,7 +392,7 @@ def test_tt_entries_meet_in_the_middle(dims, ranks, n):
     assert rel_err(got, O.tt_entries(cores, coords)) < 1e-12
 
 
-@pytest.mark.parametrize("path", ["hash", "part", "sort", "group"])
+@pytest.mark.parametrize("path", ["hash", "part", "sort", "group", "lin"])
 def test_fiber_counts_all_paths(path, monkeypatch):
     """Exact distinct fixed-tuple counts per pivot through every device path
     (shared hash set, bucket partition + shared hash sets, radix sort),

@@ -28,7 +28,7 @@ def step():
 for _ in range(3):
     step()
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA]) as prof:
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     step()
     torch.cuda.synchronize()
 def short(name):
@@ -37,9 +37,13 @@ def short(name):
 
 
 ev = []
+api = []
 for x in prof.events():
     if x.device_type == torch.autograd.DeviceType.CUDA:
         ev.append((x.time_range.start, x.time_range.end, short(x.name)))
+    elif x.name.startswith("cuda") or x.name.startswith("cu"):
+        api.append((x.time_range.start, x.time_range.end, x.name))
+api.sort()
 ev.sort()
 t0, t1 = ev[0][0], max(x[1] for x in ev)
 busy = 0.0
@@ -56,6 +60,19 @@ span = t1 - t0
 print(f"config {cfg}: {len(ev)} device activities, span {span / 1e3:.3f} ms, busy {busy / 1e3:.3f} ms, "
       f"idle {(span - busy) / 1e3:.3f} ms")
 gaps.sort(reverse=True)
+gap_at = {}
+cur = t0
+for i, (st, en, name) in enumerate(ev):
+    if st > cur:
+        gap_at[(cur, st)] = st - cur
+    cur = max(cur, en)
+for (a, b), g in sorted(gap_at.items(), key=lambda x: -x[1])[:ngaps]:
+    inside = [(x[2], round(x[1] - x[0], 1)) for x in api if x[0] < b and x[1] > a]
+    agg = {}
+    for nm, dt in inside:
+        agg[nm] = agg.get(nm, 0.0) + dt
+    top = sorted(agg.items(), key=lambda x: -x[1])[:4]
+    print(f"  gap {g:8.1f} us  runtime calls inside: {len(inside)}  top {top}")
 for g, p, n in gaps[:ngaps]:
     print(f"  gap {g:8.1f} us  after {str(p)[:60]:60s} before {str(n)[:60]}")
 by = {}
