@@ -74,6 +74,10 @@ struct ftt_ctx {
   int64_t syncs = 0;
   double sync_wait_ms = 0.0;
   int *sticky = nullptr;
+  // grow-only flag array kept all-zero between uses (the deparallelisation
+  // sweeps mark, rank and unmark only the rows they touch)
+  uint32_t *zflags = nullptr;
+  size_t zflags_cap = 0;
   // split-K tile arrival counters (zero between products; ftt_gemm.cu)
   unsigned *tile_cnt = nullptr;
   // live per-class kernel timing (off by default)
@@ -148,6 +152,10 @@ int copy_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes);
 // synchronous copy for transfers larger than the ring.
 int stage_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes);
 constexpr size_t kRingBytes = 1 << 20;
+
+// The context's zeroed flag array with at least n entries (grown and
+// cleared once; callers must leave it all-zero).
+int zero_flags(ftt_ctx *ctx, size_t n, uint32_t **out);
 
 // Persistent device buffer owned by the context (freed on destroy).
 int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes);

@@ -124,6 +124,20 @@ int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes) {
   return FTT_OK;
 }
 
+int zero_flags(ftt_ctx *ctx, size_t n, uint32_t **out) {
+  if (n > ctx->zflags_cap) {
+    if (ctx->zflags) FTT_CUDA(cudaFreeAsync(ctx->zflags, ctx->stream));
+    ctx->zflags = nullptr;
+    ctx->zflags_cap = 0;
+    const size_t cap = align_up(n + n / 4, 1 << 20);
+    FTT_CUDA(cudaMallocAsync((void **)&ctx->zflags, 4 * cap, ctx->stream));
+    FTT_CUDA(cudaMemsetAsync(ctx->zflags, 0, 4 * cap, ctx->stream));
+    ctx->zflags_cap = cap;
+  }
+  *out = ctx->zflags;
+  return FTT_OK;
+}
+
 void owned_free(ftt_ctx *ctx, void *p) {
   if (!p) return;
   for (size_t i = 0; i < ctx->owned.size(); ++i) {
@@ -241,6 +255,7 @@ int ftt_destroy(ftt_ctx *ctx) {
   for (auto &p : ctx->owned) cudaFreeAsync(p.first, ctx->stream);
   ctx->owned.clear();
   if (ctx->arena.base) cudaFreeAsync(ctx->arena.base, ctx->stream);
+  if (ctx->zflags) cudaFreeAsync(ctx->zflags, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);

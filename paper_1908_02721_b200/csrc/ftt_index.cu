@@ -251,62 +251,85 @@ constexpr int CP_THREADS = 256;
 constexpr int CP_ITEMS = 16;
 constexpr int CP_TILE = CP_THREADS * CP_ITEMS;
 
+// Dynamic length: n = min(nmax, *n_dev * mult) when n_dev is given (a count
+// produced on the device by an earlier kernel; grids are sized for nmax and
+// blocks past n exit).
+__device__ __forceinline__ int64_t dyn_n(int64_t nmax, const int64_t *n_dev, int64_t mult) {
+  return n_dev ? min(nmax, *n_dev * mult) : nmax;
+}
+
 template <class Pred>
-__global__ void __launch_bounds__(CP_THREADS) k_count(int64_t n, Pred pred, int64_t *block_counts) {
+__global__ void __launch_bounds__(CP_THREADS) k_count(int64_t nmax, Pred pred, int64_t *block_counts,
+                                                      const int64_t *n_dev = nullptr,
+                                                      int64_t mult = 1) {
+  const int64_t n = dyn_n(nmax, n_dev, mult);
+  const int64_t ntile = (n + CP_TILE - 1) / CP_TILE;
   __shared__ int s_w[CP_THREADS / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wbase = (int64_t)blockIdx.x * CP_TILE + warp * (32 * CP_ITEMS);
-  int cnt = 0;
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {  // grid-stride tiles
+    const int64_t wbase = tile * CP_TILE + warp * (32 * CP_ITEMS);
+    int cnt = 0;
 #pragma unroll 4
-  for (int j = 0; j < CP_ITEMS; ++j) {
-    int64_t i = wbase + j * 32 + lane;
-    bool f = i < n && pred(i);
-    cnt += __popc(__ballot_sync(0xffffffffu, f));
-  }
-  if (lane == 0) s_w[warp] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t t = 0;
-    for (int w = 0; w < CP_THREADS / 32; ++w) t += s_w[w];
-    block_counts[blockIdx.x] = t;
+    for (int j = 0; j < CP_ITEMS; ++j) {
+      int64_t i = wbase + j * 32 + lane;
+      bool f = i < n && pred(i);
+      cnt += __popc(__ballot_sync(0xffffffffu, f));
+    }
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int w = 0; w < CP_THREADS / 32; ++w) t += s_w[w];
+      block_counts[tile] = t;
+    }
+    __syncthreads();
   }
 }
 
 // emit(i, rank_excl, flag) is called for every i < n; rank_excl = number of
 // flagged items before i (global).
 template <class Pred, class Emit>
-__global__ void __launch_bounds__(CP_THREADS) k_emit(int64_t n, Pred pred, Emit emit,
-                                                     const int64_t *block_offsets) {
+__global__ void __launch_bounds__(CP_THREADS) k_emit(int64_t nmax, Pred pred, Emit emit,
+                                                     const int64_t *block_offsets,
+                                                     const int64_t *n_dev = nullptr,
+                                                     int64_t mult = 1) {
+  const int64_t n = dyn_n(nmax, n_dev, mult);
+  const int64_t ntile = (n + CP_TILE - 1) / CP_TILE;
   __shared__ int s_w[CP_THREADS / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wbase = (int64_t)blockIdx.x * CP_TILE + warp * (32 * CP_ITEMS);
-  // first: this warp's count (re-evaluate pred; cheap relative to a
-  // second smem round trip of flags)
-  uint32_t balls[CP_ITEMS];
-  int cnt = 0;
-#pragma unroll
-  for (int j = 0; j < CP_ITEMS; ++j) {
-    int64_t i = wbase + j * 32 + lane;
-    bool f = i < n && pred(i);
-    balls[j] = __ballot_sync(0xffffffffu, f);
-    cnt += __popc(balls[j]);
-  }
-  if (lane == 0) s_w[warp] = cnt;
-  __syncthreads();
-  int64_t run = block_offsets[blockIdx.x];
-  for (int w = 0; w < warp; ++w) run += s_w[w];
   const uint32_t lt = lanemask_lt();
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {  // grid-stride tiles
+    const int64_t wbase = tile * CP_TILE + warp * (32 * CP_ITEMS);
+    // first: this warp's count (re-evaluate pred; cheap relative to a
+    // second smem round trip of flags)
+    uint32_t balls[CP_ITEMS];
+    int cnt = 0;
 #pragma unroll
-  for (int j = 0; j < CP_ITEMS; ++j) {
-    int64_t i = wbase + j * 32 + lane;
-    bool f = (balls[j] >> lane) & 1u;
-    if (i < n) emit(i, run + __popc(balls[j] & lt), f);
-    run += __popc(balls[j]);
+    for (int j = 0; j < CP_ITEMS; ++j) {
+      int64_t i = wbase + j * 32 + lane;
+      bool f = i < n && pred(i);
+      balls[j] = __ballot_sync(0xffffffffu, f);
+      cnt += __popc(balls[j]);
+    }
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    int64_t run = block_offsets[tile];
+    for (int w = 0; w < warp; ++w) run += s_w[w];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < CP_ITEMS; ++j) {
+      int64_t i = wbase + j * 32 + lane;
+      bool f = (balls[j] >> lane) & 1u;
+      if (i < n) emit(i, run + __popc(balls[j] & lt), f);
+      run += __popc(balls[j]);
+    }
   }
 }
 
-__global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total) {
+__global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total,
+                              const int64_t *n_dev = nullptr, int64_t mult = 1) {
   // single block, 1024 threads, chunked exclusive scan
+  if (n_dev) nb = min(nb, (*n_dev * mult + CP_TILE - 1) / CP_TILE);
   __shared__ int64_t s[1024];
   __shared__ int64_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -335,15 +358,18 @@ __global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total) {
 // and the count pass together.
 template <class Pred, class Emit>
 int compact(ftt_ctx *ctx, int64_t n, Pred pred, Emit emit, int64_t *block_counts,
-            int64_t *total_dev, int tag = PT_SEGMENT, double alg_bytes = 0.0) {
+            int64_t *total_dev, int tag = PT_SEGMENT, double alg_bytes = 0.0,
+            const int64_t *n_dev = nullptr, int64_t mult = 1) {
   if (n <= 0) return FTT_OK;
   int64_t nb = ceil_div(n, CP_TILE);
+  // dynamic lengths: a bounded grid strides over the live tiles
+  const unsigned grid = (unsigned)(n_dev ? std::min<int64_t>(nb, 8 * (int64_t)ctx->num_sms) : nb);
   const int pb = tag >= 0 ? prof_begin(ctx) : -1;
-  k_count<Pred><<<(unsigned)nb, CP_THREADS, 0, ctx->stream>>>(n, pred, block_counts);
+  k_count<Pred><<<grid, CP_THREADS, 0, ctx->stream>>>(n, pred, block_counts, n_dev, mult);
   FTT_LAUNCHED(ctx);
-  k_scan_counts<<<1, 1024, 0, ctx->stream>>>(block_counts, nb, total_dev);
+  k_scan_counts<<<1, 1024, 0, ctx->stream>>>(block_counts, nb, total_dev, n_dev, mult);
   FTT_LAUNCHED(ctx);
-  k_emit<Pred, Emit><<<(unsigned)nb, CP_THREADS, 0, ctx->stream>>>(n, pred, emit, block_counts);
+  k_emit<Pred, Emit><<<grid, CP_THREADS, 0, ctx->stream>>>(n, pred, emit, block_counts, n_dev, mult);
   FTT_LAUNCHED(ctx);
   prof_end(ctx, pb, tag, alg_bytes, 0.0);
   return FTT_OK;
@@ -2405,41 +2431,43 @@ int ftt_index_sweeps_all(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R, int3
       prod = std::min<int64_t>(prod * dims[k], (int64_t)1 << 40);
     }
   }
+  // flag rows per step: r_other * n_k with r_other the previous step's count
+  // (read on the device: no host round trip between steps); the flag array
+  // is the context's persistent zeroed one, sized for the static bound
   int64_t bmax = 1;
   for (int s = 0; s < nsteps; ++s) {
-    // the per-step flag path's own condition (depar_from_keys), on the bound
-    const bool flag_ok = bound[s] <= ((int64_t)1 << 31) - 1 &&
-                         (bound[s] <= ((int64_t)1 << 24) || bound[s] <= 8 * R);
-    if (!flag_ok) {
+    if (bound[s] > ((int64_t)1 << 31) - 1) {
       set_error("ftt_index_sweeps_all: flag bound too large");
       return FTT_ERR_INVALID;
     }
     bmax = std::max(bmax, bound[s]);
   }
-  FTT_CHECK(arena_reserve(ctx, align_up(4 * bmax) + compact_scratch_bytes(bmax) +
-                                   align_up(8 * (size_t)(nsteps + 1)) + 4096));
-  uint32_t *present = take<uint32_t>(ctx, bmax);
+  uint32_t *present = nullptr;
+  FTT_CHECK(zero_flags(ctx, (size_t)bmax, &present));
+  FTT_CHECK(arena_reserve(ctx, compact_scratch_bytes(bmax) + align_up(8 * (size_t)(nsteps + 1)) +
+                                   4096));
   int64_t *bc = take<int64_t>(ctx, ceil_div(bmax, CP_TILE) + 1);
   int64_t *counts = take<int64_t>(ctx, nsteps + 1);
-  FTT_CUDA(cudaMemsetAsync(present, 0, 4 * (size_t)bmax, ctx->stream));
   const int pb = prof_begin(ctx);
   double alg = 0.0;
   for (int s = 0; s < nsteps; ++s) {
-    // previous step of the same side: its map and (right side) its count
+    // previous step of the same side: its map and its count
     const bool first_of_side = (s == 0) || side[s - 1] != side[s];
     SweepKey sk{side[s], fixed_lin, stride[s], nk[s], 1, first_of_side ? nullptr : maps[s - 1],
                 make_div63((uint64_t)stride[s]), make_div63((uint64_t)nk[s])};
     if (side[s] == 1 && !first_of_side) sk.r_other_dev = counts + (s - 1);
+    const int64_t *ndev = first_of_side ? nullptr : counts + (s - 1);
+    const int64_t nrows = first_of_side ? nk[s] : bound[s];
     k_sweep_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present);
     FTT_LAUNCHED(ctx);
-    FTT_CHECK(compact(ctx, bound[s], FlagPred{present}, KeptEmit{present, kept[s]}, bc, counts + s,
-                      -1));
+    FTT_CHECK(compact(ctx, nrows, FlagPred{present}, KeptEmit{present, kept[s]}, bc, counts + s, -1,
+                      0.0, ndev, nk[s]));
     k_sweep_gather<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present, maps[s]);
     FTT_LAUNCHED(ctx);
     k_unmark<<<grid_for(std::min(R, bound[s]), 256, 4), 256, 0, ctx->stream>>>(
         kept[s], counts + s, std::min(R, bound[s]), present);
     FTT_LAUNCHED(ctx);
-    alg += (double)R * (16.0 + 4.0 + 16.0 + 4.0 + 8.0) + 4.0 * (double)bound[s];
+    alg += (double)R * (16.0 + 4.0 + 16.0 + 4.0 + 8.0);
   }
   prof_end(ctx, pb, PT_SWEEP, alg, 0.0);
   FTT_CHECK(copy_to_host(ctx, n_kept_out, counts, sizeof(int64_t) * nsteps));

@@ -218,19 +218,31 @@ def select_p(a: SparseTensor, target_ranks=None, precise: bool = False, c_svd: f
         if len(targets) != d - 1:
             raise ValueError(f"need {d - 1} interior rank targets")
     counts = _fiber_counts_device(a) if not precise else None
+    # exact-int cost model (fasttt.py:456-558) in one tight loop: bounds of
+    # _upper_bond_bounds, feasibility caps, then flops_fasttt's three sums
+    outer = [size // pre[k] for k in range(d + 1)]
+    caps = [min(pre[k], outer[k]) for k in range(1, d)]
+    if targets is not None:
+        caps = [min(c, t) for c, t in zip(caps, targets)]
     best_pivot, best_cost = 0, math.inf
     for pivot in range(d):
         if precise:
-            rt = _lossless_bond_ranks(build_structured_tt(a, pivot))
+            rt = list(_lossless_bond_ranks(build_structured_tt(a, pivot)))
         else:
-            rt = _upper_bond_bounds(dims, pivot, counts[pivot])
-        r_est = []
-        for k in range(1, d):
-            feas = min(rt[k - 1], pre[k], size // pre[k])
-            if targets is not None:
-                feas = min(feas, targets[k - 1])
-            r_est.append(feas)
-        cost = _flops_core(dims, pivot, (1,) + tuple(rt) + (1,), (1,) + tuple(r_est) + (1,), c_svd)
+            R = counts[pivot]
+            rt = [min(R, pre[k]) if k <= pivot else min(R, outer[k]) for k in range(1, d)]
+        r = [1] + [min(x, c) for x, c in zip(rt, caps)] + [1]
+        rt = [1] + rt + [1]
+        p1 = pivot + 1
+        m, n = rt[p1 - 1] * dims[p1 - 1], rt[p1]
+        total = m * n * (m if m < n else n)
+        for i in range(p1 + 1, d):
+            m, n = r[i - 1] * dims[i - 1], rt[i]
+            total += m * n * (m if m < n else n)
+        for i in range(2, p1 + 1):
+            m, n = rt[i - 1], dims[i - 1] * r[i]
+            total += m * n * (m if m < n else n)
+        cost = c_svd * float(total)
         if cost < best_cost:
             best_cost, best_pivot = cost, pivot
     return best_pivot
@@ -296,12 +308,18 @@ def _index_sweeps_batched(df):
         else:
             bounds.append(min(R, prod_r) * dims[k])
             prod_r *= dims[k]
-    if any(not (b <= 2 ** 31 - 1 and (b <= 2 ** 24 or b <= 8 * R)) for b in bounds):
+    if any(b > 2 ** 31 - 1 for b in bounds):
         return None
-    kept = [_empty(max(min(R, b), 1), "i64") for b in bounds]
-    maps = [_empty(max(R, 1), "i64") for _ in steps]
-    kp = (nat.ctypes.c_void_p * len(steps))(*[t.data_ptr() for t in kept])
-    mp = (nat.ctypes.c_void_p * len(steps))(*[t.data_ptr() for t in maps])
+    # one allocation each for every step's kept rows and maps (views)
+    ksz = [max(min(R, b), 1) for b in bounds]
+    kbuf = _empty(sum(ksz), "i64")
+    mbuf = _empty(max(R, 1) * len(steps), "i64")
+    offs = np.cumsum([0] + ksz)
+    kept = [kbuf[offs[i]:offs[i + 1]] for i in range(len(steps))]
+    maps = [mbuf[i * max(R, 1):(i + 1) * max(R, 1)] for i in range(len(steps))]
+    base_k, base_m = kbuf.data_ptr(), mbuf.data_ptr()
+    kp = (nat.ctypes.c_void_p * len(steps))(*[base_k + 8 * int(offs[i]) for i in range(len(steps))])
+    mp = (nat.ctypes.c_void_p * len(steps))(*[base_m + 8 * i * max(R, 1) for i in range(len(steps))])
     counts = (nat.ctypes.c_int64 * len(steps))()
     nat.check(nat.lib().ftt_index_sweeps_all(nat.context(), nat.ptr(df.fixed_lin), R, d,
                                               nat.i64_array(dims), p, kp, mp, counts),
