@@ -245,6 +245,194 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(
   }
 }
 
+// ---- onesweep pass, persistent CTAs with TMA tile prefetch ---------------
+// The same pass as k_onesweep (stable 8-bit LSD digit pass: warp match.any
+// ranking, decoupled look-back, digit-ordered staging, coalesced runs) but
+// each CTA loops over tiles claimed from the tile counter, and as soon as
+// the current tile sits in registers the NEXT claimed tile is copied
+// global -> shared by the bulk-copy engine (cp.async.bulk, one elected
+// thread, completion on an mbarrier), so its HBM latency overlaps this
+// tile's ranking, look-back and scatter.  A tile's predecessors are always
+// some CTA's current tile or already finished, so the look-back cannot
+// deadlock on a prefetched tile.  Tiles whose bytes are not 16-byte
+// multiples (the last one) are read with ordinary loads.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+template <bool HAS_VALS, class DG>
+__global__ void __launch_bounds__(RS_THREADS, HAS_VALS ? 2 : 3) k_onesweep_tma(
+    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, int64_t n, DG dgf, const uint32_t *__restrict__ digit_start,
+    uint32_t *__restrict__ status, uint32_t *__restrict__ tile_counter, int64_t ntiles) {
+  constexpr int ITEMS = RS_ITEMS, TILE = RS_TILE;
+  __shared__ uint32_t s_warp[RS_WARPS][RADIX];
+  __shared__ uint32_t s_excl[RADIX];
+  __shared__ uint32_t s_gbase[RADIX];
+  __shared__ uint32_t s_wsum[RS_WARPS];
+  __shared__ int64_t s_next;
+  __shared__ __align__(8) uint64_t s_bar;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  uint64_t *s_keys = reinterpret_cast<uint64_t *>(s_dyn);               // staging keys
+  uint32_t *s_vals = reinterpret_cast<uint32_t *>(s_dyn + 8 * TILE);    // staging payloads
+  // prefetch buffer after the staging one (keys only: 8 + 8 bytes per key)
+  uint64_t *l_keys = reinterpret_cast<uint64_t *>(s_dyn + (HAS_VALS ? 12 : 8) * TILE);
+  uint32_t *l_vals = reinterpret_cast<uint32_t *>(s_dyn + 20 * TILE);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = lanemask_lt();
+  auto full_tile = [&](int64_t t) { return (t + 1) * TILE <= n; };
+  // claim + prefetch (thread 0); returns the claimed tile via s_next
+  auto claim_and_prefetch = [&]() {
+    const int64_t t = atomicAdd(tile_counter, 1u);
+    s_next = t;
+    if (t < ntiles && full_tile(t)) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const unsigned kb = 8u * TILE, vb = HAS_VALS ? 4u * TILE : 0u;
+      mbar_expect_tx(&s_bar, kb + vb);
+      bulk_g2s(l_keys, kin + t * TILE, kb, &s_bar);
+      if (HAS_VALS) bulk_g2s(l_vals, vin + t * TILE, vb, &s_bar);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    claim_and_prefetch();
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  int64_t tile = s_next;
+  while (tile < ntiles) {
+    for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_warp[0][0])[i] = 0;
+    const int64_t base = tile * TILE;
+    const int64_t wbase = base + warp * (32 * ITEMS);
+    const int woff = warp * (32 * ITEMS);
+    uint64_t k[ITEMS];
+    uint32_t v[ITEMS];
+    uint32_t rank[ITEMS];
+    const bool bulk = full_tile(tile);
+    if (bulk) {
+      mbar_wait(&s_bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        k[i] = l_keys[woff + i * 32 + lane];
+        if (HAS_VALS) v[i] = l_vals[woff + i * 32 + lane];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int64_t idx = wbase + i * 32 + lane;
+        k[i] = idx < n ? kin[idx] : 0;
+        if (HAS_VALS) v[i] = idx < n ? vin[idx] : 0;
+      }
+    }
+    __syncthreads();  // prefetch buffer consumed, counters cleared
+    if (tid == 0) claim_and_prefetch();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t idx = wbase + i * 32 + lane;
+      const uint32_t dg = idx < n ? dgf(k[i]) : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+      const int leader = __ffs(peers) - 1;
+      uint32_t b = 0;
+      if (dg < 256 && lane == leader) {
+        b = s_warp[warp][dg];
+        s_warp[warp][dg] = b + __popc(peers);
+      }
+      b = __shfl_sync(0xffffffffu, b, leader);
+      rank[i] = b + __popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    const int dgt = tid;  // RS_THREADS == RADIX
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      const uint32_t c = s_warp[w][dgt];
+      s_warp[w][dgt] = run;
+      run += c;
+    }
+    const uint32_t total = run;
+    uint32_t *st = status + tile * RADIX + dgt;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      st_relaxed(st, FLAG_INC | total);
+    } else {
+      st_relaxed(st, FLAG_AGG | total);
+      int64_t j = tile - 1;
+      while (true) {
+        uint32_t sv;
+        do {
+          sv = ld_relaxed(status + j * RADIX + dgt);
+        } while ((sv & ~VAL_MASK) == 0);
+        excl += sv & VAL_MASK;
+        if ((sv & ~VAL_MASK) == FLAG_INC) break;
+        --j;
+      }
+      st_relaxed(st, FLAG_INC | (excl + total));
+    }
+    s_gbase[dgt] = digit_start[dgt] + excl;
+    uint32_t x = total;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+    s_excl[dgt] = wpre + x - total;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t idx = wbase + i * 32 + lane;
+      if (idx < n) {
+        const uint32_t dg = dgf(k[i]);
+        const uint32_t pos = s_excl[dg] + s_warp[warp][dg] + rank[i];
+        s_keys[pos] = k[i];
+        if (HAS_VALS) s_vals[pos] = v[i];
+      }
+    }
+    __syncthreads();
+    const int tile_n = (int)min((int64_t)TILE, n - base);
+    for (int j = tid; j < tile_n; j += RS_THREADS) {
+      const uint64_t key = s_keys[j];
+      const uint32_t dg = dgf(key);
+      const uint32_t out = s_gbase[dg] + (j - s_excl[dg]);
+      kout[out] = key;
+      if (HAS_VALS) vout[out] = s_vals[j];
+    }
+    __syncthreads();  // staging reused by the next tile; s_next published
+    tile = s_next;
+  }
+}
+
 // ---------------------------------------------------------- compaction
 // Warp-striped blocks of COMPACT_TILE items.  Pred: bool(int64 i).
 constexpr int CP_THREADS = 256;
@@ -1187,14 +1375,34 @@ int onesweep_passes_t(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_
     uint32_t *st = status + a * ntiles * RADIX;
     using DG = decltype(mk(0));
     static bool attr_set = false;
+    // TMA prefetch: keys-only passes (3 CTAs / SM fit); passes with a
+    // payload need 96 KB and run 2 CTAs / SM, measured slower than the
+    // 3-CTA non-persistent pass (FTT_TMA_SORT=all forces them)
+    static const char *tma_env = getenv("FTT_TMA_SORT");
+    static const bool tma_off = tma_env && !strcmp(tma_env, "off");
+    static const bool tma_all = tma_env && !strcmp(tma_env, "all");
+    const bool use_tma = !tma_off && (!has_vals || tma_all);
     if (!attr_set) {
       const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
       FTT_CUDA(cudaFuncSetAttribute(k_onesweep<true, RS_ITEMS, DG>, at, 12 * RS_TILE));
       FTT_CUDA(cudaFuncSetAttribute(k_onesweep<false, RS_ITEMS, DG>, at, 12 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep_tma<true, DG>, at, 24 * RS_TILE));
+      FTT_CUDA(cudaFuncSetAttribute(k_onesweep_tma<false, DG>, at, 16 * RS_TILE));
       attr_set = true;
     }
     const int pb = prof_begin(ctx);
-    if (has_vals) {
+    // persistent: two CTAs per SM, each prefetching its next tile by TMA
+    const bool aligned = ((uintptr_t)ksrc % 16 == 0) && (!has_vals || (uintptr_t)vsrc % 16 == 0);
+    if (use_tma && aligned && ntiles > 2 * (int64_t)ctx->num_sms) {
+      const unsigned grid =
+          (unsigned)std::min<int64_t>(ntiles, (has_vals ? 2 : 3) * (int64_t)ctx->num_sms);
+      if (has_vals)
+        k_onesweep_tma<true, DG><<<grid, RS_THREADS, 24 * RS_TILE, ctx->stream>>>(
+            ksrc, vsrc, kdst, vdst, n, mk(p), ghist + p * RADIX, st, counters + p, ntiles);
+      else
+        k_onesweep_tma<false, DG><<<grid, RS_THREADS, 16 * RS_TILE, ctx->stream>>>(
+            ksrc, nullptr, kdst, nullptr, n, mk(p), ghist + p * RADIX, st, counters + p, ntiles);
+    } else if (has_vals) {
       k_onesweep<true, RS_ITEMS, DG><<<(unsigned)ntiles, RS_THREADS, 12 * RS_TILE, ctx->stream>>>(
           ksrc, vsrc, kdst, vdst, n, mk(p), ghist + p * RADIX, st, counters + p);
     } else {
