@@ -51,7 +51,7 @@ struct SparseOperand {
   int32_t *cidx_r = nullptr; // CSR column per entry
   double *v_r = nullptr;     // CSR values
   int64_t *cptr = nullptr;   // nA + 1
-  uint64_t *keyc = nullptr;  // CSC keys: col * mA + row (sorted)
+  uint64_t *keyc = nullptr;  // CSC keys: the column (sorted, rows ascending within)
   int32_t *ridx_c = nullptr; // CSC row per entry
   int32_t *cidx_c = nullptr; // CSC column per entry
   double *v_c = nullptr;     // CSC values
