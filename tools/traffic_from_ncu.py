@@ -17,16 +17,17 @@ CLASSES = [
     ("sort", ("k_onesweep", "k_part_scatter")),
     ("hist", ("k_keys_hist", "k_hist", "k_distinct_hash", "k_linearize")),
     ("segment", ("k_count", "k_emit", "k_scan_counts", "k_count_changes", "k_distinct_",
-                 "k_part_count")),
+                 "k_part_count", "k_sel_count", "k_group_count")),
     ("sweep", ("k_sweep",)),
     ("scatter", ("k_pivot_scatter", "k_side_core", "k_scatter_", "k_sp_entries", "k_sp_gather",
                  "k_gather_i32", "k_sp_bitmap", "k_lower_bounds", "k_scan_blocks", "k_scan_fix",
                  "k_seg_counts")),
     ("gemm", ("k_dgemm", "k_splitk_reduce", "k_sum_partials", "k_spmm_", "k_sp_resid",
-              "k_seg_reduce", "k_sp_sum", "k_resid_")),
+              "k_seg_reduce", "k_sp_sum", "k_resid_", "k_gram_", "k_sp_on_dd")),
     ("qr_panel", ("k_panel", "k_larft", "k_extract_v")),
     ("jacobi", ("k_jacobi", "k_svd_small", "k_tsqr", "k_qr_root", "k_chol")),
-    ("entries", ("k_entries", "k_mitm", "k_half_", "k_seg_")),
+    ("entries", ("k_entries", "k_mitm", "k_half_", "k_seg_", "k_left_vec", "k_right_vec",
+                 "k_inner_struct", "k_sum_fixed")),
 ]
 
 UNIT = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "ns": 1e-3, "nsecond": 1e-3,
@@ -64,6 +65,10 @@ def main():
     path = sys.argv[1]
     out_json = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
     out_md = sys.argv[sys.argv.index("--md") + 1] if "--md" in sys.argv else None
+    # --total KEY: also record the capture's summed DRAM bytes under KEY
+    # (e.g. index_path: one select_p + fibers + sweeps pass, for bench.py's
+    # index leg); --merge: update an existing json instead of replacing it
+    total_key = sys.argv[sys.argv.index("--total") + 1] if "--total" in sys.argv else None
     agg = collections.defaultdict(lambda: {"launches": 0, "us": 0.0, "dram_bytes": 0.0})
     kern = collections.defaultdict(lambda: {"launches": 0, "us": 0.0, "dram_bytes": 0.0})
     for rec in load(path):
@@ -89,9 +94,19 @@ def main():
     ss = [agg[c] for c in ("sort", "hist", "segment") if agg[c]["launches"]]
     if ss:
         res["sort+hist+segment"] = sum(v["dram_bytes"] for v in ss) / sum(v["launches"] for v in ss)
+    if total_key:
+        res = {total_key: sum(v["dram_bytes"] for v in agg.values()),
+               total_key + "_us": tot_us}
     if out_json:
+        old = {}
+        if "--merge" in sys.argv:
+            try:
+                old = json.load(open(out_json))
+            except Exception:  # noqa: BLE001
+                old = {}
+        old.update({k: round(v, 1) for k, v in res.items()})
         with open(out_json, "w") as fh:
-            json.dump({k: round(v, 1) for k, v in res.items()}, fh, indent=1)
+            json.dump(old, fh, indent=1)
     if out_md:
         with open(out_md, "w") as fh:
             fh.write(text + "\n")
