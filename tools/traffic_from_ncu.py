@@ -35,6 +35,8 @@ UNIT = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "ns": 1e-3, "nsecon
 
 
 def classify(name):
+    for ns in ("<unnamed>::", "unnamed>::", "(anonymous namespace)::", "ftt::"):
+        name = name.replace(ns, "")
     short = name.split("(")[0].split("::")[-1]
     short = short.replace("void ", "").split("<")[0].strip()
     for cls, prefixes in CLASSES:
