@@ -165,7 +165,7 @@ class SparseTensor:
         object.__setattr__(t, "coords", c)
         object.__setattr__(t, "values", v)
         object.__setattr__(t, "_lin", None)
-        object.__setattr__(t, "_dev", (coords_d, values_d, None))
+        object.__setattr__(t, "_dev", (coords_d, values_d, None, None))
         object.__setattr__(t, "_pin", None)
         return t
 
@@ -198,48 +198,89 @@ class SparseTensor:
         return out.reshape(self.shape)
 
     # -- device copy (host -> HBM once; reused by every GPU call on this tensor)
+    # _dev = (coords or None, values, lin or None, values_ready event or None)
+    def _pinned(self):
+        pin = self._pin
+        if pin is None:
+            torch = nat.torch_mod()
+            compact = self._lin is not None and self.nnz > 0
+            src = self._lin if compact else self.coords
+            pc = torch.empty(src.shape, dtype=torch.int64, pin_memory=True)
+            pv = torch.empty(self.values.shape, dtype=torch.float64, pin_memory=True)
+            pc.numpy()[...] = src
+            pv.numpy()[...] = self.values
+            pin = (pc, pv)
+            object.__setattr__(self, "_pin", pin)
+        return pin
+
+    def _upload(self):
+        """H2D of the canonical form: `lin` on the current stream (the index
+        kernels start on it), the values on a side stream whose completion
+        event the consumers wait for -- select_p's counts (which read only
+        `lin`) overlap the values' transfer."""
+        torch = nat.torch_mod()
+        pin = self._pinned()
+        compact = self._lin is not None and self.nnz > 0
+        main = torch.cuda.current_stream()
+        lin = pin[0].to("cuda", non_blocking=True)
+        side = _side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            v = pin[1].to("cuda", non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        v.record_stream(main)
+        if compact:
+            object.__setattr__(self, "_dev", (None, v, lin, ev))
+        else:  # no canonical linear index on the host: these are the coordinates
+            object.__setattr__(self, "_dev", (lin, v, None, ev))
+
     def device_arrays(self):
         """``(coords, values)`` as CUDA tensors (cached).  The host side is
         staged once in pinned memory; what crosses PCIe is the canonical
         linear index (8 B per nonzero) and the values, and the coordinate
-        rows are rebuilt on the device (``ftt_delinearize``) -- 16 B per
-        nonzero instead of 8d + 8."""
+        rows are rebuilt on the device (``ftt_delinearize``) only when a
+        caller needs them."""
         if self._dev is None:
+            self._upload()
+        c, v, lin, ev = self._dev
+        if ev is not None:
+            nat.torch_mod().cuda.current_stream().wait_event(ev)
+        if c is None:
             torch = nat.torch_mod()
-            pin = self._pin
-            compact = self._lin is not None and self.nnz > 0
-            if pin is None:
-                src = self._lin if compact else self.coords
-                pc = torch.empty(src.shape, dtype=torch.int64, pin_memory=True)
-                pv = torch.empty(self.values.shape, dtype=torch.float64, pin_memory=True)
-                pc.numpy()[...] = src
-                pv.numpy()[...] = self.values
-                pin = (pc, pv)
-                object.__setattr__(self, "_pin", pin)
-            c = pin[0].to("cuda", non_blocking=True)
-            v = pin[1].to("cuda", non_blocking=True)
-            lin = None
-            if compact:
-                coords = torch.empty(self.coords.shape, dtype=torch.int64, device="cuda")
-                nat.check(nat.lib().ftt_delinearize(nat.context(), nat.ptr(c), self.nnz, self.ndim,
-                                                    nat.i64_array(self.shape), nat.ptr(coords)),
-                          "ftt_delinearize")
-                lin, c = c, coords
-            object.__setattr__(self, "_dev", (c, v, lin))
-        return self._dev[0], self._dev[1]
+            c = torch.empty(self.coords.shape, dtype=torch.int64, device="cuda")
+            nat.check(nat.lib().ftt_delinearize(nat.context(), nat.ptr(lin), self.nnz, self.ndim,
+                                                nat.i64_array(self.shape), nat.ptr(c)),
+                      "ftt_delinearize")
+        object.__setattr__(self, "_dev", (c, v, lin, None))
+        return c, v
+
+    def device_lin_values(self):
+        """``(lin, values, values_ready)``: the canonical linear index and the
+        values on the device without the coordinate rows; `values_ready` is
+        an event the consumer of `values` must wait for (or None)."""
+        if self._dev is None:
+            self._upload()
+        c, v, lin, ev = self._dev
+        if lin is None:
+            lin = self.device_lin()
+            c, v, lin, ev = self._dev
+        return lin, v, ev
 
     def device_lin(self):
         """The canonical C-order linear index on the device (cached): the
         compact form the index kernels read (8 B per nonzero)."""
-        c, v = self.device_arrays()
+        if self._dev is None:
+            self._upload()
         lin = self._dev[2]
         if lin is None:
+            c, v = self.device_arrays()
             torch = nat.torch_mod()
             lin = torch.empty(max(self.nnz, 1), dtype=torch.int64, device="cuda")
             nat.check(nat.lib().ftt_linearize(nat.context(), nat.ptr(c), self.nnz, self.ndim,
                                               nat.i64_array(self.shape), nat.ptr(lin)),
                       "ftt_linearize")
-            object.__setattr__(self, "_dev", (c, v, lin))
+            object.__setattr__(self, "_dev", (c, v, lin, None))
         return lin
 
     @property
@@ -314,6 +355,19 @@ class FiberSet:
         coords[:, rest] = self.fixed_coords[owner]
         coords[:, self.pivot] = self.pivot_index
         return SparseTensor(self.shape, coords, self.values)
+
+
+_SIDE = {}
+
+
+def _side_stream():
+    """One side stream per device for the values' H2D copy."""
+    torch = nat.torch_mod()
+    dev = torch.cuda.current_device()
+    st = _SIDE.get(dev)
+    if st is None:
+        st = _SIDE[dev] = torch.cuda.Stream(dev)
+    return st
 
 
 def frobenius_norm(t) -> float:
@@ -410,8 +464,10 @@ def extract_nonzero_fibers(t: SparseTensor, pivot: int) -> FiberSet:
     if t.nnz == 0:
         return FiberSet(t.shape, pivot, np.zeros((0, max(d - 1, 0)), np.int64),
                         np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
-    c, v = t.device_arrays()
-    df = fibers_device(t.shape, pivot, c, v, t.nnz, lin_d=t.device_lin())
+    lin, v, ev = t.device_lin_values()
+    if ev is not None:
+        nat.torch_mod().cuda.current_stream().wait_event(ev)
+    df = fibers_device(t.shape, pivot, None, v, t.nnz, lin_d=lin)
     fixed = df.fixed_coords_host() if d > 1 else np.zeros((df.R, 0), np.int64)
     return FiberSet(t.shape, pivot, fixed, df.indptr.cpu().numpy(), df.pivot_index.cpu().numpy(),
                     df.values.cpu().numpy(), _dev=df)

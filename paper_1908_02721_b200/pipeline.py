@@ -188,7 +188,9 @@ def _upper_bond_bounds(dims, pivot: int, num_fibers: int):
 def _fiber_counts_device(a: SparseTensor):
     if a.nnz == 0:
         return [0] * a.ndim
-    c, _ = a.device_arrays()
+    # the coordinate rows serve only the overflow fallback: passed when the
+    # tensor already holds them, else the native side rebuilds them from lin
+    c = a._dev[0] if a._dev is not None else None
     counts = (nat.ctypes.c_int64 * a.ndim)()
     nat.check(nat.lib().ftt_fiber_counts_lin(nat.context(), nat.ptr(a.device_lin()), nat.ptr(c),
                                              a.nnz, a.ndim, nat.i64_array(a.shape), counts),
@@ -1102,7 +1104,7 @@ def _normalize(eps, mode):
 
 
 def fasttt_device(a: SparseTensor, coords_d, values_d, eps, pivot, mode, fixed_ranks,
-                  precise_pivot, c_svd, report=True) -> DeviceResult:
+                  precise_pivot, c_svd, report=True, values_ready=None) -> DeviceResult:
     """The decomposition on device arrays (COO already in HBM)."""
     d = a.ndim
     dims = a.shape
@@ -1122,6 +1124,8 @@ def fasttt_device(a: SparseTensor, coords_d, values_d, eps, pivot, mode, fixed_r
     # once at the end (the COO values are validated finite up front)
     nat.check(lib.ftt_set_deferred_checks(ctx, 1), "ftt_set_deferred_checks")
     try:
+        if values_ready is not None:  # the values' H2D overlapped select_p
+            _torch().cuda.current_stream().wait_event(values_ready)
         res = _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, notes,
                                   report)
     finally:
@@ -1164,6 +1168,8 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
         norm_a = math.sqrt(na2)
         inner = _inner_error_structured(df, sw, out, na2)
         if inner is None:
+            if coords_d is None:
+                coords_d, _ = a.device_arrays()
             inner = _inner_error_device(coords_d, values_d, nnz, out, na2)
         exact_shapes = [tuple(c.shape) for c in cores]
         total = _diff_total(exact_shapes, [tuple(c.shape) for c in out])
@@ -1202,11 +1208,15 @@ def fasttt(a: SparseTensor, eps: float | None = 1e-14, pivot: int | None = None,
     wall0 = time.perf_counter()
     cpu0 = time.process_time()
     eps, mode = _normalize(eps, mode)
+    ready = None
     if a.nnz:
-        coords_d, values_d = a.device_arrays()
+        # lin + values only (no coordinate rows); the values' copy runs on a
+        # side stream under select_p's counts
+        _, values_d, ready = a.device_lin_values()
     else:
-        coords_d = values_d = None
-    res = fasttt_device(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, precise_pivot, c_svd)
+        values_d = None
+    res = fasttt_device(a, None, values_d, eps, pivot, mode, fixed_ranks, precise_pivot, c_svd,
+                        values_ready=ready)
     if res.zero and res.cores is None:
         tt = tt_zero(a.shape)
         return tt, DecompositionReport(
