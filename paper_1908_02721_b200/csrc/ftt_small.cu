@@ -41,7 +41,9 @@ namespace ftt {
 namespace {
 
 constexpr double kEps = 2.220446049250313e-16;
-constexpr int LEAF_NT = 256;  // TSQR / QR kernels: 256 threads, one row each
+constexpr int LEAF_NT = 256;  // TSQR / QR kernels: 256 threads, one row each ...
+constexpr int LEAF_MAX = 512; // ... 512 for n <= 16 (half the leaves, fewer tree levels)
+inline int leaf_rows(int n) { return n <= 16 ? LEAF_MAX : LEAF_NT; }
 constexpr int SVD_NT = 1024;  // SVD kernel: 32 warps, one per pair of a Jacobi round (n <= 64)
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -76,7 +78,7 @@ __device__ __forceinline__ double reduce_scatter(double (&v)[32], int lane) {
 
 template <int NMAX>
 struct Scratch {
-  double red[LEAF_NT / 32][NMAX];  // per-warp partial sums (QR kernels: LEAF_NT threads)
+  double red[LEAF_MAX / 32][NMAX];  // per-warp partial sums (QR kernels: <= LEAF_MAX threads)
   double rowc[NMAX];              // row c (pivot row) of the current step
   double wv[NMAX];                // w_j of the current step
   double sc[4];                   // tau, beta, scal
@@ -316,7 +318,7 @@ __device__ bool load_row(double (&a)[NMAX], int mb, int n, const double *__restr
 // is formed from the reflectors staged in shared memory (dynamic, m_b x n).
 // status[0] |= 1 on a non-finite input.
 template <int NMAX>
-__global__ void __launch_bounds__(LEAF_NT, 1) k_tsqr_level(int64_t M, int n,
+__global__ void __launch_bounds__(NMAX <= 16 ? LEAF_MAX : LEAF_NT, 1) k_tsqr_level(int64_t M, int n,
                                                             const double *__restrict__ A,
                                                             int64_t lda, int trans,
                                                             double *__restrict__ Rs, int64_t ldr,
@@ -324,8 +326,8 @@ __global__ void __launch_bounds__(LEAF_NT, 1) k_tsqr_level(int64_t M, int n,
                                                             int root, int *__restrict__ status) {
   extern __shared__ double Sref[];
   __shared__ Scratch<NMAX> sc;
-  const int64_t r0 = (int64_t)blockIdx.x * LEAF_NT;
-  const int mb = (int)min((int64_t)LEAF_NT, M - r0);
+  const int64_t r0 = (int64_t)blockIdx.x * blockDim.x;  // leaf rows = threads (grid > 1)
+  const int mb = (int)min((int64_t)blockDim.x, M - r0);
   const int k = min(mb, n);
   const int i = threadIdx.x;
   double a[NMAX];
@@ -452,13 +454,14 @@ int set_attrs() {
 void launch_level(ftt_ctx *ctx, int n, unsigned grid, int64_t M, const double *A, int64_t lda,
                   int trans, double *Rs, int64_t ldr, double *Qo, int64_t ldq, int root,
                   int *status) {
-  const size_t smem = 8 * (size_t)std::min<int64_t>(M, LEAF_NT) * n;
+  const int leaf = leaf_rows(n);
+  const size_t smem = 8 * (size_t)std::min<int64_t>(M, leaf) * n;
   // a single short block (tree roots, 16..64 rows) runs with just enough
   // warps for its rows and columns: fewer warps per barrier and reduction
-  unsigned nt = LEAF_NT;
+  unsigned nt = (unsigned)leaf;
   if (grid == 1) {
-    const int64_t need = std::max<int64_t>(std::min<int64_t>(M, LEAF_NT), n);
-    nt = (unsigned)std::min<int64_t>(LEAF_NT, ceil_div(need, 32) * 32);
+    const int64_t need = std::max<int64_t>(std::min<int64_t>(M, leaf), n);
+    nt = (unsigned)std::min<int64_t>(leaf, ceil_div(need, 32) * 32);
   }
   switch (nmax_for(n)) {
     case 8:
@@ -496,7 +499,7 @@ struct Tree {
 Tree make_tree(int64_t M, int n, int64_t root_rows_max) {
   Tree t;
   t.rows.push_back(M);
-  while (t.rows.back() > root_rows_max) t.rows.push_back(ceil_div(t.rows.back(), LEAF_NT) * n);
+  while (t.rows.back() > root_rows_max) t.rows.push_back(ceil_div(t.rows.back(), leaf_rows(n)) * n);
   return t;
 }
 
@@ -842,7 +845,7 @@ static int tsqr_reduce(ftt_ctx *ctx, int64_t M, int n, const double *A, int64_t 
   int cur_trans = trans;
   for (size_t l = 0; l + 1 < t.rows.size(); ++l) {
     const int64_t Ml = t.rows[l];
-    const int64_t nb = ceil_div(Ml, LEAF_NT);
+    const int64_t nb = ceil_div(Ml, leaf_rows(n));
     double *Qo = nullptr, *Rs = nullptr;
     FTT_CHECK(owned_alloc(ctx, (void **)&Qo, 8 * (size_t)Ml * n));
     FTT_CHECK(owned_alloc(ctx, (void **)&Rs, 8 * (size_t)t.rows[l + 1] * n));
@@ -869,7 +872,8 @@ static int tsqr_expand(ftt_ctx *ctx, const Tree &t, int n, int r, const std::vec
   std::vector<double *> tmp;
   for (int l = nl - 1; l >= 0; --l) {
     const int64_t Ml = t.rows[l];
-    const int64_t nb = ceil_div(Ml, LEAF_NT);
+    const int leaf = leaf_rows(n);
+    const int64_t nb = ceil_div(Ml, leaf);
     double *dst = Out;
     int64_t dld = ldo;
     if (l > 0) {
@@ -877,8 +881,8 @@ static int tsqr_expand(ftt_ctx *ctx, const Tree &t, int n, int r, const std::vec
       dld = Ml;
       tmp.push_back(dst);
     }
-    dim3 grid((unsigned)nb, (unsigned)ceil_div(LEAF_NT, EX_ROWS));
-    k_tsqr_expand<<<grid, 256, 0, ctx->stream>>>(Ml, n, r, LEAF_NT, qs[2 * l], Ml, cur, cur_ld, dst,
+    dim3 grid((unsigned)nb, (unsigned)ceil_div(leaf, EX_ROWS));
+    k_tsqr_expand<<<grid, 256, 0, ctx->stream>>>(Ml, n, r, leaf, qs[2 * l], Ml, cur, cur_ld, dst,
                                                  dld);
     FTT_LAUNCHED(ctx);
     cur = dst;
@@ -905,7 +909,7 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, i
   std::vector<double *> qs;
   const double *root;
   int64_t root_ld;
-  FTT_CHECK(tsqr_reduce(ctx, M, n, A, lda, trans, LEAF_NT, &t, &qs, &root, &root_ld, status));
+  FTT_CHECK(tsqr_reduce(ctx, M, n, A, lda, trans, leaf_rows(n), &t, &qs, &root, &root_ld, status));
   const int64_t Mr = t.rows.back();
   if (t.rows.size() == 1) {
     launch_level(ctx, n, 1, Mr, root, root_ld, trans, R, ldr, Q, ldq, 1, status);
@@ -948,7 +952,7 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   std::vector<double *> qs;
   const double *root;
   int64_t root_ld;
-  FTT_CHECK(tsqr_reduce(ctx, M, n, A, lda, trans, LEAF_NT, &t, &qs, &root, &root_ld, status));
+  FTT_CHECK(tsqr_reduce(ctx, M, n, A, lda, trans, leaf_rows(n), &t, &qs, &root, &root_ld, status));
   const int64_t Mr = t.rows.back();
   const bool single = t.rows.size() == 1;
   double *Qr = nullptr, *W = nullptr;
