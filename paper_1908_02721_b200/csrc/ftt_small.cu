@@ -764,9 +764,13 @@ __global__ void __launch_bounds__(QJ_NT) k_jacobi_qr(int m, int n, const double 
           b += __shfl_xor_sync(0xffffffffu, b, o);
           gg += __shfl_xor_sync(0xffffffffu, gg, o);
         }
-        if (ok && a > floor && b > floor && fabs(gg) > tol * sqrt(a * b)) {
-          const double zeta = (b - a) / (2.0 * gg);
-          const double t = copysign(1.0 / (fabs(zeta) + sqrt(1.0 + zeta * zeta)), zeta);
+        // the same test and angle as the other Jacobi kernels with two fewer
+        // fp64 sqrt/div on the warp's serial chain: |g| > tol sqrt(ab) as
+        // g^2 > tol^2 ab, and t = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2)),
+        // d = b - a (= sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = d / 2g)
+        if (ok && a > floor && b > floor && gg * gg > tol * tol * (a * b)) {
+          const double dd = b - a;
+          const double t = copysign(1.0, dd) * (2.0 * gg) / (fabs(dd) + sqrt(dd * dd + 4.0 * gg * gg));
           const double cs = rsqrt(1.0 + t * t);
           const double sn = cs * t;
           double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
