@@ -33,6 +33,17 @@ int qr_factor(ftt_ctx *ctx, int64_t m, int64_t n, double *A, int64_t lda, double
 int qr_apply_q(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, const double *Tblk,
                int64_t r, double *Z, int64_t ldz, double *ws, size_t ws_elems);
 size_t qr_apply_workspace_elems(int64_t m, int64_t n, int64_t r);
+// The block T factors of an already factored A (reflectors below the
+// diagonal, tau) in qr_factor's layout, so that qr_apply_q can use them.
+int qr_build_tblk(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
+                  const double *tau, double *Tblk, double *ws, size_t ws_elems);
+
+// Householder QR with column pivoting of an n x n matrix (ftt_qrcp.cu): B is
+// overwritten (scratch); Out (n x n, ld n) gets the reflectors below the
+// diagonal and R2 on and above it in pivoted order, tau (n), perm (n device
+// ints: pivoted position -> original column).
+bool qrcp_ok(int64_t n);
+int qrcp_factor(ftt_ctx *ctx, int64_t n, double *B, double *Out, double *tau, int *perm);
 
 // Numerical rank r of the sketch Y (mA x k <= 64) and its pivot order
 // (sel_dev, k entries; the first r span Y) from a pivoted Cholesky of the

@@ -565,6 +565,22 @@ int qr_factor(ftt_ctx *ctx, int64_t m, int64_t n, double *A, int64_t lda, double
   return FTT_OK;
 }
 
+int qr_build_tblk(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
+                  const double *tau, double *Tblk, double *ws, size_t ws_elems) {
+  QrWs w;
+  if (!carve(ws, ws_elems, m, n, &w)) {
+    set_error("qr_build_tblk: workspace too small");
+    return FTT_ERR_INVALID;
+  }
+  const int64_t k = std::min(m, n);
+  for (int64_t J = 0; J < k; J += QR_NBO) {
+    const int jbo = (int)std::min<int64_t>(QR_NBO, k - J);
+    FTT_CHECK(build_t(ctx, m - J, jbo, A + J + J * lda, lda, tau + J,
+                      Tblk + (J / QR_NBO) * QR_NBO * QR_NBO, jbo, w));
+  }
+  return FTT_OK;
+}
+
 int qr_apply_q(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, const double *Tblk,
                int64_t r, double *Z, int64_t ldz, double *ws, size_t ws_elems) {
   QrWs w;

@@ -47,6 +47,10 @@ struct SvdState {
   std::vector<int64_t> perm;  // sorted position -> column of Y
   int sweeps = 0;
   bool precond = false;  // Jacobi ran on R2^T (QR of R^T) instead of R^T
+  // Jacobi ran on R2^T with R Pi = Q2 R2 (pivoted QR of R: A Pi = (Q Q2) R2);
+  // B holds Q2's reflectors and R2, piv the pivoting (device ints)
+  bool pivoted = false;
+  int *piv = nullptr;
   bool direct = false;   // Jacobi ran on A_tall itself (Y aliases Af)
   bool small = false;    // narrow path (ftt_small.cu): Af holds U = Q P, Y = R^T P
   // low-rank path (ftt_svd_lowrank_f64): A_tall ~= Qk Bk with a certified
@@ -518,6 +522,26 @@ __global__ void __launch_bounds__(JT, NS == 4 ? 2 : 3) k_jacobi_persistent(int64
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = -1;
 }
+// R (n x n, ld n, zero below the diagonal) from the factored A.
+__global__ void k_upper(int64_t n, const double *__restrict__ A, int64_t lda, double *__restrict__ R) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / n, i = t - j * n;
+    R[i + j * n] = i <= j ? A[i + j * lda] : 0.0;
+  }
+}
+
+// V[piv[i], :] = W[i, :] (rows back to the original column order).
+__global__ void k_unpivot_rows(int64_t n, int64_t r, const int *__restrict__ piv,
+                               const double *__restrict__ W, int64_t ldw, double *__restrict__ V,
+                               int64_t ldv) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * r;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / n, i = t - j * n;
+    V[piv[i] + j * ldv] = W[i + j * ldw];
+  }
+}
+
 // X = R^T from the factored A (upper triangle = R), n x n.
 __global__ void k_rt(int64_t n, const double *__restrict__ A, int64_t lda, double *__restrict__ X) {
   int64_t total = n * n;
@@ -675,6 +699,7 @@ void svd_state_release(ftt_ctx *ctx, SvdState *s) {
   owned_free(ctx, s->B);
   owned_free(ctx, s->tau2);
   owned_free(ctx, s->Tb2);
+  owned_free(ctx, s->piv);
   owned_free(ctx, s->Qk);
   owned_free(ctx, s->Bk);
   svd_state_release(ctx, s->inner);
@@ -780,14 +805,27 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
   {
     static const char *pc = getenv("FTT_PRECOND");
     st->precond = !st->direct && nA > 1 && pc && pc[0] == '1';  // off by default
+    // pivoted QR of R before the Jacobi (FTT_QRCP=0 off, =1 for every
+    // size): on by default for 96..1024 columns, where R stays L2-resident
+    // and the BLAS-2 pivoted factorization costs a few ms (config 4's
+    // 2064 x 766 operand: Jacobi 88 -> 33 ms incl. the QRCP).  Wider
+    // operands are left unpivoted: on config 3's 25168 x 4916 operand the
+    // QRCP streams R from HBM every step (~0.6 s) and its more accurate small
+    // singular values moved a tail decision away from LAPACK gesdd's
+    // (rank 1975 vs the reference's 1971).
+    static const char *qp = getenv("FTT_QRCP");
+    const bool qp_all = qp && qp[0] == '1', qp_off = qp && qp[0] == '0';
+    st->pivoted = !st->direct && !st->precond && !qp_off && qrcp_ok(nA) && nA >= 96 &&
+                  (qp_all || nA <= 1024);
   }
   if (!st->direct) FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->P, 8 * (size_t)nA * nA));
-  if (st->precond) {
+  if (st->precond || st->pivoted) {
     FTT_CHECK(owned_alloc(ctx, (void **)&st->B, 8 * (size_t)nA * nA));
     FTT_CHECK(owned_alloc(ctx, (void **)&st->tau2, 8 * (size_t)nA));
     FTT_CHECK(owned_alloc(ctx, (void **)&st->Tb2, 8 * qr_tblk_elems(nA, nA)));
   }
+  if (st->pivoted) FTT_CHECK(owned_alloc(ctx, (void **)&st->piv, 4 * (size_t)nA));
   // tall orientation A_tall (mA x nA, column-major): M itself when m >= n,
   // else M^T.  A row-major M is the column-major M^T.
   const bool need_t = a_row_major ? !st->transposed : st->transposed;
@@ -821,6 +859,14 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->B);
     FTT_LAUNCHED(ctx);
     FTT_CHECK(qr_factor(ctx, nA, nA, st->B, nA, st->tau2, st->Tb2, ws, wse));
+    k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->B, nA, st->Y);
+    FTT_LAUNCHED(ctx);
+  } else if (st->pivoted) {
+    // R (upper triangle of the factored A) -> R Pi = Q2 R2 -> X = R2^T
+    k_upper<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->Af, mA, st->Y);
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(qrcp_factor(ctx, nA, st->Y, st->B, st->tau2, st->piv));
+    FTT_CHECK(qr_build_tblk(ctx, nA, nA, st->B, nA, st->tau2, st->Tb2, ws, wse));
     k_rt<<<grid_for(nA * nA, 256, 4), 256, 0, ctx->stream>>>(nA, st->B, nA, st->Y);
     FTT_LAUNCHED(ctx);
   } else {
@@ -1039,6 +1085,22 @@ int svd_raw_vectors(ftt_ctx *ctx, SvdState *st, int64_t rank, double *UA, double
                                                                         sel, nullptr, VA, nA);
     FTT_LAUNCHED(ctx);
     FTT_CHECK(qr_apply_q(ctx, nA, nA, st->B, nA, st->Tb2, rank, VA, nA, ws, wse));
+  } else if (st->pivoted) {
+    // A Pi = (Q Q2) R2, R2 = P Sigma Yhat^T:  V_A = Pi Yhat[:, sel],
+    // U_A = Q [Q2 P[:, sel]; 0]
+    double *W = nullptr;
+    FTT_CHECK(owned_alloc(ctx, (void **)&W, 8 * (size_t)nA * rank));
+    k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA,
+                                                                        sel, inv, W, nA);
+    FTT_LAUNCHED(ctx);
+    k_unpivot_rows<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, rank, st->piv, W, nA,
+                                                                         VA, nA);
+    FTT_LAUNCHED(ctx);
+    owned_free(ctx, W);
+    k_gather_cols<<<grid_for(mA * rank, 256, 4), 256, 0, ctx->stream>>>(mA, nA, rank, st->P, nA,
+                                                                        sel, nullptr, UA, mA);
+    FTT_LAUNCHED(ctx);
+    FTT_CHECK(qr_apply_q(ctx, nA, nA, st->B, nA, st->Tb2, rank, UA, mA, ws, wse));
   } else {
     // V_A = Y[:, sel] / sigma ;  U_A = Q [P[:, sel]; 0]
     k_gather_cols<<<grid_for(nA * rank, 256, 4), 256, 0, ctx->stream>>>(nA, nA, rank, st->Y, nA,
