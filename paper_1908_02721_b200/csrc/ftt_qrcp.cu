@@ -112,19 +112,43 @@ __global__ void __launch_bounds__(QP_NT) k_qrcp(int n, double *__restrict__ B, i
         }
       p = bidx;
     } else {
-      double best = -1.0;
+      // the CTAs' candidates, one per thread (G <= QP_NT), block arg-max
+      // (largest norm, ties to the lowest logical position)
+      double bv = -1.0;
       int bpos = n;
-      for (int g = 0; g < G; ++g) {
-        const double v = cand_v[g];
+      for (int g = tid; g < G; g += QP_NT) {
         const int c = cand_i[g];
         if (c < 0) continue;
+        const double v = cand_v[g];
         const int pos = ipos[c];
-        if (v > best || (v == best && pos < bpos)) {
-          best = v;
+        if (v > bv || (v == bv && pos < bpos)) {
+          bv = v;
           bpos = pos;
         }
       }
-      p = perm[bpos];
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        if (ov > bv || (ov == bv && op < bpos)) {
+          bv = ov;
+          bpos = op;
+        }
+      }
+      __shared__ double s_pv[QP_NT / 32];
+      __shared__ int s_pp[QP_NT / 32];
+      if (lane == 0) {
+        s_pv[warp] = bv;
+        s_pp[warp] = bpos;
+      }
+      __syncthreads();
+      double best = -1.0;
+      int pbest = n;
+      for (int w = 0; w < nw; ++w)
+        if (s_pv[w] > best || (s_pv[w] == best && s_pp[w] < pbest)) {
+          best = s_pv[w];
+          pbest = s_pp[w];
+        }
+      p = perm[pbest];
     }
     __syncthreads();
     // swap logical positions j and ipos[p] (every CTA, identically)
