@@ -1062,6 +1062,9 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
     return FTT_ERR_NOCONV;
   }
   if (sweeps) *sweeps = st[1];
+  static const bool debug = getenv("FTT_DEBUG") != nullptr;
+  if (debug) fprintf(stderr, "[ftt] direct small svd m=%lld n=%lld sweeps %d\n", (long long)m,
+                     (long long)n, st[1]);
   memcpy(norms_host, h.data() + 2, 8 * (size_t)n);
   return FTT_OK;
 }
