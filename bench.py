@@ -486,7 +486,7 @@ def index_leg(ft, nat, lib, ctx, roof, a, cd, vd, cfg, name, reps):
 
     def once():
         P._fiber_counts_device(a)
-        df = ft.coo.fibers_device(a.shape, pivot, cd, vd, nnz)
+        df = ft.coo.fibers_device(a.shape, pivot, None, vd, nnz, lin_d=a.device_lin())
         sw = P.index_sweeps_device(df)
         return df, sw
 

@@ -2009,10 +2009,13 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
   }
 }
 
-// Fiber keys straight from lin: key = fixed_lin * n_p + i_p with
-// fixed_lin = (lin / T) * S + lin mod S, i_p = (lin / S) mod n_p (S = prod of
-// the dims after the pivot, T = n_p S), identity payload, digit histograms
-// of every pass.  Reads 8 B per nonzero instead of the d coordinates.
+// Fiber keys straight from lin: key = fixed_lin = (lin / T) * S + lin mod S
+// (S = prod of the dims after the pivot, T = n_p S), identity payload, digit
+// histograms of every pass.  The pivot index is NOT in the key: lin order is
+// (prefix, i_p, suffix), so a STABLE sort by the fixed tuple alone leaves
+// equal tuples in ascending i_p -- the reference's lexsort order
+// (tensor.py:387-389) with log2(n_p) fewer key bits (config 5: 55 bits, 7
+// passes instead of 8).  Reads 8 B per nonzero instead of the d coordinates.
 struct LinKeySpec {
   uint64_t S, mS, T, mT, np, mN;
   int shS, shT, shN;
@@ -2022,10 +2025,33 @@ __device__ __forceinline__ uint64_t lin_fiber_key(uint64_t x, const LinKeySpec &
   const uint64_t a = udiv_magic(x, ks.mS, ks.shS);  // lin / S
   const uint64_t lo = x - a * ks.S;
   const uint64_t hi = udiv_magic(x, ks.mT, ks.shT);  // lin / T
-  const uint64_t i = a - hi * ks.np;
-  if (ip) *ip = i;
-  return (hi * ks.S + lo) * ks.np + i;
+  if (ip) *ip = a - hi * ks.np;
+  return hi * ks.S + lo;
 }
+
+// Emit of the fiber extraction on the fixed-tuple keys: the pivot index is
+// re-derived from lin[perm[i]] (a gather from the chunk the sort just read).
+struct FiberEmitLin {
+  const uint64_t *k;
+  const uint32_t *perm;
+  const double *vals_in;
+  const uint64_t *lin;
+  LinKeySpec ks;
+  int64_t *fixed_lin, *indptr, *fiber_of, *pivot_index;
+  double *vals_out;
+  __device__ void operator()(int64_t i, int64_t r, bool f) const {
+    const uint32_t src = perm[i];
+    if (f) {
+      indptr[r] = i;
+      fixed_lin[r] = (int64_t)k[i];
+    }
+    if (fiber_of) fiber_of[i] = f ? r : r - 1;
+    uint64_t ip = 0;
+    lin_fiber_key(lin[src], ks, &ip);
+    pivot_index[i] = (int64_t)ip;
+    vals_out[i] = vals_in[src];
+  }
+};
 
 __global__ void __launch_bounds__(256) k_keys_hist_lin(const uint64_t *__restrict__ lin, int64_t n,
                                                        LinKeySpec ks, int num_passes,
@@ -2172,7 +2198,7 @@ int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, 
 }
 
 int fiber_keys_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, const int64_t *dims,
-                   int32_t pivot, uint64_t **kres, uint32_t **vres) {
+                   int32_t pivot, uint64_t **kres, uint32_t **vres, LinKeySpec *spec_out) {
   int64_t w[32];
   c_strides(d, dims, w);
   LinKeySpec ks;
@@ -2182,8 +2208,10 @@ int fiber_keys_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, co
   magic_u63(ks.S, &ks.mS, &ks.shS);
   magic_u63(ks.T, &ks.mT, &ks.shT);
   magic_u63(ks.np, &ks.mN, &ks.shN);
-  uint64_t bound = 1;
-  for (int k = 0; k < d; ++k) bound *= (uint64_t)dims[k];
+  uint64_t bound = 1;  // fixed tuples < prod of the other extents
+  for (int k = 0; k < d; ++k)
+    if (k != pivot) bound *= (uint64_t)dims[k];
+  *spec_out = ks;
   int num_passes = (bit_length(bound - 1) + 7) / 8;
   if (num_passes < 1) num_passes = 1;
   uint32_t *ghist = take<uint32_t>(ctx, 8 * RADIX);
@@ -2466,13 +2494,14 @@ int ftt_extract_fibers_lin(ftt_ctx *ctx, const int64_t *lin, const double *value
   FTT_CHECK(arena_reserve(ctx, sort_coords_bytes(nnz, true) + compact_scratch_bytes(nnz) + 1024));
   uint64_t *kr;
   uint32_t *vr;
+  LinKeySpec ks;
   FTT_CHECK(fiber_keys_lin(ctx, reinterpret_cast<const uint64_t *>(lin), nnz, d, dims_host, pivot,
-                           &kr, &vr));
+                           &kr, &vr, &ks));
   int64_t *bc = take<int64_t>(ctx, ceil_div(nnz, CP_TILE) + 1);
   int64_t *total = take<int64_t>(ctx, 1);
-  AdjDiffPred pred{kr, make_div63((uint64_t)dims_host[pivot])};
-  FiberEmit emit{kr, vr, values, make_div63((uint64_t)dims_host[pivot]), fixed_lin, indptr, fiber_of,
-                 pivot_index, values_out};
+  AdjDiffPred pred{kr, make_div63(1)};
+  FiberEmitLin emit{kr, vr, values, reinterpret_cast<const uint64_t *>(lin), ks, fixed_lin, indptr,
+                    fiber_of, pivot_index, values_out};
   FTT_CHECK(compact(ctx, nnz, pred, emit, bc, total, PT_SEGMENT, 44.0 * (double)nnz));
   int64_t R = 0;
   FTT_CHECK(copy_to_host(ctx, &R, total, sizeof(R)));
