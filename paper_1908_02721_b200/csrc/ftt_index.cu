@@ -655,10 +655,11 @@ struct SweepKey {
   const int64_t *map_in;
   Div63 dstride, dnk;
   const int64_t *r_other_dev = nullptr;  // device-resident r_other (batched sweeps)
-  __device__ int64_t operator()(int64_t f) const {
+  __device__ int64_t operator()(int64_t f) const { return with_map(f, map_in ? map_in[f] : 0); }
+  // the key with the previous step's map value m given (fused kernels)
+  __device__ int64_t with_map(int64_t f, int64_t m) const {
     const uint64_t q = dstride.quo((uint64_t)fixed_lin[f]);
     int64_t ik = (int64_t)(q - dnk.quo(q) * (uint64_t)nk);
-    int64_t m = map_in ? map_in[f] : 0;
     const int64_t ro = r_other_dev ? *r_other_dev : r_other;
     return side == 0 ? m * nk + ik : ik * ro + m;
   }
@@ -683,6 +684,21 @@ __global__ void k_sweep_gather(int64_t R, SweepKey key, const uint32_t *present,
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
        f += (int64_t)gridDim.x * blockDim.x)
     map_out[f] = (int64_t)present[key(f)];
+}
+
+// Step s's gather fused with step s+1's mark: map_s[f] = rank of key_s(f),
+// then key_{s+1}(f) -- which needs exactly that map value (same side) or
+// none (first step of the other side) -- is marked in the other flag array.
+// One pass over the fibers per step instead of two.
+__global__ void k_sweep_gather_mark(int64_t R, SweepKey key, const uint32_t *present,
+                                    int64_t *map_out, SweepKey next, int next_uses_map,
+                                    uint32_t *present_next) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < R;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = (int64_t)present[key(f)];
+    map_out[f] = m;
+    present_next[next.with_map(f, next_uses_map ? m : 0)] = 1u;
+  }
 }
 
 __global__ void k_sweep_keys(int64_t R, SweepKey key, uint64_t *keys) {
@@ -2679,32 +2695,47 @@ int ftt_index_sweeps_all(ftt_ctx *ctx, const int64_t *fixed_lin, int64_t R, int3
     }
     bmax = std::max(bmax, bound[s]);
   }
-  uint32_t *present = nullptr;
-  FTT_CHECK(zero_flags(ctx, (size_t)bmax, &present));
+  // two zeroed flag arrays: step s ranks in flags[s & 1] while marking step
+  // s + 1's keys in the other (fused gather + mark)
+  uint32_t *zf = nullptr;
+  FTT_CHECK(zero_flags(ctx, 2 * (size_t)bmax, &zf));
+  uint32_t *flags[2] = {zf, zf + bmax};
   FTT_CHECK(arena_reserve(ctx, compact_scratch_bytes(bmax) + align_up(8 * (size_t)(nsteps + 1)) +
                                    4096));
   int64_t *bc = take<int64_t>(ctx, ceil_div(bmax, CP_TILE) + 1);
   int64_t *counts = take<int64_t>(ctx, nsteps + 1);
   const int pb = prof_begin(ctx);
   double alg = 0.0;
-  for (int s = 0; s < nsteps; ++s) {
+  auto key_of = [&](int st) {
     // previous step of the same side: its map and its count
+    const bool first = (st == 0) || side[st - 1] != side[st];
+    SweepKey sk{side[st], fixed_lin, stride[st], nk[st], 1, first ? nullptr : maps[st - 1],
+                make_div63((uint64_t)stride[st]), make_div63((uint64_t)nk[st])};
+    if (side[st] == 1 && !first) sk.r_other_dev = counts + (st - 1);
+    return sk;
+  };
+  k_sweep_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, key_of(0), flags[0]);
+  FTT_LAUNCHED(ctx);
+  for (int s = 0; s < nsteps; ++s) {
     const bool first_of_side = (s == 0) || side[s - 1] != side[s];
-    SweepKey sk{side[s], fixed_lin, stride[s], nk[s], 1, first_of_side ? nullptr : maps[s - 1],
-                make_div63((uint64_t)stride[s]), make_div63((uint64_t)nk[s])};
-    if (side[s] == 1 && !first_of_side) sk.r_other_dev = counts + (s - 1);
+    const SweepKey sk = key_of(s);
+    uint32_t *present = flags[s & 1];
     const int64_t *ndev = first_of_side ? nullptr : counts + (s - 1);
     const int64_t nrows = first_of_side ? nk[s] : bound[s];
-    k_sweep_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present);
-    FTT_LAUNCHED(ctx);
     FTT_CHECK(compact(ctx, nrows, FlagPred{present}, KeptEmit{present, kept[s]}, bc, counts + s, -1,
                       0.0, ndev, nk[s]));
-    k_sweep_gather<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present, maps[s]);
+    if (s + 1 < nsteps) {
+      const bool next_first = side[s + 1] != side[s];
+      k_sweep_gather_mark<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(
+          R, sk, present, maps[s], key_of(s + 1), next_first ? 0 : 1, flags[(s + 1) & 1]);
+    } else {
+      k_sweep_gather<<<grid_for(R, 256, 4), 256, 0, ctx->stream>>>(R, sk, present, maps[s]);
+    }
     FTT_LAUNCHED(ctx);
     k_unmark<<<grid_for(std::min(R, bound[s]), 256, 4), 256, 0, ctx->stream>>>(
         kept[s], counts + s, std::min(R, bound[s]), present);
     FTT_LAUNCHED(ctx);
-    alg += (double)R * (16.0 + 4.0 + 16.0 + 4.0 + 8.0);
+    alg += (double)R * (16.0 + 4.0 + 8.0 + 4.0);
   }
   prof_end(ctx, pb, PT_SWEEP, alg, 0.0);
   FTT_CHECK(copy_to_host(ctx, n_kept_out, counts, sizeof(int64_t) * nsteps));
