@@ -4,9 +4,11 @@
 // the blocked Householder QR / Jacobi SVD.  tcgen05 has no f64 kind on
 // sm_100a (ptxas rejects .kind::f64), so DMMA is the fp64 tensor path.
 //
-// CTA tile 64x64x16, 4 warps (2x2, 32x32 each = 4x4 DMMA tiles), register
-// prefetch of the next k-tile into a second shared buffer.  Split-K with a
-// deterministic reduction when the output has too few tiles for 148 SMs.
+// CTA tile TBM x TBN x 16 (64x64 by default; 128 x {16,32,40,48} for narrow
+// outputs, {16,32,48} x 128 for short ones, 16/32/48 squares for small ones), 4
+// warps, k-tiles staged through an NSTAGE-deep cp.async ring in dynamic
+// shared memory.  Split-K with a deterministic reduction when the output has
+// too few tiles for 148 SMs.
 #include "ftt_common.cuh"
 #include "ftt_dense.cuh"
 
@@ -32,9 +34,8 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 // R0 = C read-only, stored transposed when c_trans (R0(row, col) at
 // C[col + row * ldc]).  Used by the certified low-rank SVD to form
 // ||A - Q B||_F without materialising the residual.
-// Tile TBM x TBN (64x64, 128x32 for narrow outputs, 32x128 for short ones),
-// 4 warps of 32x32 each (4x4 DMMA 8x8 tiles), BK = 16, register prefetch of
-// the next k-tile into the second shared buffer.
+// Tile TBM x TBN, 4 warps of (TBM/WM) x (TBN/WN) (MI x NJ DMMA 8x8 tiles),
+// BK = 16, NSTAGE k-tiles in flight.
 // Called by every thread after thread 0 wrote this CTA's npart entry: the
 // last CTA of the grid to arrive (counter, reset by it) sums the nt
 // partials in index order into *out (replaces a separate k_sum_partials).
@@ -63,6 +64,33 @@ __device__ __forceinline__ void last_cta_sum(const double *npart, int64_t nt, do
   }
 }
 
+// cp.async (LDGSTS) helpers: 8-byte element copies with zero fill when
+// `bytes` is 0 (out-of-range rows / columns / k), grouped per k-stage.
+__device__ __forceinline__ void gm_cp8(double *smem, const double *gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void gm_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void gm_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// k-stages in flight per CTA (the LDGSTS ring): the long-K Gram-type
+// products (Q^T A over 10^5..3*10^5 rows) were latency bound at one
+// register-prefetched stage (~1 TB/s); NSTAGE-1 stages ahead keep
+// ~50-100 KB per SM in flight.
+#ifndef FTT_GEMM_STAGES
+#define FTT_GEMM_STAGES 4
+#endif
+constexpr int NSTAGE = FTT_GEMM_STAGES;
+// warps along M for a TBM x TBN tile (4 warps per CTA)
+__host__ __device__ constexpr int tile_wm(int tbm, int tbn) { return tbn == 128 ? 1 : (tbm == 128 ? 4 : 2); }
+constexpr size_t gemm_smem_bytes(int tbm, int tbn) {
+  return sizeof(double) * (size_t)NSTAGE * BK * ((tbm + PAD) + (tbn + PAD));
+}
+
 template <bool TA, bool TB, int EPI = 0, int TBM = 64, int TBN = 64>
 __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, double alpha,
                                               const double *__restrict__ A, int64_t lda,
@@ -72,25 +100,39 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
                                               double *__restrict__ npart = nullptr,
                                               unsigned *__restrict__ tile_cnt = nullptr,
                                               double *__restrict__ sum_out = nullptr) {
-  constexpr int WM = TBM / 32;           // warps along M
+  constexpr int WM = tile_wm(TBM, TBN);  // warps along M
+  constexpr int WN = 4 / WM;             // warps along N
+  constexpr int MI = TBM / WM / 8;       // 8x8 DMMA tiles per warp along M
+  constexpr int NJ = TBN / WN / 8;       // ... along N
+  constexpr int LA = TBM + PAD, LB = TBN + PAD;
   constexpr int RA = TBM * BK / GT;      // A-tile elements per thread
   constexpr int RB = TBN * BK / GT;      // B-tile elements per thread
-  __shared__ double As[2][BK][TBM + PAD];
-  __shared__ double Bs[2][BK][TBN + PAD];
+  static_assert(WM * WN == 4 && MI * 8 * WM == TBM && NJ * 8 * WN == TBN, "tile shape");
+  static_assert(RA * GT == TBM * BK && RB * GT == TBN * BK, "tile load split");
+  static_assert(LA % 16 == 4 || LA % 16 == 12, "A row stride must be conflict-free");
+  static_assert(LB % 16 == 4 || LB % 16 == 12, "B row stride must be conflict-free");
+  extern __shared__ __align__(16) double gm_smem[];
+  double *const As0 = gm_smem;                         // [NSTAGE][BK][LA]
+  double *const Bs0 = gm_smem + (size_t)NSTAGE * BK * LA;  // [NSTAGE][BK][LB]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp % WM) * 32, wn = (warp / WM) * 32;
+  const int wm = (warp % WM) * (MI * 8), wn = (warp / WM) * (NJ * 8);
   const int64_t tm = (int64_t)blockIdx.x * TBM, tn = (int64_t)blockIdx.y * TBN;
   const int64_t kb = (int64_t)blockIdx.z * kps;
   const int64_t ke = min(k, kb + kps);
+  const int64_t nk = ke > kb ? (ke - kb + BK - 1) / BK : 0;
 
-  double acc[4][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double ra[RA], rb[RB];
-  auto load = [&](int64_t k0) {
+  // issue the copies of k-tile t into ring slot t % NSTAGE
+  auto issue = [&](int64_t t) {
+    const int slot = (int)(t % NSTAGE);
+    const int64_t k0 = kb + t * BK;
+    double *As = As0 + (size_t)slot * BK * LA;
+    double *Bs = Bs0 + (size_t)slot * BK * LB;
 #pragma unroll
     for (int r = 0; r < RA; ++r) {
       const int e = r * GT + tid;
@@ -103,9 +145,8 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
         i = e / BK;
       }
       const int64_t gi = tm + i, gk = k0 + kk;
-      double v = 0.0;
-      if (gi < m && gk < ke) v = TA ? A[gk + gi * lda] : A[gi + gk * lda];
-      ra[r] = v;
+      const bool ok = gi < m && gk < ke;
+      gm_cp8(As + kk * LA + i, ok ? (TA ? A + gk + gi * lda : A + gi + gk * lda) : A, ok ? 8 : 0);
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
@@ -119,73 +160,46 @@ __global__ void __launch_bounds__(GT) k_dgemm(int64_t m, int64_t n, int64_t k, d
         kk = e / TBN;
       }
       const int64_t gj = tn + j, gk = k0 + kk;
-      double w = 0.0;
-      if (gj < n && gk < ke) w = TB ? B[gj + gk * ldb] : B[gk + gj * ldb];
-      rb[r] = w;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int r = 0; r < RA; ++r) {
-      const int e = r * GT + tid;
-      int i, kk;
-      if (!TA) {
-        i = e % TBM;
-        kk = e / TBM;
-      } else {
-        kk = e % BK;
-        i = e / BK;
-      }
-      As[buf][kk][i] = ra[r];
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const int e = r * GT + tid;
-      int j, kk;
-      if (!TB) {
-        kk = e % BK;
-        j = e / BK;
-      } else {
-        j = e % TBN;
-        kk = e / TBN;
-      }
-      Bs[buf][kk][j] = rb[r];
+      const bool ok = gj < n && gk < ke;
+      gm_cp8(Bs + kk * LB + j, ok ? (TB ? B + gj + gk * ldb : B + gk + gj * ldb) : B, ok ? 8 : 0);
     }
   };
 
-  int buf = 0;
-  if (kb < ke) {
-    load(kb);
-    store(0);
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nk) issue(s);
+    gm_commit();
   }
-  __syncthreads();
-  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
-    const bool more = k0 + BK < ke;
-    if (more) load(k0 + BK);
+  for (int64_t t = 0; t < nk; ++t) {
+    gm_wait<NSTAGE - 2>();  // k-tile t has landed (this thread's copies) ...
+    __syncthreads();        // ... everyone's, and slot (t-1) % NSTAGE is free
+    if (t + NSTAGE - 1 < nk) issue(t + NSTAGE - 1);
+    gm_commit();
+    const int slot = (int)(t % NSTAGE);
+    const double *As = As0 + (size_t)slot * BK * LA;
+    const double *Bs = Bs0 + (size_t)slot * BK * LB;
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
-      double a[4], b[4];
+      double a[MI], b[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+      for (int i = 0; i < MI; ++i) a[i] = As[(ks + (lane & 3)) * LA + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
+      for (int j = 0; j < NJ; ++j) b[j] = Bs[(ks + (lane & 3)) * LB + wn + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    if (more) store(buf ^ 1);
-    __syncthreads();
-    buf ^= 1;
   }
+  gm_wait<0>();
   // epilogue
   double ss = 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < MI; ++i) {
     int64_t row = tm + wm + i * 8 + (lane >> 2);
     if (row >= m) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         int64_t col = tn + wn + j * 8 + 2 * (lane & 3) + h;
@@ -411,29 +425,72 @@ __global__ void __launch_bounds__(128) k_resid_cols(int64_t m, int64_t n, int k,
   last_cta_sum(npart, (int64_t)gridDim.x * gridDim.y, sum_out, counter);
 }
 
-// Tile shape for an m x n output: narrow outputs (n <= 32) use 128x32,
-// short ones (m <= 32) 32x128 -- a 64x64 tile would spend half or more of
-// its DMMAs on padding.
-enum TileShape { T64x64 = 0, T128x32 = 1, T32x128 = 2 };
+// Tile shape for an m x n output: the DMMA work of a tile is TBM x TBN
+// whatever the valid part, so narrow outputs (a 40-wide sketch, a 16-rank
+// core) get a tile whose short side just covers them -- a 64x64 tile spent
+// 37% of config 5's largest product (104,976 x 40 x 512) on padding.
+enum TileShape {
+  T64x64 = 0, T128x32, T32x128, T128x16, T16x128, T128x40, T128x48, T48x128, T48x48, T32x32, T16x16
+};
 inline TileShape pick_tile(int64_t m, int64_t n) {
-  if (n <= 32 && m > 32) return T128x32;
-  if (m <= 32 && n > 32) return T32x128;
+  if (m > 48 && n <= 48) {
+    if (n <= 16) return T128x16;
+    if (n <= 32) return T128x32;
+    return n <= 40 ? T128x40 : T128x48;
+  }
+  if (n > 48 && m <= 48) return m <= 16 ? T16x128 : (m <= 32 ? T32x128 : T48x128);
+  if (m <= 48 && n <= 48 && (m > 32 || n > 32)) return T48x48;
+  if (m <= 32 && n <= 32) return m <= 16 && n <= 16 ? T16x16 : T32x32;
   return T64x64;
 }
-inline int tile_m(TileShape t) { return t == T128x32 ? 128 : (t == T32x128 ? 32 : 64); }
-inline int tile_n(TileShape t) { return t == T128x32 ? 32 : (t == T32x128 ? 128 : 64); }
+inline int tile_m(TileShape t) {
+  switch (t) {
+    case T128x32: case T128x16: case T128x40: case T128x48: return 128;
+    case T32x128: return 32;
+    case T16x128: return 16;
+    case T48x128: case T48x48: return 48;
+    case T32x32: return 32;
+    case T16x16: return 16;
+    default: return 64;
+  }
+}
+inline int tile_n(TileShape t) {
+  switch (t) {
+    case T32x128: case T16x128: case T48x128: return 128;
+    case T128x32: return 32;
+    case T128x16: return 16;
+    case T128x40: return 40;
+    case T128x48: case T48x48: return 48;
+    case T32x32: return 32;
+    case T16x16: return 16;
+    default: return 64;
+  }
+}
 
-// Deterministic split-K reduction.  Block = 64 outputs x 4 split groups:
-// thread (o, g) sums the contiguous group g of the partials of output o in
-// split order (loads unrolled 8 deep so they are in flight together), then
-// the 4 group sums are added in group order.  Fixed association for a given
-// `splits`, so results are bit-reproducible.
-constexpr int SR_OUT = 64, SR_GRP = 4;
-__global__ void __launch_bounds__(SR_OUT *SR_GRP) k_splitk_reduce(
+// one k_dgemm instantiation: opt in to its dynamic shared memory once
+template <bool TA, bool TB, int EPI, int TBM, int TBN, typename... Args>
+void launch_dgemm(dim3 grid, cudaStream_t st, Args... args) {
+  constexpr size_t smem = gemm_smem_bytes(TBM, TBN);
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      k_dgemm<TA, TB, EPI, TBM, TBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  (void)attr;
+  k_dgemm<TA, TB, EPI, TBM, TBN><<<grid, GT, smem, st>>>(args...);
+}
+
+// Deterministic split-K reduction.  Block = 64 outputs x G split groups
+// (G = blockDim / 64: 4, or 16 for > 256 splits): thread (o, g) sums the
+// contiguous group g of the partials of output o in split order (loads
+// unrolled 8 deep so they are in flight together), then the G group sums
+// are added in group order.  G is a function of `splits`, so the
+// association is fixed and results are bit-reproducible.
+constexpr int SR_OUT = 64, SR_GRP_MAX = 16;
+inline int splitk_reduce_threads(int splits) { return SR_OUT * (splits > 256 ? 16 : 4); }
+__global__ void __launch_bounds__(SR_OUT *SR_GRP_MAX) k_splitk_reduce(
     int64_t m, int64_t n, int splits, const double *__restrict__ partial, double alpha, double beta,
     double *__restrict__ C, int64_t ldc) {
-  __shared__ double gs[SR_GRP][SR_OUT];
+  __shared__ double gs[SR_GRP_MAX][SR_OUT];
   const int64_t total = m * n;
+  const int SR_GRP = (int)blockDim.x / SR_OUT;
   const int o = threadIdx.x % SR_OUT, g = threadIdx.x / SR_OUT;
   const int per = (splits + SR_GRP - 1) / SR_GRP;
   const int z0 = g * per, z1 = min(splits, z0 + per);
@@ -455,7 +512,6 @@ __global__ void __launch_bounds__(SR_OUT *SR_GRP) k_splitk_reduce(
     __syncthreads();
     if (g == 0 && t < total) {
       double tot = gs[0][o];
-#pragma unroll
       for (int q = 1; q < SR_GRP; ++q) tot += gs[q][o];
       const int64_t col = t / m, row = t - col * m;
       double v = alpha * tot;
@@ -517,12 +573,14 @@ __global__ void k_orth_defect(int64_t n, const double *__restrict__ G, int64_t l
 // small output (Gram matrices, B = Q^T A, train-norm contractions) otherwise
 // run a handful of CTAs that walk all of K one BK step at a time (latency
 // bound, ~0.7 us per step).  Aim for ~8 CTAs per SM, at least 128 K per CTA
-// (8 BK steps), at most 256 splits (the reduction's serial depth).
-int64_t splitk_count(int64_t tiles, int64_t k, int num_sms) {
+// (8 BK steps), at most 256 splits (the reduction's serial depth) -- 1024
+// for tiles of <= 1024 outputs, whose per-split DMMA work is small (the
+// 32 x 32 Gram of a 314,928-row panel ran 77 k-steps per CTA at 256).
+int64_t splitk_count(int64_t tiles, int64_t k, int num_sms, int64_t tile_elems) {
   if (tiles >= 2 * (int64_t)num_sms || k < 512) return 1;
   int64_t s = ceil_div(8 * (int64_t)num_sms, tiles);
   s = std::min<int64_t>(s, k / 128);
-  s = std::min<int64_t>(s, 256);
+  s = std::min<int64_t>(s, tile_elems <= 1024 ? 1024 : (tile_elems <= 2048 ? 512 : 256));
   return std::max<int64_t>(s, 1);
 }
 
@@ -541,7 +599,7 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
   int64_t tiles = tiles_m * tiles_n;
   int splits = 1;
   {
-    int64_t s = splitk_count(tiles, k, ctx->num_sms);
+    int64_t s = splitk_count(tiles, k, ctx->num_sms, (int64_t)tile_m(ts) * tile_n(ts));
     if (splitk_ws) s = std::min<int64_t>(s, (int64_t)(splitk_ws_elems / (size_t)(m * n)));
     else s = 1;
     if (s > 1) splits = (int)s;
@@ -562,16 +620,32 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
                     tile_elems * splits <= 256 * GT)
                        ? ctx->tile_cnt
                        : nullptr;
+  static const bool dbg = getenv("FTT_DEBUG_GEMM") != nullptr;
+  cudaEvent_t dev[2];
+  if (dbg) {
+    cudaEventCreate(&dev[0]);
+    cudaEventCreate(&dev[1]);
+    cudaEventRecord(dev[0], ctx->stream);
+  }
   const int pb = prof_begin(ctx);
 #define FTT_GEMM_LAUNCH(TA_, TB_, M_, N_)                                                     \
-  k_dgemm<TA_, TB_, 0, M_, N_><<<grid, GT, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, \
-                                                            beta, C, ldc, kps, part, 0,      \
-                                                            nullptr, tcnt)
-#define FTT_GEMM_TILES(TA_, TB_)                                  \
-  do {                                                            \
-    if (ts == T128x32) FTT_GEMM_LAUNCH(TA_, TB_, 128, 32);        \
-    else if (ts == T32x128) FTT_GEMM_LAUNCH(TA_, TB_, 32, 128);   \
-    else FTT_GEMM_LAUNCH(TA_, TB_, 64, 64);                       \
+  launch_dgemm<TA_, TB_, 0, M_, N_>(grid, ctx->stream, m, n, k, alpha, A, lda, B, ldb, beta, C, \
+                                    ldc, kps, part, 0, (double *)nullptr, tcnt, (double *)nullptr)
+#define FTT_GEMM_TILES(TA_, TB_)                                         \
+  do {                                                                   \
+    switch (ts) {                                                        \
+      case T128x32: FTT_GEMM_LAUNCH(TA_, TB_, 128, 32); break;           \
+      case T32x128: FTT_GEMM_LAUNCH(TA_, TB_, 32, 128); break;           \
+      case T128x16: FTT_GEMM_LAUNCH(TA_, TB_, 128, 16); break;           \
+      case T16x128: FTT_GEMM_LAUNCH(TA_, TB_, 16, 128); break;           \
+      case T128x40: FTT_GEMM_LAUNCH(TA_, TB_, 128, 40); break;           \
+      case T128x48: FTT_GEMM_LAUNCH(TA_, TB_, 128, 48); break;           \
+      case T48x128: FTT_GEMM_LAUNCH(TA_, TB_, 48, 128); break;           \
+      case T48x48: FTT_GEMM_LAUNCH(TA_, TB_, 48, 48); break;             \
+      case T32x32: FTT_GEMM_LAUNCH(TA_, TB_, 32, 32); break;             \
+      case T16x16: FTT_GEMM_LAUNCH(TA_, TB_, 16, 16); break;             \
+      default: FTT_GEMM_LAUNCH(TA_, TB_, 64, 64); break;                 \
+    }                                                                    \
   } while (0)
   if (!ta && !tb) FTT_GEMM_TILES(false, false);
   else if (!ta && tb) FTT_GEMM_TILES(false, true);
@@ -582,12 +656,23 @@ int gemm(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double a
   FTT_LAUNCHED(ctx);
   if (splits > 1 && !tcnt) {
     const int64_t rb = std::min<int64_t>(ceil_div(m * n, SR_OUT), 4 * (int64_t)ctx->num_sms);
-    k_splitk_reduce<<<(unsigned)rb, SR_OUT * SR_GRP, 0, ctx->stream>>>(m, n, splits, part, alpha,
-                                                                      beta, C, ldc);
+    k_splitk_reduce<<<(unsigned)rb, splitk_reduce_threads(splits), 0, ctx->stream>>>(
+        m, n, splits, part, alpha, beta, C, ldc);
     FTT_LAUNCHED(ctx);
   }
   prof_end(ctx, pb, PT_GEMM, 8.0 * ((double)m * k + (double)k * n + 2.0 * m * n),
            2.0 * (double)m * n * k);
+  if (dbg) {
+    cudaEventRecord(dev[1], ctx->stream);
+    cudaEventSynchronize(dev[1]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, dev[0], dev[1]);
+    fprintf(stderr, "[gemm] %c%c m=%lld n=%lld k=%lld tile=%d splits=%d %.1f us %.2f TF/s\n",
+            ta ? 'T' : 'N', tb ? 'T' : 'N', (long long)m, (long long)n, (long long)k, (int)ts,
+            splits, 1e3 * ms, 2.0 * m * n * k / (ms * 1e-3) / 1e12);
+    cudaEventDestroy(dev[0]);
+    cudaEventDestroy(dev[1]);
+  }
   return FTT_OK;
 }
 
@@ -702,8 +787,8 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
   double *sum = out_dev ? out_dev : npart + nt;
   unsigned *cnt = ctx->tile_cnt + kTileCnt + 1;
 #define FTT_RESID_LAUNCH(TA_, TB_)                                                              \
-  k_dgemm<TA_, TB_, 1><<<grid, GT, 0, ctx->stream>>>(m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldr, \
-                                                     kps, nullptr, r_trans, npart, cnt, sum)
+  launch_dgemm<TA_, TB_, 1, 64, 64>(grid, ctx->stream, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldr, \
+                                    kps, (double *)nullptr, r_trans, npart, cnt, sum)
   if (!ta && !tb) FTT_RESID_LAUNCH(false, false);
   else if (!ta && tb) FTT_RESID_LAUNCH(false, true);
   else if (ta && !tb) FTT_RESID_LAUNCH(true, false);
@@ -718,7 +803,7 @@ int gemm_resid_sumsq(ftt_ctx *ctx, int ta, int tb, int64_t m, int64_t n, int64_t
 size_t gemm_splitk_elems(int64_t m, int64_t n, int64_t k) {
   const TileShape ts = pick_tile(m, n);
   int64_t tiles = ceil_div(m, tile_m(ts)) * ceil_div(n, tile_n(ts));
-  int64_t s = splitk_count(tiles, k, kNumSMs);
+  int64_t s = splitk_count(tiles, k, kNumSMs, (int64_t)tile_m(ts) * tile_n(ts));
   return s > 1 ? (size_t)(s * m * n) : 0;
 }
 

@@ -206,6 +206,190 @@ __device__ void apply_q(const double *Sref, const double *tau_s, double (&z)[NMA
   __syncthreads();
 }
 
+// ---- several rows per thread (n <= 16) --------------------------------
+// The one-row-per-thread kernels above spend each column step on a CTA-wide
+// reduce-scatter of n partial dots: with 512 threads that is 16 warps x 31
+// fp64 shuffles per step (the shuffle unit serialises ~1 warp-shuffle per
+// clock), so a 512 x 16 leaf took ~53 us and a leaf level ran one CTA per SM.
+// Here a thread owns RPT rows (i = threadIdx.x + r * blockDim.x, coalesced),
+// sums its rows' products locally first, and the warp reduce-scatter halves
+// from the first stage (16 shuffles for 16 slots): 4x fewer warps per step,
+// ~2x fewer shuffles per warp, and a 512-row leaf is a 128-thread CTA that
+// shares its SM with others.
+
+// W slots over 32 lanes by recursive halving: at offset s = 16, 8, ...
+// each lane keeps the half of its live slots selected by its lane bit and
+// adds the partner's copy; once one slot is left the remaining offsets add
+// whole values.  Lane l ends with the warp total of slot (l >> (5 - log2 W))
+// (all lanes of a slot hold the same bits: fp add commutes).
+template <int W>
+__device__ __forceinline__ double rs_halving(double (&v)[32], int lane) {
+  int live = W;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    if (live > 1) {
+      const int h = live / 2;
+      const bool upper = (lane & s) != 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < h) {
+          const double send = upper ? v[j] : v[j + h];
+          const double keep = upper ? v[j + h] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+      live = h;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], s);
+    }
+  }
+  return v[0];
+}
+template <int W>
+__device__ __forceinline__ int rs_slot(int lane) {
+  constexpr int sh = W >= 32 ? 0 : (W >= 16 ? 1 : (W >= 8 ? 2 : (W >= 4 ? 3 : (W >= 2 ? 4 : 5))));
+  return (lane >> sh) & (W - 1);
+}
+template <int W>
+__device__ __forceinline__ bool rs_writer(int lane) {
+  constexpr int sh = W >= 32 ? 0 : (W >= 16 ? 1 : (W >= 8 ? 2 : (W >= 4 ? 3 : (W >= 2 ? 4 : 5))));
+  return (lane & ((1 << sh) - 1)) == 0;
+}
+
+// red[warp][u] = sum over the warp's rows of x_r * b[r][u] (u < NMAX <= 16)
+template <int NMAX, int RPT>
+__device__ __forceinline__ void rows_partials(double (*red)[NMAX], const double (&x)[RPT],
+                                              const double (&b)[RPT][NMAX]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double p[32];
+#pragma unroll
+  for (int u = 0; u < 32; ++u) p[u] = 0.0;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r)
+#pragma unroll
+    for (int u = 0; u < NMAX; ++u) p[u] = fma(x[r], b[r][u], p[u]);
+  const double tot = rs_halving<NMAX>(p, lane);
+  if (rs_writer<NMAX>(lane)) red[warp][rs_slot<NMAX>(lane)] = tot;
+}
+
+// reg_qr for RPT rows per thread (row i = threadIdx.x + r blockDim.x; the
+// pivot rows c < n <= 16 are slot 0 of threads c).  Same outputs as reg_qr.
+template <int NMAX, int RPT>
+__device__ void reg_qr_m(double (&a)[RPT][NMAX], int m, int n, double *Sref, Scratch<NMAX> &sc) {
+  const int t = threadIdx.x, T = blockDim.x;
+  const int k = min(m, n);
+  for (int c = 0; c < k; ++c) {
+    const int nc = n - c;
+    if (t == c) {
+#pragma unroll
+      for (int u = 0; u < NMAX; ++u) sc.rowc[u] = a[0][u];
+    }
+    double x[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * T;
+      x[r] = (i > c && i < m) ? a[r][0] : 0.0;
+    }
+    rows_partials<NMAX, RPT>(sc.red, x, a);
+    __syncthreads();
+    if (t < nc) {  // thread u: column c + u (u = 0: the pivot's scalars)
+      const double xx = sum_warps<NMAX>(sc.red, 0);
+      const double alpha = sc.rowc[0];
+      double tau, beta, scal;
+      if (xx == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+        scal = 0.0;
+      } else {
+        beta = -copysign(sqrt(alpha * alpha + xx), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (t == 0) {
+        sc.tau[c] = tau;
+        sc.beta[c] = beta;
+        sc.sc[0] = tau;
+        sc.sc[1] = beta;
+        sc.sc[2] = scal;
+      } else {
+        sc.wv[t] = tau * (sc.rowc[t] + scal * sum_warps<NMAX>(sc.red, t));
+      }
+    } else if (t < NMAX) {
+      sc.wv[t] = 0.0;  // columns past n - c do not move
+    }
+    __syncthreads();
+    const double tau = sc.sc[0], beta = sc.sc[1], scal = sc.sc[2];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * T;
+      if (i > c && i < m) {
+        const double v = scal * a[r][0];
+        if (tau != 0.0) {
+#pragma unroll
+          for (int u = 1; u < NMAX; ++u) a[r][u] = fma(-sc.wv[u], v, a[r][u]);
+        }
+        a[r][0] = v;
+      } else if (i == c) {
+        if (tau != 0.0) {
+#pragma unroll
+          for (int u = 1; u < NMAX; ++u) a[r][u] -= sc.wv[u];
+        }
+        a[r][0] = beta;
+      }
+      if (i < m) Sref[i + (size_t)c * m] = a[r][0];
+#pragma unroll
+      for (int u = 0; u + 1 < NMAX; ++u) a[r][u] = a[r][u + 1];
+      a[r][NMAX - 1] = 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// z <- Q z (apply_q) for RPT rows per thread.
+template <int NMAX, int RPT>
+__device__ void apply_q_m(const double *Sref, const double *tau_s, double (&z)[RPT][NMAX], int m,
+                          int k, int ncol, Scratch<NMAX> &sc) {
+  const int t = threadIdx.x, T = blockDim.x;
+  for (int c = k - 1; c >= 0; --c) {
+    const double tau = tau_s[c];
+    if (tau == 0.0) continue;
+    double v[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * T;
+      v[r] = i == c ? 1.0 : ((i > c && i < m) ? Sref[i + (size_t)c * m] : 0.0);
+    }
+    rows_partials<NMAX, RPT>(sc.red, v, z);
+    __syncthreads();
+    if (t < ncol) sc.wv[t] = tau * sum_warps<NMAX>(sc.red, t);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int u = 0; u < NMAX; ++u)
+        if (u < ncol) z[r][u] = fma(-sc.wv[u], v[r], z[r][u]);
+  }
+  __syncthreads();
+}
+
+template <int NMAX, int RPT>
+__device__ bool load_rows(double (&a)[RPT][NMAX], int mb, int n, const double *__restrict__ buf,
+                          int64_t ld, int trans, int64_t r0) {
+  int bad = 0;
+  const int t = threadIdx.x, T = blockDim.x;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * T;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+      double v = 0.0;
+      if (i < mb && j < n) v = trans ? buf[j + (r0 + i) * ld] : buf[(r0 + i) + (int64_t)j * ld];
+      bad |= !isfinite(v);
+      a[r][j] = v;
+    }
+  }
+  return !__syncthreads_or(bad);
+}
+
 __device__ __forceinline__ void rr_pair(int ne, int round, int c, int *p, int *q) {
   // circle method over ne (even) players, player ne-1 fixed
   const int L = ne - 1;
@@ -276,6 +460,116 @@ __device__ int cta_jacobi(double *X, double *P, int n, double tol, double floor,
     if (!__syncthreads_or(any)) return sw + 1;
   }
   return -1;
+}
+
+// One-sided Jacobi on X (n x n, n <= NM <= 16, ld ldx) accumulating P (ld
+// ldp), both in shared memory, run by ONE warp out of registers: lane c < 16
+// holds column c of X, lane 16 + c column c of P.  Round r of the circle
+// method pairs column c with (2 r - c) mod (ne - 1) (column ne - 1 with r),
+// so each lane finds its partner arithmetically and one shuffle per element
+// brings the partner's column (X and P lanes in the same instruction).  Both
+// lanes of a pair form the same dots in the same order (bit-identical
+// decision and angle); the P lanes then fetch their column's rotation.  No
+// shared memory or barriers inside the sweep: the smem variants spent most
+// of their time on bank conflicts (all columns of an n = 16 block start in
+// the same bank) and on the serial fp64 div/sqrt chain, here one sqrt and one
+// rsqrt per round:
+//   r = sqrt(d^2 + 4 g^2), w = |d| + r, rho = rsqrt(w^2 + 4 g^2),
+//   c = w rho, s = sgn(d) 2 g rho      (d = |x_q|^2 - |x_p|^2, g = x_p . x_q)
+// which is the same rotation as t = sgn(d) 2g / (|d| + r), c = 1/sqrt(1+t^2).
+// Convergence rule as cta_jacobi.  Writes X and P back; returns the sweeps
+// used (-1 if max_sweeps was exhausted).  Call from one full warp.
+template <int NM>
+__device__ int warp_jacobi_cols(double *X, int ldx, double *P, int ldp, int n, double tol,
+                                double floor, int max_sweeps) {
+  static_assert(NM <= 16, "one lane per column, P in the upper half-warp");
+  const int lane = threadIdx.x & 31, c = lane & 15;
+  const bool isP = lane >= 16;
+  double x[NM];
+#pragma unroll
+  for (int i = 0; i < NM; ++i)
+    x[i] = (c < n && i < n) ? (isP ? P[i + c * ldp] : X[i + c * ldx]) : 0.0;
+  const int ne = n + (n & 1), L = ne - 1;
+  const double tol2 = tol * tol;
+  int sweeps = n > 1 ? -1 : 1;
+  for (int sw = 0; sw < max_sweeps && n > 1; ++sw) {
+    int any = 0;
+    for (int round = 0; round < L; ++round) {
+      int pa;
+      if (c == L) pa = round;
+      else if (c == round) pa = L;
+      else {
+        pa = 2 * round - c;
+        pa = pa < 0 ? pa + L : (pa >= L ? pa - L : pa);
+      }
+      const bool live = c < n && pa < n;
+      const bool first = c < pa;
+      const int src = (lane & 16) | (pa & 15);
+      // |own column|^2 (4 chains), then the partner's column and its norm:
+      // both lanes of a pair hold the same a = |x_p|^2, b = |x_q|^2 bits
+      double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NM; i += 4) {
+        q0 = fma(x[i], x[i], q0);
+        if (i + 1 < NM) q1 = fma(x[i + 1], x[i + 1], q1);
+        if (i + 2 < NM) q2 = fma(x[i + 2], x[i + 2], q2);
+        if (i + 3 < NM) q3 = fma(x[i + 3], x[i + 3], q3);
+      }
+      const double sx = (q0 + q1) + (q2 + q3);
+      double y[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) y[i] = __shfl_sync(0xffffffffu, x[i], src);
+      const double sy = __shfl_sync(0xffffffffu, sx, src);
+      double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NM; i += 4) {
+        g0 = fma(x[i], y[i], g0);
+        if (i + 1 < NM) g1 = fma(x[i + 1], y[i + 1], g1);
+        if (i + 2 < NM) g2 = fma(x[i + 2], y[i + 2], g2);
+        if (i + 3 < NM) g3 = fma(x[i + 3], y[i + 3], g3);
+      }
+      const double g = (g0 + g1) + (g2 + g3);
+      const double a = first ? sx : sy, b = first ? sy : sx;
+      int rot = (!isP && live && a > floor && b > floor && g * g > tol2 * (a * b)) ? 1 : 0;
+      double cs = 1.0, sn = 0.0;
+      if (rot) {
+        const double dd = b - a, gd = 2.0 * g;
+        const double r = sqrt(fma(dd, dd, gd * gd));
+        const double w = fabs(dd) + r;
+        const double rho = rsqrt(fma(w, w, gd * gd));
+        cs = w * rho;
+        sn = copysign(1.0, dd) * gd * rho;
+      }
+      const double pcs = __shfl_sync(0xffffffffu, cs, c), psn = __shfl_sync(0xffffffffu, sn, c);
+      const int prot = __shfl_sync(0xffffffffu, rot, c);
+      if (isP) {
+        cs = pcs;
+        sn = psn;
+        rot = prot;
+      }
+      if (rot) {
+        // x_p <- c x_p - s x_q ,  x_q <- c x_q + s x_p
+        const double s2 = first ? -sn : sn;
+#pragma unroll
+        for (int i = 0; i < NM; ++i) x[i] = fma(cs, x[i], s2 * y[i]);
+      }
+      any |= rot;
+    }
+    if (!__any_sync(0xffffffffu, any)) {
+      sweeps = sw + 1;
+      break;
+    }
+  }
+  if (c < n) {
+#pragma unroll
+    for (int i = 0; i < NM; ++i)
+      if (i < n) {
+        if (isP) P[i + c * ldp] = x[i];
+        else X[i + c * ldx] = x[i];
+      }
+  }
+  __syncwarp();
+  return sweeps;
 }
 
 // Block reduction with a fixed order (deterministic).
@@ -361,6 +655,312 @@ __global__ void __launch_bounds__(NMAX <= 16 ? LEAF_MAX : LEAF_NT, 1) k_tsqr_lev
   }
 }
 
+// k_tsqr_level for n <= 16 with RPT rows per thread (leaf = blockDim * RPT
+// rows; same outputs).
+constexpr int LEAF_RPT = 2;
+template <int NMAX, int RPT>
+__global__ void __launch_bounds__(LEAF_MAX / RPT) k_tsqr_level_m(
+    int64_t M, int n, const double *__restrict__ A, int64_t lda, int trans, double *__restrict__ Rs,
+    int64_t ldr, double *__restrict__ Qo, int64_t ldq, int root, int *__restrict__ status) {
+  extern __shared__ double Sref[];
+  __shared__ Scratch<NMAX> sc;
+  const int T = blockDim.x, t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * T * RPT;
+  const int mb = (int)min((int64_t)T * RPT, M - r0);
+  const int k = min(mb, n);
+  double a[RPT][NMAX];
+  if (!load_rows<NMAX, RPT>(a, mb, n, A, lda, trans, r0)) {
+    if (t == 0) atomicOr(status, 1);
+    return;
+  }
+  reg_qr_m<NMAX, RPT>(a, mb, n, Sref, sc);
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {  // columns k.. (only when the block is wider than tall)
+    const int i = t + r * T;
+    if (i < mb) {
+#pragma unroll
+      for (int u = 0; u < NMAX; ++u)
+        if (k + u < n) Sref[i + (size_t)(k + u) * mb] = a[r][u];
+    }
+  }
+  __syncthreads();
+  if (Rs && t < n) {  // row t of R_b (sign-fixed at the root)
+    const double sg = (root && t < k && sc.beta[t] < 0.0) ? -1.0 : 1.0;
+    const int64_t rb = (int64_t)blockIdx.x * n + t;
+    for (int j = 0; j < n; ++j)
+      Rs[rb + (int64_t)j * ldr] = (t <= j && t < mb) ? sg * Sref[t + (size_t)j * mb] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * T;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) a[r][j] = (i == j && j < k) ? 1.0 : 0.0;
+  }
+  apply_q_m<NMAX, RPT>(Sref, sc.tau, a, mb, k, k, sc);
+  double sg[NMAX];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) sg[j] = j < k ? ((root && sc.beta[j] < 0.0) ? -1.0 : 1.0) : 0.0;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * T;
+    if (i < mb) {
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j)
+        if (j < n) Qo[(r0 + i) + (int64_t)j * ldq] = sg[j] * a[r][j];
+    }
+  }
+}
+
+// ---- Householder QR with the compact WY Q (n <= 16) ---------------------
+// The leaf QR of the rounding sweeps (512 x 16 blocks) is a latency chain:
+// column step c needs the reduction of step c - 1.  Each step here is one
+// CTA-wide reduction (all NMAX partial dots of the pivot column at once,
+// staged through shared memory: every thread writes its NMAX partials, G
+// threads per slot sum them, a G-lane shuffle finishes), two barriers, and
+// the pivot scalars recomputed by every thread (bit-identical, no third
+// barrier).  Columns stay at fixed registers (runtime column c picked by a
+// uniform switch), and the finished columns of the registers ARE the
+// reflectors V, so the partials of step c also give V^T v_c for free:
+// the WY factor T of H_0 .. H_{k-1} = I - V T V^T is built as the steps go,
+// and Q = [I; 0] - V (T V_1^T) is one per-row product at the end instead of
+// k more sequential reduction steps.
+template <int NMAX>
+struct WyScratch {
+  double rowc[2][NMAX];  // pivot row of step c (double-buffered by parity)
+  double tot[NMAX];      // slot totals of step c
+  double tau[NMAX], beta[NMAX];
+  double Tm[NMAX][NMAX + 1];  // WY T factor (upper triangular)
+  double Vt[NMAX][NMAX + 1];  // rows j < k of V
+  double Mm[NMAX][NMAX + 1];  // T V_1^T (or T V_1^T P for the SVD kernel)
+  double Rm[NMAX][NMAX + 1];  // R (rows < min(mb, n))
+};
+
+// Householder QR of the mb x n block held in a[RPT][NMAX] (row i = t + r NT,
+// NT = blockDim.x, a power of two with NT / NMAX <= 32).  Rotating layout:
+// at step c the pivot column is register 0, the live trailing columns
+// 1 .. n - c - 1, then the zero padding, then the finished reflectors
+// V_0 .. V_{c-1} (V_q at NMAX - c + q): after the step the row rotates left
+// by one and the new reflector entry enters at the end.  So the loop body is
+// one compact block (the fully unrolled variant was instruction-fetch bound)
+// and the partials of the pivot column against the V registers are exactly
+// the V^T v_c terms of the WY T factor.  NMAX rotations in total, so on exit
+// a[r][q] = V(i, q) for q < k.  sc.Rm = R (rows < min(mb, n)), sc.Tm = T,
+// sc.Vt = V rows < k, sc.tau / sc.beta; part = NMAX x NT doubles of shared
+// scratch.
+template <int NMAX, int RPT, int NT>
+__device__ void wy_qr(double (&a)[RPT][NMAX], int mb, int n, double *part, WyScratch<NMAX> &sc) {
+  constexpr int G = NT / NMAX;  // threads per slot in the reduction
+  static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "slot groups");
+  const int t = threadIdx.x;
+  const int k = min(mb, n);
+  for (int c = 0; c < NMAX; ++c) {
+    if (c < k) {
+      const int nc = n - c;
+      if (t == c) {
+#pragma unroll
+        for (int u = 0; u < NMAX; ++u) sc.rowc[c & 1][u] = a[0][u];
+      }
+      double x[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = t + r * NT;
+        x[r] = (i > c && i < mb) ? a[r][0] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < NMAX; ++u) {
+        double p = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) p = fma(x[r], a[r][u], p);
+        part[u * NT + t] = p;
+      }
+      __syncthreads();
+      {
+        const int u = t / G, g = t - u * G;
+        const double *pu = part + u * NT + g;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int j = 0; j < NMAX; j += 4) {
+          s0 += pu[(j + 0) * G];
+          if (j + 1 < NMAX) s1 += pu[(j + 1) * G];
+          if (j + 2 < NMAX) s2 += pu[(j + 2) * G];
+          if (j + 3 < NMAX) s3 += pu[(j + 3) * G];
+        }
+        double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+        for (int o = G >> 1; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (g == 0) sc.tot[u] = s;
+      }
+      __syncthreads();
+      const double *rc = sc.rowc[c & 1];
+      const double xx = sc.tot[0], alpha = rc[0];
+      double tau, beta, scal;
+      if (xx == 0.0) {
+        tau = 0.0;
+        beta = alpha;
+        scal = 0.0;
+      } else {
+        beta = -copysign(sqrt(alpha * alpha + xx), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (t == 0) {
+        sc.tau[c] = tau;
+        sc.beta[c] = beta;
+      }
+      // T(0:c, c) = -tau T(0:c, 0:c) (V^T v_c)(0:c), (V^T v_c)(q) = V(c, q) + scal tot(q)
+      // with V_q at register NMAX - c + q
+      if (t < c) {
+        double acc = 0.0;
+        for (int q = t; q < c; ++q) {
+          const int pq = NMAX - c + q;
+          acc = fma(sc.Tm[t][q], fma(scal, sc.tot[pq], rc[pq]), acc);
+        }
+        sc.Tm[t][c] = -tau * acc;
+      } else if (t == c) {
+        sc.Tm[c][c] = tau;
+      }
+      // w(u) = v_c^T a_u for the live columns 1 <= u < n - c
+      double w[NMAX];
+#pragma unroll
+      for (int u = 1; u < NMAX; ++u) w[u] = u < nc ? fma(scal, sc.tot[u], rc[u]) : 0.0;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = t + r * NT;
+        if (i > c && i < mb) {
+          const double v = scal * a[r][0];
+          const double tv = tau * v;
+#pragma unroll
+          for (int u = 1; u < NMAX; ++u) a[r][u] = fma(-w[u], tv, a[r][u]);
+          a[r][0] = v;
+        } else if (i == c) {
+#pragma unroll
+          for (int u = 1; u < NMAX; ++u) a[r][u] = fma(-tau, w[u], a[r][u]);
+          sc.Rm[c][c] = beta;
+          a[r][0] = 1.0;
+        } else {
+          if (i < c) sc.Rm[i][c] = a[r][0];  // R(i, c), final since step i
+          a[r][0] = 0.0;
+        }
+      }
+    } else if (c == k) {
+      // wide block (mb < n): the trailing columns k .. n-1 sit at 0 .. n-k-1
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = t + r * NT;
+        if (i < k) {
+#pragma unroll
+          for (int u = 0; u < NMAX; ++u)
+            if (u < n - k) sc.Rm[i][k + u] = a[r][u];
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const double v0 = a[r][0];
+#pragma unroll
+      for (int u = 0; u + 1 < NMAX; ++u) a[r][u] = a[r][u + 1];
+      a[r][NMAX - 1] = v0;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * NT;
+    if (i < k) {
+#pragma unroll
+      for (int u = 0; u < NMAX; ++u)
+        if (u < k) sc.Vt[i][u] = a[r][u];
+    }
+  }
+  __syncthreads();
+}
+
+// Columns [J0, J0 + NC) of Q = Z0 - V M for this thread's rows: q(r, jj) for
+// column J0 + jj, Z0 = [Ztop; 0] (Ztop k x ncol, identity when ztop is null).
+template <int NMAX, int RPT, int J0, int NC>
+__device__ __forceinline__ void wy_rows(const double (&a)[RPT][NMAX], int k, int ncol,
+                                        const double (*Mm)[NMAX + 1], const double (*ztop)[NMAX + 1],
+                                        double (&q)[RPT][NC]) {
+  const int t = threadIdx.x, T = blockDim.x;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * T;
+#pragma unroll
+    for (int jj = 0; jj < NC; ++jj) {
+      const int j = J0 + jj;
+      q[r][jj] = (i < k && j < ncol) ? (ztop ? ztop[i][j] : (i == j ? 1.0 : 0.0)) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int a2 = 0; a2 < NMAX; ++a2) {
+    if (a2 >= k) break;
+#pragma unroll
+    for (int jj = 0; jj < NC; ++jj) {
+      const double mj = J0 + jj < ncol ? Mm[a2][J0 + jj] : 0.0;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) q[r][jj] = fma(-a[r][a2], mj, q[r][jj]);
+    }
+  }
+}
+
+// Q rows of this thread to Qo (column j scaled by sg(j)), NC columns at a time.
+template <int NMAX, int RPT, int J0>
+__device__ __forceinline__ void wy_store(const double (&a)[RPT][NMAX], int k, int n, int mb,
+                                         const double (*Mm)[NMAX + 1],
+                                         const double (*ztop)[NMAX + 1], const double *sg,
+                                         double *__restrict__ Qo, int64_t ldq, int64_t r0) {
+  constexpr int NC = NMAX < 8 ? NMAX : 8;
+  if constexpr (J0 < NMAX) {
+    double q[RPT][NC];
+    wy_rows<NMAX, RPT, J0, NC>(a, k, ztop ? n : k, Mm, ztop, q);
+    const int t = threadIdx.x, T = blockDim.x;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * T;
+      if (i < mb) {
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj)
+          if (J0 + jj < n) Qo[(r0 + i) + (int64_t)(J0 + jj) * ldq] = sg[J0 + jj] * q[r][jj];
+      }
+    }
+    wy_store<NMAX, RPT, J0 + NC>(a, k, n, mb, Mm, ztop, sg, Qo, ldq, r0);
+  }
+}
+
+// TSQR level for n <= 16 with the WY Q (same outputs as k_tsqr_level).
+template <int NMAX, int RPT>
+__global__ void __launch_bounds__(LEAF_MAX / RPT) k_tsqr_wy(
+    int64_t M, int n, const double *__restrict__ A, int64_t lda, int trans, double *__restrict__ Rs,
+    int64_t ldr, double *__restrict__ Qo, int64_t ldq, int root, int *__restrict__ status) {
+  extern __shared__ double part[];  // NMAX x blockDim
+  __shared__ WyScratch<NMAX> sc;
+  const int T = blockDim.x, t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * T * RPT;
+  const int mb = (int)min((int64_t)T * RPT, M - r0);
+  const int k = min(mb, n);
+  double a[RPT][NMAX];
+  if (!load_rows<NMAX, RPT>(a, mb, n, A, lda, trans, r0)) {
+    if (t == 0) atomicOr(status, 1);
+    return;
+  }
+  wy_qr<NMAX, RPT, LEAF_MAX / RPT>(a, mb, n, part, sc);
+  // M = T V_1^T:  M(q, j) = sum_{b = q .. j} T(q, b) V(j, b)   (V(j, j) = 1)
+  for (int e = t; e < k * k; e += T) {
+    const int q = e / k, j = e - q * k;
+    double acc = 0.0;
+    for (int b = q; b <= j; ++b) acc = fma(sc.Tm[q][b], sc.Vt[j][b], acc);
+    sc.Mm[q][j] = acc;
+  }
+  if (Rs && t < n) {  // row t of R_b (sign-fixed at the root)
+    const double sg = (root && t < k && sc.beta[t] < 0.0) ? -1.0 : 1.0;
+    const int64_t rb = (int64_t)blockIdx.x * n + t;
+    for (int j = 0; j < n; ++j)
+      Rs[rb + (int64_t)j * ldr] = (t <= j && t < mb) ? sg * sc.Rm[t][j] : 0.0;
+  }
+  if (t < NMAX) sc.tot[t] = t < k ? ((root && sc.beta[t] < 0.0) ? -1.0 : 1.0) : 0.0;  // column signs
+  __syncthreads();
+  wy_store<NMAX, RPT, 0>(a, k, n, mb, sc.Mm, nullptr, sc.tot, Qo, ldq, r0);
+}
+
 // Jacobi stage of the narrow SVD: X = R^T (R n x n, ld ldr), X P = Y.
 // Writes Y, P (n x n, ld n) and norms_j = ||Y_j||; status[0] |= 2 on no
 // convergence, status[1] = sweeps.
@@ -403,6 +1003,42 @@ __global__ void __launch_bounds__(SVD_NT) k_jacobi_small(int n, const double *__
   }
 }
 
+// The same stage for n <= 16 by one warp out of registers (warp_jacobi_cols).
+template <int NM>
+__global__ void __launch_bounds__(32) k_jacobi_warp(int n, const double *__restrict__ R, int64_t ldr,
+                                                    double *__restrict__ Yo, double *__restrict__ Po,
+                                                    double *__restrict__ norms, int max_sweeps,
+                                                    int *__restrict__ status) {
+  __shared__ double X[NM * NM], P[NM * NM];
+  const int lane = threadIdx.x;
+  double f = 0.0;
+  for (int e = lane; e < n * n; e += 32) {
+    const int j = e / n, i = e - j * n;  // X(i, j) = R(j, i)
+    const double v = j <= i ? R[j + (int64_t)i * ldr] : 0.0;
+    X[e] = v;
+    P[e] = i == j ? 1.0 : 0.0;
+    f += v * v;
+  }
+  const double fro2 = warp_sum(f);
+  __syncwarp();
+  const double tol = kEps * sqrt((double)n);
+  const double floor = 0.01 * kEps * kEps * (double)n * fro2;
+  const int sweeps = warp_jacobi_cols<NM>(X, n, P, n, n, tol, floor, max_sweeps);
+  if (lane == 0) {
+    status[1] = sweeps;
+    if (sweeps < 0) atomicOr(status, 2);
+  }
+  if (lane < n) {
+    double s2 = 0.0;
+    for (int i = 0; i < n; ++i) s2 = fma(X[i + lane * n], X[i + lane * n], s2);
+    norms[lane] = sqrt(s2);
+  }
+  for (int e = lane; e < n * n; e += 32) {
+    Yo[e] = X[e];
+    Po[e] = P[e];
+  }
+}
+
 // Out rows of block b ([b L, min(M, (b+1) L))) = Q[rows, :n] * W_b where
 // W_b = W[b n : b n + n, :r] (ld ldw).  Grid (nblocks, row chunks).
 constexpr int EX_ROWS = 128;
@@ -440,8 +1076,12 @@ int set_attrs() {
   if (attrs_set) return FTT_OK;
   const int cap = (int)kSmemCapBytes;
   const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<8>, a, cap));
-  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<16>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level_m<8, 1>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level_m<8, 2>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level_m<8, 4>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level_m<16, 1>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level_m<16, 2>, a, cap));
+  FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level_m<16, 4>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<32>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<24>, a, cap));
   FTT_CUDA(cudaFuncSetAttribute(k_tsqr_level<48>, a, cap));
@@ -463,14 +1103,26 @@ void launch_level(ftt_ctx *ctx, int n, unsigned grid, int64_t M, const double *A
     const int64_t need = std::max<int64_t>(std::min<int64_t>(M, leaf), n);
     nt = (unsigned)std::min<int64_t>(leaf, ceil_div(need, 32) * 32);
   }
+  // n <= 16: rpt rows per thread
+  static const int rpt_env = getenv("FTT_TSQR_RPT") ? atoi(getenv("FTT_TSQR_RPT")) : 0;
+  const int rpt = rpt_env == 4 ? 4 : LEAF_RPT;
+  const unsigned ntm = (unsigned)(leaf / rpt);  // k_tsqr_wy's compile-time thread count
   switch (nmax_for(n)) {
     case 8:
-      k_tsqr_level<8><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
-                                                         status);
+      if (rpt == 4)
+        k_tsqr_wy<8, 4><<<grid, ntm, 8 * 8 * ntm, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo,
+                                                                 ldq, root, status);
+      else
+        k_tsqr_wy<8, 2><<<grid, ntm, 8 * 8 * ntm, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo,
+                                                                 ldq, root, status);
       break;
     case 16:
-      k_tsqr_level<16><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
-                                                          status);
+      if (rpt == 4)
+        k_tsqr_wy<16, 4><<<grid, ntm, 8 * 16 * ntm, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo,
+                                                                   ldq, root, status);
+      else
+        k_tsqr_wy<16, 2><<<grid, ntm, 8 * 16 * ntm, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo,
+                                                                   ldq, root, status);
       break;
     case 32:
       k_tsqr_level<32><<<grid, nt, smem, ctx->stream>>>(M, n, A, lda, trans, Rs, ldr, Qo, ldq, root,
@@ -503,148 +1155,20 @@ Tree make_tree(int64_t M, int n, int64_t root_rows_max) {
   return t;
 }
 
-// Hestenes one-sided Jacobi directly on a short tall block (m x n, n <= 16,
-// m * n doubles in shared memory): X P = Y with orthogonal columns; the same
-// convergence rule and noise floor as cta_jacobi.  A warp per column pair,
-// column length m looped by the lanes.  For the small inner SVDs of the
-// low-rank path (B^T, e.g. 512 x 8) this replaces a TSQR tree + Jacobi on R^T
-// + Q expansion (5 launches) by one launch.
-// wpp warps per column pair: each forms partial dots over its rows, the
-// pair's partials are summed in warp order (every warp of the pair gets the
-// bitwise same rotation), then each warp rotates its own rows.
-__global__ void __launch_bounds__(SVD_NT) k_jacobi_direct(int m, int n, const double *__restrict__ A,
-                                                          int64_t lda, int trans, int wpp,
-                                                          double *__restrict__ Yo,
-                                                          double *__restrict__ Po,
-                                                          double *__restrict__ norms,
-                                                          int max_sweeps, int *__restrict__ status,
-                                                          const double *__restrict__ extra_src,
-                                                          double *__restrict__ extra_dst) {
-  // status needs no memset: thread 0 writes both words; extra_dst receives
-  // *extra_src (a caller's device scalar riding on the same round trip)
-  extern __shared__ double S[];  // X m x n (ld m) | P n x n
-  __shared__ double red[SVD_NT / 32];
-  __shared__ double s_dot[SVD_NT / 32][3];
-  __shared__ int s_any;
-  double *X = S;
-  double *P = S + (size_t)m * n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double f = 0.0;
-  int bad = 0;
-  for (int e = tid; e < m * n; e += (int)blockDim.x) {
-    const int j = e / m, i = e - j * m;
-    const double v = trans ? A[j + (int64_t)i * lda] : A[i + (int64_t)j * lda];
-    bad |= !isfinite(v);
-    X[e] = v;
-    f += v * v;
-  }
-  for (int e = tid; e < n * n; e += (int)blockDim.x) P[e] = (e / n == e % n) ? 1.0 : 0.0;
-  if (tid == 0 && extra_src) *extra_dst = *extra_src;
-  if (__syncthreads_or(bad)) {
-    if (tid == 0) {
-      status[0] = 1;
-      status[1] = 0;
-    }
-    return;
-  }
-  const double fro2 = cta_sum(f, red);
-  const double tol = kEps * sqrt((double)n);
-  const double floor = 0.01 * kEps * kEps * (double)m * fro2;
-  const int ne = n + (n & 1), npairs = ne / 2;
-  const int pi = warp / wpp, sub = warp - pi * wpp;  // nw == npairs * wpp
-  int sweeps = -1;
-  for (int sw = 0; sw < max_sweeps && n > 1; ++sw) {
-    if (tid == 0) s_any = 0;
-    __syncthreads();
-    for (int round = 0; round < ne - 1; ++round) {
-      int p, q;
-      rr_pair(ne, round, pi, &p, &q);
-      const bool live = pi < npairs && p < n && q < n;
-      double *xp = X + (size_t)(live ? p : 0) * m, *xq = X + (size_t)(live ? q : 0) * m;
-      if (live) {
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = sub * 32 + lane; i < m; i += 32 * wpp) {
-          const double u = xp[i], v = xq[i];
-          a += u * u;
-          b += v * v;
-          g += u * v;
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-          g += __shfl_xor_sync(0xffffffffu, g, o);
-        }
-        if (lane == 0) {
-          s_dot[warp][0] = a;
-          s_dot[warp][1] = b;
-          s_dot[warp][2] = g;
-        }
-      }
-      __syncthreads();
-      if (live) {
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int w = pi * wpp; w < pi * wpp + wpp; ++w) {
-          a += s_dot[w][0];
-          b += s_dot[w][1];
-          g += s_dot[w][2];
-        }
-        if (a > floor && b > floor && fabs(g) > tol * sqrt(a * b)) {
-          const double zeta = (b - a) / (2.0 * g);
-          const double t = copysign(1.0 / (fabs(zeta) + sqrt(1.0 + zeta * zeta)), zeta);
-          const double c = rsqrt(1.0 + t * t);
-          const double sn = c * t;
-          for (int i = sub * 32 + lane; i < m; i += 32 * wpp) {
-            const double u = xp[i], v = xq[i];
-            xp[i] = c * u - sn * v;
-            xq[i] = sn * u + c * v;
-          }
-          if (sub == 0) {
-            double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
-            if (lane < n) {
-              const double pu = pp[lane], pv = pq[lane];
-              pp[lane] = c * pu - sn * pv;
-              pq[lane] = sn * pu + c * pv;
-            }
-            if (lane == 0) s_any = 1;
-          }
-        }
-      }
-      __syncthreads();
-    }
-    if (!s_any) {
-      sweeps = sw + 1;
-      break;
-    }
-    __syncthreads();
-  }
-  if (n <= 1) sweeps = 1;
-  if (tid == 0) {
-    status[0] = sweeps < 0 ? 2 : 0;
-    status[1] = sweeps;
-  }
-  for (int j = warp; j < n; j += nw) {
-    double s2 = 0.0;
-    for (int i = lane; i < m; i += 32) s2 += X[i + (size_t)j * m] * X[i + (size_t)j * m];
-    s2 = warp_sum(s2);
-    if (lane == 0) norms[j] = sqrt(s2);
-  }
-  for (int e = tid; e < m * n; e += (int)blockDim.x) Yo[e] = X[e];
-  for (int e = tid; e < n * n; e += (int)blockDim.x) Po[e] = P[e];
-}
-
-// The same factorisation for a short tall block (m x n, n <= 16) with the
-// rotations chosen on R instead of on X: X = Q R (Householder in shared
-// memory, a warp per column for the dots, 2 barriers per column), one-sided
-// Jacobi R P = Y_R by ONE warp without CTA barriers (4 lanes per column
-// pair, 8 pairs per round; the dots are over n rows instead of m), then
-// Y = Q [Y_R; 0] (the reflectors in reverse).  Same outputs, convergence rule
-// and noise floor (m of X) as k_jacobi_direct; X P = Q R P = Y.
+// SVD of a short tall block (m x n, n <= 16, in shared memory) in one CTA:
+// A_tall = Q R (Householder in shared memory, a warp per column for the
+// dots, 2 barriers per column), one-sided Jacobi on X = R^T by one warp out
+// of registers (warp_jacobi_cols; the rows of R are the better-conditioned
+// Jacobi operand, as in the TSQR path), then U = Q [P; 0] (the reflectors in
+// reverse).  Outputs as tsqr_svd: Uo = Q P (m x n), Yo = X P (n x n, column
+// norms sigma_j), so A_tall = U Sigma (Y / sigma)^T.  For the inner factor B
+// of the low-rank path (512 x 16 on config 5) this is one launch instead of
+// a TSQR tree, a Jacobi launch and the Q expansion.
 constexpr int QJ_NT = 512;
 __global__ void __launch_bounds__(QJ_NT) k_jacobi_qr(int m, int n, const double *__restrict__ A,
                                                      int64_t lda, int trans,
+                                                     double *__restrict__ Uo,
                                                      double *__restrict__ Yo,
-                                                     double *__restrict__ Po,
                                                      double *__restrict__ norms, int max_sweeps,
                                                      int *__restrict__ status,
                                                      const double *__restrict__ extra_src,
@@ -729,76 +1253,25 @@ __global__ void __launch_bounds__(QJ_NT) k_jacobi_qr(int m, int n, const double 
     // these writes before column j is read again
   }
   __syncthreads();
-  for (int e = tid; e < n * n; e += QJ_NT) {
+  for (int e = tid; e < n * n; e += QJ_NT) {  // R holds X = R^T
     const int b = e / n, a = e - b * n;
-    R[e] = a <= b ? X[a + (size_t)b * m] : 0.0;
+    R[e] = b <= a ? X[b + (size_t)a * m] : 0.0;
     P[e] = a == b ? 1.0 : 0.0;
   }
   __syncthreads();
-  // ---- one-sided Jacobi on R by warp 0: pair g = lane / 4, rows lane % 4 + 4 k
+  // ---- one-sided Jacobi on X = R^T by warp 0, out of registers
   if (warp == 0) {
     const double tol = kEps * sqrt((double)n);
     const double floor = 0.01 * kEps * kEps * (double)m * fro2;
-    const int ne = n + (n & 1), g = lane >> 2, sl = lane & 3;
-    int sweeps = -1;
-    for (int sw = 0; sw < max_sweeps && n > 1; ++sw) {
-      int any = 0;
-      for (int round = 0; round < ne - 1; ++round) {
-        int p = 0, q = 0;
-        const bool live = g < ne / 2;
-        if (live) rr_pair(ne, round, g, &p, &q);
-        const bool ok = live && p < n && q < n;
-        double *rp = R + (size_t)(ok ? p : 0) * n, *rq = R + (size_t)(ok ? q : 0) * n;
-        double a = 0.0, b = 0.0, gg = 0.0;
-        if (ok)
-          for (int i = sl; i < n; i += 4) {
-            const double u = rp[i], v = rq[i];
-            a += u * u;
-            b += v * v;
-            gg += u * v;
-          }
-        // sum over the pair's 4 lanes (xor 1, 2: bitwise the same in all 4)
-#pragma unroll
-        for (int o = 1; o <= 2; o <<= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-          gg += __shfl_xor_sync(0xffffffffu, gg, o);
-        }
-        // the same test and angle as the other Jacobi kernels with two fewer
-        // fp64 sqrt/div on the warp's serial chain: |g| > tol sqrt(ab) as
-        // g^2 > tol^2 ab, and t = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2)),
-        // d = b - a (= sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = d / 2g)
-        if (ok && a > floor && b > floor && gg * gg > tol * tol * (a * b)) {
-          const double dd = b - a;
-          const double t = copysign(1.0, dd) * (2.0 * gg) / (fabs(dd) + sqrt(dd * dd + 4.0 * gg * gg));
-          const double cs = rsqrt(1.0 + t * t);
-          const double sn = cs * t;
-          double *pp = P + (size_t)p * n, *pq = P + (size_t)q * n;
-          for (int i = sl; i < n; i += 4) {
-            const double u = rp[i], v = rq[i];
-            rp[i] = cs * u - sn * v;
-            rq[i] = sn * u + cs * v;
-            const double pu = pp[i], pv = pq[i];
-            pp[i] = cs * pu - sn * pv;
-            pq[i] = sn * pu + cs * pv;
-          }
-          any = 1;
-        }
-        __syncwarp();
-      }
-      if (!__any_sync(0xffffffffu, any)) {
-        sweeps = sw + 1;
-        break;
-      }
-    }
-    if (n <= 1) sweeps = 1;
-    if (lane == 0) s_sweeps = sweeps;
+    const int sw = n <= 8 ? warp_jacobi_cols<8>(R, n, P, n, n, tol, floor, max_sweeps)
+                          : warp_jacobi_cols<16>(R, n, P, n, n, tol, floor, max_sweeps);
+    if (lane == 0) s_sweeps = sw;
   }
   __syncthreads();
-  // ---- Y = Q [Y_R; 0]: H_{n-1} first, H_0 last
+  // ---- U = Q [P; 0]: H_{n-1} first, H_0 last
   for (int e = tid; e < m * n; e += QJ_NT) {
     const int c = e / m, i = e - c * m;
-    Y[e] = i < n ? R[i + c * n] : 0.0;
+    Y[e] = i < n ? P[i + c * n] : 0.0;
   }
   __syncthreads();
   for (int j = n - 1; j >= 0; --j) {
@@ -829,8 +1302,8 @@ __global__ void __launch_bounds__(QJ_NT) k_jacobi_qr(int m, int n, const double 
     s2 = warp_sum(s2);
     if (lane == 0) norms[j] = sqrt(s2);
   }
-  for (int e = tid; e < m * n; e += QJ_NT) Yo[e] = Y[e];
-  for (int e = tid; e < n * n; e += QJ_NT) Po[e] = P[e];
+  for (int e = tid; e < m * n; e += QJ_NT) Uo[e] = Y[e];
+  for (int e = tid; e < n * n; e += QJ_NT) Yo[e] = R[e];
 }
 
 }  // namespace
@@ -967,8 +1440,13 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   // one warp per column pair of a round: small n needs few warps (and gets
   // cheaper barriers)
   const int jt = 32 * std::max(1, std::min(SVD_NT / 32, (n + 1) / 2));
-  k_jacobi_small<<<1, jt, 16 * (size_t)n * n, ctx->stream>>>(n, R, n, Y, P, norms, max_sweeps,
-                                                              status);
+  if (n <= 8)
+    k_jacobi_warp<8><<<1, 32, 0, ctx->stream>>>(n, R, n, Y, P, norms, max_sweeps, status);
+  else if (n <= 16)
+    k_jacobi_warp<16><<<1, 32, 0, ctx->stream>>>(n, R, n, Y, P, norms, max_sweeps, status);
+  else
+    k_jacobi_small<<<1, jt, 16 * (size_t)n * n, ctx->stream>>>(n, R, n, Y, P, norms, max_sweeps,
+                                                                status);
   FTT_LAUNCHED(ctx);
   // W = Q_root P, then down the tree
   if (!single) FTT_CHECK(owned_alloc(ctx, (void **)&W, 8 * (size_t)Mr * n));
@@ -1005,47 +1483,33 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   return FTT_OK;
 }
 
+constexpr size_t kQjSmemCap = 200 * 1024;
+inline size_t qj_smem_bytes(int64_t m, int64_t n) { return 8 * (size_t)(2 * m * n + 2 * n * n); }
+
 bool direct_small_ok(int64_t m, int64_t n) {
   static const bool off = getenv("FTT_NO_DIRECT_SMALL") != nullptr;
-  return !off && n >= 1 && n <= 16 && m >= n && m * n * 8 <= 160 * 1024;
+  return !off && n >= 1 && n <= 16 && m >= n && qj_smem_bytes(m, n) <= kQjSmemCap;
 }
 
-// One-sided Jacobi directly on the short tall A_tall (m x n): Y = A_tall P
-// (m x n, ld m), P (n x n), norms_host[j] = ||Y_j|| (unsorted).
+// SVD of the short tall A_tall (m x n) in one launch (k_jacobi_qr): U = Q P
+// (m x n, ld m), Yt = R^T P (n x n, ld n), norms_host[j] = ||Yt_j||
+// (unsorted) -- the outputs of tsqr_svd.
 int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, int trans,
-                     double *Y, double *P, double *norms_host, int *sweeps,
+                     double *U, double *Yt, double *norms_host, int *sweeps,
                      const double *extra_dev, double *extra_host) {
-  static bool attr = false;
-  if (!attr) {
-    FTT_CUDA(cudaFuncSetAttribute(k_jacobi_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    attr = true;
-  }
-  double *dev = nullptr;  // status (2 ints) | pad | norms n
+  double *dev = nullptr;  // status (2 ints) | extra | norms n
   FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n)));
   int *status = reinterpret_cast<int *>(dev);
-  // warps per pair: enough that each lane holds <= ~8 rows, <= SVD_NT total
-  static const int wpp_env = getenv("FTT_DIRECT_WPP") ? atoi(getenv("FTT_DIRECT_WPP")) : 0;
-  const int npairs = (int)((n + 1) / 2);
-  int wpp = wpp_env > 0 ? wpp_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(m, 256)));
-  wpp = std::max(1, std::min(wpp, SVD_NT / 32 / std::max(1, npairs)));
-  const int jt = 32 * std::max(1, npairs) * wpp;
   const int max_sweeps = 60;
-  static const bool qr_off = getenv("FTT_NO_QR_JACOBI") != nullptr;
-  const size_t qj_smem = 8 * (size_t)(2 * m * n + 2 * n * n);
-  if (!qr_off && n <= 16 && qj_smem <= 200 * 1024) {
-    static bool qattr = false;
-    if (!qattr) {
-      FTT_CUDA(cudaFuncSetAttribute(k_jacobi_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
-      qattr = true;
-    }
-    k_jacobi_qr<<<1, QJ_NT, qj_smem, ctx->stream>>>((int)m, (int)n, A, lda, trans, Y, P, dev + 2,
-                                                    max_sweeps, status, extra_dev, dev + 1);
-  } else {
-    k_jacobi_direct<<<1, jt, 8 * (size_t)(m * n + n * n), ctx->stream>>>(
-        (int)m, (int)n, A, lda, trans, wpp, Y, P, dev + 2, max_sweeps, status, extra_dev, dev + 1);
+  static bool qattr = false;
+  if (!qattr) {
+    FTT_CUDA(cudaFuncSetAttribute(k_jacobi_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kQjSmemCap));
+    qattr = true;
   }
+  k_jacobi_qr<<<1, QJ_NT, qj_smem_bytes(m, n), ctx->stream>>>((int)m, (int)n, A, lda, trans, U, Yt,
+                                                              dev + 2, max_sweeps, status,
+                                                              extra_dev, dev + 1);
   FTT_LAUNCHED(ctx);
   std::vector<double> h(n + 2);
   FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));

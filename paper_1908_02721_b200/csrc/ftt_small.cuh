@@ -21,12 +21,12 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, i
              int64_t ldu, double *Y, double *norms_host, int *sweeps,
              const double *extra_dev = nullptr, double *extra_host = nullptr);
 
-// Short tall operands (n <= 16, m n doubles fit in shared memory): Hestenes
-// Jacobi directly on A_tall in one CTA.  Y = A_tall P (m x n), P (n x n),
-// norms_host = ||Y_j|| unsorted.
+// Short tall operands (n <= 16, A_tall and its reflectors fit in shared
+// memory): the tsqr_svd factorisation in one CTA (k_jacobi_qr).  U = Q P
+// (m x n), Yt = R^T P (n x n), norms_host = ||Yt_j|| unsorted.
 bool direct_small_ok(int64_t m, int64_t n);
 int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, int trans,
-                     double *Y, double *P, double *norms_host, int *sweeps,
+                     double *U, double *Yt, double *norms_host, int *sweeps,
                      const double *extra_dev = nullptr, double *extra_host = nullptr);
 
 }  // namespace ftt

@@ -731,21 +731,24 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
   const int64_t mA = st->mA, nA = st->nA;
   if (nA == 0) return FTT_OK;
   static const bool no_small = getenv("FTT_NO_SMALL") != nullptr;
-  if (!no_small && allow_direct && direct_small_ok(mA, nA)) {
+  // FTT_SVD_DIRECT=1: the direct path for every eligible operand (latency
+  // probes of the inner-factor kernel through ftt_svd_f64)
+  static const bool force_direct = getenv("FTT_SVD_DIRECT") != nullptr;
+  if (!no_small && (allow_direct || force_direct) && direct_small_ok(mA, nA)) {
     // short narrow operand (e.g. the k x n_A factor B of the low-rank path):
-    // one-sided Jacobi directly on A_tall in one CTA (Y = A_tall P aliases
-    // Af; phase 2 takes the `direct` branch: U = Y / sigma, V = P)
-    st->direct = true;
+    // the narrow path's factorisation in one CTA (Householder QR in shared
+    // memory, Jacobi on R^T, U = Q P); phase 2 takes the `small` branch
+    st->small = true;
     const bool need_t = a_row_major ? !st->transposed : st->transposed;
     FTT_CHECK(owned_alloc(ctx, (void **)&st->Af, 8 * (size_t)mA * nA));
-    FTT_CHECK(owned_alloc(ctx, (void **)&st->P, 8 * (size_t)nA * nA));
-    st->Y = st->Af;
+    FTT_CHECK(owned_alloc(ctx, (void **)&st->Y, 8 * (size_t)nA * nA));
     std::vector<double> raw(nA);
     const int pb = prof_begin(ctx);
-    FTT_CHECK(direct_small_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, st->P, raw.data(),
+    FTT_CHECK(direct_small_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, st->Y, raw.data(),
                                &st->sweeps, extra_dev, extra_host));
+    // QR (2 m n^2) + Q P (2 m n^2) + sweeps x n^2/2 pairs x 6 n
     prof_end(ctx, pb, PT_JACOBI, 8.0 * ((double)mA * nA * 2 + (double)nA * nA),
-             6.0 * std::max(st->sweeps, 1) * (double)nA * nA / 2.0 * (double)mA);
+             4.0 * (double)mA * nA * nA + 3.0 * std::max(st->sweeps, 1) * (double)nA * nA * nA);
     st->perm.resize(nA);
     std::iota(st->perm.begin(), st->perm.end(), 0);
     std::stable_sort(st->perm.begin(), st->perm.end(),
