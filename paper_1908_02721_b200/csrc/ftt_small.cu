@@ -1155,155 +1155,88 @@ Tree make_tree(int64_t M, int n, int64_t root_rows_max) {
   return t;
 }
 
-// SVD of a short tall block (m x n, n <= 16, in shared memory) in one CTA:
-// A_tall = Q R (Householder in shared memory, a warp per column for the
-// dots, 2 barriers per column), one-sided Jacobi on X = R^T by one warp out
-// of registers (warp_jacobi_cols; the rows of R are the better-conditioned
-// Jacobi operand, as in the TSQR path), then U = Q [P; 0] (the reflectors in
-// reverse).  Outputs as tsqr_svd: Uo = Q P (m x n), Yo = X P (n x n, column
-// norms sigma_j), so A_tall = U Sigma (Y / sigma)^T.  For the inner factor B
-// of the low-rank path (512 x 16 on config 5) this is one launch instead of
-// a TSQR tree, a Jacobi launch and the Q expansion.
-constexpr int QJ_NT = 512;
-__global__ void __launch_bounds__(QJ_NT) k_jacobi_qr(int m, int n, const double *__restrict__ A,
-                                                     int64_t lda, int trans,
-                                                     double *__restrict__ Uo,
-                                                     double *__restrict__ Yo,
-                                                     double *__restrict__ norms, int max_sweeps,
-                                                     int *__restrict__ status,
-                                                     const double *__restrict__ extra_src,
-                                                     double *__restrict__ extra_dst) {
-  extern __shared__ double S[];  // X m x n | Y m x n | R n x n | P n x n (all col-major)
-  __shared__ double red[QJ_NT / 32];
-  __shared__ double s_dot[16];
-  __shared__ double s_tau[16];
+// SVD of a short tall block (m x n, n <= 16, m <= SV_NT * RPT) in one CTA:
+// the WY Householder QR of the TSQR leaves (wy_qr), one-sided Jacobi on
+// X = R^T by warp 0 out of registers (warp_jacobi_cols; the rows of R are
+// the better-conditioned Jacobi operand) while the other warps form
+// M = T V_1^T, then U = Q [P; 0] = [P; 0] - V (M P) per row.  Outputs as
+// tsqr_svd: Uo = Q P (m x n, ld m), Yo = X P (n x n, column norms sigma_j),
+// so A_tall = U Sigma (Yo / sigma)^T.  For the inner factor B of the
+// low-rank path (512 x 16 on config 5) this is one launch instead of a TSQR
+// tree, a Jacobi launch and the Q expansion.
+constexpr int SV_NT = 256;
+template <int NMAX, int RPT>
+__global__ void __launch_bounds__(SV_NT) k_svd_wy(int m, int n, const double *__restrict__ A,
+                                                  int64_t lda, int trans, double *__restrict__ Uo,
+                                                  double *__restrict__ Yo,
+                                                  double *__restrict__ norms, int max_sweeps,
+                                                  int *__restrict__ status,
+                                                  const double *__restrict__ extra_src,
+                                                  double *__restrict__ extra_dst) {
+  extern __shared__ double part[];  // NMAX x SV_NT
+  __shared__ WyScratch<NMAX> sc;
+  __shared__ double X[NMAX * NMAX], P[NMAX * NMAX];
+  __shared__ double red[SV_NT / 32];
   __shared__ int s_sweeps;
-  double *X = S, *Y = S + (size_t)m * n, *R = Y + (size_t)m * n, *P = R + n * n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double f = 0.0;
-  int bad = 0;
-  for (int e = tid; e < m * n; e += QJ_NT) {
-    const int j = e / m, i = e - j * m;
-    const double v = trans ? A[j + (int64_t)i * lda] : A[i + (int64_t)j * lda];
-    bad |= !isfinite(v);
-    X[e] = v;
-    f += v * v;
-  }
-  if (tid == 0 && extra_src) *extra_dst = *extra_src;
-  if (__syncthreads_or(bad)) {
-    if (tid == 0) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double a[RPT][NMAX];
+  if (t == 0 && extra_src) *extra_dst = *extra_src;
+  if (!load_rows<NMAX, RPT>(a, m, n, A, lda, trans, 0)) {
+    if (t == 0) {
       status[0] = 1;
       status[1] = 0;
     }
     return;
   }
+  double f = 0.0;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r)
+#pragma unroll
+    for (int u = 0; u < NMAX; ++u) f = fma(a[r][u], a[r][u], f);
   const double fro2 = cta_sum(f, red);
-  // ---- Householder QR: column j's reflector v = [1; x_j(j+1:) / v0]
-  __shared__ double s_w[16];
-  for (int j = 0; j < n; ++j) {
-    // warp w: column c = j + w; every warp also forms |x_j(j+1:)|^2 itself
-    // (same order in every warp: bitwise the same tau), then w_c =
-    // tau (x_jc + (x_j . x_c) / v0) before anything is updated
-    const int c = j + warp;
-    double tau = 0.0, beta = 0.0, v0 = 1.0;
-    if (c < n) {
-      const double *xj = X + (size_t)j * m, *xc = X + (size_t)c * m;
-      double d = 0.0, sub = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) {
-        const double u = xj[i];
-        d += u * xc[i];
-        sub += u * u;
-      }
-      d = warp_sum(d);
-      sub = warp_sum(sub);
-      const double alpha = xj[j];
-      beta = alpha;
-      if (sub > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + sub), alpha);
-        v0 = alpha - beta;
-        tau = (beta - alpha) / beta;
-      }
-      if (lane == 0) {
-        s_w[warp] = tau * (xc[j] + d / v0);
-        if (warp == 0) {
-          s_tau[j] = tau;
-          s_dot[0] = beta;
-          s_dot[1] = v0;
-        }
-      }
-    }
-    __syncthreads();
-    tau = s_tau[j];
-    v0 = s_dot[1];
-    if (tau != 0.0) {
-      const double inv = 1.0 / v0;
-      const int nc = n - j - 1, mr = m - j;
-      for (int e = tid; e < nc * mr; e += QJ_NT) {
-        const int k = e / mr, i = j + (e - k * mr), cc = j + 1 + k;
-        X[i + (size_t)cc * m] -= s_w[k + 1] * (i == j ? 1.0 : X[i + (size_t)j * m] * inv);
-      }
-    }
-    __syncthreads();
-    if (tau != 0.0) {
-      const double inv = 1.0 / v0;
-      for (int i = j + 1 + tid; i < m; i += QJ_NT) X[i + (size_t)j * m] *= inv;
-    }
-    if (tid == 0) X[j + (size_t)j * m] = s_dot[0];
-    // the next step's dots read columns > j only, and its barrier orders
-    // these writes before column j is read again
+  wy_qr<NMAX, RPT, SV_NT>(a, m, n, part, sc);
+  for (int e = t; e < n * n; e += SV_NT) {  // X = R^T, P = I
+    const int b = e / n, i = e - b * n;
+    X[e] = b <= i ? sc.Rm[b][i] : 0.0;
+    P[e] = i == b ? 1.0 : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < n * n; e += QJ_NT) {  // R holds X = R^T
-    const int b = e / n, a = e - b * n;
-    R[e] = b <= a ? X[b + (size_t)a * m] : 0.0;
-    P[e] = a == b ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  // ---- one-sided Jacobi on X = R^T by warp 0, out of registers
   if (warp == 0) {
     const double tol = kEps * sqrt((double)n);
     const double floor = 0.01 * kEps * kEps * (double)m * fro2;
-    const int sw = n <= 8 ? warp_jacobi_cols<8>(R, n, P, n, n, tol, floor, max_sweeps)
-                          : warp_jacobi_cols<16>(R, n, P, n, n, tol, floor, max_sweeps);
+    const int sw = warp_jacobi_cols<NMAX>(X, n, P, n, n, tol, floor, max_sweeps);
     if (lane == 0) s_sweeps = sw;
+  } else {
+    // M = T V_1^T:  M(q, j) = sum_{b = q .. j} T(q, b) V(j, b)   (V(j, j) = 1)
+    for (int e = t - 32; e < n * n; e += SV_NT - 32) {
+      const int q = e / n, j = e - q * n;
+      double acc = 0.0;
+      for (int b = q; b <= j; ++b) acc = fma(sc.Tm[q][b], sc.Vt[j][b], acc);
+      sc.Mm[q][j] = acc;
+    }
   }
   __syncthreads();
-  // ---- U = Q [P; 0]: H_{n-1} first, H_0 last
-  for (int e = tid; e < m * n; e += QJ_NT) {
-    const int c = e / m, i = e - c * m;
-    Y[e] = i < n ? P[i + c * n] : 0.0;
+  // (M P) into Rm, P row-major into Vt (both free now)
+  for (int e = t; e < n * n; e += SV_NT) {
+    const int q = e / n, j = e - q * n;
+    double acc = 0.0;
+    for (int b = 0; b < n; ++b) acc = fma(sc.Mm[q][b], P[b + j * n], acc);
+    sc.Rm[q][j] = acc;
+    sc.Vt[q][j] = P[q + j * n];
   }
+  if (t < NMAX) sc.tot[t] = 1.0;  // no column signs
   __syncthreads();
-  for (int j = n - 1; j >= 0; --j) {
-    const double tau = s_tau[j];
-    if (tau == 0.0) continue;  // uniform: s_tau is shared
-    const int c = warp;
-    if (c < n) {
-      const double *v = X + (size_t)j * m, *yc = Y + (size_t)c * m;
-      double d = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) d += v[i] * yc[i];
-      d = warp_sum(d);
-      if (lane == 0) s_dot[c] = tau * (yc[j] + d);
-    }
-    __syncthreads();
-    for (int e = tid; e < n * (m - j); e += QJ_NT) {
-      const int cc = e / (m - j), i = j + e % (m - j);
-      Y[i + (size_t)cc * m] -= s_dot[cc] * (i == j ? 1.0 : X[i + (size_t)j * m]);
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
+  wy_store<NMAX, RPT, 0>(a, n, n, m, sc.Rm, sc.Vt, sc.tot, Uo, m, 0);
+  if (t == 0) {
     status[0] = s_sweeps < 0 ? 2 : 0;
     status[1] = s_sweeps;
   }
-  for (int j = warp; j < n; j += QJ_NT / 32) {
+  if (t < n) {
     double s2 = 0.0;
-    for (int i = lane; i < n; i += 32) s2 += R[i + (size_t)j * n] * R[i + (size_t)j * n];
-    s2 = warp_sum(s2);
-    if (lane == 0) norms[j] = sqrt(s2);
+    for (int i = 0; i < n; ++i) s2 = fma(X[i + t * n], X[i + t * n], s2);
+    norms[t] = sqrt(s2);
   }
-  for (int e = tid; e < m * n; e += QJ_NT) Uo[e] = Y[e];
-  for (int e = tid; e < n * n; e += QJ_NT) Yo[e] = R[e];
+  for (int e = t; e < n * n; e += SV_NT) Yo[e] = X[e];
 }
 
 }  // namespace
@@ -1483,15 +1416,12 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   return FTT_OK;
 }
 
-constexpr size_t kQjSmemCap = 200 * 1024;
-inline size_t qj_smem_bytes(int64_t m, int64_t n) { return 8 * (size_t)(2 * m * n + 2 * n * n); }
-
 bool direct_small_ok(int64_t m, int64_t n) {
   static const bool off = getenv("FTT_NO_DIRECT_SMALL") != nullptr;
-  return !off && n >= 1 && n <= 16 && m >= n && qj_smem_bytes(m, n) <= kQjSmemCap;
+  return !off && n >= 1 && n <= 16 && m >= n && m <= 4 * SV_NT;
 }
 
-// SVD of the short tall A_tall (m x n) in one launch (k_jacobi_qr): U = Q P
+// SVD of the short tall A_tall (m x n) in one launch (k_svd_wy): U = Q P
 // (m x n, ld m), Yt = R^T P (n x n, ld n), norms_host[j] = ||Yt_j||
 // (unsorted) -- the outputs of tsqr_svd.
 int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, int trans,
@@ -1501,15 +1431,18 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
   FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n)));
   int *status = reinterpret_cast<int *>(dev);
   const int max_sweeps = 60;
-  static bool qattr = false;
-  if (!qattr) {
-    FTT_CUDA(cudaFuncSetAttribute(k_jacobi_qr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kQjSmemCap));
-    qattr = true;
+  const size_t smem = 8 * (size_t)(n <= 8 ? 8 : 16) * SV_NT;
+#define FTT_SVD_WY(NM, R)                                                                      \
+  k_svd_wy<NM, R><<<1, SV_NT, smem, ctx->stream>>>((int)m, (int)n, A, lda, trans, U, Yt, dev + 2, \
+                                                   max_sweeps, status, extra_dev, dev + 1)
+  if (n <= 8) {
+    if (m <= 2 * SV_NT) FTT_SVD_WY(8, 2);
+    else FTT_SVD_WY(8, 4);
+  } else {
+    if (m <= 2 * SV_NT) FTT_SVD_WY(16, 2);
+    else FTT_SVD_WY(16, 4);
   }
-  k_jacobi_qr<<<1, QJ_NT, qj_smem_bytes(m, n), ctx->stream>>>((int)m, (int)n, A, lda, trans, U, Yt,
-                                                              dev + 2, max_sweeps, status,
-                                                              extra_dev, dev + 1);
+#undef FTT_SVD_WY
   FTT_LAUNCHED(ctx);
   std::vector<double> h(n + 2);
   FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));
