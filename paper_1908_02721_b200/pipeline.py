@@ -1186,16 +1186,42 @@ def _fasttt_device_body(a, coords_d, values_d, eps, pivot, mode, fixed_ranks, no
     return res
 
 
+_STAGE_MAX = 256 << 20  # cores up to this size go through the reused staging buffer
+_stage = __import__("threading").local()
+
+
 def _cores_to_host(cores):
-    """D2H of the final cores into pinned host buffers (torch's caching host
-    allocator), one stream sync for all of them.  ``.cpu()`` lands in fresh
-    pageable memory: 0.9 s instead of 34 ms for config 3's 1.9 GB of cores."""
+    """D2H of the final cores with one stream sync.  Up to _STAGE_MAX bytes
+    they land in a per-thread pinned staging buffer that is reused across
+    calls and are copied out into ordinary numpy arrays (a caller holding the
+    previous result no longer forces torch's host allocator to pin a fresh
+    block inside the call: that showed up as 15-45 ms outliers on config 5);
+    larger trains land in fresh pinned buffers (``.cpu()`` into pageable
+    memory: 0.9 s instead of 34 ms for config 3's 1.9 GB of cores)."""
     torch = _torch()
-    host = [torch.empty(tuple(c.shape), dtype=c.dtype, pin_memory=True) for c in cores]
-    for h, c in zip(host, cores):
-        h.copy_(c, non_blocking=True)
+    sizes = [int(c.numel()) for c in cores]
+    total = sum(sizes)
+    if 8 * total > _STAGE_MAX:
+        host = [torch.empty(tuple(c.shape), dtype=c.dtype, pin_memory=True) for c in cores]
+        for h, c in zip(host, cores):
+            h.copy_(c, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return [h.numpy() for h in host]
+    buf = getattr(_stage, "buf", None)
+    if buf is None or buf.numel() < total:
+        buf = torch.empty(max(total, 1 << 16), dtype=torch.float64, pin_memory=True)
+        _stage.buf = buf
+    off = 0
+    for n, c in zip(sizes, cores):
+        buf[off:off + n].copy_(c.reshape(-1), non_blocking=True)
+        off += n
     torch.cuda.current_stream().synchronize()
-    return [h.numpy() for h in host]
+    flat = buf.numpy()[:total].copy()
+    out, off = [], 0
+    for n, c in zip(sizes, cores):
+        out.append(flat[off:off + n].reshape(tuple(c.shape)))
+        off += n
+    return out
 
 
 def fasttt(a: SparseTensor, eps: float | None = 1e-14, pivot: int | None = None,
