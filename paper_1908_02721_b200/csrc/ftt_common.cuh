@@ -80,6 +80,12 @@ struct ftt_ctx {
   size_t zflags_cap = 0;
   // split-K tile arrival counters (zero between products; ftt_gemm.cu)
   unsigned *tile_cnt = nullptr;
+  // single-pass compaction: per-tile look-back status words tagged with a
+  // per-call epoch (never cleared), followed by the tile ticket and the
+  // exit counter (reset by the last CTA of each launch)
+  uint64_t *cp_status = nullptr;
+  size_t cp_status_cap = 0;
+  uint32_t cp_epoch = 0;
   // live per-class kernel timing (off by default)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -156,6 +162,10 @@ constexpr size_t kRingBytes = 1 << 20;
 // The context's zeroed flag array with at least n entries (grown and
 // cleared once; callers must leave it all-zero).
 int zero_flags(ftt_ctx *ctx, size_t n, uint32_t **out);
+// Look-back status for a single-pass compaction over `ntiles` tiles: the
+// status words, the ticket pair and this call's epoch (ftt_index.cu).
+int compact_status(ftt_ctx *ctx, size_t ntiles, uint64_t **status, unsigned **ticket,
+                   uint32_t *epoch);
 
 // Persistent device buffer owned by the context (freed on destroy).
 int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes);

@@ -124,6 +124,29 @@ int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes) {
   return FTT_OK;
 }
 
+int compact_status(ftt_ctx *ctx, size_t ntiles, uint64_t **status, unsigned **ticket,
+                   uint32_t *epoch) {
+  if (ntiles > ctx->cp_status_cap) {
+    if (ctx->cp_status) FTT_CUDA(cudaFreeAsync(ctx->cp_status, ctx->stream));
+    ctx->cp_status = nullptr;
+    ctx->cp_status_cap = 0;
+    const size_t cap = align_up(ntiles + ntiles / 4 + 64, 4096);
+    FTT_CUDA(cudaMallocAsync((void **)&ctx->cp_status, 8 * (cap + 1), ctx->stream));
+    FTT_CUDA(cudaMemsetAsync(ctx->cp_status, 0, 8 * (cap + 1), ctx->stream));
+    ctx->cp_status_cap = cap;
+    ctx->cp_epoch = 0;
+  }
+  // epochs 1 .. 2^30 - 1 tag the status words; on wrap the words are cleared
+  if (++ctx->cp_epoch >= (1u << 30)) {
+    FTT_CUDA(cudaMemsetAsync(ctx->cp_status, 0, 8 * ctx->cp_status_cap, ctx->stream));
+    ctx->cp_epoch = 1;
+  }
+  *status = ctx->cp_status;
+  *ticket = reinterpret_cast<unsigned *>(ctx->cp_status + ctx->cp_status_cap);
+  *epoch = ctx->cp_epoch;
+  return FTT_OK;
+}
+
 int zero_flags(ftt_ctx *ctx, size_t n, uint32_t **out) {
   if (n > ctx->zflags_cap) {
     if (ctx->zflags) FTT_CUDA(cudaFreeAsync(ctx->zflags, ctx->stream));
@@ -256,6 +279,7 @@ int ftt_destroy(ftt_ctx *ctx) {
   ctx->owned.clear();
   if (ctx->arena.base) cudaFreeAsync(ctx->arena.base, ctx->stream);
   if (ctx->zflags) cudaFreeAsync(ctx->zflags, ctx->stream);
+  if (ctx->cp_status) cudaFreeAsync(ctx->cp_status, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);

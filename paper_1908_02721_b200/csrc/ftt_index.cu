@@ -446,74 +446,6 @@ __device__ __forceinline__ int64_t dyn_n(int64_t nmax, const int64_t *n_dev, int
   return n_dev ? min(nmax, *n_dev * mult) : nmax;
 }
 
-template <class Pred>
-__global__ void __launch_bounds__(CP_THREADS) k_count(int64_t nmax, Pred pred, int64_t *block_counts,
-                                                      const int64_t *n_dev = nullptr,
-                                                      int64_t mult = 1) {
-  const int64_t n = dyn_n(nmax, n_dev, mult);
-  const int64_t ntile = (n + CP_TILE - 1) / CP_TILE;
-  __shared__ int s_w[CP_THREADS / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {  // grid-stride tiles
-    const int64_t wbase = tile * CP_TILE + warp * (32 * CP_ITEMS);
-    int cnt = 0;
-#pragma unroll 4
-    for (int j = 0; j < CP_ITEMS; ++j) {
-      int64_t i = wbase + j * 32 + lane;
-      bool f = i < n && pred(i);
-      cnt += __popc(__ballot_sync(0xffffffffu, f));
-    }
-    if (lane == 0) s_w[warp] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t t = 0;
-      for (int w = 0; w < CP_THREADS / 32; ++w) t += s_w[w];
-      block_counts[tile] = t;
-    }
-    __syncthreads();
-  }
-}
-
-// emit(i, rank_excl, flag) is called for every i < n; rank_excl = number of
-// flagged items before i (global).
-template <class Pred, class Emit>
-__global__ void __launch_bounds__(CP_THREADS) k_emit(int64_t nmax, Pred pred, Emit emit,
-                                                     const int64_t *block_offsets,
-                                                     const int64_t *n_dev = nullptr,
-                                                     int64_t mult = 1) {
-  const int64_t n = dyn_n(nmax, n_dev, mult);
-  const int64_t ntile = (n + CP_TILE - 1) / CP_TILE;
-  __shared__ int s_w[CP_THREADS / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t lt = lanemask_lt();
-  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x) {  // grid-stride tiles
-    const int64_t wbase = tile * CP_TILE + warp * (32 * CP_ITEMS);
-    // first: this warp's count (re-evaluate pred; cheap relative to a
-    // second smem round trip of flags)
-    uint32_t balls[CP_ITEMS];
-    int cnt = 0;
-#pragma unroll
-    for (int j = 0; j < CP_ITEMS; ++j) {
-      int64_t i = wbase + j * 32 + lane;
-      bool f = i < n && pred(i);
-      balls[j] = __ballot_sync(0xffffffffu, f);
-      cnt += __popc(balls[j]);
-    }
-    if (lane == 0) s_w[warp] = cnt;
-    __syncthreads();
-    int64_t run = block_offsets[tile];
-    for (int w = 0; w < warp; ++w) run += s_w[w];
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < CP_ITEMS; ++j) {
-      int64_t i = wbase + j * 32 + lane;
-      bool f = (balls[j] >> lane) & 1u;
-      if (i < n) emit(i, run + __popc(balls[j] & lt), f);
-      run += __popc(balls[j]);
-    }
-  }
-}
-
 __global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total,
                               const int64_t *n_dev = nullptr, int64_t mult = 1) {
   // single block, 1024 threads, chunked exclusive scan
@@ -541,23 +473,135 @@ __global__ void k_scan_counts(int64_t *counts, int64_t nb, int64_t *total,
   if (threadIdx.x == 0 && total) *total = carry;
 }
 
+// Single-pass compaction: each CTA claims tiles in order from a ticket,
+// ranks its flagged items with warp ballots, publishes the tile total
+// (AGG), finds its exclusive prefix by a warp-wide decoupled look-back over
+// the 32 nearest predecessors at a time (the nearest INC ends it), publishes
+// the inclusive prefix (INC) and emits.  Status words carry this call's
+// epoch, so the array is never cleared between calls; the ticket is reset by
+// the last CTA to leave.  One launch instead of count + scan + emit.
+// Status word: epoch << 34 | flag << 32 | value (counts < 2^32).
+constexpr uint64_t CPS_AGG = 1ull, CPS_INC = 2ull;
+
+__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <class Pred, class Emit>
+__global__ void __launch_bounds__(CP_THREADS) k_compact1(int64_t nmax, Pred pred, Emit emit,
+                                                         uint64_t *__restrict__ status,
+                                                         unsigned *__restrict__ ticket,
+                                                         uint32_t epoch, int64_t *total,
+                                                         const int64_t *n_dev, int64_t mult) {
+  const int64_t n = dyn_n(nmax, n_dev, mult);
+  const int64_t ntile = (n + CP_TILE - 1) / CP_TILE;
+  __shared__ int s_w[CP_THREADS / 32];
+  __shared__ int64_t s_tile;
+  __shared__ uint32_t s_excl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const uint64_t tag = (uint64_t)epoch << 34;
+  if (ntile == 0 && blockIdx.x == 0 && threadIdx.x == 0 && total) *total = 0;
+  while (true) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntile) break;
+    const int64_t wbase = tile * CP_TILE + warp * (32 * CP_ITEMS);
+    uint32_t balls[CP_ITEMS];
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < CP_ITEMS; ++j) {
+      const int64_t i = wbase + j * 32 + lane;
+      const bool f = i < n && pred(i);
+      balls[j] = __ballot_sync(0xffffffffu, f);
+      cnt += __popc(balls[j]);
+    }
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < CP_THREADS / 32; ++w) {
+      const uint32_t c = (uint32_t)s_w[w];
+      wpre += w < warp ? c : 0u;
+      tot += c;
+    }
+    if (warp == 0) {
+      uint32_t excl = 0;
+      if (tile == 0) {
+        if (lane == 0) st_relaxed64(status, tag | (CPS_INC << 32) | tot);
+      } else {
+        if (lane == 0) st_relaxed64(status + tile, tag | (CPS_AGG << 32) | tot);
+        int64_t j = tile - 1 - lane;  // lane 0 = nearest predecessor
+        while (true) {
+          const uint64_t sw = j >= 0 ? ld_relaxed64(status + j) : (tag | (CPS_INC << 32));
+          const bool valid = (sw >> 34) == epoch && ((sw >> 32) & 3u) != 0;
+          if (!__all_sync(0xffffffffu, valid)) continue;
+          const unsigned inc = __ballot_sync(0xffffffffu, ((sw >> 32) & 3u) == CPS_INC);
+          const int stop = inc ? __ffs(inc) - 1 : 31;
+          uint32_t v = lane <= stop ? (uint32_t)sw : 0u;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          excl += v;
+          if (inc) break;
+          j -= 32;
+        }
+        if (lane == 0) st_relaxed64(status + tile, tag | (CPS_INC << 32) | (uint32_t)(excl + tot));
+      }
+      if (lane == 0) {
+        s_excl = excl;
+        if (tile == ntile - 1 && total) *total = (int64_t)excl + tot;
+      }
+    }
+    __syncthreads();
+    int64_t run = (int64_t)s_excl + wpre;
+#pragma unroll
+    for (int j = 0; j < CP_ITEMS; ++j) {
+      const int64_t i = wbase + j * 32 + lane;
+      const bool f = (balls[j] >> lane) & 1u;
+      if (i < n) emit(i, run + __popc(balls[j] & lt), f);
+      run += __popc(balls[j]);
+    }
+    __syncthreads();  // s_tile / s_w / s_excl reuse
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();  // this CTA's last ticket claim before its exit count
+    if (atomicAdd(ticket + 1, 1u) == gridDim.x - 1) {
+      __threadfence();
+      ticket[0] = 0;
+      ticket[1] = 0;
+    }
+  }
+}
+
 // `tag`/`alg_bytes`: profiling class and algorithmic bytes of the whole
-// compaction (predicate reads + emitted outputs), charged to the emit pass
-// and the count pass together.
+// compaction (predicate reads + emitted outputs).  `block_counts` is unused
+// (kept for the callers' scratch layout).  n < 2^31 (every caller).
 template <class Pred, class Emit>
 int compact(ftt_ctx *ctx, int64_t n, Pred pred, Emit emit, int64_t *block_counts,
             int64_t *total_dev, int tag = PT_SEGMENT, double alg_bytes = 0.0,
             const int64_t *n_dev = nullptr, int64_t mult = 1) {
+  (void)block_counts;
   if (n <= 0) return FTT_OK;
-  int64_t nb = ceil_div(n, CP_TILE);
-  // dynamic lengths: a bounded grid strides over the live tiles
-  const unsigned grid = (unsigned)(n_dev ? std::min<int64_t>(nb, 8 * (int64_t)ctx->num_sms) : nb);
+  if (n >= ((int64_t)1 << 31)) {
+    set_error("compaction length %lld exceeds 2^31", (long long)n);
+    return FTT_ERR_INVALID;
+  }
+  const int64_t nb = ceil_div(n, CP_TILE);
+  uint64_t *status = nullptr;
+  unsigned *ticket = nullptr;
+  uint32_t epoch = 0;
+  FTT_CHECK(compact_status(ctx, (size_t)nb, &status, &ticket, &epoch));
+  // dynamic lengths: a bounded grid claims the live tiles
+  const unsigned grid = (unsigned)std::min<int64_t>(nb, 8 * (int64_t)ctx->num_sms);
   const int pb = tag >= 0 ? prof_begin(ctx) : -1;
-  k_count<Pred><<<grid, CP_THREADS, 0, ctx->stream>>>(n, pred, block_counts, n_dev, mult);
-  FTT_LAUNCHED(ctx);
-  k_scan_counts<<<1, 1024, 0, ctx->stream>>>(block_counts, nb, total_dev, n_dev, mult);
-  FTT_LAUNCHED(ctx);
-  k_emit<Pred, Emit><<<grid, CP_THREADS, 0, ctx->stream>>>(n, pred, emit, block_counts, n_dev, mult);
+  k_compact1<Pred, Emit><<<grid, CP_THREADS, 0, ctx->stream>>>(n, pred, emit, status, ticket,
+                                                               epoch, total_dev, n_dev, mult);
   FTT_LAUNCHED(ctx);
   prof_end(ctx, pb, tag, alg_bytes, 0.0);
   return FTT_OK;

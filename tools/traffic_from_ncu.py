@@ -16,7 +16,7 @@ import sys
 CLASSES = [
     ("sort", ("k_onesweep", "k_part_scatter")),
     ("hist", ("k_keys_hist", "k_hist", "k_distinct_hash", "k_linearize")),
-    ("segment", ("k_count", "k_emit", "k_scan_counts", "k_count_changes", "k_distinct_",
+    ("segment", ("k_compact", "k_count", "k_emit", "k_scan_counts", "k_count_changes", "k_distinct_",
                  "k_part_count", "k_sel_count", "k_group_count")),
     ("sweep", ("k_sweep",)),
     ("scatter", ("k_pivot_scatter", "k_side_core", "k_scatter_", "k_sp_entries", "k_sp_gather",
