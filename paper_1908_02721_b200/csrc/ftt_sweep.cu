@@ -95,6 +95,7 @@ struct Driver {
   double delta, left, right;
   const int64_t *targets;
   int interval_ok;
+  std::vector<double *> tmp;  // allocated, not yet owned by a core: freed if a step fails
 
   int alloc(double **p, size_t elems) {
     cudaError_t e = cudaMallocAsync((void **)p, 8 * std::max<size_t>(elems, 1), ctx->stream);
@@ -103,7 +104,23 @@ struct Driver {
       set_error("sweep: allocation of %zu doubles failed", elems);
       return FTT_ERR_OOM;
     }
+    tmp.push_back(*p);
     return FTT_OK;
+  }
+  void forget(double *p) {
+    for (size_t i = tmp.size(); i-- > 0;)
+      if (tmp[i] == p) {
+        tmp.erase(tmp.begin() + i);
+        return;
+      }
+  }
+  void drop(double *p) {
+    forget(p);
+    cudaFreeAsync(p, ctx->stream);
+  }
+  void drop_all() {
+    for (double *p : tmp) cudaFreeAsync(p, ctx->stream);
+    tmp.clear();
   }
   void release(Core &c) {
     if (c.owned && c.data) cudaFreeAsync(c.data, ctx->stream);
@@ -112,6 +129,7 @@ struct Driver {
   }
   void replace(int k, double *data, int64_t r0, int64_t n, int64_t r1) {
     release(cs[k]);
+    forget(data);
     Core c;
     c.kind = 0;
     c.r0 = r0;
@@ -247,7 +265,7 @@ struct Driver {
                             nw, nn * c));
         replace(k + 1, nw, rank, nn, c);
       }
-      cudaFreeAsync(V, ctx->stream);
+      drop(V);
     }
     for (int k = d - 1; k > pivot; --k) {  // fasttt.py:342-347
       FTT_CHECK(densify(k));
@@ -264,7 +282,7 @@ struct Driver {
       FTT_CHECK(alloc(&Y, (size_t)a * b * q));
       FTT_CHECK(ftt_dgemm(ctx, 0, 0, q, a * b, c, 1.0, R, q, cs[k - 1].data, c, 0.0, Y, q));
       replace(k - 1, Y, a, b, q);
-      cudaFreeAsync(R, ctx->stream);
+      drop(R);
     }
     for (int k = pivot; k > 0; --k) {  // fasttt.py:348-355
       FTT_CHECK(densify(k));
@@ -300,7 +318,7 @@ struct Driver {
                             rank));
         replace(k - 1, nw, a, b, rank);
       }
-      cudaFreeAsync(V, ctx->stream);
+      drop(V);
     }
     for (int k = 0; k < d; ++k) {
       FTT_CHECK(densify(k));
@@ -369,6 +387,7 @@ int ftt_sweep_rounding(ftt_ctx *ctx, int32_t d, int32_t pivot, const ftt_core_de
   const int rc = dr.run(&zero);
   if (rc != FTT_OK || zero) {
     for (auto &c : dr.cs) dr.release(c);
+    dr.drop_all();
     *zero_out = zero;
     for (int k = 0; k < d; ++k) out_ptrs[k] = nullptr;
     return rc;
