@@ -438,6 +438,50 @@ int ftt_sweep_rounding(ftt_ctx *ctx, int32_t d, int32_t pivot,
 /* Release a device buffer returned by ftt_sweep_rounding (stream-ordered). */
 int ftt_free_device(ftt_ctx *ctx, void *p);
 
+/* ------------------------------------------------------- fasttt driver */
+/* What ftt_fasttt_lin hands back.  Device buffers the caller releases with
+ * ftt_free_device: fiber_slab (fixed_lin, indptr, fiber_of, pivot_index,
+ * values_f point into it), kept_slab (step s's kept rows at kept_off[s],
+ * step_counts[s] entries; steps ordered as ftt_index_sweeps_all: modes
+ * 0..p-1 then d-1..p+1), maps_slab (step s's fiber map at s * max(R, 1)),
+ * and the output train: out_slab when non-NULL (every core inside it, back
+ * to back in mode order), else each out_cores[k] on its own. */
+typedef struct {
+  int32_t pivot;        /* the pivot used (select_p's choice when asked) */
+  int32_t zero;         /* a truncation reached rank 0: the cores are zeros (1, n_k, 1) */
+  int32_t fallback;     /* 1: nothing was produced, use the step-by-step entry points */
+  int32_t inner_valid;  /* dot / nb hold the report's terms */
+  int32_t lazy_pivot;   /* the pivot core stayed as its entries */
+  int32_t status_flags; /* ftt_take_status (bit 0: non-finite input) */
+  int64_t num_fibers;
+  int64_t step_counts[32];
+  int64_t kept_off[32];
+  int64_t pivot_shape[3];
+  int64_t out_shapes[96];
+  int64_t out_total;    /* elements of the output train */
+  double na2, pnorm, dot, nb;
+  void *fiber_slab;
+  int64_t *fixed_lin, *indptr, *fiber_of, *pivot_index;
+  double *values_f;
+  int64_t *kept_slab, *maps_slab;
+  double *out_slab;
+  double *out_cores[32];
+} ftt_fasttt_result;
+/* fasttt (fasttt.py:634-749) for static (mode 0) and dynamic (mode 1)
+ * budgets in one call on the canonical COO (lin strictly increasing +
+ * values, device): select_p when pivot < 0 (fasttt.py:501-558, exact-int
+ * cost model), extract_nonzero_fibers, _index_sweeps, the structured train
+ * with the pivot core kept as its entries below 2 % density, the rounding
+ * sweeps, and with report != 0 the inner-product identity's terms
+ * (na2 = |a|^2, dot = <a, b>, nb = |b|).  values_ready (optional
+ * cudaEvent_t) is waited for after select_p, before the values are read.
+ * Sets res->fallback instead of failing when an extent or bound exceeds
+ * the fused path's limits. */
+int ftt_fasttt_lin(ftt_ctx *ctx, const int64_t *lin, const double *values,
+                   int64_t nnz, int32_t d, const int64_t *dims, int32_t pivot,
+                   int32_t mode, double eps, double c_svd, int32_t report,
+                   void *values_ready, ftt_fasttt_result *res);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,8 @@ SIGNATURES = {
     "ftt_sweep_rounding": [_c_p, _c_i32, _c_i32, _c_p, _c_p, _c_i32, _c_d, _c_d, _c_d, _c_p,
                            _c_i32, _c_p, _c_p, ctypes.POINTER(ctypes.c_int32)],
     "ftt_free_device": [_c_p, _c_p],
+    "ftt_fasttt_lin": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, _c_i32, _c_d, _c_d,
+                       _c_i32, _c_p, _c_p],
     "ftt_delinearize": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_p],
     "ftt_sync_stats": [_c_p, ctypes.POINTER(ctypes.c_int64), _P_d],
     "ftt_tt_norm": [_c_p, _c_i32, _P_i64, _P_i64, ctypes.POINTER(_c_p), _P_d],

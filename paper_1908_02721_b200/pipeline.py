@@ -81,6 +81,9 @@ __all__ = [
 
 _MODES = ("static", "dynamic", "fixed_rank")
 _ERROR_MEASURE_CAP = 20_000_000  # fasttt.py:74
+# FTT_STEPWISE=1: orchestrate the stages from Python (the fallback path) even
+# where the fused native driver applies -- the cross-check of the two
+_STEPWISE = __import__("os").environ.get("FTT_STEPWISE") == "1"
 
 
 class _FlopCounter:
@@ -687,15 +690,15 @@ class _NativeCore:
     __cuda_array_interface__ (zero copy) and released (ftt_free_device,
     stream-ordered) when the last tensor viewing it is gone."""
 
-    __slots__ = ("ptr", "shape", "__weakref__")
+    __slots__ = ("ptr", "shape", "typestr", "__weakref__")
 
-    def __init__(self, ptr, shape):
-        self.ptr, self.shape = int(ptr), tuple(int(x) for x in shape)
+    def __init__(self, ptr, shape, typestr="<f8"):
+        self.ptr, self.shape, self.typestr = int(ptr), tuple(int(x) for x in shape), typestr
 
     @property
     def __cuda_array_interface__(self):
-        return {"shape": self.shape, "typestr": "<f8", "data": (self.ptr, False), "version": 3,
-                "strides": None}
+        return {"shape": self.shape, "typestr": self.typestr, "data": (self.ptr, False),
+                "version": 3, "strides": None}
 
     def __del__(self):
         try:
@@ -1083,12 +1086,27 @@ class DecompositionReport:
 class DeviceResult:
     """fasttt_device output: device cores + everything the report needs."""
 
-    __slots__ = ("cores", "pivot", "mode", "eps", "num_fibers", "ranks_lossless", "ranks",
-                 "eps_actual", "eps_actual_method", "eps_actual_inner", "notes", "zero")
+    __slots__ = ("_cores", "slab", "shapes", "pivot", "mode", "eps", "num_fibers",
+                 "ranks_lossless", "ranks", "eps_actual", "eps_actual_method", "eps_actual_inner",
+                 "notes", "zero")
 
     def __init__(self, **kw):
-        for k in self.__slots__:
+        self._cores = kw.pop("cores", None)
+        for k in self.__slots__[1:]:
             setattr(self, k, kw.get(k))
+
+    @property
+    def cores(self):
+        """Device cores; a train the fused driver returned as one slab
+        (``slab`` flat f64, ``shapes``) is split into views on first use."""
+        if self._cores is None and self.slab is not None:
+            out, off = [], 0
+            for sh in self.shapes:
+                n = sh[0] * sh[1] * sh[2]
+                out.append(self.slab[off:off + n].view(sh))
+                off += n
+            self._cores = out
+        return self._cores
 
 
 def _normalize(eps, mode):
@@ -1103,6 +1121,139 @@ def _normalize(eps, mode):
     return eps, mode
 
 
+class _FastttResult(nat.ctypes.Structure):
+    """ftt_fasttt_result (include/fasttt_b200.h)."""
+
+    _fields_ = [("pivot", nat.ctypes.c_int32), ("zero", nat.ctypes.c_int32),
+                ("fallback", nat.ctypes.c_int32), ("inner_valid", nat.ctypes.c_int32),
+                ("lazy_pivot", nat.ctypes.c_int32), ("status_flags", nat.ctypes.c_int32),
+                ("num_fibers", nat.ctypes.c_int64), ("step_counts", nat.ctypes.c_int64 * 32),
+                ("kept_off", nat.ctypes.c_int64 * 32), ("pivot_shape", nat.ctypes.c_int64 * 3),
+                ("out_shapes", nat.ctypes.c_int64 * 96), ("out_total", nat.ctypes.c_int64),
+                ("na2", nat.ctypes.c_double), ("pnorm", nat.ctypes.c_double),
+                ("dot", nat.ctypes.c_double), ("nb", nat.ctypes.c_double),
+                ("fiber_slab", nat.ctypes.c_void_p), ("fixed_lin", nat.ctypes.c_void_p),
+                ("indptr", nat.ctypes.c_void_p), ("fiber_of", nat.ctypes.c_void_p),
+                ("pivot_index", nat.ctypes.c_void_p), ("values_f", nat.ctypes.c_void_p),
+                ("kept_slab", nat.ctypes.c_void_p), ("maps_slab", nat.ctypes.c_void_p),
+                ("out_slab", nat.ctypes.c_void_p), ("out_cores", nat.ctypes.c_void_p * 32)]
+
+
+def _fused_structure(r: "_FastttResult", dims, nnz: int):
+    """DeviceFibers / DeviceSweeps views over the buffers ftt_fasttt_lin
+    returned (each slab is owned by one holder the views keep alive)."""
+    from .coo import DeviceFibers
+
+    torch = _torch()
+    d, p, R = len(dims), int(r.pivot), int(r.num_fibers)
+    fib = torch.as_tensor(_NativeCore(r.fiber_slab, (5 * nnz + 1,), "<i8"), device="cuda")
+    df = DeviceFibers(tuple(dims), p, R, nnz, fib[:R], fib[nnz:nnz + R + 1],
+                      fib[2 * nnz + 1:3 * nnz + 1], fib[3 * nnz + 1:4 * nnz + 1],
+                      fib[4 * nnz + 1:5 * nnz + 1].view(torch.float64))
+    nsteps = d - 1
+    cnt = [int(r.step_counts[s]) for s in range(nsteps)]
+    off = [int(r.kept_off[s]) for s in range(nsteps)]
+    ktot = off[-1] + max(cnt[-1], 1) if nsteps else 1
+    kb = torch.as_tensor(_NativeCore(r.kept_slab, (max(ktot, 1),), "<i8"), device="cuda")
+    mb = torch.as_tensor(_NativeCore(r.maps_slab, (max(R, 1) * nsteps,), "<i8"), device="cuda")
+    left, right = [], []
+    t_map, r_prev, s_map, r_next = None, 1, None, 1
+    for s in range(nsteps):
+        kept = kb[off[s]:off[s] + cnt[s]]
+        m = mb[s * max(R, 1):s * max(R, 1) + R]
+        if s < p:
+            left.append((kept, r_prev))
+            t_map, r_prev = m, cnt[s]
+        else:
+            right.append((kept, r_next))
+            s_map, r_next = m, cnt[s]
+    return df, DeviceSweeps(left, t_map, r_prev, right, s_map, r_next)
+
+
+def _fasttt_fused(a: SparseTensor, values_d, eps, pivot, mode, c_svd, report, values_ready):
+    """fasttt_device through ftt_fasttt_lin (static / dynamic budgets): one
+    native call from select_p to the report's inner-product terms; None when
+    the native side asks for the step-by-step path."""
+    torch = _torch()
+    d, dims, nnz = a.ndim, a.shape, a.nnz
+    lib, ctx = nat.lib(), nat.context()
+    r = _FastttResult()
+    ev = nat.ctypes.c_void_p(values_ready.cuda_event) if values_ready is not None else None
+    try:
+        nat.check(lib.ftt_fasttt_lin(ctx, nat.ptr(a.device_lin()), nat.ptr(values_d), nnz, d,
+                                     nat.i64_array(dims), -1 if pivot is None else int(pivot),
+                                     0 if mode == "static" else 1, float(eps), float(c_svd),
+                                     1 if report else 0, ev, nat.ctypes.byref(r)),
+                  "ftt_fasttt_lin")
+    except MemoryError as e:
+        if "pivot core" in str(e):
+            shape = tuple(int(x) for x in r.pivot_shape)
+            raise MemoryError(f"pivot core {shape} does not fit in device memory") from e
+        raise
+    if r.fallback:
+        return None
+    if r.status_flags & 1:
+        raise ValueError("matrix entries must be finite")
+    free = lib.ftt_free_device
+    vp = nat.ctypes.c_void_p
+    notes = []
+    zero = bool(r.zero)
+    shapes = [tuple(int(x) for x in r.out_shapes[3 * k:3 * k + 3]) for k in range(d)]
+    if r.out_slab:
+        slab = torch.as_tensor(_NativeCore(r.out_slab, (max(int(r.out_total), 1),)), device="cuda")
+        cores = None
+    else:
+        slab = None
+        cores = [torch.as_tensor(_NativeCore(r.out_cores[k], shapes[k]), device="cuda")
+                 for k in range(d)]
+    p = int(r.pivot)
+    cnt = [int(r.step_counts[s]) for s in range(d - 1)]
+    bonds = [0] * (d - 1)
+    for s in range(d - 1):
+        bonds[s if s < p else d - 2 - (s - p)] = cnt[s]
+    res = DeviceResult(cores=cores, slab=slab, shapes=shapes, pivot=p, mode=mode, eps=eps,
+                       num_fibers=int(r.num_fibers), ranks_lossless=tuple(bonds),
+                       ranks=tuple(sh[2] for sh in shapes[:-1]), notes=notes, zero=zero)
+    structure = None
+    if report:
+        na2 = float(r.na2)
+        if r.inner_valid:
+            nb2 = float(r.nb) ** 2
+            inner = math.sqrt(max(na2 - 2.0 * float(r.dot) + nb2, 0.0) / na2)
+        else:
+            coords_d, _ = a.device_arrays()
+            inner = _inner_error_device(coords_d, values_d, nnz, res.cores, na2)
+        # shapes of the lossless train (0/1 cores + pivot core)
+        exact, rp, rn = [None] * d, 1, 1
+        for s in range(d - 1):
+            if s < p:
+                exact[s] = (rp, dims[s], cnt[s])
+                rp = cnt[s]
+            else:
+                k = d - 1 - (s - p)
+                exact[k] = (cnt[s], dims[k], rn)
+                rn = cnt[s]
+        exact[p] = (rp, dims[p], rn)
+        total = _diff_total(exact, shapes)
+        if total <= _ERROR_MEASURE_CAP:
+            df, sw = structure = _fused_structure(r, dims, nnz)
+            train, _ = _structured_train(df, sw)
+            res.eps_actual = _dev_relative_error([_as_dense(c) for c in train], res.cores,
+                                                 math.sqrt(na2))
+            res.eps_actual_method = "tt_difference"
+        else:
+            res.eps_actual = inner
+            res.eps_actual_method = "inner_identity"
+            notes.append("exact-difference error measure too large; reported value is the "
+                         "inner-product identity (resolution ~1e-8)")
+        res.eps_actual_inner = inner
+    if structure is None:
+        for ptr in (r.fiber_slab, r.kept_slab, r.maps_slab):
+            if ptr:
+                free(ctx, vp(ptr))
+    return res
+
+
 def fasttt_device(a: SparseTensor, coords_d, values_d, eps, pivot, mode, fixed_ranks,
                   precise_pivot, c_svd, report=True, values_ready=None) -> DeviceResult:
     """The decomposition on device arrays (COO already in HBM)."""
@@ -1110,6 +1261,13 @@ def fasttt_device(a: SparseTensor, coords_d, values_d, eps, pivot, mode, fixed_r
     dims = a.shape
     nnz = a.nnz
     notes = []
+    if (mode in ("static", "dynamic") and not precise_pivot and nnz and d >= 2
+            and not _STEPWISE and __import__("os").environ.get("FTT_PY_SWEEP") != "1"):
+        if pivot is not None:
+            _check_pivot(pivot, d)
+        res = _fasttt_fused(a, values_d, eps, pivot, mode, c_svd, report, values_ready)
+        if res is not None:
+            return res
     if pivot is None:
         pivot = select_p(a, target_ranks=fixed_ranks if mode == "fixed_rank" else None,
                          precise=precise_pivot, c_svd=c_svd)
@@ -1190,6 +1348,26 @@ _STAGE_MAX = 256 << 20  # cores up to this size go through the reused staging bu
 _stage = __import__("threading").local()
 
 
+def _slab_to_host(slab, shapes):
+    """D2H of a train held as one device slab: one copy into the reused
+    pinned staging buffer, one sync, numpy views of one host array."""
+    torch = _torch()
+    total = int(slab.numel())
+    buf = getattr(_stage, "buf", None)
+    if buf is None or buf.numel() < total:
+        buf = torch.empty(max(total, 1 << 16), dtype=torch.float64, pin_memory=True)
+        _stage.buf = buf
+    buf[:total].copy_(slab, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    flat = buf.numpy()[:total].copy()
+    out, off = [], 0
+    for sh in shapes:
+        n = sh[0] * sh[1] * sh[2]
+        out.append(flat[off:off + n].reshape(sh))
+        off += n
+    return out
+
+
 def _cores_to_host(cores):
     """D2H of the final cores with one stream sync.  Up to _STAGE_MAX bytes
     they land in a per-thread pinned staging buffer that is reused across
@@ -1251,7 +1429,10 @@ def fasttt(a: SparseTensor, eps: float | None = 1e-14, pivot: int | None = None,
             eps_actual_method="exact", eps_actual_inner=0.0, flops_fasttt_model=0.0,
             flops_ttsvd_model=0.0, wall_time_s=time.perf_counter() - wall0,
             cpu_time_s=time.process_time() - cpu0, warnings=tuple(res.notes))
-    tt = TTTensor(_cores_to_host(res.cores), copy=False)
+    if res.slab is not None and res._cores is None:
+        tt = TTTensor(_slab_to_host(res.slab, res.shapes), copy=False)
+    else:
+        tt = TTTensor(_cores_to_host(res.cores), copy=False)
     report = DecompositionReport(
         shape=a.shape, nnz=a.nnz, pivot=res.pivot, mode=mode, eps=eps, num_fibers=res.num_fibers,
         ranks_lossless=res.ranks_lossless, ranks=tt.ranks[1:-1], eps_actual=res.eps_actual,

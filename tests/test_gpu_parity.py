@@ -675,3 +675,56 @@ def test_native_sweep_matches_python_driver(monkeypatch):
             assert rep_n.ranks == rep_p.ranks, run["tag"]
             for a, b in zip(tt_n.cores, tt_p.cores):
                 assert np.array_equal(a, b), run["tag"]
+
+
+def test_fused_driver_matches_stepwise(monkeypatch):
+    """fasttt() in one native call (ftt_fasttt_lin) against the step-by-step
+    orchestration of the same kernels from pipeline.py: the same pivot, the
+    same lossless and final ranks, bit-identical cores and the same report
+    fields, on the small reference suite (static / dynamic, explicit and auto
+    pivots, a rank-0 truncation) and on configs 1 and 2."""
+    g = load_golden("small")
+    assert g is not None
+    cases, z = g
+    todo = []
+    for case in cases[:16]:
+        if "runs" not in case:
+            continue
+        i = case["id"]
+        t = ft.SparseTensor(case["shape"], z[f"t{i}_coords"], z[f"t{i}_values"])
+        for run in case["runs"]:
+            if run["mode"] in ("static", "dynamic"):
+                todo.append((t, dict(eps=run["eps"], pivot=run["pivot"], mode=run["mode"]),
+                             run["tag"]))
+        todo.append((t, dict(eps=1e-8), f"t{i} auto"))
+        todo.append((t, dict(eps=0.999999, pivot=0), f"t{i} loose"))
+    for cfg in (1, 2):
+        shape, coords, vals, eps = G.gen_config(cfg)
+        todo.append((ft.SparseTensor(shape, coords, vals), dict(eps=eps), f"c{cfg}"))
+    fused_calls = []
+    real = P._fasttt_fused
+
+    def spy(*a, **k):
+        r = real(*a, **k)
+        fused_calls.append(r is not None)
+        return r
+
+    monkeypatch.setattr(P, "_fasttt_fused", spy)
+    for t, kw, tag in todo:
+        monkeypatch.setattr(P, "_STEPWISE", True)
+        tt_s, rep_s = ft.fasttt(t, **kw)
+        monkeypatch.setattr(P, "_STEPWISE", False)
+        n0 = len(fused_calls)
+        tt_f, rep_f = ft.fasttt(t, **kw)
+        assert fused_calls[n0:] == [True], tag
+        assert rep_f.pivot == rep_s.pivot, tag
+        assert rep_f.num_fibers == rep_s.num_fibers, tag
+        assert tuple(rep_f.ranks_lossless) == tuple(rep_s.ranks_lossless), tag
+        assert tuple(rep_f.ranks) == tuple(rep_s.ranks), tag
+        assert rep_f.eps_actual_method == rep_s.eps_actual_method, tag
+        assert rep_f.eps_actual == rep_s.eps_actual, tag
+        assert rep_f.eps_actual_inner == rep_s.eps_actual_inner, tag
+        assert rep_f.flops_fasttt_model == rep_s.flops_fasttt_model, tag
+        assert tuple(rep_f.warnings) == tuple(rep_s.warnings), tag
+        for a, b in zip(tt_f.cores, tt_s.cores):
+            assert a.shape == b.shape and np.array_equal(a, b), tag
