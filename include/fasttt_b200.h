@@ -438,6 +438,11 @@ int ftt_sweep_rounding(ftt_ctx *ctx, int32_t d, int32_t pivot,
 /* Release a device buffer returned by ftt_sweep_rounding (stream-ordered). */
 int ftt_free_device(ftt_ctx *ctx, void *p);
 
+/* How many truncation steps of this process ran the certified low-rank
+ * path on a scattered carry's compact form and were accepted (the operand
+ * of fasttt.py:334-341 after a 0/1 core, never materialised; test probe). */
+int64_t ftt_scatter_steps(void);
+
 /* ------------------------------------------------------- fasttt driver */
 /* What ftt_fasttt_lin hands back.  Device buffers the caller releases with
  * ftt_free_device: fiber_slab (fixed_lin, indptr, fiber_of, pivot_index,

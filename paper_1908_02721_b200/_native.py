@@ -94,6 +94,7 @@ SIGNATURES = {
     "ftt_sweep_rounding": [_c_p, _c_i32, _c_i32, _c_p, _c_p, _c_i32, _c_d, _c_d, _c_d, _c_p,
                            _c_i32, _c_p, _c_p, ctypes.POINTER(ctypes.c_int32)],
     "ftt_free_device": [_c_p, _c_p],
+    "ftt_scatter_steps": [],
     "ftt_fasttt_lin": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, _c_i32, _c_d, _c_d,
                        _c_i32, _c_p, _c_p],
     "ftt_delinearize": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_p],
@@ -110,6 +111,7 @@ _RESTYPES = {
     "ftt_version": ctypes.c_char_p,
     "ftt_last_error": ctypes.c_char_p,
     "ftt_kernel_launches": ctypes.c_int64,
+    "ftt_scatter_steps": ctypes.c_int64,
     "ftt_free_host": None,
 }
 

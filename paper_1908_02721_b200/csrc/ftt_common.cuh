@@ -70,6 +70,10 @@ struct ftt_ctx {
   // deferred status checks: narrow-QR non-finite flags OR into `sticky`
   // (device int) instead of a host round trip per call (ftt_take_status)
   bool defer_checks = false;
+  // ||A||_F^2 of the next low-rank operand when the caller knows it (the
+  // sweep driver: a scattered carry keeps the norm of S V^T); consumed and
+  // cleared by the next ftt_svd_lowrank* call
+  double fro2_hint = 0.0;
   // host round trips (copy_to_host) and the host time spent blocked in them
   int64_t syncs = 0;
   double sync_wait_ms = 0.0;

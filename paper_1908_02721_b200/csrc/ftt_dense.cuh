@@ -86,6 +86,29 @@ int sparse_qt_a(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, do
 int sparse_resid(ftt_ctx *ctx, SparseOperand &op, int64_t kr, const double *Q, const double *B,
                  double *out_dev);
 
+// Scattered operand of a right-sweep step (ftt_scatter.cu): carry V (K x r,
+// col-major, ld ldv) times a 0/1 core given by its kept rows (K ascending
+// values i * mA + c'), as A_tall (mA x r n): A_tall[c', a n + i] = V[c, a].
+struct ScatterOperand {
+  int64_t mA = 0, n = 0, r = 0, K = 0;
+  const int64_t *kept = nullptr;
+  const double *V = nullptr;
+  int64_t ldv = 0;
+  int32_t *pos = nullptr;   // n x mA: entry at (i, c') or -1 (scatter_operand_build)
+  int64_t *iptr = nullptr;  // n + 1: first entry of each block column
+};
+bool scatter_operand_ok(int64_t mA, int64_t n, int64_t r, int64_t K);
+int scatter_operand_build(ftt_ctx *ctx, ScatterOperand *op);
+void scatter_operand_free(ftt_ctx *ctx, ScatterOperand *op);
+int scatter_sketch(ftt_ctx *ctx, const ScatterOperand &op, int64_t k, double *Y);
+int scatter_qt_a(ftt_ctx *ctx, const ScatterOperand &op, int64_t kr, const double *Q, double *B);
+int scatter_resid(ftt_ctx *ctx, const ScatterOperand &op, int64_t kr, const double *Q,
+                  const double *B, double *out_dev);
+// The certified low-rank path (ftt_svd.cu) on a scattered operand: M is
+// (r n) x mA row-major, m = r n < mA; same outputs as ftt_svd_lowrank_f64.
+int svd_lowrank_scatter(ftt_ctx *ctx, ScatterOperand *op, int64_t k, double delta2, double *s_host,
+                        double *rest2_host, int32_t *accepted);
+
 int check_finite(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, bool *ok);
 int copy_matrix(ftt_ctx *ctx, int64_t m, int64_t n, const double *src, int64_t lds, double *dst,
                 int64_t ldd);

@@ -228,7 +228,9 @@ int run(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz, int
     right = denom != 0.0 ? sqrt((double)(d - 1 - pivot)) / denom * eps * pnorm : 0.0;
     left = denom != 0.0 ? sqrt((double)pivot) / denom * eps * pnorm : 0.0;
   }
-  // ---- rounding sweeps (fasttt.py:324-356)
+  // ---- rounding sweeps (fasttt.py:324-356); the sparse first step's
+  // operand norm is ||a||^2, already on the host
+  if (pc.kind == 3 && na2 > 0.0) ctx->fro2_hint = na2;
   double *out[32];
   int32_t zero = 0;
   FTT_CHECK(ftt_sweep_rounding(ctx, d, pivot, descs.data(), &sp, mode, delta, left, right, nullptr,

@@ -17,6 +17,7 @@
 // the accumulated 32x32 rotation to the pair's columns of X and P.  A sweep
 // with no rotation anywhere ends the iteration.
 #include <algorithm>
+#include <atomic>
 #include <numeric>
 #include <vector>
 
@@ -1125,6 +1126,7 @@ using namespace ftt;
 extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
                            int32_t a_row_major, double *s_host) {
   if (!ctx || m < 0 || n < 0) return FTT_ERR_INVALID;
+  ctx->fro2_hint = 0.0;
   svd_state_free(ctx);
   SvdState *st = new SvdState();
   ctx->svd = st;
@@ -1137,8 +1139,13 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
 // the entries of a sparse one (sp != nullptr, ftt_sparse.cu).
 static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda,
                        int32_t a_row_major, SparseOperand *sp, int64_t k, double delta2,
-                       double *s_host, double *rest2_host, int32_t *accepted) {
+                       double *s_host, double *rest2_host, int32_t *accepted,
+                       ScatterOperand *sc = nullptr) {
   if (!ctx || m < 0 || n < 0 || !accepted || !rest2_host) return FTT_ERR_INVALID;
+  // ||A||_F^2 when the caller knows it (consumed here)
+  const double fro2_known = ctx->fro2_hint;
+  ctx->fro2_hint = 0.0;
+  const bool have_fro2 = fro2_known > 0.0 && std::isfinite(fro2_known);
   svd_state_free(ctx);
   SvdState *st = new SvdState();
   ctx->svd = st;
@@ -1152,7 +1159,7 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   *accepted = 0;
   *rest2_host = -1.0;
   if (nA == 0 || k <= 0 || k >= nA) return FTT_OK;
-  if (sp && k > 64) return FTT_OK;  // sparse products handle sketches <= 64 wide
+  if ((sp || sc) && k > 64) return FTT_OK;  // sparse products handle sketches <= 64 wide
   // The tall view A_tall (mA x nA) is read straight from the caller's buffer:
   // `buf` col-major with leading dimension `ld`, stored transposed when
   // `need_t`.  A strided (non-packed) input is packed once first.
@@ -1165,8 +1172,16 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   double *fro2_dev = nullptr;
   FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 3)));
   double *rest2_dev = fro2_dev + kSumSqBlocks + 2;  // after sum_squares' partials
-  if (sp) {
-    FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->v_r, fro2_dev + 1, fro2_dev));
+  if (sc) {
+    if (!have_fro2) {
+      if (sc->ldv != sc->K) {
+        set_error("scattered operand: strided carry without a known norm");
+        return FTT_ERR_INVALID;
+      }
+      FTT_CHECK(sum_squares_dev(ctx, sc->K * sc->r, sc->V, fro2_dev + 1, fro2_dev));
+    }
+  } else if (sp) {
+    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->v_r, fro2_dev + 1, fro2_dev));
   } else {
     const int64_t inner = need_t ? nA : mA;
     if (lda != inner) {
@@ -1175,11 +1190,11 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
       buf = st->Af;
       ld = inner;
     }
-    FTT_CHECK(sum_squares_dev(ctx, mA * nA, buf, fro2_dev + 1, fro2_dev));
+    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, mA * nA, buf, fro2_dev + 1, fro2_dev));
   }
   auto finite_or_decline = [&]() -> int {
     // non-finite energy: either a non-finite entry (error) or an overflow
-    if (sp) return FTT_OK;  // entries are validated finite: overflow, full SVD decides
+    if (sp || sc) return FTT_OK;  // entries are validated finite: overflow, full SVD decides
     bool ok = true;
     FTT_CHECK(check_finite(ctx, need_t ? nA : mA, need_t ? mA : nA, buf, ld, &ok));
     if (!ok) {
@@ -1192,11 +1207,13 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   FTT_CHECK(owned_alloc(ctx, (void **)&Yk, 8 * (size_t)mA * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Qk, 8 * (size_t)mA * k));
   FTT_CHECK(owned_alloc(ctx, (void **)&st->Bk, 8 * (size_t)k * nA));
-  const size_t ske = sp ? 1 : std::max({gemm_splitk_elems(mA, k, nA), gemm_splitk_elems(k, nA, mA),
+  const size_t ske = (sp || sc) ? 1 : std::max({gemm_splitk_elems(mA, k, nA), gemm_splitk_elems(k, nA, mA),
                                         gemm_splitk_elems(mA, nA, k), (size_t)1});
   FTT_CHECK(owned_alloc(ctx, (void **)&sk, 8 * ske));
   // range finder: Y = A Omega, Q = qr(Y), B = Q^T A, residual A - Q B (in place)
-  if (sp) {
+  if (sc) {
+    FTT_CHECK(scatter_sketch(ctx, *sc, k, Yk));
+  } else if (sp) {
     FTT_CHECK(sparse_sketch(ctx, *sp, k, Yk));
   } else {
     FTT_CHECK(owned_alloc(ctx, (void **)&Om, 8 * (size_t)nA * k));
@@ -1213,7 +1230,8 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
     int64_t kr = 0;
     int64_t *sel = nullptr;
     FTT_CHECK(owned_alloc(ctx, (void **)&sel, 8 * (size_t)k));
-    FTT_CHECK(sketch_rank(ctx, mA, k, Yk, 1e-11, sel, &kr, fro2_dev, &fro2));
+    FTT_CHECK(sketch_rank(ctx, mA, k, Yk, 1e-11, sel, &kr, have_fro2 ? nullptr : fro2_dev, &fro2));
+    if (have_fro2) fro2 = fro2_known;
     if (kr == 0 || !std::isfinite(fro2)) {
       owned_free(ctx, sel);
       owned_free(ctx, Om);
@@ -1232,7 +1250,8 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
     owned_free(ctx, sel);
     k = kr;
   } else {
-    FTT_CHECK(copy_to_host(ctx, &fro2, fro2_dev, sizeof(double)));
+    if (have_fro2) fro2 = fro2_known;
+    else FTT_CHECK(copy_to_host(ctx, &fro2, fro2_dev, sizeof(double)));
     if (!std::isfinite(fro2)) {
       owned_free(ctx, Om);
       owned_free(ctx, Yk);
@@ -1250,7 +1269,8 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
     FTT_CHECK(launch_identity(ctx, mA, k, st->Qk, mA));
     FTT_CHECK(qr_apply_q(ctx, mA, k, Yk, mA, Tb, k, st->Qk, mA, ws, wse));
   }
-  if (sp) FTT_CHECK(sparse_qt_a(ctx, *sp, k, st->Qk, st->Bk));
+  if (sc) FTT_CHECK(scatter_qt_a(ctx, *sc, k, st->Qk, st->Bk));
+  else if (sp) FTT_CHECK(sparse_qt_a(ctx, *sp, k, st->Qk, st->Bk));
   else FTT_CHECK(gemm(ctx, 1, need_t, k, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, k, sk, ske));
   // A narrow B (k <= 64) is factored speculatively before the certificate is
   // read: the residual energy then comes back with the singular values in
@@ -1258,7 +1278,8 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   const bool speculate = tsqr_ok(std::max(k, nA), std::min(k, nA)) &&
                          !getenv("FTT_NO_SPECULATE");
   if (speculate) {
-    if (sp) FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
+    if (sc) FTT_CHECK(scatter_resid(ctx, *sc, k, st->Qk, st->Bk, rest2_dev));
+    else if (sp) FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
     else FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
                                     nullptr, rest2_dev));
     st->inner = new SvdState();
@@ -1269,8 +1290,9 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
       st->inner = nullptr;
       FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
     }
-  } else if (sp) {
-    FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
+  } else if (sp || sc) {
+    if (sc) FTT_CHECK(scatter_resid(ctx, *sc, k, st->Qk, st->Bk, rest2_dev));
+    else FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
     FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
   } else {
     FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
@@ -1315,6 +1337,27 @@ extern "C" int ftt_svd_lowrank_f64(ftt_ctx *ctx, int64_t m, int64_t n, const dou
   return lowrank_run(ctx, m, n, A, lda, a_row_major, nullptr, k, delta2, s_host, rest2_host,
                      accepted);
 }
+
+static std::atomic<int64_t> g_scatter_steps{0};
+
+int ftt::svd_lowrank_scatter(ftt_ctx *ctx, ScatterOperand *op, int64_t k, double delta2,
+                             double *s_host, double *rest2_host, int32_t *accepted) {
+  const int64_t m = op->r * op->n, n = op->mA;
+  if (!ctx || !accepted || !rest2_host || m >= n || !scatter_operand_ok(op->mA, op->n, op->r, op->K)) {
+    set_error("svd_lowrank_scatter: invalid operand");
+    return FTT_ERR_INVALID;
+  }
+  *accepted = 0;
+  *rest2_host = -1.0;
+  FTT_CHECK(scatter_operand_build(ctx, op));
+  const int rc = lowrank_run(ctx, m, n, nullptr, 0, 1, nullptr, k, delta2, s_host, rest2_host,
+                             accepted, op);
+  scatter_operand_free(ctx, op);
+  if (rc == FTT_OK && *accepted) ++g_scatter_steps;
+  return rc;
+}
+
+extern "C" int64_t ftt_scatter_steps(void) { return g_scatter_steps.load(); }
 
 extern "C" int ftt_svd_lowrank_sparse_f64(ftt_ctx *ctx, int64_t m, int64_t n, int64_t nnz,
                                           const int64_t *fiber_of, const int64_t *pivot_index,

@@ -14,7 +14,9 @@
 
 #include <vector>
 
-#include "ftt_common.cuh"
+#include <stdlib.h>
+
+#include "ftt_dense.cuh"
 #include "../../include/fasttt_b200.h"
 
 namespace ftt {
@@ -78,13 +80,23 @@ double tail_error(const std::vector<double> &s, int64_t rank, double rest2) {
 }
 
 struct Core {
-  int kind = 0;  // 0 dense, 1 side L, 2 side R, 3 sparse pivot
+  // 0 dense, 1 side L, 2 side R, 3 sparse pivot, 4 side R times a carry kept
+  // unscattered (sv: K x r0 col-major, ld K; ftt_scatter.cu)
+  int kind = 0;
   int64_t r0 = 0, n = 0, r1 = 0;
   double *data = nullptr;
   bool owned = false;  // allocated here (freed when replaced)
   const int64_t *kept = nullptr;
   int64_t K = 0, r_other = 0;
+  double *sv = nullptr;
 };
+
+// Dense operands at least this large (elements) stay unscattered for the
+// low-rank path of the next step (FTT_SCATTER_MIN overrides: tests).
+int64_t scatter_min_elems() {
+  const char *e = getenv("FTT_SCATTER_MIN");
+  return e ? atoll(e) : ((int64_t)1 << 22);
+}
 
 struct Driver {
   ftt_ctx *ctx;
@@ -124,6 +136,8 @@ struct Driver {
   }
   void release(Core &c) {
     if (c.owned && c.data) cudaFreeAsync(c.data, ctx->stream);
+    if (c.sv) drop(c.sv);
+    c.sv = nullptr;
     c.data = nullptr;
     c.owned = false;
   }
@@ -147,6 +161,8 @@ struct Driver {
     if (c.kind == 3) {
       FTT_CHECK(ftt_pivot_core_scatter(ctx, sp->nnz, sp->fiber_of, sp->pivot_index, sp->values,
                                        sp->t_map, sp->s_map, c.r0, c.n, c.r1, buf, nullptr));
+    } else if (c.kind == 4) {
+      FTT_CHECK(ftt_scatter_cols(ctx, c.r0, c.K, c.kept, c.sv, c.K, c.n * c.r1, buf));
     } else {
       FTT_CHECK(ftt_side_core_dense(ctx, c.kind == 1 ? 0 : 1, c.kept, c.K, c.n, c.r_other, buf));
     }
@@ -180,6 +196,16 @@ struct Driver {
           FTT_CHECK(ftt_svd_lowrank_sparse_f64(ctx, m, n, sp->nnz, sp->fiber_of, sp->pivot_index,
                                                sp->values, sp->t_map, sp->s_map, c.n, kk,
                                                dlt * dlt, sv.data(), &r2, &acc));
+        } else if (c.kind == 4) {
+          ScatterOperand so;
+          so.mA = c.r1;
+          so.n = c.n;
+          so.r = c.r0;
+          so.K = c.K;
+          so.kept = c.kept;
+          so.V = c.sv;
+          so.ldv = c.K;
+          FTT_CHECK(svd_lowrank_scatter(ctx, &so, kk, dlt * dlt, sv.data(), &r2, &acc));
         } else {
           FTT_CHECK(ftt_svd_lowrank_f64(ctx, m, n, c.data, row_major ? n : m, row_major ? 1 : 0,
                                         kk, dlt * dlt, sv.data(), &r2, &acc));
@@ -194,6 +220,7 @@ struct Driver {
         }
       }
     }
+    ctx->fro2_hint = 0.0;
     if (cs[k].kind != 0) FTT_CHECK(densify(k));
     const int64_t mn = std::min(m, n);
     s->assign(std::max<int64_t>(mn, 1), 0.0);
@@ -231,6 +258,10 @@ struct Driver {
   int run(int32_t *zero) {
     *zero = 0;
     int64_t hint = -1;
+    // ||operand||_F^2 of a step whose operand is a scattered carry S V^T:
+    // the retained singular values' squares (V has orthonormal columns)
+    double fro2_next = 0.0;
+    const int64_t sc_min = scatter_min_elems();
     for (int k = pivot; k < d - 1; ++k) {  // fasttt.py:334-341
       Core &C = cs[k];
       const int64_t r0 = C.r0, n = C.n, r1 = C.r1, m = r0 * n;
@@ -238,7 +269,10 @@ struct Driver {
       const bool hd = step_delta(true, k, &dl);
       std::vector<double> s;
       double rest2 = 0.0;
+      if (fro2_next > 0.0) ctx->fro2_hint = fro2_next;
+      fro2_next = 0.0;
       FTT_CHECK(values(k, m, r1, true, hd, dl, hint, policy == 0 && interval_ok, &s, &rest2));
+      ctx->fro2_hint = 0.0;
       const int64_t rank = decide(true, k, s, m, r1, rest2);
       hint = rank;
       if (rank == 0) {
@@ -253,6 +287,27 @@ struct Driver {
       Core &N = cs[k + 1];
       double *nw = nullptr;
       if (N.kind == 1 || N.kind == 2) {
+        if (N.K == r1)
+          for (int64_t i = 0; i < rank; ++i) fro2_next += s[i] * s[i];
+        // the next step's operand (rank n x r_other): left unscattered when
+        // its low-rank path can run on the compact form (ftt_scatter.cu)
+        double dn = 0.0;
+        const int64_t mn2 = rank * N.n;
+        const bool defer = N.kind == 2 && k + 1 < d - 1 && N.K == r1 && mn2 < N.r_other &&
+                           mn2 * N.r_other >= sc_min && step_delta(true, k + 1, &dn) && dn > 0.0 &&
+                           lowrank_k(mn2, rank) > 0 &&
+                           scatter_operand_ok(N.r_other, N.n, rank, N.K);
+        if (defer) {
+          Core c4 = N;
+          c4.kind = 4;
+          c4.r0 = rank;
+          c4.r1 = N.r_other;
+          c4.sv = V;
+          c4.data = nullptr;
+          c4.owned = false;
+          cs[k + 1] = c4;
+          continue;  // V lives on as the core's carry
+        }
         FTT_CHECK(alloc(&nw, (size_t)rank * N.n * N.r_other));
         FTT_CHECK(ftt_scatter_cols(ctx, rank, N.K, N.kept, V, r1, N.n * N.r_other, nw));
         const int64_t nn = N.n, ro = N.r_other;
@@ -267,6 +322,7 @@ struct Driver {
       }
       drop(V);
     }
+    fro2_next = 0.0;
     for (int k = d - 1; k > pivot; --k) {  // fasttt.py:342-347
       FTT_CHECK(densify(k));
       const int64_t r0 = cs[k].r0, n = cs[k].n, r1 = cs[k].r1;
@@ -291,7 +347,10 @@ struct Driver {
       const bool hd = step_delta(false, k, &dl);
       std::vector<double> s;
       double rest2 = 0.0;
+      if (fro2_next > 0.0) ctx->fro2_hint = fro2_next;
+      fro2_next = 0.0;
       FTT_CHECK(values(k, m, r0, false, hd, dl, hint, policy == 0 && interval_ok, &s, &rest2));
+      ctx->fro2_hint = 0.0;
       const int64_t rank = decide(false, k, s, m, r0, rest2);
       hint = rank;
       if (rank == 0) {
@@ -306,6 +365,8 @@ struct Driver {
       Core &Pv = cs[k - 1];
       double *nw = nullptr;
       if (Pv.kind == 1 || Pv.kind == 2) {
+        if (Pv.K == r0)
+          for (int64_t i = 0; i < rank; ++i) fro2_next += s[i] * s[i];
         FTT_CHECK(alloc(&nw, (size_t)Pv.r_other * Pv.n * rank));
         FTT_CHECK(ftt_scatter_rows(ctx, Pv.K, rank, Pv.kept, V, rank, Pv.r_other * Pv.n, nw));
         const int64_t ro = Pv.r_other, nn = Pv.n;

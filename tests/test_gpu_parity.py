@@ -728,3 +728,31 @@ def test_fused_driver_matches_stepwise(monkeypatch):
         assert tuple(rep_f.warnings) == tuple(rep_s.warnings), tag
         for a, b in zip(tt_f.cores, tt_s.cores):
             assert a.shape == b.shape and np.array_equal(a, b), tag
+
+
+@pytest.mark.parametrize("dims,R,s,pivot", [((24,) * 6, 5, 3, 1), ((12, 40, 9, 6, 16, 20), 4, 4, 1),
+                                            ((8, 6, 40, 40, 40), 6, 3, 0)])
+def test_scattered_carry_matches_dense(dims, R, s, pivot, monkeypatch):
+    """Right-sweep steps whose operand is a carry times a 0/1 core run the
+    certified low-rank path on the compact (unscattered) form
+    (ftt_scatter.cu).  Forced on at small sizes (FTT_SCATTER_MIN=1) and
+    compared with the dense-operand path (FTT_SCATTER_MIN huge): the same
+    ranks, entries within 1e-10; and the forced run is repeatable bit for
+    bit (fixed summation orders)."""
+    t = _rank_r_sparse(dims, R, s, seed=7)
+    probe_rng = np.random.default_rng(11)
+    probe = np.concatenate([t.coords[:20000],
+                            np.stack([probe_rng.integers(0, n, 4000) for n in dims], 1)])
+    monkeypatch.setenv("FTT_SCATTER_MIN", str(1 << 60))
+    tt_d, rep_d = ft.fasttt(t, eps=1e-9, pivot=pivot)
+    monkeypatch.setenv("FTT_SCATTER_MIN", "1")
+    from paper_1908_02721_b200 import _native as nat
+    n0 = nat.lib().ftt_scatter_steps()
+    tt_s, rep_s = ft.fasttt(t, eps=1e-9, pivot=pivot)
+    assert nat.lib().ftt_scatter_steps() > n0, "the scattered path did not run"
+    tt_s2, _ = ft.fasttt(t, eps=1e-9, pivot=pivot)
+    assert tuple(rep_s.ranks) == tuple(rep_d.ranks)
+    assert rel_err(ft.tt_entries(tt_s, probe), ft.tt_entries(tt_d, probe)) <= RECON_TOL
+    assert rel_err(ft.tt_entries(tt_s, t.coords), t.values) <= 1e-8
+    for a, b in zip(tt_s.cores, tt_s2.cores):
+        assert np.array_equal(a, b)

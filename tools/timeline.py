@@ -73,6 +73,12 @@ for (a, b), g in sorted(gap_at.items(), key=lambda x: -x[1])[:ngaps]:
         agg[nm] = agg.get(nm, 0.0) + dt
     top = sorted(agg.items(), key=lambda x: -x[1])[:4]
     print(f"  gap {g:8.1f} us  runtime calls inside: {len(inside)}  top {top}")
+if "--gapdetail" in sys.argv:
+    for (a, b), g in sorted(gap_at.items(), key=lambda x: -x[1])[3:7]:
+        print(f"  -- gap {g:.1f} us: host API calls from 15 us before its start to its end")
+        for x in api:
+            if x[1] > a - 15 and x[0] < b:
+                print(f"     t={x[0] - a:8.1f} dur={x[1] - x[0]:7.1f}  {x[2]}")
 for g, p, n in gaps[:ngaps]:
     print(f"  gap {g:8.1f} us  after {str(p)[:60]:60s} before {str(n)[:60]}")
 by = {}
