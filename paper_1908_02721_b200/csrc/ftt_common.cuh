@@ -62,6 +62,7 @@ struct ftt_ctx {
   int64_t launches = 0;
   int num_sms = ftt::kNumSMs;
   void *pinned = nullptr;  // small pinned host scratch (64 KiB)
+  unsigned post_seq = 0;   // sequence word of the last k_post (copy_to_host)
   // pinned ring for stream-ordered host->device staging without a sync
   // (stage_to_device); one event fences the latest staged copy
   char *ring = nullptr;
