@@ -128,6 +128,32 @@ constexpr size_t CQ_SMEM = sizeof(double) * CQ_MAX * (CQ_MAX + 1);
 // Numerical rank r of the sketch Y (mA x k, ld mA) from a pivoted Cholesky
 // of Y^T Y (relative pivot cutoff tau) and the pivot order (sel_dev[0..r)
 // are the columns of a well-conditioned spanning subset).
+// The same factorisation without the host round trip: the rank word lands in
+// *rank_dev (a device int the caller reads back later with other results).
+int sketch_rank_async(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau,
+                      int64_t *sel_dev, int *rank_dev) {
+  if (k <= 0 || k > CQ_MAX) {
+    set_error("sketch_rank: k out of range");
+    return FTT_ERR_INVALID;
+  }
+  static bool attr = false;
+  if (!attr) {
+    FTT_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)CQ_SMEM));
+    attr = true;
+  }
+  const size_t ske = std::max(gemm_splitk_elems(k, k, mA), (size_t)1);
+  double *blk = nullptr;  // G (k x k) | split-K space
+  FTT_CHECK(owned_alloc(ctx, (void **)&blk, 8 * ((size_t)k * k + ske)));
+  double *G = blk, *sk = G + (size_t)k * k;
+  FTT_CHECK(gemm(ctx, 1, 0, k, k, mA, 1.0, Y, mA, Y, mA, 0.0, G, k, sk, ske));
+  k_chol_inv<<<1, CQ_NT, CQ_SMEM, ctx->stream>>>((int)k, G, k, tau, rank_dev, sel_dev, nullptr,
+                                                 nullptr);
+  FTT_LAUNCHED(ctx);
+  owned_free(ctx, blk);
+  return FTT_OK;
+}
+
 int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau, int64_t *sel_dev,
                 int64_t *rank, const double *aux_dev, double *aux_host) {
   *rank = 0;

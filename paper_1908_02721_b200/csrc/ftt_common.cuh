@@ -75,6 +75,12 @@ struct ftt_ctx {
   // sweep driver: a scattered carry keeps the norm of S V^T); consumed and
   // cleared by the next ftt_svd_lowrank* call
   double fro2_hint = 0.0;
+  // the rank the next low-rank operand is expected to have (the previous
+  // step's, set by the sweep driver): the sketch's numerical rank is then
+  // read back with the singular values instead of in its own round trip and
+  // the step redone if it differs (which also clears spec_ok for the sweep)
+  int64_t rank_hint = 0;
+  bool spec_ok = true;
   // host round trips (copy_to_host) and the host time spent blocked in them
   int64_t syncs = 0;
   double sync_wait_ms = 0.0;

@@ -52,6 +52,10 @@ int qrcp_factor(ftt_ctx *ctx, int64_t n, double *B, double *Out, double *tau, in
 int sketch_rank(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau, int64_t *sel_dev,
                 int64_t *rank, const double *aux_dev = nullptr, double *aux_host = nullptr);
 
+// Without the round trip: the rank word goes to *rank_dev (device).
+int sketch_rank_async(ftt_ctx *ctx, int64_t mA, int64_t k, const double *Y, double tau,
+                      int64_t *sel_dev, int *rank_dev);
+
 // Sparse operand of the first truncation step (ftt_sparse.cu): the entries
 // of the pivot core as A_tall (mA x nA = M or M^T) in CSR (by row) and CSC
 // (by column, rows ascending) order.

@@ -1346,16 +1346,16 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, i
 
 int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda, int trans,
              double *U, int64_t ldu, double *Y, double *norms_host, int *sweeps,
-             const double *extra_dev, double *extra_host) {
+             const double *extra_dev, double *extra_host, int extra_n) {
   const int n = (int)n64;
   FTT_CHECK(set_attrs());
-  // status (2 ints) | norms n | R n x n | P n x n
   double *dev = nullptr;
-  // status (2 ints) | extra | norms n | R n x n | P n x n
-  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n + 2 * (size_t)n * n)));
+  // status (2 ints) | extra | norms n | extras 1..3, pad | R n x n | P n x n
+  // (R keeps the 16-byte alignment it had without the extras)
+  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n + 4 + 2 * (size_t)n * n)));
   int *status = reinterpret_cast<int *>(dev);
   double *norms = dev + 2;
-  double *R = norms + n;
+  double *R = norms + n + 4;
   double *P = R + (size_t)n * n;
   FTT_CUDA(cudaMemsetAsync(status, 0, 16, ctx->stream));
   Tree t;
@@ -1394,12 +1394,20 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n64, const double *A, int64_t lda,
   if (W) owned_free(ctx, W);
   for (double *p : qs) owned_free(ctx, p);
   // one round trip: status, the caller's device scalar and the norms
-  if (extra_dev)
+  const int xn = extra_dev ? std::max(1, std::min(extra_n, 4)) : 1;
+  if (extra_dev) {
     FTT_CUDA(cudaMemcpyAsync(dev + 1, extra_dev, sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
-  std::vector<double> h(n + 2);
-  FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));
-  if (extra_dev && extra_host) *extra_host = h[1];
+    if (xn > 1)
+      FTT_CUDA(cudaMemcpyAsync(dev + 2 + n, extra_dev + 1, sizeof(double) * (xn - 1),
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  std::vector<double> h(n + 2 + 3);
+  FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 1 + xn)));
+  if (extra_dev && extra_host) {
+    extra_host[0] = h[1];
+    for (int x = 1; x < xn; ++x) extra_host[x] = h[n + 1 + x];
+  }
   owned_free(ctx, dev);
   int st[2];
   memcpy(st, h.data(), 8);
@@ -1426,9 +1434,9 @@ bool direct_small_ok(int64_t m, int64_t n) {
 // (unsorted) -- the outputs of tsqr_svd.
 int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, int trans,
                      double *U, double *Yt, double *norms_host, int *sweeps,
-                     const double *extra_dev, double *extra_host) {
-  double *dev = nullptr;  // status (2 ints) | extra | norms n
-  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n)));
+                     const double *extra_dev, double *extra_host, int extra_n) {
+  double *dev = nullptr;  // status (2 ints) | extra | norms n | extras 1..3
+  FTT_CHECK(owned_alloc(ctx, (void **)&dev, 8 * (size_t)(2 + n + 3)));
   int *status = reinterpret_cast<int *>(dev);
   const int max_sweeps = 60;
   const size_t smem = 8 * (size_t)(n <= 8 ? 8 : 16) * SV_NT;
@@ -1444,9 +1452,16 @@ int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_
   }
 #undef FTT_SVD_WY
   FTT_LAUNCHED(ctx);
-  std::vector<double> h(n + 2);
-  FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 2)));
-  if (extra_dev && extra_host) *extra_host = h[1];
+  const int xn = extra_dev ? std::max(1, std::min(extra_n, 4)) : 1;
+  if (extra_dev && xn > 1)
+    FTT_CUDA(cudaMemcpyAsync(dev + 2 + n, extra_dev + 1, sizeof(double) * (xn - 1),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+  std::vector<double> h(n + 2 + 3);
+  FTT_CHECK(copy_to_host(ctx, h.data(), dev, 8 * (size_t)(n + 1 + xn)));
+  if (extra_dev && extra_host) {
+    extra_host[0] = h[1];
+    for (int x = 1; x < xn; ++x) extra_host[x] = h[n + 1 + x];
+  }
   owned_free(ctx, dev);
   int st[2];
   memcpy(st, h.data(), 8);

@@ -16,10 +16,10 @@ int tsqr_q(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int
 // Thin SVD core: U = Q P (M x n, ld ldu), Y = R^T P (n x n), norms_host[j] =
 // ||Y_j|| (unsorted; sigma up to the caller's permutation).  One host round
 // trip, which also brings back the caller's device scalar extra_dev (if any)
-// into *extra_host.
+// into *extra_host (extra_n consecutive doubles, 1 <= extra_n <= 4).
 int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, int trans, double *U,
              int64_t ldu, double *Y, double *norms_host, int *sweeps,
-             const double *extra_dev = nullptr, double *extra_host = nullptr);
+             const double *extra_dev = nullptr, double *extra_host = nullptr, int extra_n = 1);
 
 // Short tall operands (n <= 16, A_tall and its reflectors fit in shared
 // memory): the tsqr_svd factorisation in one CTA (k_jacobi_qr).  U = Q P
@@ -27,6 +27,7 @@ int tsqr_svd(ftt_ctx *ctx, int64_t M, int64_t n, const double *A, int64_t lda, i
 bool direct_small_ok(int64_t m, int64_t n);
 int direct_small_svd(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int64_t lda, int trans,
                      double *U, double *Yt, double *norms_host, int *sweeps,
-                     const double *extra_dev = nullptr, double *extra_host = nullptr);
+                     const double *extra_dev = nullptr, double *extra_host = nullptr,
+                     int extra_n = 1);
 
 }  // namespace ftt

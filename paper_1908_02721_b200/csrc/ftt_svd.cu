@@ -723,7 +723,7 @@ namespace {
 // A_tall (U = Y / sigma) may be used for short narrow operands.
 int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A, int64_t lda,
                int32_t a_row_major, const double *extra_dev = nullptr,
-               double *extra_host = nullptr, bool allow_direct = false) {
+               double *extra_host = nullptr, bool allow_direct = false, int extra_n = 1) {
   st->m = m;
   st->n = n;
   st->transposed = m < n;
@@ -746,7 +746,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     std::vector<double> raw(nA);
     const int pb = prof_begin(ctx);
     FTT_CHECK(direct_small_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, st->Y, raw.data(),
-                               &st->sweeps, extra_dev, extra_host));
+                               &st->sweeps, extra_dev, extra_host, extra_n));
     // QR (2 m n^2) + Q P (2 m n^2) + sweeps x n^2/2 pairs x 6 n
     prof_end(ctx, pb, PT_JACOBI, 8.0 * ((double)mA * nA * 2 + (double)nA * nA),
              4.0 * (double)mA * nA * nA + 3.0 * std::max(st->sweeps, 1) * (double)nA * nA * nA);
@@ -768,7 +768,7 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     std::vector<double> raw(nA);
     const int pb = prof_begin(ctx);
     FTT_CHECK(tsqr_svd(ctx, mA, nA, A, lda, need_t ? 1 : 0, st->Af, mA, st->Y, raw.data(),
-                       &st->sweeps, extra_dev, extra_host));
+                       &st->sweeps, extra_dev, extra_host, extra_n));
     // QR (4 m n^2 / 3) + Q formation + Q P, plus sweeps x n^2/2 pairs x 10 n
     prof_end(ctx, pb, PT_JACOBI, 8.0 * ((double)mA * nA * 3 + (double)nA * nA * 2),
              (double)mA * nA * nA * (8.0 / 3.0 + 2.0) + 5.0 * std::max(st->sweeps, 1) *
@@ -1127,6 +1127,7 @@ extern "C" int ftt_svd_f64(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, 
                            int32_t a_row_major, double *s_host) {
   if (!ctx || m < 0 || n < 0) return FTT_ERR_INVALID;
   ctx->fro2_hint = 0.0;
+  ctx->rank_hint = 0;
   svd_state_free(ctx);
   SvdState *st = new SvdState();
   ctx->svd = st;
@@ -1145,6 +1146,8 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   // ||A||_F^2 when the caller knows it (consumed here)
   const double fro2_known = ctx->fro2_hint;
   ctx->fro2_hint = 0.0;
+  const int64_t rank_hint = ctx->rank_hint;
+  ctx->rank_hint = 0;
   const bool have_fro2 = fro2_known > 0.0 && std::isfinite(fro2_known);
   svd_state_free(ctx);
   SvdState *st = new SvdState();
@@ -1170,18 +1173,21 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
   // ||A||_F^2 stays on the device until the sketch rank comes back (one host
   // round trip for both); a non-finite entry is diagnosed there
   double *fro2_dev = nullptr;
-  FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 3)));
-  double *rest2_dev = fro2_dev + kSumSqBlocks + 2;  // after sum_squares' partials
+  FTT_CHECK(owned_alloc(ctx, (void **)&fro2_dev, 8 * (size_t)(kSumSqBlocks + 6)));
+  // after sum_squares' partials: rest2 | sketch rank word | ||A||_F^2 (read
+  // back together)
+  double *rest2_dev = fro2_dev + kSumSqBlocks + 2;
+  double *fro2_out = rest2_dev + 2;
   if (sc) {
     if (!have_fro2) {
       if (sc->ldv != sc->K) {
         set_error("scattered operand: strided carry without a known norm");
         return FTT_ERR_INVALID;
       }
-      FTT_CHECK(sum_squares_dev(ctx, sc->K * sc->r, sc->V, fro2_dev + 1, fro2_dev));
+      FTT_CHECK(sum_squares_dev(ctx, sc->K * sc->r, sc->V, fro2_dev + 1, fro2_out));
     }
   } else if (sp) {
-    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->v_r, fro2_dev + 1, fro2_dev));
+    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->v_r, fro2_dev + 1, fro2_out));
   } else {
     const int64_t inner = need_t ? nA : mA;
     if (lda != inner) {
@@ -1190,7 +1196,7 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
       buf = st->Af;
       ld = inner;
     }
-    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, mA * nA, buf, fro2_dev + 1, fro2_dev));
+    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, mA * nA, buf, fro2_dev + 1, fro2_out));
   }
   auto finite_or_decline = [&]() -> int {
     // non-finite energy: either a non-finite entry (error) or an overflow
@@ -1222,41 +1228,118 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
     FTT_CHECK(gemm(ctx, need_t, 0, mA, k, nA, 1.0, buf, ld, Om, nA, 0.0, Yk, mA, sk, ske));
   }
   static const char *qr_mode = getenv("FTT_SKETCH_QR");  // test override: householder
-  if (k <= 64 && !(qr_mode && !strcmp(qr_mode, "householder"))) {
-    // numerical rank of the sketch (pivoted Cholesky of its Gram, directions
-    // below ~3e-6 of the largest dropped -- the residual certificate below
-    // decides whether the basis suffices), then Householder TSQR of only the
-    // r spanning columns (ftt_cholqr.cu, ftt_small.cu)
-    int64_t kr = 0;
-    int64_t *sel = nullptr;
-    FTT_CHECK(owned_alloc(ctx, (void **)&sel, 8 * (size_t)k));
-    FTT_CHECK(sketch_rank(ctx, mA, k, Yk, 1e-11, sel, &kr, have_fro2 ? nullptr : fro2_dev, &fro2));
-    if (have_fro2) fro2 = fro2_known;
-    if (kr == 0 || !std::isfinite(fro2)) {
-      owned_free(ctx, sel);
-      owned_free(ctx, Om);
-      owned_free(ctx, Yk);
-      owned_free(ctx, sk);
-      owned_free(ctx, fro2_dev);
-      return std::isfinite(fro2) ? FTT_OK : finite_or_decline();  // full SVD instead
-    }
-    double *Ys = nullptr;
-    FTT_CHECK(owned_alloc(ctx, (void **)&Ys, 8 * (size_t)mA * kr));
-    k_gather_cols<<<grid_for(mA * kr, 256, 4), 256, 0, ctx->stream>>>(mA, mA, kr, Yk, mA, sel,
-                                                                      nullptr, Ys, mA);
-    FTT_LAUNCHED(ctx);
-    FTT_CHECK(tsqr_q(ctx, mA, kr, Ys, mA, 0, st->Qk, mA, nullptr, 0, false));
-    owned_free(ctx, Ys);
+  static const bool no_speculate = getenv("FTT_NO_SPECULATE") != nullptr;
+  static const bool no_rank_spec = getenv("FTT_NO_RANK_SPEC") != nullptr;
+  const bool small_qr = k <= 64 && !(qr_mode && !strcmp(qr_mode, "householder"));
+  int64_t *sel = nullptr;
+  auto bail = [&]() {
     owned_free(ctx, sel);
+    owned_free(ctx, Om);
+    owned_free(ctx, Yk);
+    owned_free(ctx, sk);
+    owned_free(ctx, fro2_dev);
+  };
+  // Range basis from the kr spanning sketch columns, B = Q^T A, the
+  // certificate residual and (narrow B) its factorisation, speculatively,
+  // before the certificate is read: residual energy, singular values and --
+  // when the sketch rank was assumed (rank_spec) -- the rank word and
+  // ||A||_F^2 all come back in the inner factorisation's one round trip.
+  bool rank_spec = false;
+  double extras[3] = {0.0, 0.0, 0.0};  // rest2 | rank word | ||A||_F^2
+  auto project = [&](int64_t kr) -> int {
+    if (small_qr) {
+      double *Ys = nullptr;
+      FTT_CHECK(owned_alloc(ctx, (void **)&Ys, 8 * (size_t)mA * kr));
+      k_gather_cols<<<grid_for(mA * kr, 256, 4), 256, 0, ctx->stream>>>(mA, mA, kr, Yk, mA, sel,
+                                                                        nullptr, Ys, mA);
+      FTT_LAUNCHED(ctx);
+      FTT_CHECK(tsqr_q(ctx, mA, kr, Ys, mA, 0, st->Qk, mA, nullptr, 0, false));
+      owned_free(ctx, Ys);
+    }
+    if (sc) FTT_CHECK(scatter_qt_a(ctx, *sc, kr, st->Qk, st->Bk));
+    else if (sp) FTT_CHECK(sparse_qt_a(ctx, *sp, kr, st->Qk, st->Bk));
+    else FTT_CHECK(gemm(ctx, 1, need_t, kr, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, kr, sk,
+                        ske));
+    const bool speculate = tsqr_ok(std::max(kr, nA), std::min(kr, nA)) && !no_speculate;
+    if (speculate) {
+      if (sc) FTT_CHECK(scatter_resid(ctx, *sc, kr, st->Qk, st->Bk, rest2_dev));
+      else if (sp) FTT_CHECK(sparse_resid(ctx, *sp, kr, st->Qk, st->Bk, rest2_dev));
+      else FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, kr, st->Qk, mA, st->Bk, kr, buf, ld,
+                                      need_t, nullptr, rest2_dev));
+      st->inner = new SvdState();
+      if (svd_factor(ctx, st->inner, kr, nA, st->Bk, kr, 0, rest2_dev, extras, true,
+                     rank_spec ? 3 : 1) != FTT_OK) {
+        // speculative factorisation failed: decide on the certificate alone
+        // (an accepted certificate re-runs the factorisation below and reports)
+        svd_state_release(ctx, st->inner);
+        st->inner = nullptr;
+        FTT_CHECK(copy_to_host(ctx, extras, rest2_dev, (rank_spec ? 3 : 1) * sizeof(double)));
+      }
+      rest2 = extras[0];
+    } else if (sp || sc) {
+      if (sc) FTT_CHECK(scatter_resid(ctx, *sc, kr, st->Qk, st->Bk, rest2_dev));
+      else FTT_CHECK(sparse_resid(ctx, *sp, kr, st->Qk, st->Bk, rest2_dev));
+      FTT_CHECK(copy_to_host(ctx, extras, rest2_dev, (rank_spec ? 3 : 1) * sizeof(double)));
+      rest2 = extras[0];
+    } else {
+      FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, kr, st->Qk, mA, st->Bk, kr, buf, ld, need_t,
+                                 &rest2));
+      if (rank_spec) FTT_CHECK(copy_to_host(ctx, extras, rest2_dev, 3 * sizeof(double)));
+    }
+    return FTT_OK;
+  };
+  if (small_qr) {
+    // numerical rank of the sketch (pivoted Cholesky of its Gram, directions
+    // below ~3e-6 of the largest dropped -- the residual certificate decides
+    // whether the basis suffices), then Householder TSQR of only the r
+    // spanning columns (ftt_cholqr.cu, ftt_small.cu).  With the caller's
+    // rank hint the rank word is not waited for: the step runs at the hinted
+    // rank and is redone at the true one if they differ.
+    int64_t kr = 0;
+    FTT_CHECK(owned_alloc(ctx, (void **)&sel, 8 * (size_t)k));
+    rank_spec = ctx->spec_ok && !no_rank_spec && rank_hint > 0 && rank_hint <= k &&
+                rank_hint < nA;
+    if (rank_spec) {
+      FTT_CUDA(cudaMemsetAsync(rest2_dev + 1, 0, 8, ctx->stream));
+      FTT_CHECK(sketch_rank_async(ctx, mA, k, Yk, 1e-11, sel,
+                                  reinterpret_cast<int *>(rest2_dev + 1)));
+      kr = rank_hint;
+      FTT_CHECK(project(kr));
+      int kr_true = 0;
+      memcpy(&kr_true, &extras[1], sizeof(int));
+      fro2 = have_fro2 ? fro2_known : extras[2];
+      if (kr_true != kr || !std::isfinite(fro2)) {
+        // wrong guess: no further guesses in this sweep; redo at the true rank
+        ctx->spec_ok = false;
+        rank_spec = false;
+        if (st->inner) {
+          svd_state_release(ctx, st->inner);
+          st->inner = nullptr;
+        }
+        kr = kr_true;
+        if (kr == 0 || !std::isfinite(fro2)) {
+          bail();
+          return std::isfinite(fro2) ? FTT_OK : finite_or_decline();  // full SVD instead
+        }
+        FTT_CHECK(project(kr));
+      }
+    } else {
+      FTT_CHECK(sketch_rank(ctx, mA, k, Yk, 1e-11, sel, &kr, have_fro2 ? nullptr : fro2_out, &fro2));
+      if (have_fro2) fro2 = fro2_known;
+      if (kr == 0 || !std::isfinite(fro2)) {
+        bail();
+        return std::isfinite(fro2) ? FTT_OK : finite_or_decline();  // full SVD instead
+      }
+      FTT_CHECK(project(kr));
+    }
+    owned_free(ctx, sel);
+    sel = nullptr;
     k = kr;
   } else {
     if (have_fro2) fro2 = fro2_known;
-    else FTT_CHECK(copy_to_host(ctx, &fro2, fro2_dev, sizeof(double)));
+    else FTT_CHECK(copy_to_host(ctx, &fro2, fro2_out, sizeof(double)));
     if (!std::isfinite(fro2)) {
-      owned_free(ctx, Om);
-      owned_free(ctx, Yk);
-      owned_free(ctx, sk);
-      owned_free(ctx, fro2_dev);
+      bail();
       return finite_or_decline();
     }
     size_t wse = qr_workspace_elems(mA, k);
@@ -1268,35 +1351,7 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
     FTT_CHECK(qr_factor(ctx, mA, k, Yk, mA, tau, Tb, ws, wse));
     FTT_CHECK(launch_identity(ctx, mA, k, st->Qk, mA));
     FTT_CHECK(qr_apply_q(ctx, mA, k, Yk, mA, Tb, k, st->Qk, mA, ws, wse));
-  }
-  if (sc) FTT_CHECK(scatter_qt_a(ctx, *sc, k, st->Qk, st->Bk));
-  else if (sp) FTT_CHECK(sparse_qt_a(ctx, *sp, k, st->Qk, st->Bk));
-  else FTT_CHECK(gemm(ctx, 1, need_t, k, nA, mA, 1.0, st->Qk, mA, buf, ld, 0.0, st->Bk, k, sk, ske));
-  // A narrow B (k <= 64) is factored speculatively before the certificate is
-  // read: the residual energy then comes back with the singular values in
-  // one host round trip (a rejected certificate wastes one small SVD).
-  const bool speculate = tsqr_ok(std::max(k, nA), std::min(k, nA)) &&
-                         !getenv("FTT_NO_SPECULATE");
-  if (speculate) {
-    if (sc) FTT_CHECK(scatter_resid(ctx, *sc, k, st->Qk, st->Bk, rest2_dev));
-    else if (sp) FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
-    else FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
-                                    nullptr, rest2_dev));
-    st->inner = new SvdState();
-    if (svd_factor(ctx, st->inner, k, nA, st->Bk, k, 0, rest2_dev, &rest2, true) != FTT_OK) {
-      // speculative factorisation failed: decide on the certificate alone
-      // (an accepted certificate re-runs the factorisation below and reports)
-      svd_state_release(ctx, st->inner);
-      st->inner = nullptr;
-      FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
-    }
-  } else if (sp || sc) {
-    if (sc) FTT_CHECK(scatter_resid(ctx, *sc, k, st->Qk, st->Bk, rest2_dev));
-    else FTT_CHECK(sparse_resid(ctx, *sp, k, st->Qk, st->Bk, rest2_dev));
-    FTT_CHECK(copy_to_host(ctx, &rest2, rest2_dev, sizeof(double)));
-  } else {
-    FTT_CHECK(gemm_resid_sumsq(ctx, 0, 0, mA, nA, k, st->Qk, mA, st->Bk, k, buf, ld, need_t,
-                               &rest2));
+    FTT_CHECK(project(k));
   }
   owned_free(ctx, Om);
   owned_free(ctx, Yk);

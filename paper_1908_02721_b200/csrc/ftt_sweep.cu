@@ -257,6 +257,7 @@ struct Driver {
 
   int run(int32_t *zero) {
     *zero = 0;
+    ctx->spec_ok = true;
     int64_t hint = -1;
     // ||operand||_F^2 of a step whose operand is a scattered carry S V^T:
     // the retained singular values' squares (V has orthonormal columns)
@@ -271,8 +272,10 @@ struct Driver {
       double rest2 = 0.0;
       if (fro2_next > 0.0) ctx->fro2_hint = fro2_next;
       fro2_next = 0.0;
+      ctx->rank_hint = hint > 0 ? hint : 0;
       FTT_CHECK(values(k, m, r1, true, hd, dl, hint, policy == 0 && interval_ok, &s, &rest2));
       ctx->fro2_hint = 0.0;
+      ctx->rank_hint = 0;
       const int64_t rank = decide(true, k, s, m, r1, rest2);
       hint = rank;
       if (rank == 0) {
@@ -349,8 +352,10 @@ struct Driver {
       double rest2 = 0.0;
       if (fro2_next > 0.0) ctx->fro2_hint = fro2_next;
       fro2_next = 0.0;
+      ctx->rank_hint = hint > 0 ? hint : 0;
       FTT_CHECK(values(k, m, r0, false, hd, dl, hint, policy == 0 && interval_ok, &s, &rest2));
       ctx->fro2_hint = 0.0;
+      ctx->rank_hint = 0;
       const int64_t rank = decide(false, k, s, m, r0, rest2);
       hint = rank;
       if (rank == 0) {
