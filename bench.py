@@ -16,7 +16,9 @@ deparallelisation sweeps -> rounding sweeps -> error report).
 * ``e2e``: the public drop-in call ``fasttt(SparseTensor)`` from pinned host
   buffers: H2D of the canonical COO (linear index + values), the
   decomposition, D2H of every core.
-* ``roofline``: the dominant kernel class by live CUDA-event time;
+* ``roofline``: on config 5 the metric's sort/segment roofline (the index
+  pass against SURVEY 8(d)'s algorithmic bytes); ``roofline_dominant_class``
+  the dominant kernel class by live CUDA-event time;
   ``roofline_sort_segment`` / ``index_path``: SURVEY 8(d)'s algorithmic bytes
   of the index path over its measured time.
 * ``--impl reference``: the reference algorithm's CPU implementation (the
@@ -440,6 +442,21 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, name, a, eps)
 
+    # The line's `roofline`: the metric's own ("% HBM roofline of
+    # sort/segment") -- the index pass against SURVEY 8(d)'s algorithmic bytes
+    # -- on the config that section judges it on (config 5); elsewhere (the
+    # index kernels are L2-resident and launch-bound on configs 1-4) and
+    # without the index leg, the dominant kernel class by live time.
+    roof_dom = roof(dom, d)
+    roof_main = roof_dom
+    if ileg is not None and args.config == 5:
+        roof_main = dict(ileg["roofline"])
+        roof_main["kernel_class"] = "index pass (select_p counts, fiber sort + segmentation, sweeps)"
+        roof_main["launches"] = sum(v["launches"] for v in ileg["per_class"].values())
+        roof_main["ms_total"] = ileg["ms_per_pass"]
+        roof_main["alg_bytes_per_launch"] = ileg["roofline"]["alg_bytes"]
+        roof_main["unit_of_launch"] = "one index pass over the config-5 COO (8,503,056 nonzeros)"
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -453,7 +470,8 @@ def run_ours(args):
             "timing": {"l2": "flushed (256 MiB write) between steps",
                        "parallelism": f"replicas x{world}",
                        "steps_ms": [round(x, 4) for x in times]},
-            "roofline": roof(dom, d),
+            "roofline": roof_main,
+            "roofline_dominant_class": roof_dom,
             "roofline_sort_segment": roof_sort,
             "index_path": ileg,
             "cpu_baseline": cpu,

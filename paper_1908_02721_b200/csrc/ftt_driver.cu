@@ -54,6 +54,21 @@ int pick_pivot(int d, const int64_t *dims, const int64_t *counts, double c_svd) 
   return best;
 }
 
+// The output train into one slab: block (x, k) copies a stride of core k.
+struct PackSrc {
+  const double *src[32];
+  int64_t off[33];
+};
+__global__ void k_pack_cores(PackSrc p, double *__restrict__ slab) {
+  const int k = blockIdx.y;
+  const int64_t n = p.off[k + 1] - p.off[k];
+  const double *__restrict__ s = p.src[k];
+  double *__restrict__ d = slab + p.off[k];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
 struct Bufs {  // device buffers of one call, released on an error return
   ftt_ctx *ctx;
   std::vector<void *> v;
@@ -266,19 +281,30 @@ int run(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz, int
       return FTT_ERR_OOM;
     }
     bufs.adopt(slab);
-    int64_t off = 0;
+    PackSrc ps;
+    int64_t off = 0, widest = 1;
     for (int k = 0; k < d; ++k) {
       const int64_t el =
           res->out_shapes[3 * k] * res->out_shapes[3 * k + 1] * res->out_shapes[3 * k + 2];
-      if (zero) {
-        cudaMemsetAsync(slab + off, 0, 8 * (size_t)el, ctx->stream);
-      } else {
-        cudaMemcpyAsync(slab + off, out[k], 8 * (size_t)el, cudaMemcpyDeviceToDevice, ctx->stream);
+      ps.src[k] = out[k];
+      ps.off[k] = off;
+      widest = std::max(widest, el);
+      off += el;
+    }
+    ps.off[d] = off;
+    if (zero) {
+      FTT_CUDA(cudaMemsetAsync(slab, 0, 8 * (size_t)std::max<int64_t>(total, 1), ctx->stream));
+    } else {  // one launch for all d cores
+      k_pack_cores<<<dim3((unsigned)std::min<int64_t>(ceil_div(widest, 1024), 64), (unsigned)d), 256,
+                     0, ctx->stream>>>(ps, slab);
+      FTT_LAUNCHED(ctx);
+    }
+    for (int k = 0; k < d; ++k) {
+      if (!zero) {
         cudaFreeAsync(out[k], ctx->stream);
         bufs.forget(out[k]);
       }
-      out[k] = slab + off;
-      off += el;
+      out[k] = slab + ps.off[k];
     }
     res->out_slab = slab;
   }
@@ -302,7 +328,13 @@ int run(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz, int
       for (int s = 0; s < nsteps; ++s) kp[s] = kept[s];
       FTT_CHECK(ftt_inner_structured(ctx, d, dims, ranks, cp, pivot, kp, oc, R, indptr, pidx, vals,
                                      t_map, s_map, &res->dot));
-      FTT_CHECK(ftt_tt_norm(ctx, d, dims, ranks, cp, &res->nb));
+      // ||b||: the sweeps leave cores 1..d-1 right-orthogonal (QR sweep, then
+      // the V factors of the second SVD sweep), so the train's norm is core
+      // 0's (fasttt.py:598 computes tt_norm of the same train)
+      double nb2 = 0.0;
+      FTT_CHECK(ftt_dot(ctx, res->out_shapes[0] * res->out_shapes[1] * res->out_shapes[2], out[0],
+                        nullptr, &nb2));
+      res->nb = sqrt(nb2);
       res->inner_valid = 1;
     }
   }

@@ -1045,7 +1045,9 @@ def _inner_error_structured(df, sw: DeviceSweeps, approx_d, na2):
         nat.i64_array(counts or [0]), df.R, nat.ptr(df.indptr), nat.ptr(df.pivot_index),
         nat.ptr(df.values), nat.ptr(sw.t_map), nat.ptr(sw.s_map), nat.ctypes.byref(dot)),
         "ftt_inner_structured")
-    nb2 = dev_tt_norm(cs) ** 2
+    # the rounding sweeps leave cores 1..d-1 right-orthogonal, so the train's
+    # norm is core 0's (same value as ftt_fasttt_lin's report terms)
+    nb2 = math.sqrt(device_dot(cs[0].reshape(-1), None)) ** 2
     return math.sqrt(max(na2 - 2.0 * float(dot.value) + nb2, 0.0) / na2)
 
 

@@ -39,11 +39,11 @@ unset FTT_JCLUSTER
 # 4. full captures of the top kernels (source-mapped)
 python tools/profile_index.py 5 > /dev/null 2>&1 &&
   $NCU --profile-from-start off --set full --import-source on \
-    -k regex:"k_sel_count|k_onesweep|k_keys_hist_lin|k_emit|k_sweep_mark" -c 8 -o $OUT/full_c5_index -f \
+    -k regex:"k_sel_count|k_onesweep|k_keys_hist_lin|k_compact1|k_sweep_gather_mark|k_hist_hashmod" -c 10 -o $OUT/full_c5_index -f \
     python tools/profile_index.py 5 > $OUT/ncu_full_c5_index.log 2>&1
 python tools/profile_step.py 5 > /dev/null 2>&1 &&
   $NCU --profile-from-start off --set full --import-source on \
-    -k regex:"k_tsqr_level|k_jacobi_qr|k_sp_on_dd|k_spmm_seg|k_spmm_rows|k_dgemm" -c 8 -o $OUT/full_c5_round -f \
+    -k regex:"k_tsqr_wy|k_svd_wy|k_sp_on_dd|k_spmm_seg|k_spmm_rows|k_dgemm|k_sc_w|k_sc_ysum|k_sc_qta|k_sc_resid|k_resid_cols" -c 14 -o $OUT/full_c5_round -f \
     python tools/profile_step.py 5 > $OUT/ncu_full_c5_round.log 2>&1
 for f in $OUT/*.ncu-rep; do
   [ -f "$f" ] || continue

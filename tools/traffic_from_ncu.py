@@ -20,12 +20,13 @@ CLASSES = [
                  "k_part_count", "k_sel_count", "k_group_count")),
     ("sweep", ("k_sweep",)),
     ("scatter", ("k_pivot_scatter", "k_side_core", "k_scatter_", "k_sp_entries", "k_sp_gather",
+                 "k_sc_pos", "k_sc_iptr", "k_pack_cores",
                  "k_gather_i32", "k_sp_bitmap", "k_lower_bounds", "k_scan_blocks", "k_scan_fix",
                  "k_seg_counts")),
-    ("gemm", ("k_dgemm", "k_splitk_reduce", "k_sum_partials", "k_spmm_", "k_sp_resid",
+    ("gemm", ("k_dgemm", "k_splitk_reduce", "k_sum_partials", "k_spmm_", "k_sp_resid", "k_sc_",
               "k_seg_reduce", "k_sp_sum", "k_resid_", "k_gram_", "k_sp_on_dd")),
     ("qr_panel", ("k_panel", "k_larft", "k_extract_v")),
-    ("jacobi", ("k_jacobi", "k_svd_small", "k_tsqr", "k_qr_root", "k_chol")),
+    ("jacobi", ("k_jacobi", "k_svd_small", "k_svd_wy", "k_tsqr", "k_qr_root", "k_chol")),
     ("entries", ("k_entries", "k_mitm", "k_half_", "k_seg_", "k_left_vec", "k_right_vec",
                  "k_inner_struct", "k_sum_fixed")),
 ]
