@@ -420,6 +420,12 @@ typedef struct {
   const int64_t *fiber_of, *pivot_index;
   const double *values;
   const int64_t *t_map, *s_map;
+  /* optional (0 / NULL when unknown): the fiber structure the entries came
+   * from (tensor.py:374-403: num_fibers fibers, fiber f holds entries
+   * indptr[f] .. indptr[f+1]) -- lets the first step index its operand by
+   * fiber instead of sorting the entries */
+  int64_t num_fibers;
+  const int64_t *indptr;
 } ftt_sparse_pivot;
 /* _sweep_rounding (fasttt.py:324-356) in one call: SVD sweep p..d-2, QR
  * sweep d-1..p+1, SVD sweep p..1, with policy 0 = static (delta per step,

@@ -74,12 +74,30 @@ struct SparseOperand {
   int64_t max_segs = 0;
   double *Qr = nullptr;      // row-major copy of the range basis (sparse_qt_a)
   int64_t ldq = 0;           // its row stride (kr rounded up to even)
+  // fiber-level CSR (transposed operand with the fiber structure at hand):
+  // rptr indexes fperm (fibers by row, ascending); no cidx_r / v_r
+  bool by_fiber = false;
+  uint32_t *fperm = nullptr;
+  int64_t *fe0 = nullptr;   // sorted fiber j: first entry,
+  int32_t *flen = nullptr;  // entry count,
+  int32_t *fcb = nullptr;   // first column of its block (t_map * n_p)
+  const int64_t *f_indptr = nullptr, *f_pidx = nullptr, *f_tmap = nullptr;
+  const double *f_vals = nullptr;
+  int64_t f_np = 0;
 };
 // M (m x n): entry e at row t_map[f] * np + pidx[e], column s_map[f]
 // (f = fiber_of[e]; a NULL map means 0).
 int sparse_operand_build(ftt_ctx *ctx, SparseOperand *op, int64_t nnz, const int64_t *fiber_of,
                          const int64_t *pidx, const double *vals, const int64_t *tmap,
-                         const int64_t *smap, int64_t np, int64_t m, int64_t n);
+                         const int64_t *smap, int64_t np, int64_t m, int64_t n, int64_t R = 0,
+                         const int64_t *indptr = nullptr);
+// ftt_svd_lowrank_sparse_f64 with the fiber structure (R fibers, indptr) for
+// the fiber-level CSR (ftt_svd.cu).
+int svd_lowrank_sparse(ftt_ctx *ctx, int64_t m, int64_t n, int64_t nnz, const int64_t *fiber_of,
+                       const int64_t *pivot_index, const double *values, const int64_t *t_map,
+                       const int64_t *s_map, int64_t n_p, int64_t R, const int64_t *indptr,
+                       int64_t k, double delta2, double *s_host, double *rest2_host,
+                       int32_t *accepted);
 void sparse_operand_free(ftt_ctx *ctx, SparseOperand *op);
 // Y (mA x k col-major) = A_tall Omega with the range finder's test matrix.
 int sparse_sketch(ftt_ctx *ctx, const SparseOperand &op, int64_t k, double *Y);

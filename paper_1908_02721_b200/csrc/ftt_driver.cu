@@ -208,7 +208,7 @@ int run(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz, int
   pc.r1 = r_next;
   const u128 pelems = (u128)r_prev * (u128)np * (u128)r_next;
   const double density = (double)nnz / (double)std::max<u128>(pelems, 1);
-  ftt_sparse_pivot sp{nnz, fiber_of, pidx, vals, t_map, s_map};
+  ftt_sparse_pivot sp{nnz, fiber_of, pidx, vals, t_map, s_map, R, indptr};
   double pnorm = 0.0;
   double *pdense = nullptr;
   if (density < 0.02 && pivot < d - 1) {  // pipeline._SPARSE_PIVOT_DENSITY

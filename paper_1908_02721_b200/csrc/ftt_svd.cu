@@ -1187,7 +1187,9 @@ static int lowrank_run(ftt_ctx *ctx, int64_t m, int64_t n, const double *A, int6
       FTT_CHECK(sum_squares_dev(ctx, sc->K * sc->r, sc->V, fro2_dev + 1, fro2_out));
     }
   } else if (sp) {
-    if (!have_fro2) FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->v_r, fro2_dev + 1, fro2_out));
+    if (!have_fro2)
+      FTT_CHECK(sum_squares_dev(ctx, sp->nnz, sp->by_fiber ? sp->f_vals : sp->v_r, fro2_dev + 1,
+                                fro2_out));
   } else {
     const int64_t inner = need_t ? nA : mA;
     if (lda != inner) {
@@ -1429,11 +1431,20 @@ extern "C" int ftt_svd_lowrank_sparse_f64(ftt_ctx *ctx, int64_t m, int64_t n, in
     set_error("ftt_svd_lowrank_sparse_f64: operand too large for 32-bit entry indices");
     return FTT_ERR_INVALID;
   }
+  return svd_lowrank_sparse(ctx, m, n, nnz, fiber_of, pivot_index, values, t_map, s_map, n_p, 0,
+                            nullptr, k, delta2, s_host, rest2_host, accepted);
+}
+
+int ftt::svd_lowrank_sparse(ftt_ctx *ctx, int64_t m, int64_t n, int64_t nnz,
+                            const int64_t *fiber_of, const int64_t *pivot_index,
+                            const double *values, const int64_t *t_map, const int64_t *s_map,
+                            int64_t n_p, int64_t R, const int64_t *indptr, int64_t k,
+                            double delta2, double *s_host, double *rest2_host, int32_t *accepted) {
   *accepted = 0;
   *rest2_host = -1.0;
   SparseOperand op;
   FTT_CHECK(sparse_operand_build(ctx, &op, nnz, fiber_of, pivot_index, values, t_map, s_map, n_p, m,
-                                 n));
+                                 n, R, indptr));
   const int rc = lowrank_run(ctx, m, n, nullptr, 0, 1, &op, k, delta2, s_host, rest2_host, accepted);
   sparse_operand_free(ctx, &op);
   return rc;

@@ -193,9 +193,9 @@ struct Driver {
         double r2 = 0.0;
         int32_t acc = 0;
         if (c.kind == 3) {
-          FTT_CHECK(ftt_svd_lowrank_sparse_f64(ctx, m, n, sp->nnz, sp->fiber_of, sp->pivot_index,
-                                               sp->values, sp->t_map, sp->s_map, c.n, kk,
-                                               dlt * dlt, sv.data(), &r2, &acc));
+          FTT_CHECK(svd_lowrank_sparse(ctx, m, n, sp->nnz, sp->fiber_of, sp->pivot_index,
+                                       sp->values, sp->t_map, sp->s_map, c.n, sp->num_fibers,
+                                       sp->indptr, kk, dlt * dlt, sv.data(), &r2, &acc));
         } else if (c.kind == 4) {
           ScatterOperand so;
           so.mA = c.r1;

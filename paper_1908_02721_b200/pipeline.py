@@ -682,7 +682,8 @@ class _CoreDesc(nat.ctypes.Structure):
 class _SparsePivot(nat.ctypes.Structure):
     _fields_ = [("nnz", nat.ctypes.c_int64), ("fiber_of", nat.ctypes.c_void_p),
                 ("pivot_index", nat.ctypes.c_void_p), ("values", nat.ctypes.c_void_p),
-                ("t_map", nat.ctypes.c_void_p), ("s_map", nat.ctypes.c_void_p)]
+                ("t_map", nat.ctypes.c_void_p), ("s_map", nat.ctypes.c_void_p),
+                ("num_fibers", nat.ctypes.c_int64), ("indptr", nat.ctypes.c_void_p)]
 
 
 class _NativeCore:
@@ -734,7 +735,8 @@ def _sweep_rounding_device(cores, pivot: int, policy: _Trunc):
             sp = _SparsePivot(df.nnz, df.fiber_of.data_ptr(), df.pivot_index.data_ptr(),
                               df.values.data_ptr(),
                               sw.t_map.data_ptr() if sw.t_map is not None else None,
-                              sw.s_map.data_ptr() if sw.s_map is not None else None)
+                              sw.s_map.data_ptr() if sw.s_map is not None else None,
+                              df.R, df.indptr.data_ptr())
         else:
             c = c.contiguous()
             keep.append(c)
