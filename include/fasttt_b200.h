@@ -449,6 +449,15 @@ int ftt_free_device(ftt_ctx *ctx, void *p);
  * of fasttt.py:334-341 after a 0/1 core, never materialised; test probe). */
 int64_t ftt_scatter_steps(void);
 
+/* The canonical linear index of the NEXT call that reads `lin`
+ * (ftt_fiber_counts_lin, ftt_extract_fibers_lin, ftt_fasttt_lin) is still
+ * arriving from the host: chunk j, lin[0 .. ends[j]), is present once the
+ * cudaEvent_t events[j] has fired (ends ascending, <= 8 chunks).  select_p's
+ * forward counts (fasttt.py:536-541) then start on the chunks present and
+ * overlap the rest of the transfer; every other reader waits for the last
+ * event.  The chunk list is consumed by that call. */
+int ftt_set_lin_chunks(ftt_ctx *ctx, int32_t nchunks, const int64_t *ends, void *const *events);
+
 /* ------------------------------------------------------- fasttt driver */
 /* What ftt_fasttt_lin hands back.  Device buffers the caller releases with
  * ftt_free_device: fiber_slab (fixed_lin, indptr, fiber_of, pivot_index,

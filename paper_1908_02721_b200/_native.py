@@ -95,6 +95,7 @@ SIGNATURES = {
                            _c_i32, _c_p, _c_p, ctypes.POINTER(ctypes.c_int32)],
     "ftt_free_device": [_c_p, _c_p],
     "ftt_scatter_steps": [],
+    "ftt_set_lin_chunks": [_c_p, _c_i32, _P_i64, ctypes.POINTER(_c_p)],
     "ftt_fasttt_lin": [_c_p, _c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_i32, _c_i32, _c_d, _c_d,
                        _c_i32, _c_p, _c_p],
     "ftt_delinearize": [_c_p, _c_p, _c_i64, _c_i32, _P_i64, _c_p],

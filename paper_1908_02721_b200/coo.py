@@ -102,7 +102,7 @@ class SparseTensor:
     duplicate coordinates raise :class:`FormatError` (they are never summed).
     """
 
-    __slots__ = ("shape", "coords", "values", "_lin", "_dev", "_pin")
+    __slots__ = ("shape", "coords", "values", "_lin", "_dev", "_pin", "_linq")
 
     def __init__(self, shape, coords, values):
         dims = check_shape(shape)
@@ -145,6 +145,7 @@ class SparseTensor:
         # form the COO travels to the device in (8 B per nonzero instead of 8d)
         object.__setattr__(self, "_lin", slin)
         object.__setattr__(self, "_dev", None)
+        object.__setattr__(self, "_linq", None)
         object.__setattr__(self, "_pin", None)
 
     def __setattr__(self, name, value):
@@ -166,6 +167,7 @@ class SparseTensor:
         object.__setattr__(t, "values", v)
         object.__setattr__(t, "_lin", None)
         object.__setattr__(t, "_dev", (coords_d, values_d, None, None))
+        object.__setattr__(t, "_linq", None)
         object.__setattr__(t, "_pin", None)
         return t
 
@@ -222,18 +224,55 @@ class SparseTensor:
         pin = self._pinned()
         compact = self._lin is not None and self.nnz > 0
         main = torch.cuda.current_stream()
-        lin = pin[0].to("cuda", non_blocking=True)
         side = _side_stream()
-        side.wait_stream(main)
+        n = int(pin[0].shape[0])
+        linq = None
+        if compact and n >= _LIN_CHUNK_MIN:
+            # large inputs: lin goes up in chunks on the side stream, each with
+            # its event -- the first reader (select_p's forward counts,
+            # ftt_set_lin_chunks) starts on the chunks present instead of
+            # after the whole 8 B x nnz transfer
+            lin = torch.empty(n, dtype=torch.int64, device="cuda")
+            side.wait_stream(main)
+            ends, evs = [], []
+            with torch.cuda.stream(side):
+                for j in range(_LIN_CHUNKS):
+                    lo, hi = n * j // _LIN_CHUNKS, n * (j + 1) // _LIN_CHUNKS
+                    lin[lo:hi].copy_(pin[0][lo:hi], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(side)
+                    ends.append(hi)
+                    evs.append(e)
+            lin.record_stream(side)
+            linq = (ends, evs)
+        else:
+            lin = pin[0].to("cuda", non_blocking=True)
+            side.wait_stream(main)
         with torch.cuda.stream(side):
             v = pin[1].to("cuda", non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(side)
         v.record_stream(main)
+        object.__setattr__(self, "_linq", linq)
         if compact:
             object.__setattr__(self, "_dev", (None, v, lin, ev))
         else:  # no canonical linear index on the host: these are the coordinates
             object.__setattr__(self, "_dev", (lin, v, None, ev))
+
+    def _lin_arrived(self):
+        """Make the current stream wait for a chunked `lin` upload (readers
+        other than the fused fasttt call, which takes the chunk events)."""
+        q = self._linq
+        if q is not None:
+            nat.torch_mod().cuda.current_stream().wait_event(q[1][-1])
+            object.__setattr__(self, "_linq", None)
+
+    def take_lin_chunks(self):
+        """``(ends, events)`` of a chunked `lin` upload still in flight, or
+        None; the caller takes over the waiting (ftt_set_lin_chunks)."""
+        q = self._linq
+        object.__setattr__(self, "_linq", None)
+        return q
 
     def device_arrays(self):
         """``(coords, values)`` as CUDA tensors (cached).  The host side is
@@ -243,6 +282,7 @@ class SparseTensor:
         caller needs them."""
         if self._dev is None:
             self._upload()
+        self._lin_arrived()
         c, v, lin, ev = self._dev
         if ev is not None:
             nat.torch_mod().cuda.current_stream().wait_event(ev)
@@ -255,12 +295,16 @@ class SparseTensor:
         object.__setattr__(self, "_dev", (c, v, lin, None))
         return c, v
 
-    def device_lin_values(self):
+    def device_lin_values(self, keep_chunks=False):
         """``(lin, values, values_ready)``: the canonical linear index and the
         values on the device without the coordinate rows; `values_ready` is
-        an event the consumer of `values` must wait for (or None)."""
+        an event the consumer of `values` must wait for (or None).  With
+        `keep_chunks` a chunked `lin` upload is left in flight for
+        `take_lin_chunks`."""
         if self._dev is None:
             self._upload()
+        if not keep_chunks:
+            self._lin_arrived()
         c, v, lin, ev = self._dev
         if lin is None:
             lin = self.device_lin()
@@ -272,6 +316,7 @@ class SparseTensor:
         compact form the index kernels read (8 B per nonzero)."""
         if self._dev is None:
             self._upload()
+        self._lin_arrived()
         lin = self._dev[2]
         if lin is None:
             c, v = self.device_arrays()
@@ -292,6 +337,7 @@ class SparseTensor:
     def drop_device_copy(self) -> None:
         """Forget the cached device arrays (the next GPU call re-uploads)."""
         object.__setattr__(self, "_dev", None)
+        object.__setattr__(self, "_linq", None)
 
 
 class FiberSet:
@@ -358,6 +404,10 @@ class FiberSet:
 
 
 _SIDE = {}
+
+
+_LIN_CHUNK_MIN = 1 << 21  # nonzeros from which `lin` is uploaded in chunks
+_LIN_CHUNKS = 4
 
 
 def _side_stream():

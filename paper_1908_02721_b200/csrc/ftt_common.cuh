@@ -81,6 +81,17 @@ struct ftt_ctx {
   // the step redone if it differs (which also clears spec_ok for the sweep)
   int64_t rank_hint = 0;
   bool spec_ok = true;
+  // `lin` still arriving from the host in chunks (ftt_set_lin_chunks): chunk
+  // j covers lin[0 .. lin_ends[j]) once lin_events[j] has fired.  Consumed by
+  // the next call that reads lin: select_p's forward counts start on the
+  // chunks present, everything else waits for the last event.
+  // the values' host -> device copy still in flight (ftt_fasttt_lin): waited
+  // for by the first kernel that reads them (the fiber emit), so that the
+  // key sort, which reads only lin, overlaps the transfer
+  cudaEvent_t values_event = nullptr;
+  int lin_nchunks = 0;
+  int64_t lin_ends[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaEvent_t lin_events[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // host round trips (copy_to_host) and the host time spent blocked in them
   int64_t syncs = 0;
   double sync_wait_ms = 0.0;
@@ -177,6 +188,9 @@ int zero_flags(ftt_ctx *ctx, size_t n, uint32_t **out);
 // status words, the ticket pair and this call's epoch (ftt_index.cu).
 int compact_status(ftt_ctx *ctx, size_t ntiles, uint64_t **status, unsigned **ticket,
                    uint32_t *epoch);
+
+// Make the stream wait for every pending lin chunk (and forget them).
+int lin_chunks_wait_all(ftt_ctx *ctx);
 
 // Persistent device buffer owned by the context (freed on destroy).
 int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes);

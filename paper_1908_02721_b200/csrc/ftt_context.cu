@@ -170,6 +170,13 @@ int stage_to_device(ftt_ctx *ctx, void *dev, const void *host, size_t bytes) {
   return FTT_OK;
 }
 
+int lin_chunks_wait_all(ftt_ctx *ctx) {
+  const int n = ctx->lin_nchunks;
+  ctx->lin_nchunks = 0;
+  if (n > 0) FTT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->lin_events[n - 1], 0));
+  return FTT_OK;
+}
+
 int owned_alloc(ftt_ctx *ctx, void **p, size_t bytes) {
   *p = nullptr;
   if (bytes == 0) bytes = 256;
@@ -412,6 +419,24 @@ int ftt_profile_read(ftt_ctx *ctx, int32_t tag, double *ms_out, int64_t *launche
   if (launches_out) *launches_out = n;
   if (bytes_out) *bytes_out = bytes;
   if (flops_out) *flops_out = flops;
+  return FTT_OK;
+}
+
+int ftt_set_lin_chunks(ftt_ctx *ctx, int32_t nchunks, const int64_t *ends, void *const *events) {
+  if (!ctx || nchunks < 0 || nchunks > 8 || (nchunks && (!ends || !events))) {
+    ftt::set_error("ftt_set_lin_chunks: invalid arguments");
+    return FTT_ERR_INVALID;
+  }
+  ctx->lin_nchunks = nchunks;
+  for (int j = 0; j < nchunks; ++j) {
+    if (!events[j] || ends[j] < (j ? ends[j - 1] : 0)) {
+      ctx->lin_nchunks = 0;
+      ftt::set_error("ftt_set_lin_chunks: chunk ends must ascend, events must be set");
+      return FTT_ERR_INVALID;
+    }
+    ctx->lin_ends[j] = ends[j];
+    ctx->lin_events[j] = (cudaEvent_t)events[j];
+  }
   return FTT_OK;
 }
 

@@ -106,8 +106,9 @@ int run(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz, int
     pivot = pick_pivot(d, dims, counts, c_svd);
   }
   res->pivot = pivot;
-  if (values_ready)
-    FTT_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)values_ready, 0));
+  // the values are first read by the fiber emit: the extraction waits for
+  // their upload there, after the key sort (which reads only lin)
+  ctx->values_event = (cudaEvent_t)values_ready;
   // ---- fibers (tensor.py:374-403)
   int64_t *fixed_lin, *indptr, *fiber_of, *pidx;
   double *vals;
@@ -125,6 +126,10 @@ int run(ftt_ctx *ctx, const int64_t *lin, const double *values, int64_t nnz, int
   int64_t R = 0;
   FTT_CHECK(ftt_extract_fibers_lin(ctx, lin, values, nnz, d, dims, pivot, fixed_lin, indptr,
                                    fiber_of, pidx, vals, &R));
+  if (ctx->values_event) {  // (a path that did not reach the emit)
+    FTT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->values_event, 0));
+    ctx->values_event = nullptr;
+  }
   res->num_fibers = R;
   res->fixed_lin = fixed_lin;
   res->indptr = indptr;
@@ -354,6 +359,13 @@ int ftt_fasttt_lin(ftt_ctx *ctx, const int64_t *lin, const double *values, int64
     return FTT_ERR_INVALID;
   }
   memset(res, 0, sizeof(*res));
+  struct ChunkWait {  // a chunked lin upload nobody consumed: the stream waits for it
+    ftt_ctx *c;
+    ~ChunkWait() {
+      lin_chunks_wait_all(c);
+      c->values_event = nullptr;  // (an error return before the emit)
+    }
+  } chunk_wait{ctx};
   for (int k = 0; k < d; ++k)
     if (dims[k] < 1 || dims[k] >= ((int64_t)1 << 31)) return res->fallback = 1, FTT_OK;
   if (nnz >= ((int64_t)1 << 30)) return res->fallback = 1, FTT_OK;

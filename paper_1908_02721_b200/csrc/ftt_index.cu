@@ -1969,7 +1969,7 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
                                                    SelSpec sp,
                                                    unsigned long long *__restrict__ count,
                                                    int *__restrict__ flag,
-                                                   int *__restrict__ unsorted) {
+                                                   int *__restrict__ unsorted, unsigned blk_off) {
   extern __shared__ unsigned long long smem[];
   uint64_t *skey = reinterpret_cast<uint64_t *>(smem);             // SC_CAP keys
   unsigned *tab32 = reinterpret_cast<unsigned *>(smem + SC_CAP);   // SC_SLOTS positions
@@ -1977,7 +1977,7 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
   __shared__ unsigned s_j[2];
   __shared__ unsigned long long s_cnt;
   const int lane = threadIdx.x & 31;
-  const int64_t c0 = (int64_t)blockIdx.x * SC_L;
+  const int64_t c0 = ((int64_t)blockIdx.x + blk_off) * SC_L;
   auto grp = [&](int64_t i) -> uint64_t { return sel_group<POW2>(K[i], sp); };
   if (threadIdx.x < 2) s_j[threadIdx.x] = 0xffffffffu;
   __syncthreads();
@@ -2206,12 +2206,34 @@ int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, 
     attr = true;
   }
   const unsigned nb = (unsigned)ceil_div(nnz, SC_L);
-  auto count = [&](const uint64_t *keys, const SelSpec &sp, int *uns) {
-    if (pow2) k_sel_count<true><<<nb, SC_NT, smem, ctx->stream>>>(keys, nnz, sp, cnt, flags, uns);
-    else k_sel_count<false><<<nb, SC_NT, smem, ctx->stream>>>(keys, nnz, sp, cnt, flags, uns);
+  auto count = [&](const uint64_t *keys, const SelSpec &sp, int *uns, unsigned b0, unsigned b1) {
+    if (b1 <= b0) return;
+    if (pow2)
+      k_sel_count<true><<<b1 - b0, SC_NT, smem, ctx->stream>>>(keys, nnz, sp, cnt, flags, uns, b0);
+    else
+      k_sel_count<false><<<b1 - b0, SC_NT, smem, ctx->stream>>>(keys, nnz, sp, cnt, flags, uns, b0);
   };
   int pb = prof_begin(ctx);
-  count(lin, fwd, unsorted);
+  {
+    // lin may still be arriving from the host in chunks (ftt_set_lin_chunks):
+    // the forward counts of the blocks whose window (SC_L + the SC_CAP
+    // look-ahead + 1) lies inside the chunks present start at once
+    const int nch = ctx->lin_nchunks;
+    ctx->lin_nchunks = 0;
+    unsigned b0 = 0;
+    for (int j = 0; j < nch; ++j) {
+      FTT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->lin_events[j], 0));
+      const int64_t have = std::min<int64_t>(ctx->lin_ends[j], nnz);
+      unsigned b1 = nb;
+      if (j + 1 < nch && have < nnz) {
+        const int64_t full = (have - SC_CAP - 1) / SC_L - 1;  // last block wholly covered
+        b1 = (unsigned)std::max<int64_t>(b0, std::min<int64_t>(nb, full + 1));
+      }
+      count(lin, fwd, unsorted, b0, b1);
+      b0 = b1;
+    }
+    count(lin, fwd, unsorted, b0, nb);
+  }
   FTT_LAUNCHED(ctx);
   prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz, 0.0);
   if (rev.np > 0) {
@@ -2238,7 +2260,7 @@ int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, 
                                   return g;
                                 }));
     pb = prof_begin(ctx);
-    count(kr, rev, unsorted + 1);
+    count(kr, rev, unsorted + 1, 0, nb);
     FTT_LAUNCHED(ctx);
     prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz, 0.0);
   }
@@ -2466,6 +2488,10 @@ int ftt_fiber_counts_lin(ftt_ctx *ctx, const int64_t *lin, const int64_t *coords
     set_error("nnz exceeds the 2^30 sort limit");
     return FTT_ERR_INVALID;
   }
+  struct ChunkGuard {  // whatever path runs, no pending lin chunk survives the call
+    ftt_ctx *c;
+    ~ChunkGuard() { c->lin_nchunks = 0; }
+  } chunk_guard{ctx};
   if (nnz == 0) {
     for (int p = 0; p < d; ++p) counts_host[p] = 0;
     return FTT_OK;
@@ -2476,9 +2502,12 @@ int ftt_fiber_counts_lin(ftt_ctx *ctx, const int64_t *lin, const int64_t *coords
   const char *path = getenv("FTT_COUNT_PATH");
   const bool force_lin = path && !strcmp(path, "lin");
   const bool force_other = path && !force_lin;
-  if (force_other && coords)
+  if (force_other && coords) {
+    FTT_CHECK(lin_chunks_wait_all(ctx));
     return ftt_fiber_counts_all(ctx, coords, nnz, d, dims_host, counts_host);
+  }
   if (!force_lin && 8 * T <= ((int64_t)32 << 20)) {
+    FTT_CHECK(lin_chunks_wait_all(ctx));
     // small inputs: one pass, d L2-resident global hash sets (as
     // ftt_fiber_counts_all), keys derived from lin
     int group = (int)std::max<int64_t>(1, std::min<int64_t>(d, ((int64_t)1 << 29) / T));
@@ -2545,6 +2574,7 @@ int ftt_extract_fibers_lin(ftt_ctx *ctx, const int64_t *lin, const double *value
     set_error("nnz exceeds the 2^30 sort limit");
     return FTT_ERR_INVALID;
   }
+  FTT_CHECK(lin_chunks_wait_all(ctx));
   if (nnz == 0) {
     *num_fibers_out = 0;
     k_set_i64<<<1, 1, 0, ctx->stream>>>(indptr, 0);
@@ -2560,6 +2590,10 @@ int ftt_extract_fibers_lin(ftt_ctx *ctx, const int64_t *lin, const double *value
   int64_t *bc = take<int64_t>(ctx, ceil_div(nnz, CP_TILE) + 1);
   int64_t *total = take<int64_t>(ctx, 1);
   AdjDiffPred pred{kr, make_div63(1)};
+  if (ctx->values_event) {  // the values' upload overlapped the key sort (ftt_fasttt_lin)
+    FTT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->values_event, 0));
+    ctx->values_event = nullptr;
+  }
   FiberEmitLin emit{kr, vr, values, reinterpret_cast<const uint64_t *>(lin), ks, fixed_lin, indptr,
                     fiber_of, pivot_index, values_out};
   FTT_CHECK(compact(ctx, nnz, pred, emit, bc, total, PT_SEGMENT, 44.0 * (double)nnz));

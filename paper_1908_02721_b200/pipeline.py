@@ -1183,6 +1183,12 @@ def _fasttt_fused(a: SparseTensor, values_d, eps, pivot, mode, c_svd, report, va
     lib, ctx = nat.lib(), nat.context()
     r = _FastttResult()
     ev = nat.ctypes.c_void_p(values_ready.cuda_event) if values_ready is not None else None
+    chunks = a.take_lin_chunks()
+    if chunks is not None:  # lin still arriving: the native side waits chunk by chunk
+        ends, evs = chunks
+        nat.check(lib.ftt_set_lin_chunks(
+            ctx, len(ends), nat.i64_array(ends),
+            (nat.ctypes.c_void_p * len(evs))(*[e.cuda_event for e in evs])), "ftt_set_lin_chunks")
     try:
         nat.check(lib.ftt_fasttt_lin(ctx, nat.ptr(a.device_lin()), nat.ptr(values_d), nnz, d,
                                      nat.i64_array(dims), -1 if pivot is None else int(pivot),
@@ -1272,6 +1278,7 @@ def fasttt_device(a: SparseTensor, coords_d, values_d, eps, pivot, mode, fixed_r
         res = _fasttt_fused(a, values_d, eps, pivot, mode, c_svd, report, values_ready)
         if res is not None:
             return res
+    a._lin_arrived()  # (a chunked upload the fused call did not take over)
     if pivot is None:
         pivot = select_p(a, target_ranks=fixed_ranks if mode == "fixed_rank" else None,
                          precise=precise_pivot, c_svd=c_svd)
@@ -1420,7 +1427,8 @@ def fasttt(a: SparseTensor, eps: float | None = 1e-14, pivot: int | None = None,
     if a.nnz:
         # lin + values only (no coordinate rows); the values' copy runs on a
         # side stream under select_p's counts
-        _, values_d, ready = a.device_lin_values()
+        # (a large lin arrives in chunks: the fused call starts on the first)
+        _, values_d, ready = a.device_lin_values(keep_chunks=True)
     else:
         values_d = None
     res = fasttt_device(a, None, values_d, eps, pivot, mode, fixed_ranks, precise_pivot, c_svd,
