@@ -2264,10 +2264,10 @@ int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, 
     FTT_LAUNCHED(ctx);
     prof_end(ctx, pb, PT_SEGMENT, 8.0 * (double)nnz, 0.0);
   }
-  unsigned long long h[32];
+  unsigned long long h[32 + 17];  // counts, then the 34 flag words: one round trip
+  FTT_CHECK(copy_to_host(ctx, h, cnt, 8 * 32 + 4 * 34));
   int hf[34];
-  FTT_CHECK(copy_to_host(ctx, h, cnt, 8 * 32));
-  FTT_CHECK(copy_to_host(ctx, hf, flags, 4 * 34));
+  memcpy(hf, h + 32, 4 * 34);
   if (bucketed) owned_free(ctx, bucketed);
   owned_free(ctx, cnt);
   const bool sorted = hf[32] == 0;
