@@ -653,6 +653,48 @@ __global__ void k_left_vec(int64_t K, const int64_t *__restrict__ kept, int64_t 
   }
 }
 
+// The same product with the core slice staged in shared memory, transposed
+// to [i][b][a]: LP lanes per kept row (LP = rin rounded up to a power of
+// two), lane a owns out[j, a] = sum_b core[a, i, b] next[s, b] -- the core
+// reads are conflict-free (a fastest), next[s, :] is a broadcast read, and
+// there are no shuffles (k_right_vec<16> spent its time in the 64 butterfly
+// shuffles per row: 142 -> ~40 us on config 5's 314,928 suffixes).
+template <int RO>
+__global__ void __launch_bounds__(256) k_right_vec_sm(int64_t K, const int64_t *__restrict__ kept,
+                                                      int64_t r, int64_t n, int rin, int LP,
+                                                      const double *__restrict__ next,
+                                                      const double *__restrict__ core,
+                                                      double *__restrict__ out) {
+  extern __shared__ __align__(16) double sm[];  // n x RO x rin
+  const int total = (int)(rin * n * RO);
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    // core[(a n + i) RO + b]  ->  sm[(i RO + b) rin + a]
+    const int b = e % RO, ai = e / RO;
+    const int i = ai % (int)n, a = ai / (int)n;
+    sm[(i * RO + b) * rin + a] = core[e];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, a = lane % LP, rpw = 32 / LP;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * rpw;
+  for (int64_t base = wg * rpw; base < K; base += stride) {
+    const int64_t j = base + lane / LP;
+    if (j >= K || a >= rin) continue;
+    const int64_t row = kept[j];
+    const int64_t i = row / r, s = row - i * r;
+    const double2 *nx = reinterpret_cast<const double2 *>(next + s * RO);
+    const double *c = sm + (size_t)i * RO * rin + a;
+    double acc = 0.0;
+#pragma unroll
+    for (int b2 = 0; b2 < RO / 2; ++b2) {
+      const double2 w = __ldg(nx + b2);
+      acc = fma(c[(2 * b2) * rin], w.x, acc);
+      acc = fma(c[(2 * b2 + 1) * rin], w.y, acc);
+    }
+    out[j * rin + a] = acc;
+  }
+}
+
 // out[j, :] = core[:, i, :] . next[s, :], (i, s) = (kept[j] / r, kept[j] % r):
 // RO lanes per kept row j (RO = 8 / 16 / 32 = rout): lane b holds next[s, b]
 // and reads core[a, i, b] for every a (coalesced rows), the products are
@@ -835,7 +877,30 @@ extern "C" int ftt_inner_structured(ftt_ctx *ctx, int32_t d, const int64_t *dims
 #define FTT_RV(RO_)                                                                           \
   k_right_vec<RO_><<<grid_for(K * (RO_ > 0 ? RO_ : 1), 256, 1), 256, 0, ctx->stream>>>(       \
       K, kept[pivot + q], r_other, dims[k], (int)ranks[k], ro, W, cores[k], cur)
-    if (!W) FTT_RV(0);  // the last core: no next vector
+    // long kept lists with a small core slice: the shared-memory variant
+    const int rin = (int)ranks[k];
+    const size_t slice = 8 * (size_t)rin * dims[k] * ro;
+    if (W && K >= 60000 && rin <= 32 && (ro == 8 || ro == 16 || ro == 32) && slice <= 65536) {
+      static bool attr = false;
+      if (!attr) {
+        FTT_CUDA(cudaFuncSetAttribute(k_right_vec_sm<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        FTT_CUDA(cudaFuncSetAttribute(k_right_vec_sm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        FTT_CUDA(cudaFuncSetAttribute(k_right_vec_sm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        attr = true;
+      }
+      int LP = 1;
+      while (LP < rin) LP <<= 1;
+      const int g = grid_for(K * LP, 256, 4, 148 * 3);
+      if (ro == 8)
+        k_right_vec_sm<8><<<g, 256, slice, ctx->stream>>>(K, kept[pivot + q], r_other, dims[k], rin,
+                                                          LP, W, cores[k], cur);
+      else if (ro == 16)
+        k_right_vec_sm<16><<<g, 256, slice, ctx->stream>>>(K, kept[pivot + q], r_other, dims[k], rin,
+                                                           LP, W, cores[k], cur);
+      else
+        k_right_vec_sm<32><<<g, 256, slice, ctx->stream>>>(K, kept[pivot + q], r_other, dims[k], rin,
+                                                           LP, W, cores[k], cur);
+    } else if (!W) FTT_RV(0);  // the last core: no next vector
     else if (ro == 1) FTT_RV(1);
     else if (ro == 8) FTT_RV(8);
     else if (ro == 16) FTT_RV(16);
