@@ -446,7 +446,7 @@ extern "C" int ftt_tt_entries(ftt_ctx *ctx, int32_t d, const int64_t *dims_host,
   for (int k = 0; k < d; ++k) steps += (double)ranks_host[k];
   if (rmax <= 64 && d >= 4 && (double)n * steps > 4e8 && n < ((int64_t)1 << 31))
     return entries_mitm(ctx, t, coords, n, out);
-  if (rmax <= 8 && !getenv("FTT_ENTRIES_GRP")) {
+  if (rmax <= 8) {
     double steps_sum = 0.0;
     for (int k = 0; k < d; ++k) steps_sum += (double)ranks_host[k] * ranks_host[k + 1];
     const int pb = prof_begin(ctx);

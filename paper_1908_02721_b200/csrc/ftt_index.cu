@@ -1810,8 +1810,7 @@ int fiber_counts_partition(ftt_ctx *ctx, const int64_t *coords, int64_t nnz, int
   // (fibers with several nonzeros land whole in one bucket: the variance of a
   // bucket's fill is ~mean x (average fiber size), hence the wide margin)
   const int64_t cap = std::min<int64_t>(nnz, mean + 16 * (int64_t)std::sqrt((double)mean) + 256);
-  static const char *gs = getenv("FTT_PART_GROUP");  // A/B knob: pivots per pass
-  const int G = std::max(1, std::min(std::min((int)d, PC_MAXG), gs ? atoi(gs) : 1));
+  const int G = 1;  // pivots per pass (more per pass measured no faster)
   const int nb = kNumSMs;
   LinSpec ls;
   ls.d = d;

@@ -1104,8 +1104,7 @@ void launch_level(ftt_ctx *ctx, int n, unsigned grid, int64_t M, const double *A
     nt = (unsigned)std::min<int64_t>(leaf, ceil_div(need, 32) * 32);
   }
   // n <= 16: rpt rows per thread
-  static const int rpt_env = getenv("FTT_TSQR_RPT") ? atoi(getenv("FTT_TSQR_RPT")) : 0;
-  const int rpt = rpt_env == 4 ? 4 : LEAF_RPT;
+  const int rpt = LEAF_RPT;  // (4 rows per thread measured slower: DESIGN 4e)
   const unsigned ntm = (unsigned)(leaf / rpt);  // k_tsqr_wy's compile-time thread count
   switch (nmax_for(n)) {
     case 8:

@@ -75,8 +75,7 @@ constexpr int CH = 64;      // rows per staged chunk
 // recompute.  They only pick rotations (convergence is decided on fresh
 // Grams), and each costs 31 rounds x 3 CTA barriers: measured on config 4's
 // 2064 x 766 operand, 1 inner sweep = 23 outer sweeps / 97 ms, 3 = 21 / 153 ms.
-constexpr int MAX_INNER = 3;
-__device__ int g_max_inner = 1;  // A/B knob FTT_JINNER (1..3)
+__device__ int g_max_inner = 1;  // inner two-sided sweeps per block pair (up to 3 supported)
 int g_last_csize = 1;             // debug print only
 
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
@@ -159,7 +158,7 @@ __device__ __forceinline__ void pair_of(int nblk, int step, int c, int *a, int *
 // Convergence is decided on the FRESH Gram only (entries from the current
 // columns): pair (i, j) needs work iff both columns are above the noise
 // floor (|x|^2 > floor) and |g_ij| > tol sqrt(g_ii g_jj).  The inner
-// two-sided sweeps (at most MAX_INNER) use Rutishauser's diagonal update
+// two-sided sweeps (at most 3) use Rutishauser's diagonal update
 // g_pp -= t g_pq, g_qq += t g_pq; entries derived there are only used to
 // pick the next rotations, never to declare convergence, so rounding in
 // them (after cancellation between near-parallel columns) cannot stall the
@@ -883,9 +882,8 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     int nblk = (int)ceil_div(nA, JB);
     if (nblk & 1) ++nblk;
     // relative orthogonality target sqrt(n) eps (LAPACK dgesvj's);
-    // FTT_JTOL scales it (measured: no effect on sweep counts up to 16x)
-    static const double jtol_scale = getenv("FTT_JTOL") ? atof(getenv("FTT_JTOL")) : 1.0;
-    const double tol = jtol_scale * 2.220446049250313e-16 * sqrt((double)nA);
+    // (scaling it up to 16x was measured to leave the sweep counts unchanged)
+    const double tol = 2.220446049250313e-16 * sqrt((double)nA);
     // noise floor: columns with |x|^2 <= (0.1 eps)^2 * rows * ||X||_F^2 are
     // below the backward error of the QR and are not orthogonalised further
     double fro2 = 0.0;
@@ -893,15 +891,6 @@ int svd_factor(ftt_ctx *ctx, SvdState *st, int64_t m, int64_t n, const double *A
     const double floor = 0.01 * 2.220446049250313e-16 * 2.220446049250313e-16 * (double)mX * fro2;
     const int max_sweeps = 60;
     FTT_CUDA(cudaMemsetAsync(rot, 0, sizeof(unsigned long long) * 64, ctx->stream));
-    static bool inner_set = false;
-    if (!inner_set) {
-      const char *e = getenv("FTT_JINNER");
-      if (e) {
-        const int v = std::max(1, std::min(MAX_INNER, atoi(e)));
-        FTT_CUDA(cudaMemcpyToSymbol(g_max_inner, &v, sizeof(int)));
-      }
-      inner_set = true;
-    }
     static int coresident = 0, coresident3 = 0;
     if (!coresident) {
       int per_sm = 0, per_sm3 = 0;
