@@ -355,6 +355,10 @@ int ftt_fasttt_lin(ftt_ctx *ctx, const int64_t *lin, const double *values, int64
                    int32_t report, void *values_ready, ftt_fasttt_result *res) {
   if (!ctx || !lin || !values || !dims || !res || nnz < 1 || d < 2 || d > 32 || pivot >= d ||
       mode < 0 || mode > 1) {
+    if (ctx) {  // a chunk list set for this call does not outlive it
+      ctx->lin_nchunks = 0;
+      ctx->values_event = nullptr;
+    }
     set_error("ftt_fasttt_lin: invalid arguments");
     return FTT_ERR_INVALID;
   }

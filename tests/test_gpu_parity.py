@@ -756,3 +756,30 @@ def test_scattered_carry_matches_dense(dims, R, s, pivot, monkeypatch):
     assert rel_err(ft.tt_entries(tt_s, t.coords), t.values) <= 1e-8
     for a, b in zip(tt_s.cores, tt_s2.cores):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("count_path", [None, "lin"])
+def test_chunked_lin_upload_matches(count_path, monkeypatch):
+    """fasttt() with the linear index uploaded in chunks whose events the
+    native call takes over (ftt_set_lin_chunks: select_p's forward counts run
+    piecewise on the chunks present; the values are waited for at the fiber
+    emit) against the single-copy upload: same pivot, bit-identical cores --
+    with select_p on its small-input path (waits for every chunk), forced
+    onto the chunk-count path, and with an explicit pivot."""
+    from paper_1908_02721_b200 import coo as C
+
+    if count_path:
+        monkeypatch.setenv("FTT_COUNT_PATH", count_path)
+    t = _rank_r_sparse((20, 18, 22, 16, 24), 5, 4, seed=21)
+    runs = []
+    for chunk_min in (1 << 60, 1):
+        monkeypatch.setattr(C, "_LIN_CHUNK_MIN", chunk_min)
+        for kw in (dict(eps=1e-9), dict(eps=1e-9, pivot=3), dict(eps=1e-6, mode="dynamic")):
+            t.drop_device_copy()
+            tt, rep = ft.fasttt(t, **kw)
+            runs.append((rep.pivot, rep.num_fibers, tuple(rep.ranks), tt.cores))
+    half = len(runs) // 2
+    for a, b in zip(runs[:half], runs[half:]):
+        assert a[:3] == b[:3]
+        for x, y in zip(a[3], b[3]):
+            assert np.array_equal(x, y)
