@@ -14,9 +14,9 @@ python bench.py > $OUT/bench.json 2> $OUT/bench.err
 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 
 # 2. launch list of the bench command (per-launch times, cold-cache, serialised)
-python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-c5-index > $OUT/bench_small.json 2>&1 &&
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-index-leg > $OUT/bench_small.json 2>&1 &&
   $NCU --metrics gpu__time_duration.sum --csv --log-file $OUT/launches_bench_c2.csv \
-    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-c5-index > $OUT/ncu_bench.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-index-leg > $OUT/ncu_bench.log 2>&1
 
 # 3. per-launch DRAM traffic of one warm decomposition per config
 #    (ncu cannot replay the cooperative launch of clustered Jacobi pairs, so
