@@ -731,7 +731,11 @@ def test_fused_driver_matches_stepwise(monkeypatch):
 
 
 @pytest.mark.parametrize("dims,R,s,pivot", [((24,) * 6, 5, 3, 1), ((12, 40, 9, 6, 16, 20), 4, 4, 1),
-                                            ((8, 6, 40, 40, 40), 6, 3, 0)])
+                                            ((8, 6, 40, 40, 40), 6, 3, 0),
+                                            # rank 20: sketch 48 wide, 3 x 3 DMMA tiles per warp set
+                                            ((6, 6, 6, 40, 40, 40), 20, 3, 0),
+                                            # mode size 300 > 256: several column chunks per row tile
+                                            ((8, 300, 50, 50, 50), 3, 8, 0)])
 def test_scattered_carry_matches_dense(dims, R, s, pivot, monkeypatch):
     """Right-sweep steps whose operand is a carry times a 0/1 core run the
     certified low-rank path on the compact (unscattered) form
@@ -783,3 +787,38 @@ def test_chunked_lin_upload_matches(count_path, monkeypatch):
         assert a[:3] == b[:3]
         for x, y in zip(a[3], b[3]):
             assert np.array_equal(x, y)
+
+
+def test_rank_guess_redone_when_wrong(monkeypatch):
+    """The low-rank step runs at the previous step's rank without waiting for
+    the sketch's rank word and is redone at the true rank when the guess was
+    wrong.  Six terms whose factors over modes 3.. repeat with period 3 give
+    bond ranks (6, 6, 3, 3, 3): the step after the rank-6 one guesses 6 and
+    finds 3.  Against the Python sweep driver (no guessing): the same ranks,
+    bit-identical cores."""
+    dims, s = (24,) * 6, 3
+    rng = np.random.default_rng(5)
+    suffix = [([rng.choice(n, s, replace=False) for n in dims[3:]],
+               [rng.standard_normal(s) for _ in dims[3:]]) for _ in range(3)]
+    lins, vals = [], []
+    for r in range(6):
+        pos = [rng.choice(n, s, replace=False) for n in dims[:3]] + suffix[r % 3][0]
+        fac = [rng.standard_normal(s) for _ in dims[:3]] + suffix[r % 3][1]
+        grid = np.stack(np.meshgrid(*pos, indexing="ij"), -1).reshape(-1, len(dims))
+        val = np.ones(1)
+        for f in fac:
+            val = np.multiply.outer(val, f).reshape(-1)
+        lins.append(np.ravel_multi_index(grid.T, dims))
+        vals.append(val)
+    u, inv = np.unique(np.concatenate(lins), return_inverse=True)
+    vsum = np.zeros(u.size)
+    np.add.at(vsum, inv, np.concatenate(vals))
+    t = ft.SparseTensor(dims, np.stack(np.unravel_index(u, dims), 1).astype(np.int64), vsum)
+    tt_n, rep_n = ft.fasttt(t, eps=1e-9, pivot=1)
+    assert tuple(rep_n.ranks) == (6, 6, 3, 3, 3)
+    monkeypatch.setenv("FTT_PY_SWEEP", "1")
+    tt_p, rep_p = ft.fasttt(t, eps=1e-9, pivot=1)
+    assert tuple(rep_p.ranks) == tuple(rep_n.ranks)
+    for a, b in zip(tt_n.cores, tt_p.cores):
+        assert np.array_equal(a, b)
+    assert rel_err(ft.tt_entries(tt_n, t.coords), t.values) <= 1e-8
