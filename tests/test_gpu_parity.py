@@ -421,9 +421,10 @@ def _rank_r_sparse(dims, R, s, seed):
     """Sum of R sparse rank-1 terms (s seeded positions per mode), coalesced."""
     rng = np.random.default_rng(seed)
     lins, vals = [], []
+    ss = s if isinstance(s, (tuple, list)) else (s,) * len(dims)
     for _ in range(R):
-        pos = [rng.choice(n, s, replace=False) for n in dims]
-        fac = [rng.standard_normal(s) for _ in dims]
+        pos = [rng.choice(n, sk, replace=False) for n, sk in zip(dims, ss)]
+        fac = [rng.standard_normal(sk) for sk in ss]
         grid = np.stack(np.meshgrid(*pos, indexing="ij"), -1).reshape(-1, len(dims))
         val = np.ones(1)
         for f in fac:
@@ -468,8 +469,11 @@ def test_sparse_pivot_core_lowrank_matches_dense(dims, R, s, pivot, monkeypatch)
     kk = min(len(s_sp), len(s_de))
     assert np.max(np.abs(s_sp[:kk] - s_de[:kk])) <= 1e-12 * s_de[0]
     assert rest_sp <= 1e-6 * delta * delta and rest_de <= 1e-6 * delta * delta
-    # end to end through the sparse first step (forced for the denser cases)
+    # end to end through the sparse first step (forced for the denser cases:
+    # the step-by-step orchestration honours the Python density threshold and
+    # hands the fiber structure to the native sweep -> fiber-level CSR)
     monkeypatch.setattr(P, "_SPARSE_PIVOT_DENSITY", 1.0)
+    monkeypatch.setattr(P, "_STEPWISE", True)
     tt, rep = ft.fasttt(t, eps=1e-10, pivot=pivot)
     cores, info = O.fasttt(t.shape, t.coords, t.values, eps=1e-10, pivot=pivot, report=False)
     assert tuple(rep.ranks) == info["ranks"]
@@ -642,6 +646,7 @@ def test_sparse_pivot_core_other_modes(mode, eps, monkeypatch):
     ranks -- which always densify): ranks equal to the oracle's, entries
     within 1e-10 of the oracle train."""
     monkeypatch.setattr(P, "_SPARSE_PIVOT_DENSITY", 1.0)
+    monkeypatch.setattr(P, "_STEPWISE", True)
     t = _rank_r_sparse((24,) * 5, 5, 3, seed=99)
     kw = {"fixed_ranks": 3} if mode == "fixed_rank" else {}
     tt, rep = ft.fasttt(t, eps=eps, pivot=1, mode=mode, **kw)
@@ -822,3 +827,20 @@ def test_rank_guess_redone_when_wrong(monkeypatch):
     for a, b in zip(tt_n.cores, tt_p.cores):
         assert np.array_equal(a, b)
     assert rel_err(ft.tt_entries(tt_n, t.coords), t.values) <= 1e-8
+
+
+def test_sparse_pivot_long_fibers(monkeypatch):
+    """Fiber-level CSR of the sparse first step with fibers longer than the
+    sketch kernel's 128 shared slots (150 nonzeros per fiber: streamed from
+    global memory) and rows holding several fibers: ranks equal to the
+    oracle's, entries within 1e-10."""
+    dims = (200, 12, 12, 12, 12)
+    t = _rank_r_sparse(dims, 3, (150, 3, 3, 3, 3), seed=17)
+    monkeypatch.setattr(P, "_SPARSE_PIVOT_DENSITY", 1.0)
+    monkeypatch.setattr(P, "_STEPWISE", True)
+    tt, rep = ft.fasttt(t, eps=1e-10, pivot=0)
+    cores, info = O.fasttt(t.shape, t.coords, t.values, eps=1e-10, pivot=0, report=False)
+    assert tuple(rep.ranks) == info["ranks"]
+    rng = np.random.default_rng(3)
+    probe = np.concatenate([t.coords, np.stack([rng.integers(0, n, 20000) for n in dims], 1)])
+    assert rel_err(ft.tt_entries(tt, probe), O.tt_entries(cores, probe)) <= RECON_TOL
