@@ -560,12 +560,33 @@ __global__ void __launch_bounds__(CP_THREADS) k_compact1(int64_t nmax, Pred pred
     }
     __syncthreads();
     int64_t run = (int64_t)s_excl + wpre;
+    if constexpr (Emit::kTwoPhase) {
+      constexpr int CP_BATCH = 8;  // items whose gathers are in flight together
 #pragma unroll
-    for (int j = 0; j < CP_ITEMS; ++j) {
-      const int64_t i = wbase + j * 32 + lane;
-      const bool f = (balls[j] >> lane) & 1u;
-      if (i < n) emit(i, run + __popc(balls[j] & lt), f);
-      run += __popc(balls[j]);
+      for (int j0 = 0; j0 < CP_ITEMS; j0 += CP_BATCH) {
+        typename Emit::Item it[CP_BATCH];
+#pragma unroll
+        for (int u = 0; u < CP_BATCH; ++u) {
+          const int64_t i = wbase + (j0 + u) * 32 + lane;
+          if (i < n) it[u] = emit.load(i);
+        }
+#pragma unroll
+        for (int u = 0; u < CP_BATCH; ++u) {
+          const int j = j0 + u;
+          const int64_t i = wbase + j * 32 + lane;
+          const bool f = (balls[j] >> lane) & 1u;
+          if (i < n) emit.store(i, run + __popc(balls[j] & lt), f, it[u]);
+          run += __popc(balls[j]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CP_ITEMS; ++j) {
+        const int64_t i = wbase + j * 32 + lane;
+        const bool f = (balls[j] >> lane) & 1u;
+        if (i < n) emit(i, run + __popc(balls[j] & lt), f);
+        run += __popc(balls[j]);
+      }
     }
     __syncthreads();  // s_tile / s_w / s_excl reuse
   }
@@ -647,6 +668,7 @@ struct AdjDiffPred {  // sorted keys: key/div differs from predecessor
 };
 
 struct FiberEmit {
+  static constexpr bool kTwoPhase = false;
   const uint64_t *k;
   const uint32_t *perm;
   const double *vals_in;
@@ -672,6 +694,7 @@ struct FlagPred {
 };
 
 struct KeptEmit {  // kept[r] = row, present[row] <- rank (overwrites the flag)
+  static constexpr bool kTwoPhase = false;
   uint32_t *present;
   int64_t *kept;
   __device__ void operator()(int64_t i, int64_t r, bool f) const {
@@ -683,6 +706,7 @@ struct KeptEmit {  // kept[r] = row, present[row] <- rank (overwrites the flag)
 };
 
 struct UniqEmit {  // sort path: sorted keys with fiber payload
+  static constexpr bool kTwoPhase = false;
   const uint64_t *k;
   const uint32_t *perm;
   int64_t *kept, *map_out;
@@ -1361,6 +1385,7 @@ struct CoalescePred {
 };
 
 struct CoalesceEmit {
+  static constexpr bool kTwoPhase = false;
   CoalescePred p;
   FuseSpec fs;
   int64_t *coords;
@@ -2097,7 +2122,37 @@ __device__ __forceinline__ uint64_t lin_fiber_key(uint64_t x, const LinKeySpec &
 
 // Emit of the fiber extraction on the fixed-tuple keys: the pivot index is
 // re-derived from lin[perm[i]] (a gather from the chunk the sort just read).
+// Two-phase form (kTwoPhase): k_compact1 first loads the gathers of a batch
+// of items (perm -> lin, value: two dependent random reads per nonzero) and
+// only then stores -- interleaved with the stores, as operator() has them,
+// the loads of the next item cannot be hoisted (the outputs may alias) and
+// the kernel ran one gather chain per thread at a time (ncu: 16 % issue
+// active, long-scoreboard stalls).
 struct FiberEmitLin {
+  static constexpr bool kTwoPhase = true;
+  struct Item {
+    uint64_t key, lin;
+    double val;
+  };
+  __device__ Item load(int64_t i) const {
+    const uint32_t src = __ldg(perm + i);
+    Item it;
+    it.key = __ldg(k + i);
+    it.lin = __ldg(lin + src);
+    it.val = __ldg(vals_in + src);
+    return it;
+  }
+  __device__ void store(int64_t i, int64_t r, bool f, const Item &it) const {
+    if (f) {
+      indptr[r] = i;
+      fixed_lin[r] = (int64_t)it.key;
+    }
+    if (fiber_of) fiber_of[i] = f ? r : r - 1;
+    uint64_t ip = 0;
+    lin_fiber_key(it.lin, ks, &ip);
+    pivot_index[i] = (int64_t)ip;
+    vals_out[i] = it.val;
+  }
   const uint64_t *k;
   const uint32_t *perm;
   const double *vals_in;
@@ -2105,18 +2160,6 @@ struct FiberEmitLin {
   LinKeySpec ks;
   int64_t *fixed_lin, *indptr, *fiber_of, *pivot_index;
   double *vals_out;
-  __device__ void operator()(int64_t i, int64_t r, bool f) const {
-    const uint32_t src = perm[i];
-    if (f) {
-      indptr[r] = i;
-      fixed_lin[r] = (int64_t)k[i];
-    }
-    if (fiber_of) fiber_of[i] = f ? r : r - 1;
-    uint64_t ip = 0;
-    lin_fiber_key(lin[src], ks, &ip);
-    pivot_index[i] = (int64_t)ip;
-    vals_out[i] = vals_in[src];
-  }
 };
 
 __global__ void __launch_bounds__(256) k_keys_hist_lin(const uint64_t *__restrict__ lin, int64_t n,
