@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_compact1(int64_t nmax, Pred pred
     __syncthreads();
     int64_t run = (int64_t)s_excl + wpre;
     if constexpr (Emit::kTwoPhase) {
-      constexpr int CP_BATCH = 8;  // items whose gathers are in flight together
+      constexpr int CP_BATCH = 8;  // items whose gathers are in flight together (16: spills, 284 us)
 #pragma unroll
       for (int j0 = 0; j0 < CP_ITEMS; j0 += CP_BATCH) {
         typename Emit::Item it[CP_BATCH];
