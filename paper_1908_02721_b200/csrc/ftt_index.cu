@@ -1421,11 +1421,14 @@ template <class MkDigit>
 int onesweep_passes_t(ftt_ctx *ctx, uint64_t *keys[2], uint32_t *vals[2], int64_t n, int num_passes,
                       uint32_t *ghist, uint32_t *status, uint32_t *counters, uint64_t **kres,
                       uint32_t **vres, const uint64_t *kin, const uint32_t *vin, uint64_t *kout,
-                      uint32_t *vout, MkDigit mk) {
-  // decide which passes are needed (constant digit -> skip)
+                      uint32_t *vout, MkDigit mk, bool all_active = false) {
+  // decide which passes are needed (constant digit -> skip); hashed digits
+  // (all_active) are never constant on inputs that reach this path, so their
+  // histogram is not brought to the host (one round trip less)
   static thread_local std::vector<uint32_t> h;
   h.assign((size_t)num_passes * RADIX, 0);
-  FTT_CHECK(copy_to_host(ctx, h.data(), ghist, sizeof(uint32_t) * num_passes * RADIX));
+  if (!all_active)
+    FTT_CHECK(copy_to_host(ctx, h.data(), ghist, sizeof(uint32_t) * num_passes * RADIX));
   k_hist_scan<<<num_passes, RADIX, 0, ctx->stream>>>(ghist);
   FTT_LAUNCHED(ctx);
   // tile: RS_ITEMS = 16 keys per thread (measured on config 5: 8 / 12 / 24
@@ -2307,7 +2310,8 @@ int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, 
                                   DigitHashMod g = dg;
                                   g.shift = 8 * p;
                                   return g;
-                                }));
+                                },
+                                /*all_active=*/true));
     pb = prof_begin(ctx);
     count(kr, rev, unsorted + 1, 0, nb);
     FTT_LAUNCHED(ctx);
