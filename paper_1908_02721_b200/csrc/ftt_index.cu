@@ -2078,11 +2078,21 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
     auto slot = [](uint64_t k) -> unsigned {
       return (unsigned)((k * 0x9E3779B97F4A7C15ull) >> (64 - 13));
     };
+    unsigned long long fresh = 0;
+    if (!sp.align_hash && S == 1) {
+      // last mode in lin order: a fiber's nonzeros are adjacent (the chunk is
+      // sorted, else `unsorted` sends the caller to another count), so first
+      // occurrences are adjacent differences -- no table
+      for (int j = threadIdx.x; j < cnt; j += SC_NT)
+        fresh += j == 0 || reduce(skey[j - 1]) != reduce(skey[j]);
+      for (int o = 16; o; o >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, o);
+      if (lane == 0 && fresh) atomicAdd(count + sp.slot[q], fresh);
+      continue;
+    }
     for (int e = threadIdx.x; e < SC_SLOTS / 4; e += SC_NT)
       reinterpret_cast<uint4 *>(tab32)[e] = make_uint4(~0u, ~0u, ~0u, ~0u);
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
-    unsigned long long fresh = 0;
     for (int j = threadIdx.x; j < cnt; j += SC_NT) {  // only the chunk's live rounds
       const uint64_t r = reduce(skey[j]);
       unsigned h = slot(r);
