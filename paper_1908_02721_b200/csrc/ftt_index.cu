@@ -2005,8 +2005,10 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
                                                    int *__restrict__ flag,
                                                    int *__restrict__ unsorted, unsigned blk_off) {
   extern __shared__ unsigned long long smem[];
-  uint64_t *skey = reinterpret_cast<uint64_t *>(smem);             // SC_CAP keys
-  unsigned *tab32 = reinterpret_cast<unsigned *>(smem + SC_CAP);   // SC_SLOTS positions
+  // the chunk's keys stay in global memory: at most 32 KB per CTA, re-read
+  // through L1 by every pivot's pass; shared memory holds only the table
+  // (32 KB: 4 CTAs per SM)
+  unsigned *tab32 = reinterpret_cast<unsigned *>(smem);   // SC_SLOTS positions
   __shared__ int64_t s_start, s_end;
   __shared__ unsigned s_j[2];
   __shared__ unsigned long long s_cnt;
@@ -2057,12 +2059,11 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
   for (int q = 0; q < PER; ++q) {
     const int j = q * SC_NT + threadIdx.x;
     if (j < cnt) {
-      const uint64_t k = __ldg(K + start + j);
-      skey[j] = k;
-      if (!sp.align_hash && start + j + 1 < n) bad |= __ldg(K + start + j + 1) <= k;
+      if (!sp.align_hash && start + j + 1 < n) bad |= __ldg(K + start + j + 1) <= __ldg(K + start + j);
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(unsorted, 1);
+  const uint64_t *__restrict__ skey = K + start;
   // per pivot: the table holds chunk positions (native 32-bit shared CAS);
   // a probe that meets an occupied slot compares the fixed-tuple key of the
   // stored position, recomputed from its lin
@@ -2084,7 +2085,7 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
       // sorted, else `unsorted` sends the caller to another count), so first
       // occurrences are adjacent differences -- no table
       for (int j = threadIdx.x; j < cnt; j += SC_NT)
-        fresh += j == 0 || reduce(skey[j - 1]) != reduce(skey[j]);
+        fresh += j == 0 || reduce(__ldg(skey + j - 1)) != reduce(__ldg(skey + j));
       for (int o = 16; o; o >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, o);
       if (lane == 0 && fresh) atomicAdd(count + sp.slot[q], fresh);
       continue;
@@ -2094,7 +2095,7 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     for (int j = threadIdx.x; j < cnt; j += SC_NT) {  // only the chunk's live rounds
-      const uint64_t r = reduce(skey[j]);
+      const uint64_t r = reduce(__ldg(skey + j));
       unsigned h = slot(r);
       while (true) {
         const unsigned old = atomicCAS(tab32 + h, ~0u, (unsigned)j);
@@ -2102,7 +2103,7 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
           ++fresh;
           break;
         }
-        if (reduce(skey[old]) == r) break;
+        if (reduce(__ldg(skey + old)) == r) break;
         h = (h + 1) & (SC_SLOTS - 1);  // linear probing
       }
     }
@@ -2259,7 +2260,7 @@ int fiber_counts_lin(ftt_ctx *ctx, const uint64_t *lin, int64_t nnz, int32_t d, 
   int *unsorted = flags + 32;
   FTT_CUDA(cudaMemsetAsync(cnt, 0, 8 * 32 + 4 * 32 + 16, ctx->stream));
   static bool attr = false;
-  const size_t smem = 8 * (size_t)SC_CAP + 4 * (size_t)SC_SLOTS;
+  const size_t smem = 4 * (size_t)SC_SLOTS;
   if (!attr) {
     FTT_CUDA(cudaFuncSetAttribute(k_sel_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
