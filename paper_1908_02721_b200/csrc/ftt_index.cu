@@ -2011,7 +2011,7 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
   unsigned *tab32 = reinterpret_cast<unsigned *>(smem);   // SC_SLOTS positions
   __shared__ int64_t s_start, s_end;
   __shared__ unsigned s_j[2];
-  __shared__ unsigned long long s_cnt;
+  __shared__ unsigned s_cnt;  // first insertions of one pivot in this chunk (<= SC_CAP)
   const int lane = threadIdx.x & 31;
   const int64_t c0 = ((int64_t)blockIdx.x + blk_off) * SC_L;
   auto grp = [&](int64_t i) -> uint64_t { return sel_group<POW2>(K[i], sp); };
@@ -2079,15 +2079,15 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
     auto slot = [](uint64_t k) -> unsigned {
       return (unsigned)((k * 0x9E3779B97F4A7C15ull) >> (64 - 13));
     };
-    unsigned long long fresh = 0;
+    unsigned fresh = 0;
     if (!sp.align_hash && S == 1) {
       // last mode in lin order: a fiber's nonzeros are adjacent (the chunk is
       // sorted, else `unsorted` sends the caller to another count), so first
       // occurrences are adjacent differences -- no table
       for (int j = threadIdx.x; j < cnt; j += SC_NT)
         fresh += j == 0 || reduce(__ldg(skey + j - 1)) != reduce(__ldg(skey + j));
-      for (int o = 16; o; o >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, o);
-      if (lane == 0 && fresh) atomicAdd(count + sp.slot[q], fresh);
+      fresh = __reduce_add_sync(0xffffffffu, fresh);
+      if (lane == 0 && fresh) atomicAdd(count + sp.slot[q], (unsigned long long)fresh);
       continue;
     }
     for (int e = threadIdx.x; e < SC_SLOTS / 4; e += SC_NT)
@@ -2107,10 +2107,10 @@ __global__ void __launch_bounds__(SC_NT) k_sel_count(const uint64_t *__restrict_
         h = (h + 1) & (SC_SLOTS - 1);  // linear probing
       }
     }
-    for (int o = 16; o; o >>= 1) fresh += __shfl_down_sync(0xffffffffu, fresh, o);
+    fresh = __reduce_add_sync(0xffffffffu, fresh);
     if (lane == 0 && fresh) atomicAdd(&s_cnt, fresh);
     __syncthreads();
-    if (threadIdx.x == 0 && s_cnt) atomicAdd(count + sp.slot[q], s_cnt);
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(count + sp.slot[q], (unsigned long long)s_cnt);
   }
 }
 
